@@ -1,0 +1,207 @@
+"""ctypes wrapper of the CPU fp64 oracle (oracle/npc_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: importable from tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  The product path (paper_2208_01339_b200) never
+imports this package, and this package never imports the product.
+
+Every function names the PAPER.md passage it follows; see npc_oracle.c for the pins.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "npc_oracle.c")
+_LIB = os.path.join(_HERE, "liborc.so")
+CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain C, no GPU)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Op(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int), ("n", C.c_long),
+        ("rowptr", C.c_void_p), ("colidx", C.c_void_p), ("vals", C.c_void_p),
+        ("dim", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+        ("diag", C.c_double), ("offdiag", C.c_double),
+        ("c", C.c_void_p), ("nb", C.c_long),
+        ("browptr", C.c_void_p), ("bcolidx", C.c_void_p), ("bvals", C.c_void_p), ("d", C.c_void_p),
+        ("tmp", C.c_void_p),
+    ]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("iters", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int),
+                ("mvp", C.c_longlong), ("ddot", C.c_longlong),
+                ("relres_recursive", C.c_double), ("relres_true", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P = C.c_void_p
+        D = C.c_double
+        _lib.orc_op_apply.argtypes = [C.POINTER(_Op), P, P]
+        _lib.orc_cheb_params.argtypes = [D, D, D, P, P, P]
+        _lib.orc_cheb_rho.argtypes = [D, C.c_int, P]
+        _lib.orc_cheb_apply.argtypes = [C.POINTER(_Op), C.c_int, D, D, D, P, P, P]
+        _lib.orc_newton_zeta.argtypes = [D, D, D, C.c_int, P]
+        _lib.orc_newton_apply.argtypes = [C.POINTER(_Op), C.c_int, D, D, D, P, P, P]
+        _lib.orc_lanczos.argtypes = [C.POINTER(_Op), C.c_int, P, P, P, P]
+        _lib.orc_pcg.argtypes = [C.POINTER(_Op), C.c_int, D, D, D, P, P, D, C.c_int, P, C.POINTER(_Stats)]
+        _lib.orc_num_threads.restype = C.c_int
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+class Operator:
+    """Holds the numpy arrays alive and the C descriptor of an operator (O1)."""
+
+    def __init__(self, w: dict):
+        self.w = w
+        op = _Op()
+        kind = w["kind"]
+        op.n = int(w["n"])
+        self._keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return _p(a)
+
+        if kind == "csr":
+            op.kind = 0
+            op.rowptr = arr(w["rowptr"], np.int32)
+            op.colidx = arr(w["colidx"], np.int32)
+            op.vals = arr(w["vals"], np.float64)
+        elif kind == "stencil":
+            op.kind = 1
+            op.dim, op.nx, op.ny = int(w["dim"]), int(w["nx"]), int(w["ny"])
+            op.nz = int(w.get("nz", 1))
+            op.diag, op.offdiag = float(w["diag"]), float(w["offdiag"])
+        elif kind == "schur":
+            op.kind = 2
+            op.c = arr(w["c"], np.float64)
+            op.nb = int(w["nb"])
+            op.browptr = arr(w["browptr"], np.int32)
+            op.bcolidx = arr(w["bcolidx"], np.int32)
+            op.bvals = arr(w["bvals"], np.float64)
+            op.d = arr(w["d"], np.float64)
+            op.tmp = arr(np.zeros(op.nb), np.float64)
+        else:
+            raise ValueError(kind)
+        self.op = op
+        self.n = op.n
+
+    def apply(self, x):
+        """y = A x (O1)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.n)
+        assert lib().orc_op_apply(C.byref(self.op), _p(x), _p(y)) == 0
+        return y
+
+
+def cheb_params(alpha, beta, xi):
+    """(theta_bar, delta, sigma): PAPER.md:240-241 with Eq. thetamod, reading A1."""
+    t, d, s = C.c_double(), C.c_double(), C.c_double()
+    st = lib().orc_cheb_params(alpha, beta, xi, C.byref(t), C.byref(d), C.byref(s))
+    if st:
+        raise ValueError(f"invalid interval ({st})")
+    return t.value, d.value, s.value
+
+
+def cheb_rho(sigma, m):
+    """rho_0..rho_m by Eq. rhocheb."""
+    rho = np.empty(m + 1)
+    lib().orc_cheb_rho(sigma, m, _p(rho))
+    return rho
+
+
+def cheb_apply(op: Operator, m, alpha, beta, xi, r):
+    """p_m(A) r by Alg. 2 verbatim."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    out = np.empty(op.n)
+    work = np.empty(3 * op.n)
+    st = lib().orc_cheb_apply(C.byref(op.op), m, alpha, beta, xi, _p(r), _p(out), _p(work))
+    if st:
+        raise ValueError(f"cheb_apply failed ({st})")
+    return out
+
+
+def newton_zeta(alpha, beta, xi, nlev):
+    z = np.empty(nlev + 1)
+    assert lib().orc_newton_zeta(alpha, beta, xi, nlev, _p(z)) == 0
+    return z
+
+
+def newton_apply(op: Operator, nlev, alpha, beta, xi, r):
+    """P_nlev r by Alg. 1 step 4, zeta_1 with alpha' = theta_bar - delta."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    out = np.empty(op.n)
+    work = np.empty(3 * op.n * max(nlev, 1) + op.n)
+    assert lib().orc_newton_apply(C.byref(op.op), nlev, alpha, beta, xi, _p(r), _p(out), _p(work)) == 0
+    return out
+
+
+def lanczos(op: Operator, m, v0):
+    """m-step Lanczos from v0 (O2). Returns (alphas, betas) of T_s (s = steps taken)."""
+    v0 = np.ascontiguousarray(v0, dtype=np.float64)
+    a = np.zeros(m)
+    b = np.zeros(m)
+    work = np.empty(3 * op.n)
+    s = lib().orc_lanczos(C.byref(op.op), m, _p(v0), _p(a), _p(b), _p(work))
+    assert s >= 0
+    return a[:s], b[:s]
+
+
+def ritz_extremes(alphas, betas):
+    """Extreme eigenvalues of the Lanczos tridiagonal T_s (LAPACK via scipy: a library
+    primitive standing for 'eigenvalues of T_m')."""
+    from scipy.linalg import eigvalsh_tridiagonal
+    ev = eigvalsh_tridiagonal(alphas, betas[: len(alphas) - 1])
+    return float(ev[0]), float(ev[-1])
+
+
+def estimate_spectrum(op: Operator, m, v0):
+    return ritz_extremes(*lanczos(op, m, v0))
+
+
+def pcg(op: Operator, b, m, alpha=None, beta=None, xi=0.0, tol=1e-8, maxit=10000, x0=None,
+        history=False):
+    """Textbook PCG (O5) preconditioned by p_m(A) (m < 0: none).  Returns (x, stats dict)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(op.n) if x0 is None else np.array(x0, dtype=np.float64)
+    hist = np.zeros(maxit + 1) if history else None
+    st = _Stats()
+    if m >= 0:
+        assert alpha is not None and beta is not None
+    lib().orc_pcg(C.byref(op.op), m, float(alpha or 0.0), float(beta or 0.0), float(xi), _p(b), _p(x),
+                  tol, maxit, _p(hist), C.byref(st))
+    out = dict(iters=st.iters, converged=bool(st.converged), breakdown=bool(st.breakdown),
+               mvp=st.mvp, ddot=st.ddot, relres_recursive=st.relres_recursive,
+               relres_true=st.relres_true)
+    if history:
+        out["history"] = hist[: st.iters + 1]
+    return x, out
+
+
+def num_threads() -> int:
+    return int(lib().orc_num_threads())

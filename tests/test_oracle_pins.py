@@ -1,0 +1,343 @@
+"""Pins of the CPU oracle (oracle/) against what the paper and the mathematics fix.
+
+None of these re-types the oracle's own formula: each compares it with a printed value of
+the paper (Table tab:epsil, Fig. 1 text), a closed form (Chebyshev T_{k+1}, 1D-Laplacian
+spectrum, cosh form of rho), an invariant (spectrum bound, symmetry, Ritz interlacing), a
+library routine on a special case (dense solve, dense eigensolve), or another algorithm of
+the paper (Newton Alg. 1 vs Chebyshev Alg. 2).  Label P<n> refers to SURVEY.md §8(c).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.filterwarnings("ignore::RuntimeWarning")
+
+
+def cheb_T(k, x):
+    """T_k(x) by the three-term recurrence T_{j+1} = 2x T_j - T_{j-1} (textbook)."""
+    x = np.asarray(x, dtype=np.float64)
+    t0, t1 = np.ones_like(x), x.copy()
+    if k == 0:
+        return t0
+    for _ in range(k - 1):
+        t0, t1 = t1, 2 * x * t1 - t0
+    return t1
+
+
+def p_closed(lam, k, alpha, beta, xi):
+    """p_k(lam) from the residual-polynomial closed form of the Chebyshev preconditioner
+    on [alpha + xi*theta, beta + xi*theta]: 1 - lam p(lam) = T_{k+1}((tb - lam)/d)/T_{k+1}(tb/d)."""
+    theta = 0.5 * (alpha + beta)
+    d = 0.5 * (beta - alpha)
+    tb = theta * (1 + xi)
+    return (1.0 - cheb_T(k + 1, (tb - lam) / d) / cheb_T(k + 1, tb / d)) / lam
+
+
+# ---------------------------------------------------------------- P1 / P2: Table tab:epsil
+@pytest.fixture(scope="module")
+def tab(golden_dir):
+    with open(os.path.join(golden_dir, "tab_epsil.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def diag_op():
+    w = W.tab_epsil_diag()
+    return w, oracle.Operator(w)
+
+
+def test_P1_tab_epsil_eigenvalues(tab, diag_op):
+    w, op = diag_op
+    n = w["n"]
+    lam = np.arange(1, n + 1, dtype=np.float64)
+    for xi, _, l1, l2, l5, l10, kap, kap10 in tab["rows"]:
+        z = oracle.cheb_apply(op, 63, 1.0, float(n), xi, np.ones(n))  # p(A) 1 = p(lambda_i)
+        mu = np.sort(lam * z)
+        mu = mu / mu[-1]  # reading A2: normalised by the largest
+        got = [mu[0], mu[1], mu[4], mu[9], 1 / mu[0]]
+        want = [l1, l2, l5, l10, kap]
+        for g, e in zip(got, want):
+            assert abs(g - e) <= 6e-4 * abs(e) + 5e-6, (xi, got, want)
+        if kap10 is not None:
+            assert abs(1 / mu[9] - kap10) <= 1e-3 * kap10 + 5e-3
+        else:  # reading A3: lambda_1 == lambda_10 in the printed row, so kappa_10 == kappa
+            assert abs(1 / mu[9] - kap) <= 1e-3 * kap
+
+
+def test_P2_tab_epsil_iterations_and_P10_counters(tab, diag_op):
+    w, op = diag_op
+    for xi, iters, *_ in tab["rows"]:
+        x, st = oracle.pcg(op, w["b"], 63, 1.0, float(w["n"]), xi, tol=1e-10, maxit=500)
+        assert st["converged"] and abs(st["iters"] - iters) <= 1, (xi, st)
+        # Table tab11 counter laws: MVP = iters*(m+1) (+1 true residual); ddot = 3*iters (+3)
+        assert st["mvp"] == st["iters"] * 64 + 1
+        assert st["ddot"] == 3 * st["iters"] + 3
+        assert st["relres_true"] <= 1e-10
+        # the exact solution of the diagonal system is b_i / i
+        xe = w["b"] / np.arange(1, w["n"] + 1)
+        assert np.linalg.norm(x - xe) / np.linalg.norm(xe) < 1e-9
+
+
+# ---------------------------------------------------------------- P7: worked values
+def test_P7_spec_worked_values(golden_dir):
+    with open(os.path.join(golden_dir, "spec_worked.json")) as f:
+        g = json.load(f)
+    c = g["cheb"]
+    tb, d, s = oracle.cheb_params(c["alpha"], c["beta"], c["xi"])
+    assert (tb, d, s) == (c["theta"], c["delta"], c["sigma"])
+    rho = oracle.cheb_rho(s, 3)
+    assert rho[0] == c["rho0"] and abs(rho[1] - c["rho1"]) < 1e-15
+    nw = g["newton"]
+    z = oracle.newton_zeta(nw["alpha"], nw["beta"], nw["xi"], 2)
+    assert abs(z[0] - nw["zeta0"]) < 1e-15 and abs(z[1] - nw["zeta1"]) < 1e-14
+    # xi only rescales theta: theta_bar ratio exactly 1 + xi (Eq. thetamod)
+    tb2, d2, _ = oracle.cheb_params(1.0, 3.0, 0.05)
+    assert tb2 == 2.0 * 1.05 and d2 == 1.0
+
+
+def test_P7_degree0_and_identity():
+    n = 50
+    w = dict(kind="csr", n=n, rowptr=np.arange(n + 1, dtype=np.int32),
+             colidx=np.arange(n, dtype=np.int32), vals=np.ones(n))
+    op = oracle.Operator(w)
+    r = np.random.default_rng(0).uniform(-1, 1, n)
+    z = oracle.cheb_apply(op, 0, 0.5, 2.0, 0.1, r)  # m = 0 -> r / theta_bar (Alg. 2 step 2)
+    assert np.array_equal(z, r / (1.25 * 1.1))
+    x, st = oracle.pcg(op, r, 5, 0.5, 2.0, 0.0, tol=1e-12)  # A = I: one iteration
+    assert st["iters"] == 1 and np.allclose(x, r, rtol=0, atol=1e-14)
+    x, st = oracle.pcg(op, np.zeros(n), 5, 0.5, 2.0, 0.0, tol=1e-12)  # zero rhs
+    assert st["iters"] == 0 and st["converged"] and not x.any()
+
+
+# ---------------------------------------------------------------- P8: rho closed form
+@pytest.mark.parametrize("alpha,beta,xi", [(1.0, 3.0, 0.0), (1e-3, 8.0, 1e-3), (0.5, 0.51, 0.0)])
+def test_P8_rho_closed_form(alpha, beta, xi):
+    _, _, s = oracle.cheb_params(alpha, beta, xi)
+    rho = oracle.cheb_rho(s, 200)
+    t = math.acosh(s)
+    k = np.arange(201)
+    # rho_k = T_k(sigma)/T_{k+1}(sigma) = cosh(k t)/cosh((k+1) t); use the ratio in a stable form
+    closed = np.exp(-t) * (1 + np.exp(-2 * k * t)) / (1 + np.exp(-2 * (k + 1) * t))
+    assert np.max(np.abs(rho - closed) / closed) < 5e-14
+
+
+# ---------------------------------------------------------------- P3: 1D Laplacian eigvecs
+@pytest.mark.parametrize("k", [0, 1, 2, 10, 63, 200])
+@pytest.mark.parametrize("xi", [0.0, 1e-3])
+def test_P3_laplacian_eigenvectors(k, xi):
+    n = 200
+    rowptr, colidx, vals = W.laplacian_1d_csr(n)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    i = np.arange(1, n + 1)
+    lam_exact = 4 * np.sin(np.arange(1, n + 1) * np.pi / (2 * (n + 1))) ** 2
+    alpha, beta = lam_exact[0], lam_exact[-1]
+    pmax = np.max(np.abs(p_closed(lam_exact, k, alpha, beta, xi)))  # ||p_k(A)||_2
+    for j in [1, 2, 17, 100, 199, 200]:
+        v = np.sin(i * j * np.pi / (n + 1))
+        z = oracle.cheb_apply(op, k, alpha, beta, xi, v)
+        expect = p_closed(lam_exact[j - 1], k, alpha, beta, xi) * v
+        # error relative to ||p_k(A)|| ||v|| (p_k(lambda_j) itself may be ~0 near beta)
+        assert np.linalg.norm(z - expect) / (pmax * np.linalg.norm(v)) < 2e-11, (j, k, xi)
+
+
+def test_P3_laplacian_operator_eigenpairs():
+    """A v_j = lambda_j v_j for the 2D 5-point operator (config 1 shape, closed form)."""
+    side = 64
+    w = W.config1(side)
+    op = oracle.Operator(w)
+    x = np.arange(1, side + 1)
+    for (a, b) in [(1, 1), (3, 7), (64, 64)]:
+        v = np.outer(np.sin(x * b * np.pi / (side + 1)), np.sin(x * a * np.pi / (side + 1))).ravel()
+        lam = 4 * np.sin(a * np.pi / (2 * (side + 1))) ** 2 + 4 * np.sin(b * np.pi / (2 * (side + 1))) ** 2
+        y = op.apply(v)
+        assert np.linalg.norm(y - lam * v) <= 1e-12 * np.linalg.norm(v) * 8
+
+
+def test_P3_stencil_matches_csr():
+    """The matrix-free stencil (O1) equals the explicit CSR operator of the same grid."""
+    side = 12
+    rowptr, colidx, vals = W.grid_laplacian_csr((side, side, side), 6.0, -1.0)
+    csr = oracle.Operator(dict(kind="csr", n=side ** 3, rowptr=rowptr, colidx=colidx, vals=vals))
+    st = oracle.Operator(dict(kind="stencil", n=side ** 3, dim=3, nx=side, ny=side, nz=side,
+                              diag=6.0, offdiag=-1.0))
+    x = np.random.default_rng(3).standard_normal(side ** 3)
+    assert np.allclose(csr.apply(x), st.apply(x), rtol=0, atol=1e-13)
+    # 3D separable eigenvector, closed form eigenvalue
+    g = np.arange(1, side + 1)
+    v = np.einsum("i,j,k->ijk", np.sin(g * 2 * np.pi / (side + 1)), np.sin(g * 5 * np.pi / (side + 1)),
+                  np.sin(g * 11 * np.pi / (side + 1))).ravel()
+    lam = sum(4 * np.sin(a * np.pi / (2 * (side + 1))) ** 2 for a in (2, 5, 11))
+    assert np.linalg.norm(st.apply(v) - lam * v) <= 1e-12 * np.linalg.norm(v) * 12
+
+
+# ---------------------------------------------------------------- P4: spectrum bound
+@pytest.mark.parametrize("k", [1, 5, 20, 60])
+@pytest.mark.parametrize("xi", [0.0, 1e-2])
+def test_P4_spectrum_bound(k, xi):
+    n = 200
+    rowptr, colidx, vals = W.laplacian_1d_csr(n)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    A = np.zeros((n, n))
+    for r in range(n):
+        A[r, colidx[rowptr[r]:rowptr[r + 1]]] = vals[rowptr[r]:rowptr[r + 1]]
+    lam_exact = np.linalg.eigvalsh(A)
+    alpha, beta = lam_exact[0] * 0.9, lam_exact[-1] * 1.0  # exact-or-outer bounds
+    P = np.column_stack([oracle.cheb_apply(op, k, alpha, beta, xi, e) for e in np.eye(n)])
+    assert np.linalg.norm(P - P.T) <= 1e-13 * np.linalg.norm(P)  # p_k(A) symmetric
+    mu = np.linalg.eigvalsh(0.5 * (P @ A + (P @ A).T))
+    tb = 0.5 * (alpha + beta) * (1 + xi)
+    d = 0.5 * (beta - alpha)
+    T = float(cheb_T(k + 1, tb / d))
+    mu_alpha = 1 - float(cheb_T(k + 1, (tb - alpha) / d)) / T
+    lo, hi = min(mu_alpha, 1 - 1 / T), 1 + 1 / T
+    assert mu.min() >= lo - 1e-10 and mu.max() <= hi + 1e-10, (mu.min(), mu.max(), lo, hi)
+    assert mu.min() > 0
+
+
+# ---------------------------------------------------------------- P5: Newton == Chebyshev
+@pytest.mark.parametrize("nlev", [0, 1, 2, 3, 4, 6])
+@pytest.mark.parametrize("xi", [0.0, 1e-3])
+def test_P5_newton_equals_chebyshev(nlev, xi):
+    n = 300
+    rowptr, colidx, vals = W.laplacian_1d_csr(n)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    r = np.random.default_rng(nlev).uniform(-1, 1, n)
+    alpha, beta = 4 * math.sin(math.pi / (2 * (n + 1))) ** 2, 4.0
+    zn = oracle.newton_apply(op, nlev, alpha, beta, xi, r)
+    zc = oracle.cheb_apply(op, 2 ** nlev - 1, alpha, beta, xi, r)
+    assert np.linalg.norm(zn - zc) / np.linalg.norm(zc) < 1e-11
+
+
+def test_P5_newton_reproduces_tab_epsil_iterations(tab, diag_op):
+    """Newton nlev=6 with the alpha' reading gives the same preconditioned spectrum as
+    Chebyshev degree 63 (Table tab:epsil was produced with Newton)."""
+    w, op = diag_op
+    n = w["n"]
+    lam = np.arange(1, n + 1, dtype=np.float64)
+    for xi, _, l1, l2, l5, l10, kap, _ in tab["rows"]:
+        mu = np.sort(lam * oracle.newton_apply(op, 6, 1.0, float(n), xi, np.ones(n)))
+        mu = mu / mu[-1]
+        for g, e in zip([mu[0], mu[1], mu[4], mu[9]], [l1, l2, l5, l10]):
+            assert abs(g - e) <= 6e-4 * e + 5e-6
+
+
+# ---------------------------------------------------------------- P12: Fig. 1 / Thm 2.3
+def test_P12_fig1_first_newton_level(golden_dir):
+    with open(os.path.join(golden_dir, "spec_worked.json")) as f:
+        fig = json.load(f)["fig1"]
+    lam = np.array(sorted({x for a, b, _ in fig["pairs"] for x in (a, b)} | {0.6, 1.0, 1.3}))
+    n = lam.size
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=np.arange(n + 1, dtype=np.int32),
+                              colidx=np.arange(n, dtype=np.int32), vals=lam))
+    # interval [0.1, 1.9] -> zeta_0 = 1 so the scaled spectrum is the spectrum itself
+    mu0 = lam * oracle.newton_apply(op, 1, 0.1, 1.9, 0.0, np.ones(n))
+    zeta1 = oracle.newton_zeta(0.1, 1.9, 0.0, 1)[1]
+    for a, b, fa in fig["pairs"]:
+        ia, ib = np.searchsorted(lam, a), np.searchsorted(lam, b)
+        assert abs(mu0[ia] / zeta1 - fa) < 1e-12 and abs(mu0[ia] - mu0[ib]) < 1e-12  # cluster
+    mu1 = lam * oracle.newton_apply(op, 1, 0.1, 1.9, 0.05, np.ones(n))
+    order = np.argsort(mu1)
+    # Theorem 2.3 with xi = 0.05: the eigenvalues below alpha_eta + 2(1-eta) (0.1, 0.14, 0.18)
+    # are the 3 smallest of P_1 A, in order; the top ones no longer coincide with them.
+    assert list(order[:3]) == [0, 1, 2]
+    for a, b, _ in fig["pairs"]:
+        assert abs(mu1[np.searchsorted(lam, a)] - mu1[np.searchsorted(lam, b)]) > 1e-3
+
+
+# ---------------------------------------------------------------- P6: dense small SPD
+@pytest.mark.parametrize("seed", [0, 1])
+@pytest.mark.parametrize("k", [0, 3, 12])
+def test_P6_dense_small(seed, k):
+    n = 30
+    A, lam = W.random_spd_dense(n, seed, cond=1e2)
+    rowptr, colidx, vals = W.dense_to_csr(A)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    ev, V = np.linalg.eigh(A)
+    alpha, beta, xi = 1.0, 1e2, 1e-3
+    P_closed = (V * p_closed(ev, k, alpha, beta, xi)) @ V.T
+    P = np.column_stack([oracle.cheb_apply(op, k, alpha, beta, xi, e) for e in np.eye(n)])
+    assert np.linalg.norm(P - P_closed) / np.linalg.norm(P_closed) < 1e-11
+    b = np.random.default_rng(seed + 10).uniform(-1, 1, n)
+    x, st = oracle.pcg(op, b, k, alpha, beta, xi, tol=1e-10, maxit=200)
+    # finite termination in <= n steps holds in exact arithmetic; rounding delays plain CG
+    # (k = 0 is a scalar preconditioner) on a log-uniform spectrum, so it gets 2n.
+    assert st["converged"] and st["iters"] <= (n if k > 0 else 2 * n)
+    xs = np.linalg.solve(A, b)
+    assert np.linalg.norm(x - xs) / np.linalg.norm(xs) <= 10 * 1e-10 * 1e2
+
+
+def test_unpreconditioned_cg_matches_dense_solve():
+    n = 40
+    A, _ = W.random_spd_dense(n, 7, cond=100.0)
+    rowptr, colidx, vals = W.dense_to_csr(A)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    b = np.random.default_rng(1).standard_normal(n)
+    x, st = oracle.pcg(op, b, -1, tol=1e-12, maxit=400)
+    assert st["converged"] and st["mvp"] == st["iters"] + 1
+    assert np.allclose(x, np.linalg.solve(A, b), rtol=1e-9, atol=1e-11)
+
+
+# ---------------------------------------------------------------- P9: Lanczos
+def test_P9_lanczos_full_spectrum():
+    n = 12
+    lam = np.arange(1, n + 1, dtype=np.float64) ** 1.5
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=np.arange(n + 1, dtype=np.int32),
+                              colidx=np.arange(n, dtype=np.int32), vals=lam))
+    a, b = oracle.lanczos(op, n, np.random.default_rng(0).uniform(-1, 1, n))
+    from scipy.linalg import eigvalsh_tridiagonal
+    ev = eigvalsh_tridiagonal(a, b[: n - 1])
+    assert np.allclose(ev, lam, rtol=1e-8, atol=0)
+
+
+def test_P9_lanczos_config1_bracket():
+    w = W.config1()
+    op = oracle.Operator(w)
+    lo_ex, hi_ex = 8 * math.sin(math.pi / 130) ** 2, 8 * math.sin(64 * math.pi / 130) ** 2
+    lmin, lmax = oracle.estimate_spectrum(op, 20, w["b"])
+    assert lo_ex <= lmin and lmax <= hi_ex  # Ritz values interlace inside the spectrum
+    assert hi_ex - lmax < 0.02 * hi_ex       # the top converges fast
+    assert lmin < 20 * lo_ex
+
+
+def test_P9_lanczos_config2_small_bracket():
+    side = 16
+    w = W.config2(side)
+    op = oracle.Operator(w)
+    lo_ex = 3 * 4 * math.sin(math.pi / (2 * (side + 1))) ** 2
+    hi_ex = 3 * 4 * math.sin(side * math.pi / (2 * (side + 1))) ** 2
+    lmin, lmax = oracle.estimate_spectrum(op, 20, w["b"])
+    assert lo_ex <= lmin and lmax <= hi_ex and hi_ex - lmax < 0.05 * hi_ex
+
+
+# ---------------------------------------------------------------- P11: exact solution x* = 1
+def test_P11_config3_surrogate_exact_solution():
+    w = W.config3(side=12)
+    op = oracle.Operator(w)
+    assert np.allclose(op.apply(np.ones(w["n"])), w["b"], rtol=1e-13, atol=1e-12)  # b = A 1
+    lmin, lmax = oracle.estimate_spectrum(op, 20, w["b"])
+    x, st = oracle.pcg(op, w["b"], 20, lmin, lmax, 0.0, tol=1e-8, maxit=2000)
+    assert st["converged"] and st["relres_true"] <= 1e-8
+    assert np.max(np.abs(x - 1.0)) < 1e-3
+
+
+# ---------------------------------------------------------------- Schur operator (config 5)
+def test_schur_operator_matches_dense():
+    w = W.config5(n=300, seed=4)
+    op = oracle.Operator(w)
+    n, nb = w["n"], w["nb"]
+    B = np.zeros((nb, n))
+    for q in range(nb):
+        s, e = w["browptr"][q], w["browptr"][q + 1]
+        B[q, w["bcolidx"][s:e]] = w["bvals"][s:e]
+        assert np.all(np.diff(w["bcolidx"][s:e]) > 0) and 2 <= e - s <= 4
+    Cm = np.diag(2 + w["c"]) - np.eye(n, k=1) - np.eye(n, k=-1)
+    S = Cm + B.T @ np.diag(1 / w["d"]) @ B
+    x = np.random.default_rng(0).standard_normal(n)
+    assert np.allclose(op.apply(x), S @ x, rtol=1e-12, atol=1e-12)
+    assert np.linalg.eigvalsh(S).min() > 0

@@ -1,0 +1,63 @@
+"""Shape/structure checks of the seeded synthetic inputs (workloads/), CPU only."""
+import numpy as np
+import scipy.sparse as sp
+
+import workloads as W
+
+
+def _csr(w):
+    return sp.csr_matrix((w["vals"], w["colidx"], w["rowptr"]), shape=(w["n"], w["n"]))
+
+
+def test_config1_shape():
+    w = W.config1()
+    assert w["n"] == 4096 and w["rowptr"][-1] == 20224
+    A = _csr(w)
+    assert abs(A - A.T).max() == 0
+    assert np.all(np.diff(w["colidx"][w["rowptr"][0]:w["rowptr"][1]]) > 0)
+    assert w["b"].min() >= -1 and w["b"].max() <= 1
+
+
+def test_config1_deterministic():
+    assert np.array_equal(W.config1()["b"], W.config1()["b"])
+
+
+def test_config3_structure_small():
+    w = W.config3(side=10)
+    A = _csr(w)
+    n = w["n"]
+    assert abs(A - A.T).max() == 0
+    assert w["rowptr"][-1] == 7 * n - 6 * 10 * 10
+    # rows are weakly diagonally dominant with strict dominance at boundary cells
+    d = A.diagonal()
+    off = np.asarray(abs(A).sum(axis=1)).ravel() - d
+    assert np.all(d >= off - 1e-12) and np.all(d - off > 0)
+    for i in range(0, n, 97):
+        cols = w["colidx"][w["rowptr"][i]:w["rowptr"][i + 1]]
+        assert np.all(np.diff(cols) > 0)
+
+
+def test_config3_full_size_counts():
+    """nnz formula of the full 256^3 grid (not generated here: too big for the CPU suite)."""
+    N = 256
+    assert 7 * N ** 3 - 6 * N * N == 117_047_296
+
+
+def test_config4_surrogate():
+    w = W.config4(n=20_000)
+    A = _csr(w)
+    assert abs(A - A.T).max() < 1e-15
+    assert np.array_equal(np.sort(w["perm"]), np.arange(w["n"]))
+    deg = np.diff(w["rowptr"]) - 1
+    assert deg.min() >= 16 and deg.max() <= 40
+    assert np.allclose(np.asarray(A.sum(axis=1)).ravel(), 1e-3)  # L 1 = 0, + 1e-3 I
+
+
+def test_config5_surrogate():
+    w = W.config5(n=5000)
+    lens = np.diff(w["browptr"])
+    assert w["nb"] == 15000 and lens.min() == 2 and lens.max() == 4
+    for q in range(0, w["nb"], 7):
+        c = w["bcolidx"][w["browptr"][q]:w["browptr"][q + 1]]
+        assert np.all(np.diff(c) > 0)
+    assert w["d"].min() >= 1 and w["d"].max() <= 100 and 1 <= w["c"].min() and w["c"].max() <= 2

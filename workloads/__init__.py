@@ -1,0 +1,266 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU parity tests and bench.py.
+
+This module holds NO arithmetic of the method (no operator application, no polynomial,
+no Krylov step): it only draws random numbers and lays out the operators the method is
+applied to.  Every recipe below is the one written down in DESIGN.md §"Input recipe"
+(SURVEY.md §8(d) table "Inputs"; ambiguity readings A13-A18).  The paper's own matrices
+(Cube_5317k, DFN #1-#4, Frac16/32 -- PAPER.md:513-514, 919-944) are not available; these
+configs stand in for them (configs 1-3: PDE stencils like the fracture blocks of A,
+PAPER.md:686-689; config 4: an unstructured SPD matrix like Cube_5317k; config 5: the
+"global product - local inverse - transposed product" shape of S_u).
+
+All generators use numpy.random.default_rng(seed) (PCG64), one stream per config, in the
+draw order stated in each docstring.  Index types are int32 (max nnz 156.7M < 2^31).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = [
+    "config1", "config2", "config3", "config4", "config5",
+    "tab_epsil_diag", "laplacian_1d_csr", "random_spd_dense", "dense_to_csr",
+    "CONFIG_DEFAULTS",
+]
+
+# Per-config solver parameters (BASELINE.json "configs").
+CONFIG_DEFAULTS = {
+    1: dict(k=10, tol=1e-8, lanczos_steps=20),
+    2: dict(k=30, tol=1e-10, lanczos_steps=20),
+    3: dict(k=20, ks=(20, 50, 100), tol=1e-8, lanczos_steps=20),
+    4: dict(k=60, tol=1e-8, lanczos_steps=20),
+    5: dict(k=50, ks=(10, 50, 100, 200), tol=1e-8, lanczos_steps=20),
+}
+
+
+def _csr_from_padded(cols: np.ndarray, vals: np.ndarray, mask: np.ndarray):
+    """Compress a (n, w) padded row layout (columns already ascending per row) into CSR."""
+    counts = mask.sum(axis=1, dtype=np.int64)
+    rowptr = np.zeros(cols.shape[0] + 1, dtype=np.int64)
+    np.cumsum(counts, out=rowptr[1:])
+    assert rowptr[-1] < 2**31
+    m = mask.ravel()
+    return rowptr.astype(np.int32), cols.ravel()[m].astype(np.int32), vals.ravel()[m].astype(np.float64)
+
+
+def grid_laplacian_csr(dims, diag, offdiag):
+    """Constant-coefficient 2D 5-point / 3D 7-point Dirichlet operator as CSR.
+
+    Grid ordering i = x + nx*y + nx*ny*z (x fastest, reading A16); columns ascending.
+    """
+    dims = tuple(int(d) for d in dims)
+    n = int(np.prod(dims))
+    idx = np.arange(n, dtype=np.int64)
+    coords = []
+    stride = 1
+    strides = []
+    rem = idx
+    for d in dims:
+        coords.append(rem % d)
+        rem = rem // d
+        strides.append(stride)
+        stride *= d
+    # neighbour offsets in ascending column order: -s_last ... -s_0, 0, +s_0 ... +s_last
+    offs, conds, vals_list = [], [], []
+    for a in reversed(range(len(dims))):
+        offs.append(-strides[a]); conds.append(coords[a] > 0)
+    offs.append(0); conds.append(np.ones(n, dtype=bool))
+    for a in range(len(dims)):
+        offs.append(strides[a]); conds.append(coords[a] < dims[a] - 1)
+    w = len(offs)
+    cols = np.empty((n, w), dtype=np.int64)
+    vals = np.empty((n, w), dtype=np.float64)
+    mask = np.empty((n, w), dtype=bool)
+    for j, (o, c) in enumerate(zip(offs, conds)):
+        cols[:, j] = idx + o
+        vals[:, j] = diag if o == 0 else offdiag
+        mask[:, j] = c
+    cols[~mask] = 0
+    return _csr_from_padded(cols, vals, mask)
+
+
+def config1(side: int = 64, seed: int = 0):
+    """Config 1: 2D 5-point Laplacian, side x side (64x64 -> n=4096, nnz=20224), Dirichlet,
+    diagonal 4, off-diagonal -1, CSR.  seed 0: b = uniform(-1, 1, n).  x0 = 0."""
+    rowptr, colidx, vals = grid_laplacian_csr((side, side), 4.0, -1.0)
+    rng = np.random.default_rng(seed)
+    b = rng.uniform(-1.0, 1.0, side * side)
+    return dict(kind="csr", name=f"config1_{side}x{side}", n=side * side, rowptr=rowptr,
+                colidx=colidx, vals=vals, b=b, grid=(side, side), **CONFIG_DEFAULTS[1])
+
+
+def config2(side: int = 128, seed: int = 1):
+    """Config 2: 3D 7-point constant-coefficient Laplacian (diag 6, off -1, Dirichlet, A13),
+    side^3 grid, applied matrix-free.  seed 1: b = uniform(-1, 1, n)."""
+    n = side ** 3
+    rng = np.random.default_rng(seed)
+    b = rng.uniform(-1.0, 1.0, n)
+    return dict(kind="stencil", name=f"config2_{side}^3", n=n, dim=3, nx=side, ny=side, nz=side,
+                diag=6.0, offdiag=-1.0, b=b, **CONFIG_DEFAULTS[2])
+
+
+def config3(side: int = 256, seed: int = 2, want_b: bool = True):
+    """Config 3: 3D 7-point variable-coefficient diffusion on side^3, CSR (reading A13).
+
+    Face coefficients c = exp(2 z), z ~ N(0,1), i.i.d. per face INCLUDING boundary faces.
+    Draw order (seed 2): x-faces as C-order (z, y, x_face=side+1), then y-faces
+    (z, y_face=side+1, x), then z-faces (z_face=side+1, y, x).
+    A_ii = sum of the 6 face coefficients, A_ij = -c_face for interior faces.
+    b = A*ones, which equals the sum of the cell's boundary-face coefficients (exact
+    solution x* = 1, pin P11); it is formed from the faces, not by a product with A.
+    """
+    N = int(side)
+    rng = np.random.default_rng(seed)
+    cx = np.exp(2.0 * rng.standard_normal((N, N, N + 1)))
+    cy = np.exp(2.0 * rng.standard_normal((N, N + 1, N)))
+    cz = np.exp(2.0 * rng.standard_normal((N + 1, N, N)))
+    n = N ** 3
+    w_, e_ = cx[:, :, :N], cx[:, :, 1:]
+    s_, n_ = cy[:, :N, :], cy[:, 1:, :]
+    d_, u_ = cz[:N, :, :], cz[1:, :, :]
+    diag = (w_ + e_) + (s_ + n_) + (d_ + u_)
+    z, y, x = np.meshgrid(np.arange(N), np.arange(N), np.arange(N), indexing="ij")
+    idx = np.arange(n, dtype=np.int64)
+    cols = np.empty((n, 7), dtype=np.int64)
+    vals = np.empty((n, 7), dtype=np.float64)
+    mask = np.empty((n, 7), dtype=bool)
+    spec = [(-N * N, d_, z > 0), (-N, s_, y > 0), (-1, w_, x > 0), (0, None, None),
+            (1, e_, x < N - 1), (N, n_, y < N - 1), (N * N, u_, z < N - 1)]
+    for j, (o, c, cond) in enumerate(spec):
+        cols[:, j] = idx + o
+        if o == 0:
+            vals[:, j] = diag.ravel()
+            mask[:, j] = True
+        else:
+            vals[:, j] = -c.ravel()
+            mask[:, j] = cond.ravel()
+    del z, y, x
+    cols[~mask] = 0
+    rowptr, colidx, v = _csr_from_padded(cols, vals, mask)
+    del cols, vals, mask
+    out = dict(kind="csr", name=f"config3_{N}^3", n=n, rowptr=rowptr, colidx=colidx, vals=v,
+               grid=(N, N, N), **CONFIG_DEFAULTS[3])
+    if want_b:
+        b = np.zeros((N, N, N))
+        b[:, :, 0] += cx[:, :, 0]
+        b[:, :, N - 1] += cx[:, :, N]
+        b[:, 0, :] += cy[:, 0, :]
+        b[:, N - 1, :] += cy[:, N, :]
+        b[0, :, :] += cz[0, :, :]
+        b[N - 1, :, :] += cz[N, :, :]
+        out["b"] = b.ravel()
+        out["x_exact"] = 1.0
+    return out
+
+
+def config4(n: int = 8_000_000, seed: int = 3, knn: int = 16, shift: float = 1e-3):
+    """Config 4: graph Laplacian of a symmetric kNN graph + shift*I, RCM-ordered CSR.
+
+    Draw order (seed 3): points uniform[0,1)^3 (n x 3); edge weights uniform[0.1, 10] for the
+    undirected edges in (i<j) lexicographic order; b = uniform(-1, 1, n) in original vertex
+    order.  Edges: Euclidean knn excluding self, symmetrised by union (A18).  The matrix and b
+    are then permuted by scipy's reverse_cuthill_mckee (symmetric_mode=True), computed here
+    and shipped as `perm` (A17).  The library applies its own SELL sigma-sort on top.
+    """
+    from scipy.spatial import cKDTree
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, 3))
+    tree = cKDTree(pts)
+    _, nbr = tree.query(pts, k=knn + 1, workers=-1)
+    nbr = nbr.astype(np.int64)
+    src = np.repeat(np.arange(n, dtype=np.int64), knn + 1)
+    dst = nbr.ravel()
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    lo, hi = np.minimum(src, dst), np.maximum(src, dst)
+    key = np.unique(lo * n + hi)
+    ei, ej = key // n, key % n
+    w = rng.uniform(0.1, 10.0, key.size)
+    b = rng.uniform(-1.0, 1.0, n)
+    W = sp.coo_matrix((np.concatenate([w, w]), (np.concatenate([ei, ej]), np.concatenate([ej, ei]))),
+                      shape=(n, n)).tocsr()
+    deg = np.asarray(W.sum(axis=1)).ravel()
+    A = (sp.diags(deg + shift) - W).tocsr()
+    perm = reverse_cuthill_mckee(A, symmetric_mode=True).astype(np.int64)
+    A = A[perm][:, perm].tocsr()
+    A.sort_indices()
+    assert A.nnz < 2**31
+    return dict(kind="csr", name=f"config4_knn{knn}_{n}", n=n, rowptr=A.indptr.astype(np.int32),
+                colidx=A.indices.astype(np.int32), vals=A.data.astype(np.float64), b=b[perm],
+                perm=perm, sell_C=32, sell_sigma=256, **CONFIG_DEFAULTS[4])
+
+
+def config5(n: int = 4_000_000, seed: int = 4, rows_per_trace: int = 3):
+    """Config 5: DFN-like Schur complement S = C + B^T D^{-1} B, never assembled.
+
+    C = tridiag(-1, 2 + c, -1) (1D Laplacian plus diagonal c ~ U[1,2]); B is (3n) x n with
+    row lengths uniform in {2,3,4} at distinct sorted random columns, values N(0,1);
+    D ~ U[1,100].  Draw order (seed 4): c (n), row lengths (nb), columns (all rows at once,
+    then rows with a duplicate are redrawn one by one in row order until distinct), values
+    (nnz), D (nb), b = uniform(-1,1,n) (A14).
+    """
+    rng = np.random.default_rng(seed)
+    nb = rows_per_trace * n
+    c = rng.uniform(1.0, 2.0, n)
+    lens = rng.integers(2, 5, nb)
+    browptr = np.zeros(nb + 1, dtype=np.int64)
+    np.cumsum(lens, out=browptr[1:])
+    nnz = int(browptr[-1])
+    cols = rng.integers(0, n, nnz)
+    pad = np.full((nb, 4), np.iinfo(np.int64).max, dtype=np.int64)
+    slot = np.arange(nnz) - np.repeat(browptr[:-1], lens)
+    rowid = np.repeat(np.arange(nb), lens)
+    pad[rowid, slot] = cols
+    pad.sort(axis=1)
+    dup = np.any((pad[:, 1:] == pad[:, :-1]) & (pad[:, 1:] != np.iinfo(np.int64).max), axis=1)
+    for r in np.nonzero(dup)[0]:
+        L = int(lens[r])
+        while True:
+            cand = rng.integers(0, n, L)
+            if np.unique(cand).size == L:
+                break
+        pad[r, :] = np.iinfo(np.int64).max
+        pad[r, :L] = np.sort(cand)
+    bcol = pad[rowid, slot]
+    bval = rng.standard_normal(nnz)
+    D = rng.uniform(1.0, 100.0, nb)
+    b = rng.uniform(-1.0, 1.0, n)
+    return dict(kind="schur", name=f"config5_{n}", n=n, nb=nb, c=c, browptr=browptr.astype(np.int32),
+                bcolidx=bcol.astype(np.int32), bvals=bval, d=D, b=b, **CONFIG_DEFAULTS[5])
+
+
+def tab_epsil_diag(n: int = 100_000, seed: int = 42):
+    """The diagonal test of Table tab:epsil: A_ii = i, i = 1..1e5.
+
+    Right-hand side "random": uniform[0,1) from default_rng(42) (Appendix A.2
+    of SURVEY.md reproduces the paper's iteration column exactly with this draw)."""
+    rowptr = np.arange(n + 1, dtype=np.int32)
+    colidx = np.arange(n, dtype=np.int32)
+    vals = np.arange(1, n + 1, dtype=np.float64)
+    b = np.random.default_rng(seed).random(n)
+    return dict(kind="csr", name="tab_epsil_diag", n=n, rowptr=rowptr, colidx=colidx, vals=vals, b=b)
+
+
+def laplacian_1d_csr(n: int):
+    """tridiag(-1, 2, -1) of size n (Dirichlet), CSR."""
+    return grid_laplacian_csr((n,), 2.0, -1.0)
+
+
+def random_spd_dense(n: int, seed: int, cond: float = 1e3):
+    """Dense SPD matrix Q diag(l) Q^T with log-uniform spectrum in [1, cond]."""
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.exp(rng.uniform(0.0, np.log(cond), n))
+    lam[0], lam[-1] = 1.0, cond
+    A = (Q * lam) @ Q.T
+    return 0.5 * (A + A.T), lam
+
+
+def dense_to_csr(A: np.ndarray):
+    """Dense -> CSR with every entry stored (ascending columns)."""
+    n = A.shape[0]
+    rowptr = (np.arange(n + 1, dtype=np.int64) * n).astype(np.int32)
+    colidx = np.tile(np.arange(n, dtype=np.int32), n)
+    return rowptr, colidx, np.ascontiguousarray(A, dtype=np.float64).ravel()
