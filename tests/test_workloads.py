@@ -28,10 +28,11 @@ def test_config3_structure_small():
     n = w["n"]
     assert abs(A - A.T).max() == 0
     assert w["rowptr"][-1] == 7 * n - 6 * 10 * 10
-    # rows are weakly diagonally dominant with strict dominance at boundary cells
+    # diagonal dominance margin of each row = its boundary-face coefficients = b (x* = 1)
     d = A.diagonal()
     off = np.asarray(abs(A).sum(axis=1)).ravel() - d
-    assert np.all(d >= off - 1e-12) and np.all(d - off > 0)
+    assert np.allclose(d - off, w["b"], rtol=1e-12, atol=1e-12)
+    assert (w["b"] > 0).sum() == n - 8 ** 3
     for i in range(0, n, 97):
         cols = w["colidx"][w["rowptr"][i]:w["rowptr"][i + 1]]
         assert np.all(np.diff(cols) > 0)
