@@ -1,0 +1,443 @@
+#!/usr/bin/env python
+"""bench.py -- the north-star measurement: p_k(A) v GB/s and PCG time-to-tol (fp64) on B200.
+
+One STEP = one pass of the whole hot path over the workload:
+    npc_estimate_spectrum (20 Lanczos steps from b)  ->  npc_set_poly(k, lmin, lmax, xi)
+    -> npc_pcg_solve(b, x0 = 0, tol)   [k fused degree kernels + 1 SpMV + update per iteration]
+on config 3 of BASELINE.json (3D 7-point variable-coefficient diffusion, 256^3, CSR, b = A 1,
+tol 1e-8) at N = 1; `--config` selects another.  The operator is created (a0, setup) before the
+timed region.  value = algorithmic bytes of every kernel of the step (SURVEY §8(d) floors:
+matrix once + the vector streams each kernel must touch) / step time, in GB/s.
+ms_per_step is the PCG time-to-tol including the spectrum estimate.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--k 20] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): rows partitioned in z-slabs / row blocks over NCCL,
+strong scaling on the fixed problem; time = max over ranks of the CUDA-event time.
+--impl reference: the CPU fp64 oracle (oracle/) timed on the host cores on a bounded sample
+(one p_k(A) v application of the same workload per step), same metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ workloads / byte model
+def make_workload(cfg: int, side: int | None):
+    if cfg == 1:
+        return W.config1()
+    if cfg == 2:
+        return W.config2(side or 128)
+    if cfg == 3:
+        return W.config3(side or 256)
+    if cfg == 4:
+        return W.config4(n=side or 8_000_000)
+    if cfg == 5:
+        return W.config5(n=side or 4_000_000)
+    raise ValueError(cfg)
+
+
+def op_kind(w, cfg):
+    return {1: "csr", 2: "stencil", 3: "csr", 4: "sell", 5: "schur"}[cfg] if w["kind"] != "stencil" else "stencil"
+
+
+def matrix_bytes(w, kind):
+    """Bytes of the operator data one application must stream."""
+    n = w["n"]
+    if kind == "csr":
+        return int(w["rowptr"][-1]) * 12 + (n + 1) * 4
+    if kind == "sell":
+        return int(w["rowptr"][-1]) * 12 * 1.0366 + n / 32 * 8  # padding measured for config 4
+    if kind == "stencil":
+        return 0
+    if kind == "schur":
+        return int(w["browptr"][-1]) * 12 + n * 8 + 2 * n * 8  # D^{-1/2} folded; c; y intermediate
+    raise ValueError(kind)
+
+
+def poly_bytes(M, V, k):
+    """Algorithmic bytes of one p_k(A) r: degree 1 reads r (x) and writes s_1; degree 2 reads
+    s_1, r and writes; degrees >= 3 read s_{j-1}, s_{j-2}, r and write s_j."""
+    if k == 0:
+        return 2 * V
+    b = M + 2 * V
+    if k >= 2:
+        b += M + 3 * V
+    if k >= 3:
+        b += (k - 2) * (M + 4 * V)
+    return b
+
+
+def solve_bytes(M, V, k, iters, lanczos_steps):
+    per_iter = poly_bytes(M, V, k) + (M + 2 * V) + 10 * V  # p_k, w = A u, fused update
+    lz = lanczos_steps * ((M + 2 * V) + 7 * V)             # SpMV + two axpy/dot passes + q update
+    setup = 6 * V                                          # b/x copies, norms, r0
+    return iters * per_iter + lz + setup + (M + 3 * V)     # + final true residual
+
+
+# ------------------------------------------------------------------ clocks sampling
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def partition_rows(w, cfg, ws, rank):
+    """Row block of this rank: z-slabs for grids (configs 2, 3), contiguous blocks otherwise."""
+    n = w["n"]
+    if "grid" in w and len(w["grid"]) == 3 or w["kind"] == "stencil":
+        nz = w["grid"][2] if "grid" in w else w["nz"]
+        plane = n // nz
+        z0 = nz * rank // ws
+        z1 = nz * (rank + 1) // ws
+        return z0 * plane, z1 * plane, (z0, z1 - z0)
+    r0 = n * rank // ws
+    r1 = n * (rank + 1) // ws
+    return r0, r1, None
+
+
+def create_operator(npc, ctx, w, kind, ws, rank, cfg):
+    if ws == 1:
+        return npc.create_from_workload(ctx, w, kind), 0, w["n"]
+    r0, r1, zs = partition_rows(w, cfg, ws, rank)
+    if kind == "stencil":
+        return npc.npc_create_operator(ctx, "stencil", n_local=r1 - r0, n_global=w["n"], row_begin=r0, dim=3,
+                                       nx=w["nx"], ny=w["ny"], nz_global=w["nz"], z_begin=zs[0],
+                                       nz_local=zs[1], diag=w["diag"], offdiag=w["offdiag"]), r0, r1
+    if kind in ("csr", "sell"):
+        rp = w["rowptr"][r0:r1 + 1]
+        op = npc.npc_create_operator(ctx, kind, n_local=r1 - r0, n_global=w["n"], row_begin=r0,
+                                     rowptr=(rp - rp[0]).astype(np.int32), colidx=w["colidx"][rp[0]:rp[-1]],
+                                     vals=w["vals"][rp[0]:rp[-1]], sell_C=32, sell_sigma=256)
+        return op, r0, r1
+    raise SystemExit(f"config kind {kind} does not support --gpus > 1 in this version")
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2208_01339_b200 as npc
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    w = make_workload(cfg, args.side)
+    kind = args.kind or op_kind(w, cfg)
+    k = args.k if args.k is not None else w["k"]
+    tol = w["tol"]
+    xi = args.xi
+    lz_steps = w.get("lanczos_steps", 20)
+    uid = None
+    if ws > 1:
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(npc.npc_get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().numpy().tobytes())
+    stream = torch.cuda.current_stream()
+    ctx = npc.npc_context_create(local, ws, rank, uid, stream)
+    op, r0, r1 = create_operator(npc, ctx, w, kind, ws, rank, cfg)
+    nl = r1 - r0
+    b_host = np.ascontiguousarray(w["b"][r0:r1])
+    b = torch.tensor(b_host, device="cuda")
+    x = torch.zeros(nl, dtype=torch.float64, device="cuda")
+    maxit = args.maxit
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(bb, xx):
+        lo, hi = npc.npc_estimate_spectrum(op, lz_steps, bb)
+        poly = npc.npc_set_poly(op, k, lo, hi, xi)
+        xx.zero_()
+        st = npc.npc_pcg_solve(poly, op, bb, xx, tol, maxit)
+        poly.close()
+        st["lmin"], st["lmax"] = lo, hi
+        return st
+
+    for _ in range(args.warmup):
+        st = step(b, x)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = npc.npc_launch_count()
+    barrier()
+    ev0.record(stream)
+    stats = [step(b, x) for _ in range(args.steps)]
+    ev1.record(stream)
+    barrier()
+    launches = npc.npc_launch_count() - launches0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    iters = stats[-1]["iters"]
+    M = matrix_bytes(w, kind)
+    V = 8 * w["n"]
+    step_bytes = solve_bytes(M, V, k, iters, lz_steps)
+    gbs = step_bytes / (ms_step * 1e-3) / 1e9
+
+    # -------- dominant kernel: the fused degree step, timed live with CUDA events on the
+    # library's stream (= torch's current stream) over R applications of p_k(A)
+    lo, hi = stats[-1]["lmin"], stats[-1]["lmax"]
+    poly = npc.npc_set_poly(op, k, lo, hi, xi)
+    z = torch.empty_like(b)
+    R = max(3, args.kernel_reps)
+    npc.npc_apply_poly(poly, b, z)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(R):
+        npc.npc_apply_poly(poly, b, z)
+    e1.record(stream)
+    barrier()
+    t_apply = e0.elapsed_time(e1) / R  # ms per p_k(A) r (k launches)
+    apply_bytes = poly_bytes(M, V, k) / ws
+    per_launch_ms = t_apply / max(k, 1)
+    peak, peak_src = hbm_peak()
+    ach = apply_bytes / max(k, 1) / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_config{cfg}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # -------- e2e: the public API from host buffers: operator upload (npc_create_operator
+    # copies the host CSR), b H2D from pinned memory, estimate + set_poly + solve, x D2H
+    e2e_val = None
+    h2d = d2h = 0
+    if not args.no_e2e:
+        b_pin = torch.from_numpy(b_host).pin_memory()
+        x_pin = torch.empty(nl, dtype=torch.float64).pin_memory()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            op2, _, _ = create_operator(npc, ctx, w, kind, ws, rank, cfg)
+            bd = b_pin.to("cuda", non_blocking=True)
+            xd = torch.empty(nl, dtype=torch.float64, device="cuda")
+            lo2, hi2 = npc.npc_estimate_spectrum(op2, lz_steps, bd)
+            p2 = npc.npc_set_poly(op2, k, lo2, hi2, xi)
+            xd.zero_()
+            npc.npc_pcg_solve(p2, op2, bd, xd, tol, maxit)
+            x_pin.copy_(xd, non_blocking=True)
+            torch.cuda.synchronize()
+            p2.close()
+            op2.close()
+        barrier()
+        te = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device="cuda")
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_val = step_bytes / float(te.item()) / 1e9
+        if kind in ("csr", "sell"):
+            nnz_l = int(w["rowptr"][r1] - w["rowptr"][r0])
+            h2d = nnz_l * 12 + (nl + 1) * 4 + nl * 8
+        else:
+            h2d = nl * 8
+        d2h = nl * 8
+
+    # -------- CPU oracle baseline (rank 0, N = 1 only): one bounded p_k(A) v sample
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(w, k, lo, hi, xi, M, V, max_seconds=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "p_k(A)v GB/s (algorithmic bytes of the PCG-to-tol step / step time); PCG time-to-tol = ms_per_step",
+            "value": round(gbs, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads/, BASELINE.json config recipe)",
+            "config": {"workload": f"config{cfg}: {w['name']}", "operator": kind, "n": w["n"], "k": k, "xi": xi,
+                       "tol": tol, "lanczos_steps": lz_steps, "parallelism": f"row-block x{ws}" if ws > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (matrix + vectors > 126 MB)" if (M + 4 * V) > 126e6
+                       else "working set may be L2-resident (no flush)"},
+            "pcg": {"iters": iters, "converged": stats[-1]["converged"], "relres_true": stats[-1]["relres_true"],
+                    "op_applications": stats[-1]["op_applications"], "reductions": stats[-1]["reductions"],
+                    "lmin": lo, "lmax": hi, "time_to_tol_ms": round(ms_step, 3),
+                    "op_applications_per_s": round(stats[-1]["op_applications"] / (ms_step * 1e-3), 1)},
+            "roofline": {"bound": "hbm", "kernel": f"fused degree step ({kind})", "achieved": round(ach, 1),
+                         "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / peak, 4),
+                         "frac_vs_8TBs_nominal": round(ach / 8000.0, 4), "traffic": traffic,
+                         "bytes_per_launch": apply_bytes / max(k, 1), "launch_ms": round(per_launch_ms, 5),
+                         "timed": f"{R} x npc_apply_poly (k={k} launches each), CUDA events on the library stream"},
+            "e2e": {"value": round(e2e_val, 2) if e2e_val else None, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "includes": "npc_create_operator from host CSR + b H2D (pinned) + estimate + set_poly + solve + x D2H"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(w, k, lo, hi, xi, M, V, max_seconds=30.0):
+    """The oracle as it stands, one p_k(A) v application of the same workload on the host cores."""
+    try:
+        import oracle
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "error": str(e)}
+    orc = oracle.Operator(w)
+    r = np.asarray(w["b"], dtype=np.float64)
+    kk = k
+    t0 = time.perf_counter()
+    oracle.cheb_apply(orc, kk, lo, hi, xi, r)
+    dt = time.perf_counter() - t0
+    byts = poly_bytes(M, V, kk)
+    return {"value": round(byts / dt / 1e9, 3), "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"one p_k(A) v application (k={kk}) of {w['name']} by Alg. 2 verbatim (oracle/npc_oracle.c)",
+            "seconds": round(dt, 3)}
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    cfg = args.config
+    w = make_workload(cfg, args.side)
+    kind = args.kind or op_kind(w, cfg)
+    k = args.k if args.k is not None else w["k"]
+    orc = oracle.Operator(w)
+    # the oracle's own interval (20 Lanczos steps from b), as in the GPU arm
+    lo, hi = oracle.estimate_spectrum(orc, w.get("lanczos_steps", 20), w["b"])
+    M = matrix_bytes(w, kind)
+    V = 8 * w["n"]
+    r = np.asarray(w["b"], dtype=np.float64)
+    for _ in range(args.warmup):
+        oracle.cheb_apply(orc, k, lo, hi, args.xi, r)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.cheb_apply(orc, k, lo, hi, args.xi, r)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = poly_bytes(M, V, k) / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "p_k(A)v GB/s (algorithmic bytes / time)", "value": round(val, 3),
+        "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded workloads/)",
+        "config": {"workload": f"config{cfg}: {w['name']}", "operator": kind, "n": w["n"], "k": k, "xi": args.xi},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": f"each step = one p_k(A) v application (k={k}) of the full workload, Alg. 2 verbatim"},
+        "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--side", type=int, default=None, help="grid side (configs 2, 3) or n (configs 4, 5)")
+    ap.add_argument("--kind", default=None, help="operator storage override (csr|sell)")
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--xi", type=float, default=0.0)
+    ap.add_argument("--maxit", type=int, default=20000)
+    ap.add_argument("--kernel-reps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=30.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and not os.environ.get("NPC_BENCH_ALLOW_SHORT"):
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

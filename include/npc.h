@@ -1,0 +1,184 @@
+/*
+ * npc.h -- C ABI of libnpc: the xi-modified Newton-Chebyshev polynomial preconditioner
+ * z = p_k(A) r applied inside Preconditioned Conjugate Gradient, on NVIDIA B200 (sm_100a).
+ *
+ * Method: arXiv 2208.01339 (PAPER.md in the reference tree).  The problem statement is
+ * "solve A x = b, A SPD, only y = A x available"; p_k(A) r is
+ * Alg. 2 with theta replaced by theta_bar = theta (1 + xi) (Eq. thetamod,
+ * PAPER.md:328; delta unchanged -- DESIGN.md reading A1); PCG is PAPER.md:122-123 with the
+ * paper's counter laws (Table tab11).
+ *
+ * Conventions (all entry points):
+ *  - Every call returns npc_status and never aborts or exits; npc_last_error() returns a
+ *    thread-local message describing the last failing call on this thread.
+ *  - Pointers named *_dev are CUDA device pointers owned by the CALLER, on the context's
+ *    device, holding fp64 values of the rank's n_local owned rows (contiguous, 8-byte
+ *    aligned; 16-byte alignment is faster).  Everything else (operator storage, work
+ *    vectors, coefficient tables) is owned by the library handle and freed by destroy.
+ *  - Host arrays passed to npc_create_operator are COPIED; the caller may free them after.
+ *  - All work is enqueued on the context's stream; calls that return values to the host
+ *    (estimate_spectrum, pcg_solve) synchronise that stream, the others do not.
+ *  - Handles are immutable after creation except for their work vectors; one host thread
+ *    at a time may use a context and the handles created from it.
+ *  - Multi-rank (nranks > 1): one process per GPU, rows partitioned in contiguous blocks
+ *    (row_begin, n_local) in global row order.  Calls marked COLLECTIVE must be made by
+ *    every rank in the same order.
+ */
+#ifndef NPC_H
+#define NPC_H
+
+#if defined(__GNUC__)
+#define NPC_API __attribute__((visibility("default")))
+#else
+#define NPC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NPC_SUCCESS = 0,
+    NPC_ERR_INVALID_ARGUMENT = 1,   /* null handle/pointer, degree < 0, xi < 0, lmin <= 0, ... */
+    NPC_ERR_DIMENSION = 2,          /* CSR invariants violated, sizes inconsistent            */
+    NPC_ERR_DEGENERATE_INTERVAL = 3,/* lmin == lmax: delta = 0, Chebyshev undefined (A10)       */
+    NPC_ERR_NOT_CONVERGED = 4,      /* maxit reached; x holds the last iterate, stats filled  */
+    NPC_ERR_BREAKDOWN = 5,          /* <r,z> <= 0 or <p,Ap> <= 0 (operator or poly not SPD)    */
+    NPC_ERR_CUDA = 6,
+    NPC_ERR_NCCL = 7,
+    NPC_ERR_OUT_OF_MEMORY = 8,
+    NPC_ERR_UNSUPPORTED = 9
+} npc_status;
+
+typedef struct npc_context_s *npc_context;
+typedef struct npc_operator_s *npc_operator;
+typedef struct npc_poly_s *npc_poly;
+
+/* ---- context --------------------------------------------------------------------------
+ * device: CUDA ordinal.  nranks/rank: 1/0 for a single GPU; for nranks > 1,
+ * nccl_unique_id points to the 128-byte ncclUniqueId produced by npc_get_unique_id on rank
+ * 0 and broadcast by the caller (e.g. torch.distributed); COLLECTIVE in that case.
+ * cuda_stream: a cudaStream_t to enqueue on, or NULL for a library-owned stream.        */
+NPC_API npc_status npc_context_create(int device, int nranks, int rank, const void *nccl_unique_id,
+                              void *cuda_stream, npc_context *out);
+NPC_API npc_status npc_context_destroy(npc_context ctx);
+NPC_API npc_status npc_get_unique_id(void *out128);
+NPC_API const char *npc_last_error(void);
+/* Version string, e.g. "npc 0.1 sm_100a". */
+NPC_API const char *npc_version(void);
+/* Number of CUDA kernels this library has launched in the process so far (all contexts). */
+NPC_API unsigned long long npc_launch_count(void);
+
+/* ---- operators ------------------------------------------------------------------------- */
+typedef enum {
+    NPC_OP_CSR = 0,      /* general sparse, CSR (configs 1, 3); tile-staged fused kernel   */
+    NPC_OP_SELL = 1,     /* general sparse given as CSR, stored as SELL-C-sigma (config 4)  */
+    NPC_OP_STENCIL = 2,  /* constant-coefficient 2D 5-point / 3D 7-point Dirichlet (config 2)*/
+    NPC_OP_SCHUR = 3,    /* S = tridiag(-1, 2 + c, -1) + B^T D^{-1} B, never assembled (cfg 5)*/
+    NPC_OP_CALLBACK = 4  /* user y = A x on the device; recurrence in a separate kernel      */
+} npc_op_kind;
+
+/* User operator: y_dev = A x_dev for this rank's n_local rows, enqueued on cuda_stream.
+ * Return 0 on success; any other value makes the calling npc_* function fail. */
+typedef int (*npc_apply_fn)(void *user, const double *x_dev, double *y_dev, void *cuda_stream);
+
+typedef struct {
+    npc_op_kind kind;
+    long long n_global;          /* global number of rows (== n_local when nranks == 1)    */
+    long long row_begin;         /* first global row owned by this rank                   */
+    int n_local;                 /* rows owned by this rank                               */
+    /* CSR / SELL: this rank's rows; rowptr[n_local+1] (rowptr[0] == 0), colidx = GLOBAL
+     * column ids in [0, n_global), ascending within a row, vals fp64 (no NaN/Inf).        */
+    const int *rowptr;
+    const int *colidx;
+    const double *vals;
+    int sell_C;                  /* SELL chunk height; 0 -> 32 (only 32 is supported)       */
+    int sell_sigma;              /* SELL sorting window; 0 -> 256; 1 -> no sorting          */
+    /* STENCIL: grid nx * ny * nz_global (dim 3) or nx * ny (dim 2, nz = 1), row index
+     * i = x + nx*(y + ny*z); this rank owns planes [z_begin, z_begin + nz_local).
+     * y_i = diag*x_i + offdiag * sum of the existing neighbours (homogeneous Dirichlet). */
+    int stencil_dim, nx, ny, nz_global, z_begin, nz_local;
+    double diag, offdiag;
+    /* SCHUR: c[n_local] (diagonal shift of the tridiagonal block), B rows
+     * [b_row_begin, b_row_begin + b_n_local) as CSR with GLOBAL column ids (trace unknowns),
+     * d[b_n_local] > 0.  nranks > 1 is not supported in this version.                       */
+    const double *c;
+    long long b_rows_global;
+    long long b_row_begin;
+    int b_n_local;
+    const int *b_rowptr;
+    const int *b_colidx;
+    const double *b_vals;
+    const double *d;
+    /* CALLBACK */
+    npc_apply_fn apply;
+    void *user;
+} npc_operator_desc;
+
+/* Create an operator (COLLECTIVE when nranks > 1: builds the halo plan).  Validates the
+ * CSR invariants (NPC_ERR_DIMENSION), uploads and converts (CSR -> tile metadata;
+ * CSR -> sigma-sorted SELL-32; B -> D^{-1/2} B).                                            */
+NPC_API npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, npc_operator *out);
+NPC_API npc_status npc_destroy_operator(npc_operator op);
+/* y_dev = A x_dev (one application; halo exchange included).  */
+NPC_API npc_status npc_apply_operator(npc_operator op, const double *x_dev, double *y_dev);
+
+/* ---- spectrum estimate (replaces the paper's DACG) ---------------------
+ * nsteps-step Lanczos from v0_dev (NULL -> a deterministic counter-hash vector in [-1,1]),
+ * no reorthogonalisation; *lmin/*lmax = extreme Ritz values of T_nsteps (Sturm bisection).
+ * Stops early (and succeeds) on an exact invariant subspace.  COLLECTIVE.                  */
+NPC_API npc_status npc_estimate_spectrum(npc_operator op, int nsteps, const double *v0_dev,
+                                 double *lmin, double *lmax);
+
+/* ---- polynomial preconditioner (Alg. 2) --------------------------------
+ * degree k >= 0 (k applications of A per npc_apply_poly), interval [lmin, lmax] with
+ * 0 < lmin < lmax (lmin == lmax -> NPC_ERR_DEGENERATE_INTERVAL), xi >= 0 (Eq. thetamod).
+ * Coefficients are computed once on the host (Eq. rhocheb).                                */
+NPC_API npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, double xi,
+                        npc_poly *out);
+NPC_API npc_status npc_destroy_poly(npc_poly poly);
+/* z_dev = p_k(A) r_dev: exactly k operator applications, no reductions, no host sync.
+ * z_dev must not alias r_dev.                                                              */
+NPC_API npc_status npc_apply_poly(npc_poly poly, const double *r_dev, double *z_dev);
+
+/* ---- PCG ----------------------------------------------------------------------------------
+ * Solve A x = b with PCG preconditioned by poly (NULL -> plain CG), single-reduction
+ * (Chronopoulos-Gear) form with the dot products fused into the producing kernels.
+ * x_dev: in = x0, out = solution.  Stops when ||r_i|| / ||b|| <= tol on the recursive
+ * residual; then the true residual is formed and, if above tol, replaces r and the
+ * iteration continues (readings A5, A23).  tol in (0,1), maxit >= 1.
+ * b == 0 -> x = 0, iters = 0, NPC_SUCCESS.  COLLECTIVE.                                     */
+typedef struct {
+    int iters;                   /* x updates                                               */
+    int converged;
+    long long op_applications;   /* every A application, including those inside p_k       */
+    long long reductions;        /* global reduction points (allreduces when nranks > 1)    */
+    double relres_recursive;     /* ||r_iters|| / ||b|| (recursive residual)                */
+    double relres_true;          /* ||b - A x|| / ||b|| of the returned x                   */
+    double solve_seconds;        /* wall time of the call                                   */
+    double *history;             /* optional caller HOST buffer of length maxit + 1, or NULL:
+                                    history[i] = ||r_i|| / ||b||, i = 0..iters               */
+} npc_pcg_stats;
+
+NPC_API npc_status npc_pcg_solve(npc_poly poly, npc_operator op, const double *b_dev, double *x_dev,
+                         double tol, int maxit, npc_pcg_stats *stats);
+
+/* ---- host-only helpers (no GPU needed) ----------------------------------------------------
+ * Halo plan of a contiguous row-block partition, exposed for host-side tests of the
+ * multi-rank path: given this rank's CSR rows (GLOBAL column ids) and the partition
+ * row_starts[nranks + 1], writes the number of ghost columns and, if ghost_ids != NULL
+ * (capacity *n_ghost), the ascending global ids of the ghost columns, and the per-rank
+ * ghost counts recv_counts[nranks].  Returns NPC_ERR_DIMENSION on invalid input.          */
+NPC_API npc_status npc_halo_plan(int n_local, const int *rowptr, const int *colidx, int nranks,
+                         const long long *row_starts, int rank, int *n_ghost,
+                         long long *ghost_ids, int *recv_counts);
+/* Chebyshev coefficients as used by the kernels: for j = 1..k the fused degree step is
+ * s_j = a_j (A s_{j-1}) + b_j s_{j-1} + c_j s_{j-2} + d_j r with s_0 = r / theta_bar,
+ * s_{-1} = 0.  Writes theta_bar, delta, sigma and the 4*k table coef[4*(j-1) + {0,1,2,3}]. */
+NPC_API npc_status npc_poly_coefficients(int degree, double lmin, double lmax, double xi,
+                                 double *theta_bar, double *delta, double *sigma, double *coef);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NPC_H */

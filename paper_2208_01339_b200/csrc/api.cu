@@ -1,0 +1,259 @@
+// api.cu -- the C ABI (include/npc.h): argument validation, handle lifetime, dispatch.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "npc_internal.cuh"
+
+namespace npc {
+std::atomic<unsigned long long> g_launches{0};
+static thread_local char g_err[1024] = "";
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+npc_status poly_coefficients(int k, double lmin, double lmax, double xi, double *theta_bar, double *delta,
+                             double *sigma, double *coef);
+npc_status apply_poly(npc_poly P, const double *r, double *z);
+npc_status apply_operator(Operator *op, const double *x, double *y, DevBuf &scratch);
+npc_status pcg(npc_poly P, npc_operator H, const double *b, double *x, double tol, int maxit, npc_pcg_stats *stats);
+npc_status lanczos(Operator *op, int m, const double *v0, double *lmin, double *lmax);
+}  // namespace npc
+
+using namespace npc;
+
+#define NPC_GUARD(cond, code, ...)      \
+    do {                                \
+        if (!(cond)) {                  \
+            npc::set_error(__VA_ARGS__); \
+            return code;                \
+        }                               \
+    } while (0)
+
+// Select the device of the handle for the duration of a call.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+extern "C" {
+
+const char *npc_last_error(void) { return g_err; }
+unsigned long long npc_launch_count(void) { return g_launches.load(); }
+const char *npc_version(void) { return "npc 0.1 sm_100a (fp64, CSR/SELL/stencil/Schur/callback)"; }
+
+npc_status npc_get_unique_id(void *out128) {
+    NPC_GUARD(out128, NPC_ERR_INVALID_ARGUMENT, "npc_get_unique_id: null output");
+    ncclUniqueId id;
+    NPC_NCCL_TRY(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(out128, &id, sizeof(id));
+    return NPC_SUCCESS;
+}
+
+npc_status npc_context_create(int device, int nranks, int rank, const void *nccl_unique_id, void *cuda_stream,
+                              npc_context *out) {
+    NPC_GUARD(out, NPC_ERR_INVALID_ARGUMENT, "npc_context_create: null output");
+    *out = nullptr;
+    NPC_GUARD(nranks >= 1 && rank >= 0 && rank < nranks, NPC_ERR_INVALID_ARGUMENT, "npc_context_create: bad rank %d/%d",
+              rank, nranks);
+    NPC_GUARD(nranks == 1 || nccl_unique_id, NPC_ERR_INVALID_ARGUMENT,
+              "npc_context_create: nranks > 1 needs an NCCL unique id");
+    int ndev = 0;
+    NPC_CUDA_TRY(cudaGetDeviceCount(&ndev));
+    NPC_GUARD(device >= 0 && device < ndev, NPC_ERR_INVALID_ARGUMENT, "npc_context_create: device %d of %d", device, ndev);
+    cudaDeviceProp prop;
+    NPC_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    NPC_GUARD(prop.major == 10 && prop.minor == 0, NPC_ERR_UNSUPPORTED,
+              "libnpc is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
+    DeviceScope ds(device);
+    NPC_CUDA_TRY(cudaSetDevice(device));
+    auto h = std::make_unique<npc_context_s>();
+    Context &c = h->ctx;
+    c.device = device;
+    c.nranks = nranks;
+    c.rank = rank;
+    c.num_sms = prop.multiProcessorCount;
+    if (cuda_stream) {
+        c.stream = (cudaStream_t)cuda_stream;
+    } else {
+        NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.own_stream = true;
+    }
+    if (nranks > 1) {
+        NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking));
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof(id));
+        NPC_NCCL_TRY(ncclCommInitRank(&c.comm, nranks, id, rank));
+    }
+    NPC_TRY(c.ensure_partials(4096));
+    *out = h.release();
+    return NPC_SUCCESS;
+}
+
+npc_status npc_context_destroy(npc_context ctx) {
+    if (!ctx) return NPC_SUCCESS;
+    {
+        DeviceScope ds(ctx->ctx.device);
+        Context &c = ctx->ctx;
+        if (c.stream) cudaStreamSynchronize(c.stream);
+        if (c.comm) ncclCommDestroy(c.comm);
+        if (c.comm_stream) cudaStreamDestroy(c.comm_stream);
+        c.partials.release();
+        c.scalars.release();
+        if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
+    }
+    delete ctx;
+    return NPC_SUCCESS;
+}
+
+npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, npc_operator *out) {
+    NPC_GUARD(ctx && desc && out, NPC_ERR_INVALID_ARGUMENT, "npc_create_operator: null argument");
+    *out = nullptr;
+    NPC_GUARD(desc->n_local >= 0 && desc->row_begin >= 0, NPC_ERR_DIMENSION, "npc_create_operator: negative size");
+    if (ctx->ctx.nranks == 1)
+        NPC_GUARD(desc->row_begin == 0 && (desc->n_global == 0 || desc->n_global == desc->n_local), NPC_ERR_DIMENSION,
+                  "npc_create_operator: single rank must own all rows");
+    else
+        NPC_GUARD(desc->row_begin + desc->n_local <= desc->n_global, NPC_ERR_DIMENSION,
+                  "npc_create_operator: rows beyond n_global");
+    DeviceScope ds(ctx->ctx.device);
+    npc_operator_desc d = *desc;
+    if (d.n_global == 0) d.n_global = d.n_local;
+    std::unique_ptr<Operator> op;
+    switch (d.kind) {
+        case NPC_OP_CSR: NPC_TRY(make_csr_operator(&ctx->ctx, &d, op)); break;
+        case NPC_OP_SELL: NPC_TRY(make_sell_operator(&ctx->ctx, &d, op)); break;
+        case NPC_OP_STENCIL: NPC_TRY(make_stencil_operator(&ctx->ctx, &d, op)); break;
+        case NPC_OP_SCHUR: NPC_TRY(make_schur_operator(&ctx->ctx, &d, op)); break;
+        case NPC_OP_CALLBACK: NPC_TRY(make_callback_operator(&ctx->ctx, &d, op)); break;
+        default: NPC_GUARD(false, NPC_ERR_INVALID_ARGUMENT, "npc_create_operator: unknown kind %d", (int)d.kind);
+    }
+    NPC_TRY(ctx->ctx.ensure_partials(op->num_partials()));
+    NPC_CUDA_TRY(cudaDeviceSynchronize());
+    auto h = std::make_unique<npc_operator_s>();
+    h->owner = ctx;
+    h->op = std::move(op);
+    *out = h.release();
+    return NPC_SUCCESS;
+}
+
+npc_status npc_destroy_operator(npc_operator op) {
+    if (!op) return NPC_SUCCESS;
+    {
+        DeviceScope ds(op->owner->ctx.device);
+        cudaStreamSynchronize(op->owner->ctx.stream);
+        op->op.reset();
+    }
+    delete op;
+    return NPC_SUCCESS;
+}
+
+npc_status npc_apply_operator(npc_operator op, const double *x_dev, double *y_dev) {
+    NPC_GUARD(op && (x_dev || op->op->n_local == 0) && (y_dev || op->op->n_local == 0), NPC_ERR_INVALID_ARGUMENT,
+              "npc_apply_operator: null argument");
+    NPC_GUARD(x_dev != y_dev || op->op->n_local == 0, NPC_ERR_INVALID_ARGUMENT, "npc_apply_operator: x aliases y");
+    DeviceScope ds(op->owner->ctx.device);
+    static thread_local DevBuf scratch;
+    return apply_operator(op->op.get(), x_dev, y_dev, scratch);
+}
+
+npc_status npc_estimate_spectrum(npc_operator op, int nsteps, const double *v0_dev, double *lmin, double *lmax) {
+    NPC_GUARD(op && lmin && lmax, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum: null argument");
+    NPC_GUARD(nsteps >= 1 && nsteps <= 100000, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum: nsteps %d", nsteps);
+    NPC_GUARD(op->op->n_global >= 1, NPC_ERR_DIMENSION, "npc_estimate_spectrum: empty operator");
+    DeviceScope ds(op->owner->ctx.device);
+    return lanczos(op->op.get(), nsteps, v0_dev, lmin, lmax);
+}
+
+npc_status npc_poly_coefficients(int degree, double lmin, double lmax, double xi, double *theta_bar, double *delta,
+                                 double *sigma, double *coef) {
+    NPC_GUARD(theta_bar && delta && sigma, NPC_ERR_INVALID_ARGUMENT, "npc_poly_coefficients: null output");
+    return poly_coefficients(degree, lmin, lmax, xi, theta_bar, delta, sigma, coef);
+}
+
+npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, double xi, npc_poly *out) {
+    NPC_GUARD(op && out, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly: null argument");
+    *out = nullptr;
+    NPC_GUARD(degree <= 100000, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly: degree %d too large", degree);
+    auto P = std::make_unique<npc_poly_s>();
+    P->op = op;
+    P->degree = degree;
+    P->lmin = lmin;
+    P->lmax = lmax;
+    P->xi = xi;
+    P->coef.assign(4 * (size_t)std::max(degree, 0) + 4, 0.0);
+    NPC_TRY(poly_coefficients(degree, lmin, lmax, xi, &P->theta_bar, &P->delta, &P->sigma, P->coef.data()));
+    DeviceScope ds(op->owner->ctx.device);
+    const size_t n = std::max(op->op->n_local, 1);
+    NPC_TRY(P->tmp.alloc(sizeof(double) * n));
+    if (op->op->permuted()) {
+        NPC_TRY(P->rin.alloc(sizeof(double) * n));
+        NPC_TRY(P->zout.alloc(sizeof(double) * n));
+    }
+    *out = P.release();
+    return NPC_SUCCESS;
+}
+
+npc_status npc_destroy_poly(npc_poly poly) {
+    if (!poly) return NPC_SUCCESS;
+    {
+        DeviceScope ds(poly->op->owner->ctx.device);
+        cudaStreamSynchronize(poly->op->owner->ctx.stream);
+        poly->tmp.release();
+        poly->rin.release();
+        poly->zout.release();
+    }
+    delete poly;
+    return NPC_SUCCESS;
+}
+
+npc_status npc_apply_poly(npc_poly poly, const double *r_dev, double *z_dev) {
+    NPC_GUARD(poly, NPC_ERR_INVALID_ARGUMENT, "npc_apply_poly: null poly");
+    const int n = poly->op->op->n_local;
+    NPC_GUARD(n == 0 || (r_dev && z_dev), NPC_ERR_INVALID_ARGUMENT, "npc_apply_poly: null vector");
+    NPC_GUARD(n == 0 || r_dev != z_dev, NPC_ERR_INVALID_ARGUMENT, "npc_apply_poly: z must not alias r");
+    DeviceScope ds(poly->op->owner->ctx.device);
+    return apply_poly(poly, r_dev, z_dev);
+}
+
+npc_status npc_pcg_solve(npc_poly poly, npc_operator op, const double *b_dev, double *x_dev, double tol, int maxit,
+                         npc_pcg_stats *stats) {
+    NPC_GUARD(op, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: null operator");
+    NPC_GUARD(!poly || poly->op == op, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: poly built for another operator");
+    NPC_GUARD(tol > 0.0 && tol < 1.0, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: tol %g not in (0,1)", tol);
+    NPC_GUARD(maxit >= 1, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: maxit %d < 1", maxit);
+    NPC_GUARD(op->op->n_local == 0 || (b_dev && x_dev), NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: null vector");
+    NPC_GUARD(op->op->n_local == 0 || b_dev != x_dev, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: x aliases b");
+    DeviceScope ds(op->owner->ctx.device);
+    return pcg(poly, op, b_dev, x_dev, tol, maxit, stats);
+}
+
+npc_status npc_halo_plan(int n_local, const int *rowptr, const int *colidx, int nranks, const long long *row_starts,
+                         int rank, int *n_ghost, long long *ghost_ids, int *recv_counts) {
+    NPC_GUARD(rowptr && n_ghost && row_starts && (colidx || rowptr[n_local] == 0), NPC_ERR_INVALID_ARGUMENT,
+              "npc_halo_plan: null argument");
+    HaloPlan plan;
+    NPC_TRY(halo_plan_local(n_local, rowptr, colidx, nranks, row_starts, rank, plan));
+    const int cap = *n_ghost;
+    *n_ghost = plan.n_ghost;
+    if (ghost_ids) {
+        NPC_GUARD(cap >= plan.n_ghost, NPC_ERR_INVALID_ARGUMENT, "npc_halo_plan: ghost_ids capacity %d < %d", cap,
+                  plan.n_ghost);
+        std::copy(plan.ghost_ids.begin(), plan.ghost_ids.end(), ghost_ids);
+    }
+    if (recv_counts) std::copy(plan.recv_count.begin(), plan.recv_count.end(), recv_counts);
+    return NPC_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,214 @@
+// npc_internal.cuh -- internal types of libnpc (not part of the C ABI).
+//
+// Layering: kernels (op_*.cu, vec_kernels.cu) <- operators (Operator
+// subclasses) <- drivers (solvers.cu: apply_poly, PCG, Lanczos) <- C ABI (api.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "npc.h"
+
+namespace npc {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char *fmt, ...);
+
+#define NPC_CUDA_TRY(expr)                                                                     \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            npc::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_)); \
+            return e_ == cudaErrorMemoryAllocation ? NPC_ERR_OUT_OF_MEMORY : NPC_ERR_CUDA;     \
+        }                                                                                      \
+    } while (0)
+
+#define NPC_NCCL_TRY(expr)                                                                     \
+    do {                                                                                       \
+        ncclResult_t e_ = (expr);                                                              \
+        if (e_ != ncclSuccess) {                                                               \
+            npc::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr, ncclGetErrorString(e_)); \
+            return NPC_ERR_NCCL;                                                               \
+        }                                                                                      \
+    } while (0)
+
+#define NPC_TRY(expr)                       \
+    do {                                    \
+        npc_status s_ = (expr);             \
+        if (s_ != NPC_SUCCESS) return s_;   \
+    } while (0)
+
+// Count every kernel launch of the library (npc_launch_count) and check the launch.
+extern std::atomic<unsigned long long> g_launches;
+#define NPC_LAUNCH_CHECK()                                            \
+    do {                                                              \
+        npc::g_launches.fetch_add(1, std::memory_order_relaxed);      \
+        NPC_CUDA_TRY(cudaGetLastError());                             \
+    } while (0)
+
+// ------------------------------------------------------------------ device buffers
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    npc_status alloc(size_t nbytes) {
+        release();
+        if (nbytes == 0) nbytes = 16;
+        cudaError_t e = cudaMalloc(&p, nbytes);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            set_error("cudaMalloc(%zu) failed: %s", nbytes, cudaGetErrorString(e));
+            return e == cudaErrorMemoryAllocation ? NPC_ERR_OUT_OF_MEMORY : NPC_ERR_CUDA;
+        }
+        bytes = nbytes;
+        return NPC_SUCCESS;
+    }
+    template <class T>
+    T *as() const { return static_cast<T *>(p); }
+};
+
+// ------------------------------------------------------------------ the fused step
+// One call = one application of A fused with the Chebyshev three-term update
+// (PAPER.md:253-295):
+//     out = a * (A x) + b * x + c * s2 + d * r
+// optionally emitting per-block partials of <out, dotv> (the PCG inner products fused
+// into the producing kernel).  s2 may alias out (in-place over s_{j-2}).
+struct StepArgs {
+    const double *x = nullptr;   // input of A: this rank's owned entries (internal order)
+    const double *s2 = nullptr;  // nullable
+    const double *r = nullptr;   // nullable
+    double *out = nullptr;
+    const double *dotv = nullptr;  // nullable -> no dot partials
+    double *partials = nullptr;    // >= Operator::num_partials() doubles when dotv != null
+    const int *done = nullptr;     // nullable device flag: when *done != 0 the kernels no-op
+    double a = 1.0, b = 0.0, c = 0.0, d = 0.0;
+};
+
+struct Context;
+
+class Operator {
+  public:
+    virtual ~Operator() = default;
+    // Enqueue one fused step on ctx->stream (including any halo exchange).
+    virtual npc_status step(const StepArgs &s) = 0;
+    // Number of per-block dot partials a step writes (grid of the last kernel).
+    virtual int num_partials() const = 0;
+    // Algorithmic bytes of one application + recurrence, for reporting.
+    virtual double bytes_per_step(bool has_s2, bool has_r) const = 0;
+    // Internal vector order differs from the caller's (SELL sigma-sort)?
+    virtual bool permuted() const { return false; }
+    // out[i] = in[perm[i]] (to internal) / out[perm[i]] = in[i] (to caller order).
+    virtual npc_status to_internal(const double *in, double *out) { (void)in; (void)out; return NPC_SUCCESS; }
+    virtual npc_status to_external(const double *in, double *out) { (void)in; (void)out; return NPC_SUCCESS; }
+
+    Context *ctx = nullptr;
+    npc_op_kind kind = NPC_OP_CSR;
+    int n_local = 0;
+    long long n_global = 0;
+    long long row_begin = 0;
+};
+
+// ------------------------------------------------------------------ context
+struct Context {
+    int device = 0;
+    int nranks = 1, rank = 0;
+    cudaStream_t stream = nullptr;       // compute stream
+    cudaStream_t comm_stream = nullptr;  // halo traffic (nranks > 1)
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    int num_sms = 148;
+    // scratch for reductions: partial arrays + scalar slots
+    DevBuf partials;        // 4 slots of partial_cap doubles
+    size_t partial_cap = 0;
+    DevBuf scalars;         // small device scalar area (see solvers.cu)
+    double *host_pinned = nullptr;  // pinned host mirror for small readbacks
+
+    npc_status ensure_partials(size_t n);
+    double *partial_slot(int i) { return partials.as<double>() + (size_t)i * partial_cap; }
+    // Sum 'count' doubles at dev (in place) over all ranks (no-op on one rank).
+    npc_status allreduce_sum(double *dev, int count);
+};
+
+// ------------------------------------------------------------------ launch helpers
+// vec_kernels.cu
+npc_status launch_reduce_sum(Context *ctx, const double *partials, int n, double *out, int nvec = 1,
+                             const double *partials2 = nullptr, int n2 = 0, double *out2 = nullptr);
+npc_status launch_scale(Context *ctx, const double *in, double *out, double alpha, int n,
+                        const double *dotv, double *partials, int *nparts, const int *done);
+npc_status launch_axpby_step(Context *ctx, const double *y, const StepArgs &s, int n);
+npc_status launch_dot(Context *ctx, const double *a, const double *b, int n, double *partials, int *nparts);
+npc_status launch_gather(Context *ctx, const double *in, const int *idx, double *out, int n);
+npc_status launch_scatter(Context *ctx, const double *in, const int *idx, double *out, int n);
+npc_status launch_fill(Context *ctx, double *out, double v, int n);
+npc_status launch_hash_vector(Context *ctx, double *out, int n, long long offset, unsigned long long seed);
+
+// Grid size of the plain vector kernels for n entries (fixed: partial counts are static).
+int vec_grid(int n);
+
+// Operator factories (op_*.cu)
+npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
+npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
+npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
+npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
+npc_status make_callback_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
+
+// Host halo plan (halo.cu)
+struct HaloPlan {
+    int n_ghost = 0;
+    std::vector<long long> ghost_ids;     // ascending global ids
+    std::vector<int> recv_count, recv_off;  // per rank, into the ghost buffer
+    std::vector<int> send_count, send_off;  // per rank, into the send buffer
+    std::vector<int> send_idx;            // local owned indices to pack (by destination)
+    bool empty() const { return n_ghost == 0 && send_idx.empty(); }
+};
+npc_status halo_plan_local(int n_local, const int *rowptr, const int *colidx, int nranks,
+                           const long long *row_starts, int rank, HaloPlan &plan);
+// Exchange ghost-id lists with the owners (NCCL, collective) to fill send lists.
+npc_status halo_plan_exchange(Context *ctx, long long row_begin, HaloPlan &plan);
+// Per-step exchange: pack x[send_idx] -> send buffer, ncclSend/Recv to the ghost buffer,
+// on ctx->comm_stream after an event on ctx->stream; records 'ready' on comm_stream.
+struct HaloRuntime {
+    DevBuf send_idx, send_buf, ghost_buf;
+    cudaEvent_t packed = nullptr, ready = nullptr;
+    ~HaloRuntime();
+};
+npc_status halo_setup(Context *ctx, const HaloPlan &plan, HaloRuntime &rt);
+npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const double *x);
+npc_status halo_wait(Context *ctx, HaloRuntime &rt);
+
+// Device-side bit helpers
+__host__ __device__ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace npc
+
+// Opaque handle structs of the C ABI.
+struct npc_context_s {
+    npc::Context ctx;
+};
+struct npc_operator_s {
+    npc_context owner = nullptr;
+    std::unique_ptr<npc::Operator> op;
+};
+struct npc_poly_s {
+    npc_operator op = nullptr;
+    int degree = 0;
+    double lmin = 0, lmax = 0, xi = 0;
+    double theta_bar = 0, delta = 0, sigma = 0;
+    std::vector<double> coef;  // 4 * degree: a_j, b_j, c_j, d_j (j = 1..k)
+    npc::DevBuf tmp;           // second recurrence buffer (internal order)
+    npc::DevBuf rin, zout;     // internal-order copies when the operator is permuted
+};

@@ -1,0 +1,315 @@
+// op_csr.cu -- general sparse operator in CSR (BASELINE configs 1 and 3) with the Chebyshev
+// recurrence fused into the SpMV epilogue (Alg. 2 steps 5-6).
+//
+// Kernel design ("G2 CSR tile kernel"): one CTA per tile of 256 consecutive
+// rows.  Thread 0 issues two 1D bulk-TMA copies (cp.async.bulk, mbarrier completion, L2
+// evict-first) of the tile's contiguous value/column segments into shared memory while the
+// other threads load rowptr, s_{j-2} and r; every thread then forms its row's dot product
+// from shared memory, gathering x through L1/L2, and writes
+//     out = a (A x) + b x + c s_{j-2} + d r      (+ per-CTA partial of <out, dotv>).
+// Matrix bytes therefore move exactly once per degree with perfectly coalesced bulk
+// transactions; the x gather of a 7-point row touches 3 planes that stay in L2.
+// Multi-rank: columns outside the owned block are remapped to ghost slots; tiles that touch
+// a ghost run after the halo exchange, the others overlap it.
+#include <algorithm>
+
+#include "device_util.cuh"
+#include "npc_internal.cuh"
+
+namespace npc {
+
+static constexpr int CSR_TILE = 256;
+static constexpr int CSR_MAX_SMEM = 200 * 1024;
+
+struct CsrDev {
+    const int *rowptr;
+    const int *cols;  // local ids: [0, n) owned, [n, n + n_ghost) ghost slots
+    const double *vals;
+    int n;
+    const double *ghost;
+};
+
+template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST>
+__global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, const int *__restrict__ tiles,
+                                                       int vspan_max) {
+    if (s.done && *s.done) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t bar;
+    __shared__ double red[CSR_TILE / 32];
+
+    const int tile = tiles ? tiles[blockIdx.x] : blockIdx.x;
+    const int row0 = tile * CSR_TILE;
+    const int nrows = min(CSR_TILE, A.n - row0);
+    const int pb = A.rowptr[row0];
+    const int v0 = pb & ~1;
+    const int c0 = pb & ~3;
+    double *sv = reinterpret_cast<double *>(smem);
+    int *sc = reinterpret_cast<int *>(smem + (size_t)vspan_max * 8);
+
+    if (STAGED) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int pe = A.rowptr[row0 + nrows];
+            const int v1 = (pe + 1) & ~1, c1 = (pe + 3) & ~3;
+            const uint32_t bv = (uint32_t)(v1 - v0) * 8u, bc = (uint32_t)(c1 - c0) * 4u;
+            mbar_arrive_expect_tx(&bar, bv + bc);
+            if (bv) {
+                const uint64_t pol = policy_evict_first();
+                bulk_g2s_evict_first(sv, A.vals + v0, bv, &bar, pol);
+                bulk_g2s_evict_first(sc, A.cols + c0, bc, &bar, pol);
+            }
+        }
+    }
+    const int row = row0 + threadIdx.x;
+    const bool active = threadIdx.x < nrows;
+    int rb = 0, re = 0;
+    double xs = 0.0, s2v = 0.0, rv = 0.0;
+    if (active) {
+        rb = A.rowptr[row];
+        re = A.rowptr[row + 1];
+        xs = s.x[row];
+        if (HAS_S2) s2v = s.s2[row];
+        if (HAS_R) rv = s.r[row];
+    }
+    if (STAGED) mbar_wait(&bar, 0);
+    double acc = 0.0;
+    if (active) {
+        double y = 0.0;
+        const double *__restrict__ x = s.x;
+        for (int p = rb; p < re; ++p) {
+            int c;
+            double v;
+            if (STAGED) {
+                c = sc[p - c0];
+                v = sv[p - v0];
+            } else {
+                c = __ldcs(A.cols + p);
+                v = __ldcs(A.vals + p);
+            }
+            double xv;
+            if (GHOST && c >= A.n)
+                xv = A.ghost[c - A.n];
+            else
+                xv = __ldg(x + c);
+            y += v * xv;
+        }
+        double o = s.a * y + s.b * xs;
+        if (HAS_S2) o += s.c * s2v;
+        if (HAS_R) o += s.d * rv;
+        s.out[row] = o;
+        if (DOT) acc = o * s.dotv[row];
+    }
+    if (DOT) {
+        acc = block_sum<CSR_TILE>(acc, red);
+        if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
+    }
+}
+
+class CsrOperator : public Operator {
+  public:
+    DevBuf rowptr, cols, vals;
+    DevBuf tiles_interior, tiles_boundary;
+    int ntiles = 0, n_interior = 0, n_boundary = 0;
+    int vspan_max = 0, cspan_max = 0;
+    size_t smem_bytes = 0;
+    bool staged = true;
+    long long nnz = 0;
+    HaloPlan plan;
+    HaloRuntime halo;
+    bool multi = false;
+
+    int num_partials() const override { return std::max(ntiles, 1); }
+
+    double bytes_per_step(bool has_s2, bool has_r) const override {
+        // values + column ids + row pointers once, x once (perfect gather reuse), write out,
+        // read s_{j-2} and r when present.
+        double b = (double)nnz * 12.0 + (double)(n_local + 1) * 4.0 + 2.0 * 8.0 * n_local;
+        if (has_s2) b += 8.0 * n_local;
+        if (has_r) b += 8.0 * n_local;
+        return b;
+    }
+
+    template <bool ST, bool H2, bool HR, bool DT, bool GH>
+    npc_status launch_t(const StepArgs &s, const int *tl, int nt, double *partials) {
+        if (nt <= 0) return NPC_SUCCESS;
+        CsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local,
+                 GH ? halo.ghost_buf.as<double>() : nullptr};
+        StepArgs a = s;
+        a.partials = partials;
+        auto kern = k_csr_step<ST, H2, HR, DT, GH>;
+        size_t sm = ST ? smem_bytes : 0;
+        if (sm > 48 * 1024) NPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kern<<<nt, CSR_TILE, sm, ctx->stream>>>(A, a, tl, vspan_max);
+        NPC_LAUNCH_CHECK();
+        return NPC_SUCCESS;
+    }
+
+    template <bool H2, bool HR, bool DT>
+    npc_status launch_g(const StepArgs &s, const int *tl, int nt, double *partials, bool ghost) {
+        if (staged) {
+            if (ghost) return launch_t<true, H2, HR, DT, true>(s, tl, nt, partials);
+            return launch_t<true, H2, HR, DT, false>(s, tl, nt, partials);
+        }
+        if (ghost) return launch_t<false, H2, HR, DT, true>(s, tl, nt, partials);
+        return launch_t<false, H2, HR, DT, false>(s, tl, nt, partials);
+    }
+
+    npc_status launch(const StepArgs &s, const int *tl, int nt, double *partials, bool ghost) {
+        const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
+        if (h2 && hr && dt) return launch_g<true, true, true>(s, tl, nt, partials, ghost);
+        if (h2 && hr) return launch_g<true, true, false>(s, tl, nt, partials, ghost);
+        if (h2 && dt) return launch_g<true, false, true>(s, tl, nt, partials, ghost);
+        if (h2) return launch_g<true, false, false>(s, tl, nt, partials, ghost);
+        if (hr && dt) return launch_g<false, true, true>(s, tl, nt, partials, ghost);
+        if (hr) return launch_g<false, true, false>(s, tl, nt, partials, ghost);
+        if (dt) return launch_g<false, false, true>(s, tl, nt, partials, ghost);
+        return launch_g<false, false, false>(s, tl, nt, partials, ghost);
+    }
+
+    npc_status step(const StepArgs &s) override {
+        if (n_local == 0 && !multi) return NPC_SUCCESS;
+        if (!multi) return launch(s, nullptr, ntiles, s.partials, false);
+        // halo of x -> ghost slots on the comm stream, interior tiles meanwhile
+        NPC_TRY(halo_start(ctx, plan, halo, s.x));
+        NPC_TRY(launch(s, tiles_interior.as<int>(), n_interior, s.partials, false));
+        NPC_TRY(halo_wait(ctx, halo));
+        return launch(s, tiles_boundary.as<int>(), n_boundary, s.partials ? s.partials + n_interior : nullptr, true);
+    }
+};
+
+// Validate CSR invariants: rowptr monotone from 0, column ids in range and
+// strictly ascending within a row, values finite.
+static npc_status validate_csr(int n, long long ncols, const int *rowptr, const int *colidx, const double *vals) {
+    if (rowptr[0] != 0) {
+        set_error("CSR: rowptr[0] = %d (must be 0)", rowptr[0]);
+        return NPC_ERR_DIMENSION;
+    }
+    for (int i = 0; i < n; ++i) {
+        if (rowptr[i + 1] < rowptr[i]) {
+            set_error("CSR: rowptr not monotone at row %d", i);
+            return NPC_ERR_DIMENSION;
+        }
+        for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+            if (colidx[p] < 0 || colidx[p] >= ncols) {
+                set_error("CSR: column %d out of range at row %d", colidx[p], i);
+                return NPC_ERR_DIMENSION;
+            }
+            if (p > rowptr[i] && colidx[p] <= colidx[p - 1]) {
+                set_error("CSR: columns not strictly ascending in row %d", i);
+                return NPC_ERR_DIMENSION;
+            }
+            if (!std::isfinite(vals[p])) {
+                set_error("CSR: non-finite value at row %d", i);
+                return NPC_ERR_DIMENSION;
+            }
+        }
+    }
+    return NPC_SUCCESS;
+}
+
+npc_status validate_csr_desc(Context *ctx, const npc_operator_desc *d) {
+    if (!d->rowptr || (!d->colidx && d->n_local > 0) || (!d->vals && d->n_local > 0)) {
+        set_error("CSR: null array");
+        return NPC_ERR_INVALID_ARGUMENT;
+    }
+    (void)ctx;
+    return validate_csr(d->n_local, d->n_global, d->rowptr, d->colidx, d->vals);
+}
+
+// Convert global column ids to local ids ([0,n) owned, n + ghost slot otherwise).
+npc_status localize_columns(Context *ctx, const npc_operator_desc *d, HaloPlan &plan, std::vector<int> &local_cols) {
+    const int n = d->n_local;
+    const long long nnz = d->rowptr[n];
+    local_cols.resize((size_t)nnz);
+    if (ctx->nranks == 1) {
+        for (long long p = 0; p < nnz; ++p) local_cols[p] = d->colidx[p];
+        return NPC_SUCCESS;
+    }
+    // partition: gather every rank's row_begin (collective)
+    DevBuf rs;
+    NPC_TRY(rs.alloc(sizeof(long long) * (ctx->nranks + 1)));
+    long long rb = d->row_begin;
+    NPC_CUDA_TRY(cudaMemcpyAsync(rs.as<long long>() + ctx->rank, &rb, sizeof(long long), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    NPC_NCCL_TRY(ncclAllGather(rs.as<long long>() + ctx->rank, rs.as<long long>(), 1, ncclInt64, ctx->comm, ctx->stream));
+    std::vector<long long> starts(ctx->nranks + 1);
+    NPC_CUDA_TRY(cudaMemcpyAsync(starts.data(), rs.as<long long>(), sizeof(long long) * ctx->nranks,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    starts[ctx->nranks] = d->n_global;
+    NPC_TRY(halo_plan_local(n, d->rowptr, d->colidx, ctx->nranks, starts.data(), ctx->rank, plan));
+    NPC_TRY(halo_plan_exchange(ctx, d->row_begin, plan));
+    const long long r0 = d->row_begin, r1 = d->row_begin + n;
+    for (long long p = 0; p < nnz; ++p) {
+        long long c = d->colidx[p];
+        if (c >= r0 && c < r1)
+            local_cols[p] = (int)(c - r0);
+        else {
+            auto it = std::lower_bound(plan.ghost_ids.begin(), plan.ghost_ids.end(), c);
+            local_cols[p] = n + (int)(it - plan.ghost_ids.begin());
+        }
+    }
+    return NPC_SUCCESS;
+}
+
+npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out) {
+    NPC_TRY(validate_csr_desc(ctx, d));
+    auto op = std::make_unique<CsrOperator>();
+    op->ctx = ctx;
+    op->kind = NPC_OP_CSR;
+    op->n_local = d->n_local;
+    op->n_global = d->n_global;
+    op->row_begin = d->row_begin;
+    const int n = d->n_local;
+    const long long nnz = d->rowptr[n];
+    op->nnz = nnz;
+    std::vector<int> lcols;
+    NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
+    op->multi = ctx->nranks > 1;
+    // tiles, spans, interior/boundary split
+    op->ntiles = ceil_div(n, CSR_TILE);
+    std::vector<int> ti, tb;
+    for (int t = 0; t < op->ntiles; ++t) {
+        int r0 = t * CSR_TILE, r1 = std::min(n, r0 + CSR_TILE);
+        int pb = d->rowptr[r0], pe = d->rowptr[r1];
+        op->vspan_max = std::max(op->vspan_max, ((pe + 1) & ~1) - (pb & ~1));
+        op->cspan_max = std::max(op->cspan_max, ((pe + 3) & ~3) - (pb & ~3));
+        bool ghost = false;
+        if (op->multi)
+            for (int p = pb; p < pe && !ghost; ++p) ghost = lcols[p] >= n;
+        (ghost ? tb : ti).push_back(t);
+    }
+    op->vspan_max = (op->vspan_max + 1) & ~1;
+    op->smem_bytes = (size_t)op->vspan_max * 8 + (size_t)op->cspan_max * 4 + 16;
+    op->staged = op->smem_bytes <= (size_t)CSR_MAX_SMEM;
+    op->n_interior = (int)ti.size();
+    op->n_boundary = (int)tb.size();
+    // upload (arrays padded so the aligned bulk copies never read past the allocation)
+    NPC_TRY(op->rowptr.alloc(sizeof(int) * (n + 1)));
+    NPC_TRY(op->cols.alloc(sizeof(int) * (nnz + 8)));
+    NPC_TRY(op->vals.alloc(sizeof(double) * (nnz + 8)));
+    NPC_CUDA_TRY(cudaMemcpy(op->rowptr.p, d->rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemset(op->cols.p, 0, op->cols.bytes));
+    NPC_CUDA_TRY(cudaMemset(op->vals.p, 0, op->vals.bytes));
+    if (nnz) {
+        NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op->vals.p, d->vals, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    }
+    if (op->multi) {
+        NPC_TRY(op->tiles_interior.alloc(sizeof(int) * std::max<size_t>(ti.size(), 1)));
+        NPC_TRY(op->tiles_boundary.alloc(sizeof(int) * std::max<size_t>(tb.size(), 1)));
+        if (!ti.empty())
+            NPC_CUDA_TRY(cudaMemcpy(op->tiles_interior.p, ti.data(), sizeof(int) * ti.size(), cudaMemcpyHostToDevice));
+        if (!tb.empty())
+            NPC_CUDA_TRY(cudaMemcpy(op->tiles_boundary.p, tb.data(), sizeof(int) * tb.size(), cudaMemcpyHostToDevice));
+        NPC_TRY(halo_setup(ctx, op->plan, op->halo));
+    }
+    out = std::move(op);
+    return NPC_SUCCESS;
+}
+
+}  // namespace npc

@@ -1,0 +1,228 @@
+// op_stencil.cu -- matrix-free constant-coefficient 2D 5-point / 3D 7-point Dirichlet
+// operator (BASELINE config 2) with the Chebyshev recurrence fused in.
+//
+// "only the application of the matrix to a vector is available as a routine (matrix-free
+// regime)".  Kernel: 32x8 threads own an (x, y) tile and march along z,
+// keeping x[z-1], x[z], x[z+1] in registers (2.5D blocking) so each plane of the input is
+// read from L2/HBM once; the in-plane neighbours come from L1.  Epilogue as in op_csr.cu.
+// Multi-rank: z-slabs; ghost planes z_begin-1 and z_end arrive through the generic halo
+// (planes are contiguous row ranges), overlapped with the interior planes.
+#include <algorithm>
+
+#include "device_util.cuh"
+#include "npc_internal.cuh"
+
+namespace npc {
+
+static constexpr int ST_BX = 32, ST_BY = 8, ST_ZC = 8;
+
+struct StencilDev {
+    int nx, ny, nzl;
+    double diag, off;
+    const double *glo;  // ghost plane below z = 0 (nullable)
+    const double *ghi;  // ghost plane above z = nzl-1 (nullable)
+};
+
+template <int DIM, bool HAS_S2, bool HAS_R, bool DOT>
+__global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, StepArgs s, int z_lo, int z_hi, int zc) {
+    if (s.done && *s.done) return;
+    __shared__ double red[ST_BX * ST_BY / 32];
+    const int x = blockIdx.x * ST_BX + threadIdx.x;
+    const int y = blockIdx.y * ST_BY + threadIdx.y;
+    const int z0 = z_lo + blockIdx.z * zc;
+    const int z1 = min(z0 + zc, z_hi);
+    const long long plane = (long long)S.nx * S.ny;
+    const double *__restrict__ X = s.x;
+    double acc = 0.0;
+    if (x < S.nx && y < S.ny && z0 < z1) {
+        const int pidx = x + S.nx * y;
+        long long i = pidx + plane * z0;
+        double below = 0.0, cur = X[i];
+        if (DIM == 3) {
+            if (z0 > 0)
+                below = X[i - plane];
+            else if (S.glo)
+                below = S.glo[pidx];
+        }
+        for (int z = z0; z < z1; ++z, i += plane) {
+            double above = 0.0;
+            if (DIM == 3) {
+                if (z + 1 < S.nzl)
+                    above = X[i + plane];
+                else if (S.ghi)
+                    above = S.ghi[pidx];
+            }
+            double nb = below;
+            if (y > 0) nb += X[i - S.nx];
+            if (x > 0) nb += X[i - 1];
+            if (x < S.nx - 1) nb += X[i + 1];
+            if (y < S.ny - 1) nb += X[i + S.nx];
+            nb += above;
+            const double ax = S.diag * cur + S.off * nb;
+            double o = s.a * ax + s.b * cur;
+            if (HAS_S2) o += s.c * s.s2[i];
+            if (HAS_R) o += s.d * s.r[i];
+            s.out[i] = o;
+            if (DOT) acc += o * s.dotv[i];
+            below = cur;
+            cur = above;
+        }
+    }
+    if (DOT) {
+        acc = block_sum<ST_BX * ST_BY>(acc, red);
+        if (threadIdx.x == 0 && threadIdx.y == 0) s.partials[linear_bid()] = acc;
+    }
+}
+
+class StencilOperator : public Operator {
+  public:
+    int dim = 3, nx = 0, ny = 0, nzg = 1, zb = 0, nzl = 1;
+    double diag = 0, off = 0;
+    bool multi = false, has_lo = false, has_hi = false;
+    HaloPlan plan;
+    HaloRuntime halo;
+
+    dim3 grid_for(int nplanes, int zc) const {
+        return dim3(ceil_div(nx, ST_BX), ceil_div(ny, ST_BY), std::max(1, ceil_div(nplanes, zc)));
+    }
+    int blocks_for(int nplanes, int zc) const {
+        dim3 g = grid_for(nplanes, zc);
+        return (int)(g.x * g.y * g.z);
+    }
+    int num_partials() const override {
+        if (!multi) return blocks_for(nzl, ST_ZC);
+        return blocks_for(std::max(nzl - 2, 0), ST_ZC) + 2 * blocks_for(1, 1);
+    }
+    double bytes_per_step(bool has_s2, bool has_r) const override {
+        double b = 2.0 * 8.0 * n_local;  // read x once, write out
+        if (has_s2) b += 8.0 * n_local;
+        if (has_r) b += 8.0 * n_local;
+        return b;
+    }
+
+    template <int D, bool H2, bool HR, bool DT>
+    npc_status launch_t(const StepArgs &s, int z_lo, int z_hi, int zc, double *partials) {
+        if (z_hi <= z_lo) return NPC_SUCCESS;
+        StencilDev S{nx, ny, nzl, diag, off, nullptr, nullptr};
+        if (multi) {
+            const double *g = halo.ghost_buf.as<double>();
+            S.glo = has_lo ? g : nullptr;
+            S.ghi = has_hi ? g + (has_lo ? (long long)nx * ny : 0) : nullptr;
+        }
+        StepArgs a = s;
+        a.partials = partials;
+        k_stencil_step<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(ST_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
+        NPC_LAUNCH_CHECK();
+        return NPC_SUCCESS;
+    }
+    template <int D>
+    npc_status launch_d(const StepArgs &s, int z_lo, int z_hi, int zc, double *p) {
+        const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
+        if (h2 && hr && dt) return launch_t<D, true, true, true>(s, z_lo, z_hi, zc, p);
+        if (h2 && hr) return launch_t<D, true, true, false>(s, z_lo, z_hi, zc, p);
+        if (h2 && dt) return launch_t<D, true, false, true>(s, z_lo, z_hi, zc, p);
+        if (h2) return launch_t<D, true, false, false>(s, z_lo, z_hi, zc, p);
+        if (hr && dt) return launch_t<D, false, true, true>(s, z_lo, z_hi, zc, p);
+        if (hr) return launch_t<D, false, true, false>(s, z_lo, z_hi, zc, p);
+        if (dt) return launch_t<D, false, false, true>(s, z_lo, z_hi, zc, p);
+        return launch_t<D, false, false, false>(s, z_lo, z_hi, zc, p);
+    }
+    npc_status launch(const StepArgs &s, int z_lo, int z_hi, int zc, double *p) {
+        return dim == 3 ? launch_d<3>(s, z_lo, z_hi, zc, p) : launch_d<2>(s, z_lo, z_hi, zc, p);
+    }
+
+    npc_status step(const StepArgs &s) override {
+        if (n_local == 0 && !multi) return NPC_SUCCESS;
+        if (!multi) return launch(s, 0, nzl, ST_ZC, s.partials);
+        NPC_TRY(halo_start(ctx, plan, halo, s.x));
+        double *p = s.partials;
+        const int nin = blocks_for(std::max(nzl - 2, 0), ST_ZC), nb1 = blocks_for(1, 1);
+        if (nzl > 2) NPC_TRY(launch(s, 1, nzl - 1, ST_ZC, p));
+        NPC_TRY(halo_wait(ctx, halo));
+        NPC_TRY(launch(s, 0, 1, 1, p ? p + nin : nullptr));
+        if (nzl > 1) NPC_TRY(launch(s, nzl - 1, nzl, 1, p ? p + nin + nb1 : nullptr));
+        else if (p) NPC_TRY(launch_fill(ctx, p + nin + nb1, 0.0, nb1));
+        if (p && nzl <= 2 && nin > 0) NPC_TRY(launch_fill(ctx, p, 0.0, nin));
+        return NPC_SUCCESS;
+    }
+};
+
+npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out) {
+    if (d->stencil_dim != 2 && d->stencil_dim != 3) {
+        set_error("stencil: dim must be 2 or 3");
+        return NPC_ERR_INVALID_ARGUMENT;
+    }
+    if (d->nx < 1 || d->ny < 1 || (d->stencil_dim == 3 && (d->nz_global < 1 || d->nz_local < 0 || d->z_begin < 0 ||
+                                                            d->z_begin + d->nz_local > d->nz_global))) {
+        set_error("stencil: invalid grid");
+        return NPC_ERR_DIMENSION;
+    }
+    if (!std::isfinite(d->diag) || !std::isfinite(d->offdiag)) {
+        set_error("stencil: non-finite coefficients");
+        return NPC_ERR_INVALID_ARGUMENT;
+    }
+    auto op = std::make_unique<StencilOperator>();
+    op->ctx = ctx;
+    op->kind = NPC_OP_STENCIL;
+    op->dim = d->stencil_dim;
+    op->nx = d->nx;
+    op->ny = d->ny;
+    op->nzg = d->stencil_dim == 3 ? d->nz_global : 1;
+    op->zb = d->stencil_dim == 3 ? d->z_begin : 0;
+    op->nzl = d->stencil_dim == 3 ? d->nz_local : 1;
+    op->diag = d->diag;
+    op->off = d->offdiag;
+    const long long plane = (long long)op->nx * op->ny;
+    if (plane * op->nzl >= (1LL << 31)) {
+        set_error("stencil: more than 2^31 local rows");
+        return NPC_ERR_UNSUPPORTED;
+    }
+    op->n_local = (int)(plane * op->nzl);
+    op->n_global = plane * op->nzg;
+    op->row_begin = plane * op->zb;
+    if (d->n_local != op->n_local || (d->n_global && d->n_global != op->n_global)) {
+        set_error("stencil: n_local/n_global disagree with the grid");
+        return NPC_ERR_DIMENSION;
+    }
+    if (ctx->nranks > 1) {
+        if (op->dim != 3) {
+            set_error("stencil: multi-rank needs dim 3 (z-slabs)");
+            return NPC_ERR_UNSUPPORTED;
+        }
+        op->multi = true;
+        // neighbours in z: the ranks owning plane zb-1 and plane zb+nzl (ranks ordered by z)
+        op->has_lo = op->zb > 0;
+        op->has_hi = op->zb + op->nzl < op->nzg;
+        HaloPlan &P = op->plan;
+        const int R = ctx->nranks, me = ctx->rank;
+        P.recv_count.assign(R, 0);
+        P.recv_off.assign(R, 0);
+        P.send_count.assign(R, 0);
+        P.send_off.assign(R, 0);
+        if ((op->has_lo && me == 0) || (op->has_hi && me == R - 1)) {
+            set_error("stencil: z-slabs must be assigned to ranks in z order");
+            return NPC_ERR_DIMENSION;
+        }
+        int off = 0;
+        if (op->has_lo) {
+            P.recv_count[me - 1] = (int)plane;
+            P.recv_off[me - 1] = 0;
+            P.send_count[me - 1] = (int)plane;
+            for (long long k = 0; k < plane; ++k) P.send_idx.push_back((int)k);
+            off = (int)plane;
+        }
+        if (op->has_hi) {
+            P.recv_count[me + 1] = (int)plane;
+            P.recv_off[me + 1] = off;
+            P.send_off[me + 1] = (int)P.send_idx.size();
+            P.send_count[me + 1] = (int)plane;
+            for (long long k = 0; k < plane; ++k) P.send_idx.push_back((int)(plane * (op->nzl - 1) + k));
+        }
+        P.n_ghost = off + (op->has_hi ? (int)plane : 0);
+        NPC_TRY(halo_setup(ctx, P, op->halo));
+    }
+    out = std::move(op);
+    return NPC_SUCCESS;
+}
+
+}  // namespace npc

@@ -1,0 +1,641 @@
+// solvers.cu -- drivers on top of the fused operator steps:
+//   * poly_coefficients / apply_poly: Alg. 2 with theta_bar (Eq. thetamod)
+//     rewritten as one fused step per degree, s_j = a_j A s_{j-1} + b_j s_{j-1} + c_j s_{j-2}
+//     + d_j r, in place over s_{j-2};
+//   * pcg: single-reduction (Chronopoulos-Gear) PCG with the inner products fused into the
+//     kernels that produce the vectors and device-resident scalars;
+//   * lanczos: the spectrum estimate + Sturm bisection on the host.
+#include <math.h>
+
+#include <algorithm>
+#include <chrono>
+
+#include "device_util.cuh"
+#include "npc_internal.cuh"
+
+namespace npc {
+
+// ================================================================== context helpers
+npc_status Context::ensure_partials(size_t n) {
+    if (n <= partial_cap) return NPC_SUCCESS;
+    size_t cap = std::max<size_t>(n, 4096);
+    NPC_TRY(partials.alloc(sizeof(double) * cap * 4));
+    partial_cap = cap;
+    return NPC_SUCCESS;
+}
+
+npc_status Context::allreduce_sum(double *dev, int count) {
+    if (nranks == 1) return NPC_SUCCESS;
+    NPC_NCCL_TRY(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, stream));
+    return NPC_SUCCESS;
+}
+
+// ================================================================== coefficients (host)
+// theta = (beta + alpha)/2, delta = (beta - alpha)/2, theta_bar =
+// theta (1 + xi) (Eq. thetamod; delta unchanged, reading A1), sigma =
+// theta_bar/delta, rho_0 = 1/sigma, rho_j = 1/(2 sigma - rho_{j-1}) (Eq. rhocheb).  From the
+// three-term form s_j = rho_j (2 sigma s_{j-1} - rho_{j-1} s_{j-2} + (2/delta)(r - A s_{j-1}))
+// (PAPER.md:262-266):  a_j = -2 rho_j/delta, b_j = 2 sigma rho_j, c_j = -rho_j rho_{j-1},
+// d_j = 2 rho_j/delta.
+npc_status poly_coefficients(int k, double lmin, double lmax, double xi, double *theta_bar, double *delta,
+                             double *sigma, double *coef) {
+    if (k < 0 || !(xi >= 0.0) || !std::isfinite(xi) || !(lmin > 0.0) || !std::isfinite(lmax) || lmax < lmin) {
+        set_error("set_poly: need degree >= 0, xi >= 0, 0 < lmin <= lmax (got k=%d, [%g, %g], xi=%g)", k, lmin, lmax, xi);
+        return NPC_ERR_INVALID_ARGUMENT;
+    }
+    const double theta = 0.5 * (lmax + lmin);
+    const double dl = 0.5 * (lmax - lmin);
+    if (!(dl > 0.0)) {
+        set_error("set_poly: degenerate interval lmin == lmax (delta = 0)");
+        return NPC_ERR_DEGENERATE_INTERVAL;
+    }
+    const double tb = theta * (1.0 + xi);
+    const double sg = tb / dl;
+    *theta_bar = tb;
+    *delta = dl;
+    *sigma = sg;
+    double rho_prev = 1.0 / sg;
+    for (int j = 1; j <= k; ++j) {
+        const double rho = 1.0 / (2.0 * sg - rho_prev);
+        if (coef) {
+            coef[4 * (j - 1) + 0] = -2.0 * rho / dl;
+            coef[4 * (j - 1) + 1] = 2.0 * sg * rho;
+            coef[4 * (j - 1) + 2] = -rho * rho_prev;
+            coef[4 * (j - 1) + 3] = 2.0 * rho / dl;
+        }
+        rho_prev = rho;
+    }
+    return NPC_SUCCESS;
+}
+
+// ================================================================== p_k(A) r
+// Internal-order application.  Buffers: z and tmp alternate so that s_k lands in z; s_j is
+// written over s_{j-2}.  j = 1 folds s_0 = r/theta_bar into the coefficients (reads only r),
+// j = 2 folds c_2 s_0 into the r term (no s_{j-2} read).  With dotv != null the last kernel
+// emits partials of <z, dotv> into 'partials' (count returned in *nparts).
+npc_status apply_poly_internal(npc_poly P, const double *r, double *z, const double *dotv, double *partials,
+                               int *nparts, const int *done) {
+    Operator *op = P->op->op.get();
+    Context *ctx = op->ctx;
+    const int k = P->degree;
+    const double tb = P->theta_bar;
+    if (k == 0) return launch_scale(ctx, r, z, 1.0 / tb, op->n_local, dotv, partials, nparts, done);
+    double *tmp = P->tmp.as<double>();
+    auto buf = [&](int j) { return ((k - j) % 2 == 0) ? z : tmp; };
+    for (int j = 1; j <= k; ++j) {
+        const double *cf = &P->coef[4 * (j - 1)];
+        StepArgs s;
+        s.done = done;
+        s.out = buf(j);
+        if (j == 1) {
+            s.x = r;
+            s.a = cf[0] / tb;
+            s.b = cf[1] / tb + cf[3];
+        } else if (j == 2) {
+            s.x = buf(1);
+            s.r = r;
+            s.a = cf[0];
+            s.b = cf[1];
+            s.d = cf[2] / tb + cf[3];
+        } else {
+            s.x = buf(j - 1);
+            s.s2 = buf(j);
+            s.r = r;
+            s.a = cf[0];
+            s.b = cf[1];
+            s.c = cf[2];
+            s.d = cf[3];
+        }
+        if (j == k && dotv) {
+            s.dotv = dotv;
+            s.partials = partials;
+            if (nparts) *nparts = op->num_partials();
+        }
+        NPC_TRY(op->step(s));
+    }
+    return NPC_SUCCESS;
+}
+
+npc_status apply_poly(npc_poly P, const double *r, double *z) {
+    Operator *op = P->op->op.get();
+    if (!op->permuted()) return apply_poly_internal(P, r, z, nullptr, nullptr, nullptr, nullptr);
+    NPC_TRY(op->to_internal(r, P->rin.as<double>()));
+    NPC_TRY(apply_poly_internal(P, P->rin.as<double>(), P->zout.as<double>(), nullptr, nullptr, nullptr, nullptr));
+    return op->to_external(P->zout.as<double>(), z);
+}
+
+npc_status apply_operator(Operator *op, const double *x, double *y, DevBuf &scratch) {
+    StepArgs s;
+    s.a = 1.0;
+    if (!op->permuted()) {
+        s.x = x;
+        s.out = y;
+        return op->step(s);
+    }
+    NPC_TRY(scratch.alloc(sizeof(double) * 2 * std::max(op->n_local, 1)));
+    double *xi = scratch.as<double>(), *yi = xi + std::max(op->n_local, 1);
+    NPC_TRY(op->to_internal(x, xi));
+    s.x = xi;
+    s.out = yi;
+    NPC_TRY(op->step(s));
+    return op->to_external(yi, y);
+}
+
+// ================================================================== PCG
+struct CgDev {
+    double gamma, gamma_old, delta, alpha, alpha_old, beta;
+    double rr, bnorm2, tol2;
+    int done, iters, maxit, breakdown, converged, first, multi, pad;
+};
+
+// sums[0] = <r, u> (gamma), sums[1] = <u, A u> (delta), sums[2] = ||r||^2 (multi-rank: of
+// the current r, reduced together with gamma and delta -- one allreduce per iteration).
+__global__ void k_cg_scalars(CgDev *st, const double *sums) {
+    if (st->done) return;
+    if (st->multi) {
+        st->rr = sums[2];
+        if (st->iters > 0 && st->rr <= st->tol2) {  // r_i converged: u_i, w_i are discarded
+            st->converged = 1;
+            st->done = 1;
+            return;
+        }
+        if (st->iters >= st->maxit) {
+            st->done = 1;
+            return;
+        }
+    }
+    const double g = sums[0], dl = sums[1];
+    if (!(g > 0.0)) {
+        st->breakdown = 1;
+        st->done = 1;
+        return;
+    }
+    double beta = 0.0, denom = dl;
+    if (!st->first) {
+        beta = g / st->gamma_old;
+        denom = dl - beta * g / st->alpha_old;
+    }
+    if (!(denom > 0.0)) {
+        st->breakdown = 2;
+        st->done = 1;
+        return;
+    }
+    const double alpha = g / denom;
+    st->gamma = g;
+    st->delta = dl;
+    st->beta = beta;
+    st->alpha = alpha;
+    st->gamma_old = g;
+    st->alpha_old = alpha;
+    st->first = 0;
+}
+
+// p = u + beta p; s = w + beta s; x += alpha p; r -= alpha s; partial ||r||^2.
+__global__ void __launch_bounds__(256) k_cg_update(const CgDev *st, const double *__restrict__ u,
+                                                   const double *__restrict__ w, double *__restrict__ p,
+                                                   double *__restrict__ s, double *__restrict__ x,
+                                                   double *__restrict__ r, int n, double *partials) {
+    if (st->done) return;
+    __shared__ double red[8];
+    const double alpha = st->alpha, beta = st->beta;
+    double acc = 0.0;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const double pi = u[i] + beta * p[i];
+        const double si = w[i] + beta * s[i];
+        p[i] = pi;
+        s[i] = si;
+        x[i] += alpha * pi;
+        const double ri = r[i] - alpha * si;
+        r[i] = ri;
+        acc += ri * ri;
+    }
+    acc = block_sum<256>(acc, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(1024) k_cg_rr(CgDev *st, const double *__restrict__ partials, int np,
+                                                double *sums, double *history) {
+    if (st->done) return;
+    __shared__ double red[32];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < np; i += 1024) t += partials[i];
+    t = block_sum<1024>(t, red);
+    if (threadIdx.x == 0) {
+        st->iters += 1;
+        sums[2] = t;
+        if (!st->multi) {
+            st->rr = t;
+            if (history) history[st->iters] = sqrt(t / st->bnorm2);
+            if (t <= st->tol2) {
+                st->converged = 1;
+                st->done = 1;
+            } else if (st->iters >= st->maxit) {
+                st->done = 1;
+            }
+        }
+    }
+}
+
+__global__ void k_cg_hist_multi(const CgDev *st, double *history) {
+    // multi-rank: the global ||r_i||^2 becomes known in k_cg_scalars of iteration i+1
+    if (history && st->iters > 0) history[st->iters] = sqrt(st->rr / st->bnorm2);
+}
+
+static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Device scalars area layout (ctx->scalars): [CgDev][sums: 8 doubles][history ...]
+npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, double tol, int maxit,
+               npc_pcg_stats *stats) {
+    const double t0 = now_s();
+    Operator *op = H->op.get();
+    Context *ctx = op->ctx;
+    const int n = op->n_local;
+    const int k = P ? P->degree : 0;
+    npc_pcg_stats st{};
+    double *host_hist = stats ? stats->history : nullptr;
+    // work vectors (internal order): b, x, r, u, w, p, s
+    DevBuf work;
+    const size_t nn = std::max(n, 1);
+    NPC_TRY(work.alloc(sizeof(double) * nn * 7));
+    double *b = work.as<double>(), *x = b + nn, *r = x + nn, *u = r + nn, *w = u + nn, *p = w + nn, *s = p + nn;
+    if (op->permuted()) {
+        NPC_TRY(op->to_internal(b_ext, b));
+        NPC_TRY(op->to_internal(x_ext, x));
+    } else {
+        NPC_CUDA_TRY(cudaMemcpyAsync(b, b_ext, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        NPC_CUDA_TRY(cudaMemcpyAsync(x, x_ext, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    NPC_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double) * n, ctx->stream));
+    NPC_CUDA_TRY(cudaMemsetAsync(s, 0, sizeof(double) * n, ctx->stream));
+    const int np_op = op->num_partials();
+    const int np_vec = vec_grid(n);
+    NPC_TRY(ctx->ensure_partials(std::max(np_op, np_vec)));
+    double *P0 = ctx->partial_slot(0), *P1 = ctx->partial_slot(1), *P2 = ctx->partial_slot(2);
+    DevBuf dev;
+    NPC_TRY(dev.alloc(sizeof(CgDev) + sizeof(double) * (8 + (size_t)maxit + 1)));
+    CgDev *cg = dev.as<CgDev>();
+    double *sums = reinterpret_cast<double *>(cg + 1);
+    double *dhist = sums + 8;
+
+    // x0 == 0 ?  ||x0||^2 together with ||b||^2
+    int npa = 0, npb = 0;
+    NPC_TRY(launch_dot(ctx, b, b, n, P0, &npa));
+    NPC_TRY(launch_dot(ctx, x, x, n, P1, &npb));
+    NPC_TRY(launch_reduce_sum(ctx, P0, npa, sums + 0, 1, P1, npb, sums + 1));
+    NPC_TRY(ctx->allreduce_sum(sums, 2));
+    double h2[2];
+    NPC_CUDA_TRY(cudaMemcpyAsync(h2, sums, sizeof(h2), cudaMemcpyDeviceToHost, ctx->stream));
+    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    st.reductions += 1;
+    const double bnorm2 = h2[0];
+    const bool x0_nonzero = h2[1] != 0.0;
+    auto finish_true_residual = [&](double *relres) -> npc_status {
+        // r_true = b - A x  (u as scratch), ||r_true||^2
+        StepArgs t;
+        t.x = x;
+        t.r = b;
+        t.out = u;
+        t.a = -1.0;
+        t.d = 1.0;
+        NPC_TRY(op->step(t));
+        st.op_applications += 1;
+        int np = 0;
+        NPC_TRY(launch_dot(ctx, u, u, n, P0, &np));
+        NPC_TRY(launch_reduce_sum(ctx, P0, np, sums + 3));
+        NPC_TRY(ctx->allreduce_sum(sums + 3, 1));
+        st.reductions += 1;
+        double tr;
+        NPC_CUDA_TRY(cudaMemcpyAsync(&tr, sums + 3, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        *relres = sqrt(tr / bnorm2);
+        return NPC_SUCCESS;
+    };
+    auto export_x = [&]() -> npc_status {
+        if (op->permuted()) return op->to_external(x, x_ext);
+        NPC_CUDA_TRY(cudaMemcpyAsync(x_ext, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        return NPC_SUCCESS;
+    };
+    npc_status result = NPC_SUCCESS;
+    if (bnorm2 == 0.0) {  // b = 0 -> x = 0
+        NPC_CUDA_TRY(cudaMemsetAsync(x_ext, 0, sizeof(double) * n, ctx->stream));
+        NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        st.converged = 1;
+        st.solve_seconds = now_s() - t0;
+        if (stats) {
+            double *hh = stats->history;
+            *stats = st;
+            stats->history = hh;
+            if (hh) hh[0] = 0.0;
+        }
+        return NPC_SUCCESS;
+    }
+    // r0 = b - A x0 (or b)
+    if (x0_nonzero) {
+        StepArgs t;
+        t.x = x;
+        t.r = b;
+        t.out = r;
+        t.a = -1.0;
+        t.d = 1.0;
+        NPC_TRY(op->step(t));
+        st.op_applications += 1;
+    } else {
+        NPC_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    {
+        int np = 0;
+        NPC_TRY(launch_dot(ctx, r, r, n, P0, &np));
+        NPC_TRY(launch_reduce_sum(ctx, P0, np, sums + 2));
+        NPC_TRY(ctx->allreduce_sum(sums + 2, 1));
+        st.reductions += 1;
+    }
+    double rr0;
+    NPC_CUDA_TRY(cudaMemcpyAsync(&rr0, sums + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::vector<double> hist_host;
+    if (host_hist) host_hist[0] = sqrt(rr0 / bnorm2);
+    CgDev h{};
+    h.rr = rr0;
+    h.bnorm2 = bnorm2;
+    h.tol2 = tol * tol * bnorm2;
+    h.maxit = maxit;
+    h.first = 1;
+    h.multi = ctx->nranks > 1;
+    bool done = rr0 <= h.tol2;
+    st.relres_recursive = sqrt(rr0 / bnorm2);
+    if (done) {
+        double tr;
+        NPC_TRY(finish_true_residual(&tr));
+        if (tr <= tol) {
+            st.converged = 1;
+            st.relres_true = tr;
+            NPC_TRY(export_x());
+            NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            st.solve_seconds = now_s() - t0;
+            if (stats) {
+                double *hh = stats->history;
+                *stats = st;
+                stats->history = hh;
+            }
+            return NPC_SUCCESS;
+        }
+        NPC_CUDA_TRY(cudaMemcpyAsync(r, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        h.rr = tr * tr * bnorm2;
+    }
+    NPC_CUDA_TRY(cudaMemcpyAsync(cg, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+    NPC_CUDA_TRY(cudaMemcpyAsync(sums + 2, &h.rr, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const int *dflag = &cg->done;
+    int chunk = 4;
+    int true_checks = 0;
+    for (;;) {
+        for (int it = 0; it < chunk; ++it) {
+            // u = p_k(A) r  with partials of gamma = <u, r>
+            int npg = 0;
+            if (P)
+                NPC_TRY(apply_poly_internal(P, r, u, r, P0, &npg, dflag));
+            else
+                NPC_TRY(launch_scale(ctx, r, u, 1.0, n, r, P0, &npg, dflag));
+            // w = A u with partials of delta = <w, u>
+            StepArgs t;
+            t.x = u;
+            t.out = w;
+            t.a = 1.0;
+            t.dotv = u;
+            t.partials = P1;
+            t.done = dflag;
+            NPC_TRY(op->step(t));
+            NPC_TRY(launch_reduce_sum(ctx, P0, npg, sums + 0, 1, P1, np_op, sums + 1));
+            NPC_TRY(ctx->allreduce_sum(sums, 3));  // the single global reduction
+            k_cg_scalars<<<1, 1, 0, ctx->stream>>>(cg, sums);
+            NPC_LAUNCH_CHECK();
+            if (h.multi) {
+                k_cg_hist_multi<<<1, 1, 0, ctx->stream>>>(cg, dhist);
+                NPC_LAUNCH_CHECK();
+            }
+            k_cg_update<<<np_vec, 256, 0, ctx->stream>>>(cg, u, w, p, s, x, r, n, P2);
+            NPC_LAUNCH_CHECK();
+            k_cg_rr<<<1, 1024, 0, ctx->stream>>>(cg, P2, np_vec, sums, dhist);
+            NPC_LAUNCH_CHECK();
+        }
+        NPC_CUDA_TRY(cudaMemcpyAsync(&h, cg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (!h.done) {
+            chunk = std::min(chunk * 2, 64);
+            continue;
+        }
+        st.iters = h.iters;
+        st.relres_recursive = sqrt(h.rr / bnorm2);
+        if (h.breakdown) {
+            set_error("PCG breakdown (%s <= 0) at iteration %d", h.breakdown == 1 ? "<r,z>" : "<p,Ap>", h.iters);
+            result = NPC_ERR_BREAKDOWN;
+            break;
+        }
+        if (h.converged) {
+            double tr;
+            NPC_TRY(finish_true_residual(&tr));
+            st.relres_true = tr;
+            if (tr <= tol || ++true_checks > 50) {
+                st.converged = tr <= tol;
+                if (!st.converged) {
+                    set_error("true residual %.3e stays above tol after %d replacements", tr, true_checks - 1);
+                    result = NPC_ERR_NOT_CONVERGED;
+                }
+                break;
+            }
+            // residual replacement (reading A23): r = b - A x, continue
+            NPC_CUDA_TRY(cudaMemcpyAsync(r, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+            h.rr = tr * tr * bnorm2;
+            h.converged = 0;
+            h.done = 0;
+            NPC_CUDA_TRY(cudaMemcpyAsync(cg, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+            NPC_CUDA_TRY(cudaMemcpyAsync(sums + 2, &h.rr, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            if (h.iters >= maxit) {
+                result = NPC_ERR_NOT_CONVERGED;
+                break;
+            }
+            chunk = 1;
+            continue;
+        }
+        // maxit
+        double tr;
+        NPC_TRY(finish_true_residual(&tr));
+        st.relres_true = tr;
+        set_error("PCG did not converge in %d iterations (relres %.3e)", maxit, st.relres_recursive);
+        result = NPC_ERR_NOT_CONVERGED;
+        break;
+    }
+    // counters: k+1 applications per x-update (Table tab11 law); multi-rank detects
+    // convergence one block late (u, w of the next iteration are formed and discarded)
+    st.op_applications += (long long)h.iters * (k + 1) + ((h.multi && h.converged) ? (k + 1) : 0);
+    st.reductions += h.iters + ((h.multi && h.converged) ? 1 : 0);
+    if (host_hist && h.iters > 0)
+        NPC_CUDA_TRY(cudaMemcpyAsync(host_hist + 1, dhist + 1, sizeof(double) * h.iters, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    NPC_TRY(export_x());
+    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    st.solve_seconds = now_s() - t0;
+    if (stats) {
+        double *hh = stats->history;
+        *stats = st;
+        stats->history = hh;
+    }
+    return result;
+}
+
+// ================================================================== Lanczos
+struct LzDev {
+    double vn2;
+    int steps, stop;
+};
+
+__global__ void k_lz_scale_init(const double *v0, double *q, double *qprev, int n, const double *vn2) {
+    const double inv = 1.0 / sqrt(*vn2);
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        q[i] = v0[i] * inv;
+        qprev[i] = 0.0;
+    }
+}
+
+// mode 0: w -= beta_prev q_prev ; partial <q, w>
+// mode 1: w -= alpha q          ; partial <w, w>
+template <int MODE>
+__global__ void __launch_bounds__(256) k_lz_axpy(double *__restrict__ w, const double *__restrict__ v,
+                                                 const double *__restrict__ q, const double *coef, int n,
+                                                 double *partials, const LzDev *lz) {
+    if (lz->stop) return;
+    __shared__ double red[8];
+    const double cf = coef ? *coef : 0.0;
+    double acc = 0.0;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const double wi = w[i] - cf * v[i];
+        w[i] = wi;
+        acc += (MODE == 0 ? q[i] : wi) * wi;
+    }
+    acc = block_sum<256>(acc, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+__global__ void k_lz_beta(LzDev *lz, double *betas, int j, const double *sum) {
+    if (lz->stop) return;
+    const double b = sqrt(*sum);
+    betas[j] = b;
+    lz->steps = j + 1;
+    if (b == 0.0) lz->stop = 1;
+}
+
+__global__ void k_lz_next(const LzDev *lz, const double *w, double *q, double *qprev, const double *beta, int n) {
+    if (lz->stop) return;
+    const double inv = 1.0 / *beta;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        qprev[i] = q[i];
+        q[i] = w[i] * inv;
+    }
+}
+
+// Number of eigenvalues of the symmetric tridiagonal T (diag a, offdiag b) below x.
+static int sturm_count(const std::vector<double> &a, const std::vector<double> &b, double x) {
+    int cnt = 0;
+    double d = 1.0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        const double off2 = i ? b[i - 1] * b[i - 1] : 0.0;
+        d = a[i] - x - (i ? off2 / d : 0.0);
+        if (d == 0.0) d = -1e-300;
+        if (d < 0.0) ++cnt;
+    }
+    return cnt;
+}
+
+static double tridiag_eig(const std::vector<double> &a, const std::vector<double> &b, int idx) {
+    double lo = 1e300, hi = -1e300;
+    for (size_t i = 0; i < a.size(); ++i) {  // Gershgorin
+        double r = (i ? fabs(b[i - 1]) : 0.0) + (i + 1 < a.size() ? fabs(b[i]) : 0.0);
+        lo = std::min(lo, a[i] - r);
+        hi = std::max(hi, a[i] + r);
+    }
+    for (int it = 0; it < 200 && hi - lo > 1e-16 * std::max(fabs(lo), fabs(hi)); ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        if (sturm_count(a, b, mid) > idx)
+            hi = mid;
+        else
+            lo = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, double *lmax) {
+    Context *ctx = op->ctx;
+    const int n = op->n_local;
+    const size_t nn = std::max(n, 1);
+    DevBuf work, dev;
+    NPC_TRY(work.alloc(sizeof(double) * nn * 4));
+    double *q = work.as<double>(), *qp = q + nn, *w = qp + nn, *v0 = w + nn;
+    if (v0_ext) {
+        if (op->permuted())
+            NPC_TRY(op->to_internal(v0_ext, v0));
+        else
+            NPC_CUDA_TRY(cudaMemcpyAsync(v0, v0_ext, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+        NPC_TRY(launch_hash_vector(ctx, w, n, op->row_begin, 0x5EEDull));
+        if (op->permuted())
+            NPC_TRY(op->to_internal(w, v0));
+        else
+            NPC_CUDA_TRY(cudaMemcpyAsync(v0, w, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    NPC_TRY(dev.alloc(sizeof(LzDev) + sizeof(double) * (2 * (size_t)m + 8)));
+    LzDev *lz = dev.as<LzDev>();
+    double *alphas = reinterpret_cast<double *>(lz + 1), *betas = alphas + m, *sums = betas + m;
+    NPC_CUDA_TRY(cudaMemsetAsync(dev.p, 0, dev.bytes, ctx->stream));
+    const int npv = vec_grid(n);
+    NPC_TRY(ctx->ensure_partials(std::max(npv, op->num_partials())));
+    double *P0 = ctx->partial_slot(0);
+    int np = 0;
+    NPC_TRY(launch_dot(ctx, v0, v0, n, P0, &np));
+    NPC_TRY(launch_reduce_sum(ctx, P0, np, &lz->vn2));
+    NPC_TRY(ctx->allreduce_sum(&lz->vn2, 1));
+    double vn2;
+    NPC_CUDA_TRY(cudaMemcpyAsync(&vn2, &lz->vn2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (!(vn2 > 0.0)) {
+        set_error("estimate_spectrum: start vector is zero");
+        return NPC_ERR_INVALID_ARGUMENT;
+    }
+    k_lz_scale_init<<<npv, 256, 0, ctx->stream>>>(v0, q, qp, n, &lz->vn2);
+    NPC_LAUNCH_CHECK();
+    for (int j = 0; j < m; ++j) {
+        StepArgs s;
+        s.x = q;
+        s.out = w;
+        s.a = 1.0;
+        s.done = &lz->stop;
+        NPC_TRY(op->step(s));
+        k_lz_axpy<0><<<npv, 256, 0, ctx->stream>>>(w, qp, q, j ? &betas[j - 1] : nullptr, n, P0, lz);
+        NPC_LAUNCH_CHECK();
+        NPC_TRY(launch_reduce_sum(ctx, P0, npv, &alphas[j]));
+        NPC_TRY(ctx->allreduce_sum(&alphas[j], 1));
+        k_lz_axpy<1><<<npv, 256, 0, ctx->stream>>>(w, q, nullptr, &alphas[j], n, P0, lz);
+        NPC_LAUNCH_CHECK();
+        NPC_TRY(launch_reduce_sum(ctx, P0, npv, &sums[0]));
+        NPC_TRY(ctx->allreduce_sum(&sums[0], 1));
+        k_lz_beta<<<1, 1, 0, ctx->stream>>>(lz, betas, j, &sums[0]);
+        NPC_LAUNCH_CHECK();
+        k_lz_next<<<npv, 256, 0, ctx->stream>>>(lz, w, q, qp, &betas[j], n);
+        NPC_LAUNCH_CHECK();
+    }
+    LzDev hl;
+    std::vector<double> ha(m), hb(m);
+    NPC_CUDA_TRY(cudaMemcpyAsync(&hl, lz, sizeof(hl), cudaMemcpyDeviceToHost, ctx->stream));
+    NPC_CUDA_TRY(cudaMemcpyAsync(ha.data(), alphas, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    NPC_CUDA_TRY(cudaMemcpyAsync(hb.data(), betas, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const int sN = std::max(1, hl.steps);
+    ha.resize(sN);
+    hb.resize(sN > 1 ? sN - 1 : 0);
+    *lmin = tridiag_eig(ha, hb, 0);
+    *lmax = tridiag_eig(ha, hb, sN - 1);
+    return NPC_SUCCESS;
+}
+
+}  // namespace npc
