@@ -2,7 +2,7 @@
 """bench.py -- the north-star measurement: p_k(A) v GB/s and PCG time-to-tol (fp64) on B200.
 
 One STEP = one pass of the whole hot path over the workload:
-    npc_estimate_spectrum (20 Lanczos steps from b)  ->  npc_set_poly(k, lmin, lmax, xi)
+    npc_estimate_spectrum (20 Lanczos steps, counter-hash start)  ->  npc_set_poly(k, lmin, lmax, xi)
     -> npc_pcg_solve(b, x0 = 0, tol)   [k fused degree kernels + 1 SpMV + update per iteration]
 on config 3 of BASELINE.json (3D 7-point variable-coefficient diffusion, 256^3, CSR, b = A 1,
 tol 1e-8) at N = 1; `--config` selects another.  The operator is created (a0, setup) before the
@@ -228,7 +228,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def step(bb, xx):
-        lo, hi = npc.npc_estimate_spectrum(op, lz_steps, bb)
+        lo, hi = npc.npc_estimate_spectrum(op, lz_steps, None)
         poly = npc.npc_set_poly(op, k, lo, hi, xi)
         xx.zero_()
         st = npc.npc_pcg_solve(poly, op, bb, xx, tol, maxit)
@@ -302,7 +302,7 @@ def run_ours(args):
             op2, _, _ = create_operator(npc, ctx, w, kind, ws, rank, cfg)
             bd = b_pin.to("cuda", non_blocking=True)
             xd = torch.empty(nl, dtype=torch.float64, device="cuda")
-            lo2, hi2 = npc.npc_estimate_spectrum(op2, lz_steps, bd)
+            lo2, hi2 = npc.npc_estimate_spectrum(op2, lz_steps, None)
             p2 = npc.npc_set_poly(op2, k, lo2, hi2, xi)
             xd.zero_()
             npc.npc_pcg_solve(p2, op2, bd, xd, tol, maxit)
@@ -388,8 +388,8 @@ def run_reference(args):
     kind = args.kind or op_kind(w, cfg)
     k = args.k if args.k is not None else w["k"]
     orc = oracle.Operator(w)
-    # the oracle's own interval (20 Lanczos steps from b), as in the GPU arm
-    lo, hi = oracle.estimate_spectrum(orc, w.get("lanczos_steps", 20), w["b"])
+    # the oracle's own interval (20 Lanczos steps from the counter-hash start), as in the GPU arm
+    lo, hi = oracle.estimate_spectrum(orc, w.get("lanczos_steps", 20), W.lanczos_start(w["n"]))
     M = matrix_bytes(w, kind)
     V = 8 * w["n"]
     r = np.asarray(w["b"], dtype=np.float64)

@@ -124,11 +124,19 @@ NPC_API npc_status npc_destroy_operator(npc_operator op);
 NPC_API npc_status npc_apply_operator(npc_operator op, const double *x_dev, double *y_dev);
 
 /* ---- spectrum estimate (replaces the paper's DACG) ---------------------
- * nsteps-step Lanczos from v0_dev (NULL -> a deterministic counter-hash vector in [-1,1]),
- * no reorthogonalisation; *lmin/*lmax = extreme Ritz values of T_nsteps (Sturm bisection).
- * Stops early (and succeeds) on an exact invariant subspace.  COLLECTIVE.                  */
+ * nsteps-step Lanczos (no reorthogonalisation) from v0_dev, or, when v0_dev is NULL, from the
+ * counter-hash vector uniform[-1,1) (splitmix64 of seed 0x5EED and the GLOBAL row index + 1,
+ * so every partition draws the same vector; workloads.lanczos_start is the same generator).
+ * *lmin = smallest Ritz value of T_s (an over-estimate of lambda_min: harmless for the
+ * polynomial); *lmax = theta_max + rho, the largest Ritz value plus its residual norm
+ * rho = beta_s |e_s^T s| -- an upper estimate of lambda_max, because an interval that misses
+ * the top of the spectrum makes p_k(A) grow like T_{k+1} there (reading A11).
+ * Stops early (and succeeds, rho = 0) on an exact invariant subspace.  COLLECTIVE.
+ * The _ex variant writes {theta_min, theta_max, rho, steps taken} to out4 (host).          */
 NPC_API npc_status npc_estimate_spectrum(npc_operator op, int nsteps, const double *v0_dev,
                                  double *lmin, double *lmax);
+NPC_API npc_status npc_estimate_spectrum_ex(npc_operator op, int nsteps, const double *v0_dev,
+                                    double *out4);
 
 /* ---- polynomial preconditioner (Alg. 2) --------------------------------
  * degree k >= 0 (k applications of A per npc_apply_poly), interval [lmin, lmax] with

@@ -180,8 +180,23 @@ def ritz_extremes(alphas, betas):
     return float(ev[0]), float(ev[-1])
 
 
+def ritz_upper(alphas, betas):
+    """(theta_max, rho): the largest Ritz value of T_s and its residual norm
+    ||A y - theta y|| = beta_s |e_s^T s| (s = normalised eigenvector of T_s for theta_max;
+    beta_s = the last Lanczos beta, 0 on an invariant subspace).  theta_max + rho is the
+    upper estimate of lambda_max used for the polynomial interval (reading A11)."""
+    from scipy.linalg import eigh_tridiagonal
+    s = len(alphas)
+    ev, vec = eigh_tridiagonal(alphas, betas[: s - 1], select="i", select_range=(s - 1, s - 1))
+    return float(ev[0]), float(abs(betas[s - 1]) * abs(vec[-1, 0]))
+
+
 def estimate_spectrum(op: Operator, m, v0):
-    return ritz_extremes(*lanczos(op, m, v0))
+    """(lmin, lmax) for the polynomial: lmin = smallest Ritz value, lmax = theta_max + rho."""
+    a, b = lanczos(op, m, v0)
+    lo, _ = ritz_extremes(a, b)
+    th, rho = ritz_upper(a, b)
+    return lo, th + rho
 
 
 def pcg(op: Operator, b, m, alpha=None, beta=None, xi=0.0, tol=1e-8, maxit=10000, x0=None,

@@ -77,6 +77,7 @@ def lib():
             "npc_destroy_operator": [P],
             "npc_apply_operator": [P, P, P],
             "npc_estimate_spectrum": [P, I, P, C.POINTER(D), C.POINTER(D)],
+            "npc_estimate_spectrum_ex": [P, I, P, P],
             "npc_set_poly": [P, I, D, D, D, C.POINTER(P)],
             "npc_destroy_poly": [P],
             "npc_apply_poly": [P, P, P],
@@ -223,6 +224,13 @@ def npc_estimate_spectrum(op: Operator, nsteps: int = 20, v0=None):
     lo, hi = C.c_double(), C.c_double()
     _check(lib().npc_estimate_spectrum(op.h, int(nsteps), _ptr(v0), C.byref(lo), C.byref(hi)))
     return lo.value, hi.value
+
+
+def npc_estimate_spectrum_ex(op: Operator, nsteps: int = 20, v0=None):
+    """-> dict(theta_min, theta_max, rho, steps)."""
+    out = np.zeros(4)
+    _check(lib().npc_estimate_spectrum_ex(op.h, int(nsteps), _ptr(v0), out.ctypes.data_as(C.c_void_p)))
+    return dict(theta_min=out[0], theta_max=out[1], rho=out[2], steps=int(out[3]))
 
 
 class Poly:

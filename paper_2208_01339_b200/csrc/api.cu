@@ -21,7 +21,7 @@ npc_status poly_coefficients(int k, double lmin, double lmax, double xi, double 
 npc_status apply_poly(npc_poly P, const double *r, double *z);
 npc_status apply_operator(Operator *op, const double *x, double *y, DevBuf &scratch);
 npc_status pcg(npc_poly P, npc_operator H, const double *b, double *x, double tol, int maxit, npc_pcg_stats *stats);
-npc_status lanczos(Operator *op, int m, const double *v0, double *lmin, double *lmax);
+npc_status lanczos(Operator *op, int m, const double *v0, double *lmin, double *lmax, double *out_ex);
 }  // namespace npc
 
 using namespace npc;
@@ -173,7 +173,16 @@ npc_status npc_estimate_spectrum(npc_operator op, int nsteps, const double *v0_d
     NPC_GUARD(nsteps >= 1 && nsteps <= 100000, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum: nsteps %d", nsteps);
     NPC_GUARD(op->op->n_global >= 1, NPC_ERR_DIMENSION, "npc_estimate_spectrum: empty operator");
     DeviceScope ds(op->owner->ctx.device);
-    return lanczos(op->op.get(), nsteps, v0_dev, lmin, lmax);
+    return lanczos(op->op.get(), nsteps, v0_dev, lmin, lmax, nullptr);
+}
+
+npc_status npc_estimate_spectrum_ex(npc_operator op, int nsteps, const double *v0_dev, double *out4) {
+    NPC_GUARD(op && out4, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum_ex: null argument");
+    NPC_GUARD(nsteps >= 1 && nsteps <= 100000, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum_ex: nsteps %d", nsteps);
+    NPC_GUARD(op->op->n_global >= 1, NPC_ERR_DIMENSION, "npc_estimate_spectrum_ex: empty operator");
+    DeviceScope ds(op->owner->ctx.device);
+    double lo, hi;
+    return lanczos(op->op.get(), nsteps, v0_dev, &lo, &hi, out4);
 }
 
 npc_status npc_poly_coefficients(int degree, double lmin, double lmax, double xi, double *theta_bar, double *delta,

@@ -14,10 +14,20 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Linear thread index / block id for 3D grids.
+__device__ __forceinline__ int linear_tid() {
+    return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+}
+__device__ __forceinline__ int linear_bid() {
+    return blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+}
+
+// NT = threads per block; works for 1D/2D/3D blocks (linear thread index).
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double *red /* >= NT/32 doubles */) {
     v = warp_sum(v);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tid = linear_tid();
+    const int lane = tid & 31, warp = tid >> 5;
     if (lane == 0) red[warp] = v;
     __syncthreads();
     double t = 0.0;
@@ -28,13 +38,6 @@ __device__ __forceinline__ double block_sum(double v, double *red /* >= NT/32 do
     return t;  // valid in thread 0
 }
 
-// Linear thread index / block id for 3D grids.
-__device__ __forceinline__ int linear_tid() {
-    return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-}
-__device__ __forceinline__ int linear_bid() {
-    return blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-}
 
 // ------------------------------------------------------------------ bulk TMA (1D)
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

@@ -565,7 +565,54 @@ static double tridiag_eig(const std::vector<double> &a, const std::vector<double
     return 0.5 * (lo + hi);
 }
 
-npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, double *lmax) {
+// Solve (T - mu I) x = x (in place) for the symmetric tridiagonal T (diag a, offdiag b) by
+// Gaussian elimination with partial pivoting (the dgttrf/dgttrs scheme).
+static void tridiag_shift_solve(const std::vector<double> &a, const std::vector<double> &b, double mu,
+                                std::vector<double> &x) {
+    const int m = (int)a.size();
+    std::vector<double> d(m), du(m, 0.0), du2(m, 0.0), dl(m, 0.0);
+    std::vector<char> swp(m, 0);
+    const double tiny = 1e-300 + 1e-16 * (fabs(mu) + 1e-300);
+    for (int i = 0; i < m; ++i) {
+        d[i] = a[i] - mu;
+        if (i + 1 < m) du[i] = dl[i] = b[i];
+    }
+    for (int i = 0; i + 1 < m; ++i) {
+        if (fabs(d[i]) >= fabs(dl[i])) {
+            if (d[i] == 0.0) d[i] = tiny;
+            const double f = dl[i] / d[i];
+            dl[i] = f;
+            d[i + 1] -= f * du[i];
+        } else {
+            const double f = d[i] / dl[i];
+            d[i] = dl[i];
+            dl[i] = f;
+            const double t = du[i];
+            du[i] = d[i + 1];
+            d[i + 1] = t - f * d[i + 1];
+            if (i + 2 < m) {
+                du2[i] = du[i + 1];
+                du[i + 1] = -f * du[i + 1];
+            }
+            swp[i] = 1;
+        }
+    }
+    if (d[m - 1] == 0.0) d[m - 1] = tiny;
+    for (int i = 0; i + 1 < m; ++i) {
+        if (!swp[i]) {
+            x[i + 1] -= dl[i] * x[i];
+        } else {
+            const double t = x[i];
+            x[i] = x[i + 1];
+            x[i + 1] = t - dl[i] * x[i];
+        }
+    }
+    x[m - 1] /= d[m - 1];
+    if (m > 1) x[m - 2] = (x[m - 2] - du[m - 2] * x[m - 1]) / d[m - 2];
+    for (int i = m - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / d[i];
+}
+
+npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, double *lmax, double *out_ex) {
     Context *ctx = op->ctx;
     const int n = op->n_local;
     const size_t nn = std::max(n, 1);
@@ -631,10 +678,34 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, doub
     NPC_CUDA_TRY(cudaMemcpyAsync(hb.data(), betas, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
     NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     const int sN = std::max(1, hl.steps);
+    const double beta_last = hb[sN - 1];
     ha.resize(sN);
     hb.resize(sN > 1 ? sN - 1 : 0);
-    *lmin = tridiag_eig(ha, hb, 0);
-    *lmax = tridiag_eig(ha, hb, sN - 1);
+    const double th_min = tridiag_eig(ha, hb, 0);
+    const double th_max = tridiag_eig(ha, hb, sN - 1);
+    // Ritz residual of the top pair: ||A y - theta y|| = beta_s |e_s^T s|, s from inverse
+    // iteration on T_s - theta I (tridiagonal LU with partial pivoting).
+    double rho = 0.0;
+    if (hl.stop == 0 && beta_last > 0.0) {
+        std::vector<double> x(sN, 1.0);
+        for (int it = 0; it < 3; ++it) {
+            tridiag_shift_solve(ha, hb, th_max, x);
+            double nrm = 0.0;
+            for (double v : x) nrm += v * v;
+            nrm = sqrt(nrm);
+            if (!(nrm > 0.0) || !std::isfinite(nrm)) break;
+            for (double &v : x) v /= nrm;
+        }
+        rho = beta_last * fabs(x[sN - 1]);
+    }
+    if (out_ex) {
+        out_ex[0] = th_min;
+        out_ex[1] = th_max;
+        out_ex[2] = rho;
+        out_ex[3] = (double)hl.steps;
+    }
+    *lmin = th_min;
+    *lmax = th_max + rho;
     return NPC_SUCCESS;
 }
 

@@ -85,7 +85,7 @@ def test_operator_apply(ctx, wl, name, kind):
 def test_apply_poly_parity(ctx, wl, name, kind, k, xi):
     w = wl(name)
     orc = oracle.Operator(w)
-    lmin, lmax = oracle.estimate_spectrum(orc, 20, w["b"])  # oracle's interval on both sides (A11)
+    lmin, lmax = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))  # oracle's interval, both sides (A11)
     op = npc.create_from_workload(ctx, w, kind)
     poly = npc.npc_set_poly(op, k, lmin, lmax, xi)
     r = np.random.default_rng(11).uniform(-1, 1, w["n"])
@@ -96,22 +96,35 @@ def test_apply_poly_parity(ctx, wl, name, kind, k, xi):
 
 
 @pytest.mark.parametrize("name,kind", [("c1", "csr"), ("c2", "stencil"), ("c3", "csr"), ("c4", "sell"),
-                                       ("c5", "schur")])
+                                       ("c5", "schur"), ("c3", "sell")])
 def test_lanczos_parity(ctx, wl, name, kind):
     w = wl(name)
     orc = oracle.Operator(w)
-    lo_o, hi_o = oracle.estimate_spectrum(orc, 20, w["b"])
+    v0 = W.lanczos_start(w["n"])
+    a, b = oracle.lanczos(orc, 20, v0)
+    lo_o, _ = oracle.ritz_extremes(a, b)
+    th_o, rho_o = oracle.ritz_upper(a, b)
     op = npc.create_from_workload(ctx, w, kind)
-    lo, hi = npc.npc_estimate_spectrum(op, 20, dev(w["b"]))
-    # lambda_max has converged after 20 steps: unique to rounding.  lambda_min has not, and
-    # Lanczos without reorthogonalisation amplifies rounding once orthogonality is lost, so
-    # the bar is the oracle's own sensitivity to a 1e-15 relative perturbation of v0 (x20).
-    assert abs(hi - hi_o) <= 1e-10 * abs(hi_o)
-    spread = 0.0
+    ex = npc.npc_estimate_spectrum_ex(op, 20, dev(v0))
+    ex0 = npc.npc_estimate_spectrum_ex(op, 20, None)  # default start = the same counter hash
+    if kind != "schur":  # Schur's B^T pass uses fp64 atomics: run-to-run rounding differs
+        assert ex0 == ex
+    for key in ("theta_min", "theta_max", "rho"):
+        assert abs(ex0[key] - ex[key]) <= 1e-9 * abs(ex["theta_max"])
+    lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+    assert lo == ex["theta_min"] and hi == ex["theta_max"] + ex["rho"]
+    # theta_max has converged after 20 steps: unique to rounding.  theta_min and rho have not,
+    # and Lanczos without reorthogonalisation amplifies rounding once orthogonality is lost,
+    # so their bar is the oracle's own sensitivity to a 1e-15 relative perturbation of v0 (x20).
+    assert abs(ex["theta_max"] - th_o) <= 1e-9 * abs(th_o)
+    s_lo = s_rho = 0.0
     for s in range(3):
-        vp = w["b"] * (1 + 1e-15 * np.random.default_rng(100 + s).standard_normal(w["n"]))
-        spread = max(spread, abs(oracle.estimate_spectrum(orc, 20, vp)[0] - lo_o))
-    assert abs(lo - lo_o) <= max(1e-8 * abs(lo_o), 20 * spread), (lo, lo_o, spread)
+        vp = v0 * (1 + 1e-15 * np.random.default_rng(100 + s).standard_normal(w["n"]))
+        ap, bp = oracle.lanczos(orc, 20, vp)
+        s_lo = max(s_lo, abs(oracle.ritz_extremes(ap, bp)[0] - lo_o))
+        s_rho = max(s_rho, abs(oracle.ritz_upper(ap, bp)[1] - rho_o))
+    assert abs(ex["theta_min"] - lo_o) <= max(1e-8 * abs(lo_o), 20 * s_lo), (ex, lo_o, s_lo)
+    assert abs(ex["rho"] - rho_o) <= max(1e-6 * abs(rho_o) + 1e-12 * th_o, 20 * s_rho), (ex, rho_o, s_rho)
     assert 0 < lo < hi
 
 
@@ -125,11 +138,11 @@ def test_pcg_parity(ctx, wl, name, kind, k, xi):
     w = wl(name)
     tol = w["tol"]
     orc = oracle.Operator(w)
-    lo_o, hi_o = oracle.estimate_spectrum(orc, 20, w["b"])
+    lo_o, hi_o = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
     x_o, st_o = oracle.pcg(orc, w["b"], k, lo_o, hi_o, xi, tol=tol, maxit=20000)
     assert st_o["converged"]
     op = npc.create_from_workload(ctx, w, kind)
-    lo, hi = npc.npc_estimate_spectrum(op, 20, dev(w["b"]))
+    lo, hi = npc.npc_estimate_spectrum(op, 20, None)
     poly = npc.npc_set_poly(op, k, lo, hi, xi)
     x = torch.zeros(w["n"], dtype=torch.float64, device="cuda")
     st = npc.npc_pcg_solve(poly, op, dev(w["b"]), x, tol, 20000, history=True)
@@ -165,7 +178,7 @@ def test_callback_operator(ctx, wl):
 
     op = npc.npc_create_operator(ctx, "callback", n_local=w["n"], apply=apply)
     orc = oracle.Operator(w)
-    lmin, lmax = oracle.estimate_spectrum(orc, 20, w["b"])
+    lmin, lmax = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
     for k in (0, 1, 7, 40):
         poly = npc.npc_set_poly(op, k, lmin, lmax, 1e-3)
         r = np.random.default_rng(k).uniform(-1, 1, w["n"])
@@ -209,7 +222,7 @@ def test_zero_rhs_identity_and_x0(ctx):
     w = W.config1()
     orc = oracle.Operator(w)
     op = npc.create_from_workload(ctx, w)
-    lo, hi = oracle.estimate_spectrum(orc, 20, w["b"])
+    lo, hi = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
     poly = npc.npc_set_poly(op, 10, lo, hi, 0.0)
     x0 = np.random.default_rng(3).uniform(-1, 1, w["n"])
     _, st_o = oracle.pcg(orc, w["b"], 10, lo, hi, 0.0, tol=1e-8, x0=x0)

@@ -299,10 +299,41 @@ def test_P9_lanczos_config1_bracket():
     w = W.config1()
     op = oracle.Operator(w)
     lo_ex, hi_ex = 8 * math.sin(math.pi / 130) ** 2, 8 * math.sin(64 * math.pi / 130) ** 2
-    lmin, lmax = oracle.estimate_spectrum(op, 20, w["b"])
-    assert lo_ex <= lmin and lmax <= hi_ex  # Ritz values interlace inside the spectrum
-    assert hi_ex - lmax < 0.02 * hi_ex       # the top converges fast
-    assert lmin < 20 * lo_ex
+    for v0 in (w["b"], W.lanczos_start(w["n"])):
+        a, b = oracle.lanczos(op, 20, v0)
+        rmin, rmax = oracle.ritz_extremes(a, b)
+        assert lo_ex <= rmin and rmax <= hi_ex  # Ritz values interlace inside the spectrum
+        assert hi_ex - rmax < 0.02 * hi_ex       # the top converges fast
+        assert rmin < 20 * lo_ex
+        # the upper estimate theta_max + rho (reading A11) bounds lambda_max from above, and
+        # rho is the true residual norm of the Ritz pair (Kaniel-Paige: rho >> hi_ex - theta)
+        lmin, lmax = oracle.estimate_spectrum(op, 20, v0)
+        assert lmin == rmin and hi_ex <= lmax < hi_ex * 1.05
+
+
+def test_P9_ritz_residual_is_true_residual():
+    """rho = beta_m |s_m| equals ||A y - theta y|| of the Ritz vector y = Q s (dense check)."""
+    n = 60
+    A, _ = W.random_spd_dense(n, 3, cond=50.0)
+    rowptr, colidx, vals = W.dense_to_csr(A)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    v0 = W.lanczos_start(n)
+    m = 8
+    a, b = oracle.lanczos(op, m, v0)
+    # rebuild Q by the same three-term recurrence in numpy (dense, tiny)
+    Q = np.zeros((n, m + 1))
+    Q[:, 0] = v0 / np.linalg.norm(v0)
+    for j in range(m):
+        wv = A @ Q[:, j] - (b[j - 1] * Q[:, j - 1] if j else 0)
+        wv -= a[j] * Q[:, j]
+        Q[:, j + 1] = wv / b[j]
+    from scipy.linalg import eigh_tridiagonal
+    ev, S = eigh_tridiagonal(a, b[: m - 1])
+    y = Q[:, :m] @ S[:, -1]
+    th, rho = oracle.ritz_upper(a, b)
+    assert abs(th - ev[-1]) < 1e-12 * abs(th)
+    assert abs(rho - np.linalg.norm(A @ y - th * y)) < 1e-8 * np.linalg.norm(A, 2)
+    assert th + rho >= np.linalg.eigvalsh(A)[-1] - 1e-12
 
 
 def test_P9_lanczos_config2_small_bracket():
@@ -311,8 +342,17 @@ def test_P9_lanczos_config2_small_bracket():
     op = oracle.Operator(w)
     lo_ex = 3 * 4 * math.sin(math.pi / (2 * (side + 1))) ** 2
     hi_ex = 3 * 4 * math.sin(side * math.pi / (2 * (side + 1))) ** 2
-    lmin, lmax = oracle.estimate_spectrum(op, 20, w["b"])
-    assert lo_ex <= lmin and lmax <= hi_ex and hi_ex - lmax < 0.05 * hi_ex
+    a, b = oracle.lanczos(op, 20, W.lanczos_start(w["n"]))
+    rmin, rmax = oracle.ritz_extremes(a, b)
+    assert lo_ex <= rmin and rmax <= hi_ex and hi_ex - rmax < 0.05 * hi_ex
+    assert oracle.estimate_spectrum(op, 20, W.lanczos_start(w["n"]))[1] >= hi_ex
+
+
+def test_lanczos_start_generator():
+    """The counter-hash start vector: uniform in [-1, 1), partition-independent."""
+    v = W.lanczos_start(100_000)
+    assert -1 <= v.min() and v.max() < 1 and abs(v.mean()) < 0.01 and abs(v.var() - 1 / 3) < 0.01
+    assert np.array_equal(v[500:700], W.lanczos_start(200, offset=500))
 
 
 # ---------------------------------------------------------------- P11: exact solution x* = 1
@@ -320,7 +360,7 @@ def test_P11_config3_surrogate_exact_solution():
     w = W.config3(side=12)
     op = oracle.Operator(w)
     assert np.allclose(op.apply(np.ones(w["n"])), w["b"], rtol=1e-13, atol=1e-12)  # b = A 1
-    lmin, lmax = oracle.estimate_spectrum(op, 20, w["b"])
+    lmin, lmax = oracle.estimate_spectrum(op, 20, W.lanczos_start(w["n"]))
     x, st = oracle.pcg(op, w["b"], 20, lmin, lmax, 0.0, tol=1e-8, maxit=2000)
     assert st["converged"] and st["relres_true"] <= 1e-8
     assert np.max(np.abs(x - 1.0)) < 1e-3

@@ -18,7 +18,7 @@ import numpy as np
 
 __all__ = [
     "config1", "config2", "config3", "config4", "config5",
-    "tab_epsil_diag", "laplacian_1d_csr", "random_spd_dense", "dense_to_csr",
+    "tab_epsil_diag", "laplacian_1d_csr", "random_spd_dense", "dense_to_csr", "lanczos_start",
     "CONFIG_DEFAULTS",
 ]
 
@@ -26,7 +26,7 @@ __all__ = [
 CONFIG_DEFAULTS = {
     1: dict(k=10, tol=1e-8, lanczos_steps=20),
     2: dict(k=30, tol=1e-10, lanczos_steps=20),
-    3: dict(k=20, ks=(20, 50, 100), tol=1e-8, lanczos_steps=20),
+    3: dict(k=50, ks=(20, 50, 100), tol=1e-8, lanczos_steps=20),
     4: dict(k=60, tol=1e-8, lanczos_steps=20),
     5: dict(k=50, ks=(10, 50, 100, 200), tol=1e-8, lanczos_steps=20),
 }
@@ -241,6 +241,24 @@ def tab_epsil_diag(n: int = 100_000, seed: int = 42):
     vals = np.arange(1, n + 1, dtype=np.float64)
     b = np.random.default_rng(seed).random(n)
     return dict(kind="csr", name="tab_epsil_diag", n=n, rowptr=rowptr, colidx=colidx, vals=vals, b=b)
+
+
+LANCZOS_SEED = 0x5EED
+
+
+def lanczos_start(n: int, offset: int = 0, seed: int = LANCZOS_SEED) -> np.ndarray:
+    """Start vector of the spectrum estimate (reading A11): uniform[-1, 1) from a counter-based
+    splitmix64 hash of (seed, global row index + 1), so any row partition draws the same
+    vector.  libnpc implements the same generator on the device (npc_estimate_spectrum with
+    v0 = NULL); both sides consume it as an input."""
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+    i = np.arange(offset + 1, offset + n + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = (np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * i) & M
+        z = ((z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)) & M
+        z = ((z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)) & M
+        z = z ^ (z >> np.uint64(31))
+    return 2.0 * ((z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)) - 1.0
 
 
 def laplacian_1d_csr(n: int):
