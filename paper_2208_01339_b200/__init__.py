@@ -157,7 +157,10 @@ def npc_context_create(device: int = 0, nranks: int = 1, rank: int = 0, unique_i
         assert len(unique_id) == 128
         uid = C.cast(C.create_string_buffer(unique_id, 128), C.c_void_p)
     h = C.c_void_p()
-    _check(lib().npc_context_create(device, nranks, rank, uid, C.c_void_p(stream.cuda_stream), C.byref(h)))
+    # torch's default stream is the legacy NULL stream (handle 0); NULL means "library-owned
+    # stream" in the C ABI, so pass cudaStreamLegacy (0x1) to enqueue on torch's stream.
+    handle = stream.cuda_stream or 0x1
+    _check(lib().npc_context_create(device, nranks, rank, uid, C.c_void_p(handle), C.byref(h)))
     return Context(h, stream)
 
 

@@ -143,6 +143,7 @@ npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, n
     NPC_CUDA_TRY(cudaDeviceSynchronize());
     auto h = std::make_unique<npc_operator_s>();
     h->owner = ctx;
+    h->device = ctx->ctx.device;
     h->op = std::move(op);
     *out = h.release();
     return NPC_SUCCESS;
@@ -151,8 +152,8 @@ npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, n
 npc_status npc_destroy_operator(npc_operator op) {
     if (!op) return NPC_SUCCESS;
     {
-        DeviceScope ds(op->owner->ctx.device);
-        cudaStreamSynchronize(op->owner->ctx.stream);
+        DeviceScope ds(op->device);
+        cudaDeviceSynchronize();
         op->op.reset();
     }
     delete op;
@@ -197,6 +198,7 @@ npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, d
     NPC_GUARD(degree <= 100000, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly: degree %d too large", degree);
     auto P = std::make_unique<npc_poly_s>();
     P->op = op;
+    P->device = op->device;
     P->degree = degree;
     P->lmin = lmin;
     P->lmax = lmax;
@@ -217,8 +219,8 @@ npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, d
 npc_status npc_destroy_poly(npc_poly poly) {
     if (!poly) return NPC_SUCCESS;
     {
-        DeviceScope ds(poly->op->owner->ctx.device);
-        cudaStreamSynchronize(poly->op->owner->ctx.stream);
+        DeviceScope ds(poly->device);
+        cudaDeviceSynchronize();
         poly->tmp.release();
         poly->rin.release();
         poly->zout.release();

@@ -199,12 +199,16 @@ __host__ __device__ inline int ceil_div(long long a, long long b) { return (int)
 struct npc_context_s {
     npc::Context ctx;
 };
+// Handles record their device so that destroy never dereferences another handle: Python's
+// cyclic GC may destroy a context before its operators, or an operator before its polys.
 struct npc_operator_s {
     npc_context owner = nullptr;
+    int device = 0;
     std::unique_ptr<npc::Operator> op;
 };
 struct npc_poly_s {
     npc_operator op = nullptr;
+    int device = 0;
     int degree = 0;
     double lmin = 0, lmax = 0, xi = 0;
     double theta_bar = 0, delta = 0, sigma = 0;
