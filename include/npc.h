@@ -69,6 +69,17 @@ NPC_API const char *npc_version(void);
 /* Number of CUDA kernels this library has launched in the process so far (all contexts). */
 NPC_API unsigned long long npc_launch_count(void);
 
+/* ---- in-library kernel timing (CUDA events on the context stream) ------------------------
+ * When enabled, the library brackets its launches with CUDA events and accumulates device
+ * milliseconds and launch counts per class until the next get (which resets):
+ *   0 fused degree steps of p_k(A) r        1 operator applications outside p_k (w = A u,
+ *   2 PCG vector update                        Lanczos A q, true residual)
+ *   3 reductions and scalar kernels          4 other vector kernels (Lanczos, copies)
+ * get synchronises the context stream.                                                     */
+#define NPC_TIMING_CLASSES 5
+NPC_API npc_status npc_context_set_timing(npc_context ctx, int enable);
+NPC_API npc_status npc_context_get_timing(npc_context ctx, double *ms_out, long long *launches_out);
+
 /* ---- operators ------------------------------------------------------------------------- */
 typedef enum {
     NPC_OP_CSR = 0,      /* general sparse, CSR (configs 1, 3); tile-staged fused kernel   */

@@ -84,6 +84,8 @@ def lib():
             "npc_pcg_solve": [P, P, P, P, D, I, C.POINTER(PcgStats)],
             "npc_halo_plan": [I, P, P, I, P, I, C.POINTER(I), P, P],
             "npc_poly_coefficients": [I, D, D, D, C.POINTER(D), C.POINTER(D), C.POINTER(D), P],
+            "npc_context_set_timing": [P, I],
+            "npc_context_get_timing": [P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -162,6 +164,21 @@ def npc_context_create(device: int = 0, nranks: int = 1, rank: int = 0, unique_i
     handle = stream.cuda_stream or 0x1
     _check(lib().npc_context_create(device, nranks, rank, uid, C.c_void_p(handle), C.byref(h)))
     return Context(h, stream)
+
+
+TIMING_CLASSES = ("degree", "operator", "update", "reduce", "vector")
+
+
+def npc_context_set_timing(ctx: Context, enable: bool = True):
+    _check(lib().npc_context_set_timing(ctx.h, int(bool(enable))))
+
+
+def npc_context_get_timing(ctx: Context) -> dict:
+    """{class: (device ms, launches)} accumulated since the last get (resets)."""
+    ms = np.zeros(len(TIMING_CLASSES))
+    cnt = np.zeros(len(TIMING_CLASSES), dtype=np.int64)
+    _check(lib().npc_context_get_timing(ctx.h, ms.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p)))
+    return {c: (float(m), int(k)) for c, m, k in zip(TIMING_CLASSES, ms, cnt)}
 
 
 class Operator:

@@ -101,6 +101,26 @@ npc_status npc_context_create(int device, int nranks, int rank, const void *nccl
     return NPC_SUCCESS;
 }
 
+npc_status npc_context_set_timing(npc_context ctx, int enable) {
+    NPC_GUARD(ctx, NPC_ERR_INVALID_ARGUMENT, "npc_context_set_timing: null context");
+    ctx->ctx.timing = enable != 0;
+    return NPC_SUCCESS;
+}
+
+npc_status npc_context_get_timing(npc_context ctx, double *ms_out, long long *launches_out) {
+    NPC_GUARD(ctx, NPC_ERR_INVALID_ARGUMENT, "npc_context_get_timing: null context");
+    DeviceScope ds(ctx->ctx.device);
+    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->ctx.stream));
+    ctx->ctx.t_flush();
+    for (int i = 0; i < NPC_TIMING_CLASSES; ++i) {
+        if (ms_out) ms_out[i] = ctx->ctx.t_ms[i];
+        if (launches_out) launches_out[i] = ctx->ctx.t_cnt[i];
+        ctx->ctx.t_ms[i] = 0.0;
+        ctx->ctx.t_cnt[i] = 0;
+    }
+    return NPC_SUCCESS;
+}
+
 npc_status npc_context_destroy(npc_context ctx) {
     if (!ctx) return NPC_SUCCESS;
     {

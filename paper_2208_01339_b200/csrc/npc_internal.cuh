@@ -141,7 +141,33 @@ struct Context {
     double *partial_slot(int i) { return partials.as<double>() + (size_t)i * partial_cap; }
     // Sum 'count' doubles at dev (in place) over all ranks (no-op on one rank).
     npc_status allreduce_sum(double *dev, int count);
+
+    // ---- optional event timing (npc_context_set_timing)
+    struct Pending {
+        int cls;
+        cudaEvent_t e0, e1;
+    };
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_free;
+    std::vector<Pending> pending;
+    double t_ms[NPC_TIMING_CLASSES] = {0};
+    long long t_cnt[NPC_TIMING_CLASSES] = {0};
+    int t_begin(int cls);
+    void t_end(int idx);
+    void t_flush();  // caller has synchronised the stream
+    ~Context();
 };
+
+// RAII bracket of a launch (or a multi-kernel step) for the timing classes above.
+struct TimedScope {
+    Context *c;
+    int idx;
+    TimedScope(Context *ctx, int cls) : c(ctx), idx(ctx->timing ? ctx->t_begin(cls) : -1) {}
+    ~TimedScope() {
+        if (idx >= 0) c->t_end(idx);
+    }
+};
+enum { T_DEGREE = 0, T_OPERATOR = 1, T_UPDATE = 2, T_REDUCE = 3, T_VECTOR = 4 };
 
 // ------------------------------------------------------------------ launch helpers
 // vec_kernels.cu

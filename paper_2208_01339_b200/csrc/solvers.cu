@@ -26,8 +26,58 @@ npc_status Context::ensure_partials(size_t n) {
 
 npc_status Context::allreduce_sum(double *dev, int count) {
     if (nranks == 1) return NPC_SUCCESS;
+    TimedScope ts(this, T_REDUCE);
     NPC_NCCL_TRY(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, stream));
     return NPC_SUCCESS;
+}
+
+int Context::t_begin(int cls) {
+    cudaEvent_t e0;
+    if (ev_free.empty()) {
+        if (cudaEventCreate(&e0) != cudaSuccess) return -1;
+    } else {
+        e0 = ev_free.back();
+        ev_free.pop_back();
+    }
+    cudaEventRecord(e0, stream);
+    pending.push_back({cls, e0, nullptr});
+    return (int)pending.size() - 1;
+}
+
+void Context::t_end(int idx) {
+    cudaEvent_t e1;
+    if (ev_free.empty()) {
+        if (cudaEventCreate(&e1) != cudaSuccess) return;
+    } else {
+        e1 = ev_free.back();
+        ev_free.pop_back();
+    }
+    cudaEventRecord(e1, stream);
+    pending[idx].e1 = e1;
+}
+
+void Context::t_flush() {
+    for (auto &p : pending) {
+        if (p.e1) {
+            float ms = 0.f;
+            cudaEventSynchronize(p.e1);
+            if (cudaEventElapsedTime(&ms, p.e0, p.e1) == cudaSuccess) {
+                t_ms[p.cls] += ms;
+                t_cnt[p.cls] += 1;
+            }
+            ev_free.push_back(p.e1);
+        }
+        ev_free.push_back(p.e0);
+    }
+    pending.clear();
+}
+
+Context::~Context() {
+    for (auto &p : pending) {
+        cudaEventDestroy(p.e0);
+        if (p.e1) cudaEventDestroy(p.e1);
+    }
+    for (auto e : ev_free) cudaEventDestroy(e);
 }
 
 // ================================================================== coefficients (host)
@@ -79,7 +129,10 @@ npc_status apply_poly_internal(npc_poly P, const double *r, double *z, const dou
     Context *ctx = op->ctx;
     const int k = P->degree;
     const double tb = P->theta_bar;
-    if (k == 0) return launch_scale(ctx, r, z, 1.0 / tb, op->n_local, dotv, partials, nparts, done);
+    if (k == 0) {
+        TimedScope ts(ctx, T_DEGREE);
+        return launch_scale(ctx, r, z, 1.0 / tb, op->n_local, dotv, partials, nparts, done);
+    }
     double *tmp = P->tmp.as<double>();
     auto buf = [&](int j) { return ((k - j) % 2 == 0) ? z : tmp; };
     for (int j = 1; j <= k; ++j) {
@@ -111,6 +164,7 @@ npc_status apply_poly_internal(npc_poly P, const double *r, double *z, const dou
             s.partials = partials;
             if (nparts) *nparts = op->num_partials();
         }
+        TimedScope ts(ctx, T_DEGREE);
         NPC_TRY(op->step(s));
     }
     return NPC_SUCCESS;
@@ -130,6 +184,7 @@ npc_status apply_operator(Operator *op, const double *x, double *y, DevBuf &scra
     if (!op->permuted()) {
         s.x = x;
         s.out = y;
+        TimedScope ts(op->ctx, T_OPERATOR);
         return op->step(s);
     }
     NPC_TRY(scratch.alloc(sizeof(double) * 2 * std::max(op->n_local, 1)));
@@ -137,7 +192,10 @@ npc_status apply_operator(Operator *op, const double *x, double *y, DevBuf &scra
     NPC_TRY(op->to_internal(x, xi));
     s.x = xi;
     s.out = yi;
-    NPC_TRY(op->step(s));
+    {
+        TimedScope ts(op->ctx, T_OPERATOR);
+        NPC_TRY(op->step(s));
+    }
     return op->to_external(yi, y);
 }
 
@@ -299,7 +357,10 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         t.out = u;
         t.a = -1.0;
         t.d = 1.0;
-        NPC_TRY(op->step(t));
+        {
+            TimedScope ts(ctx, T_OPERATOR);
+            NPC_TRY(op->step(t));
+        }
         st.op_applications += 1;
         int np = 0;
         NPC_TRY(launch_dot(ctx, u, u, n, P0, &np));
@@ -339,7 +400,10 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         t.out = r;
         t.a = -1.0;
         t.d = 1.0;
-        NPC_TRY(op->step(t));
+        {
+            TimedScope ts(ctx, T_OPERATOR);
+            NPC_TRY(op->step(t));
+        }
         st.op_applications += 1;
     } else {
         NPC_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -405,22 +469,38 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
             t.dotv = u;
             t.partials = P1;
             t.done = dflag;
-            NPC_TRY(op->step(t));
-            NPC_TRY(launch_reduce_sum(ctx, P0, npg, sums + 0, 1, P1, np_op, sums + 1));
+            {
+                TimedScope ts(ctx, T_OPERATOR);
+                NPC_TRY(op->step(t));
+            }
+            {
+                TimedScope ts(ctx, T_REDUCE);
+                NPC_TRY(launch_reduce_sum(ctx, P0, npg, sums + 0, 1, P1, np_op, sums + 1));
+            }
             NPC_TRY(ctx->allreduce_sum(sums, 3));  // the single global reduction
-            k_cg_scalars<<<1, 1, 0, ctx->stream>>>(cg, sums);
-            NPC_LAUNCH_CHECK();
+            {
+                TimedScope ts(ctx, T_REDUCE);
+                k_cg_scalars<<<1, 1, 0, ctx->stream>>>(cg, sums);
+                NPC_LAUNCH_CHECK();
+            }
             if (h.multi) {
                 k_cg_hist_multi<<<1, 1, 0, ctx->stream>>>(cg, dhist);
                 NPC_LAUNCH_CHECK();
             }
-            k_cg_update<<<np_vec, 256, 0, ctx->stream>>>(cg, u, w, p, s, x, r, n, P2);
-            NPC_LAUNCH_CHECK();
-            k_cg_rr<<<1, 1024, 0, ctx->stream>>>(cg, P2, np_vec, sums, dhist);
-            NPC_LAUNCH_CHECK();
+            {
+                TimedScope ts(ctx, T_UPDATE);
+                k_cg_update<<<np_vec, 256, 0, ctx->stream>>>(cg, u, w, p, s, x, r, n, P2);
+                NPC_LAUNCH_CHECK();
+            }
+            {
+                TimedScope ts(ctx, T_REDUCE);
+                k_cg_rr<<<1, 1024, 0, ctx->stream>>>(cg, P2, np_vec, sums, dhist);
+                NPC_LAUNCH_CHECK();
+            }
         }
         NPC_CUDA_TRY(cudaMemcpyAsync(&h, cg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (ctx->timing) ctx->t_flush();
         if (!h.done) {
             chunk = std::min(chunk * 2, 64);
             continue;
@@ -657,19 +737,40 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, doub
         s.out = w;
         s.a = 1.0;
         s.done = &lz->stop;
-        NPC_TRY(op->step(s));
-        k_lz_axpy<0><<<npv, 256, 0, ctx->stream>>>(w, qp, q, j ? &betas[j - 1] : nullptr, n, P0, lz);
-        NPC_LAUNCH_CHECK();
-        NPC_TRY(launch_reduce_sum(ctx, P0, npv, &alphas[j]));
+        {
+            TimedScope ts(ctx, T_OPERATOR);
+            NPC_TRY(op->step(s));
+        }
+        {
+            TimedScope ts(ctx, T_VECTOR);
+            k_lz_axpy<0><<<npv, 256, 0, ctx->stream>>>(w, qp, q, j ? &betas[j - 1] : nullptr, n, P0, lz);
+            NPC_LAUNCH_CHECK();
+        }
+        {
+            TimedScope ts(ctx, T_REDUCE);
+            NPC_TRY(launch_reduce_sum(ctx, P0, npv, &alphas[j]));
+        }
         NPC_TRY(ctx->allreduce_sum(&alphas[j], 1));
-        k_lz_axpy<1><<<npv, 256, 0, ctx->stream>>>(w, q, nullptr, &alphas[j], n, P0, lz);
-        NPC_LAUNCH_CHECK();
-        NPC_TRY(launch_reduce_sum(ctx, P0, npv, &sums[0]));
+        {
+            TimedScope ts(ctx, T_VECTOR);
+            k_lz_axpy<1><<<npv, 256, 0, ctx->stream>>>(w, q, nullptr, &alphas[j], n, P0, lz);
+            NPC_LAUNCH_CHECK();
+        }
+        {
+            TimedScope ts(ctx, T_REDUCE);
+            NPC_TRY(launch_reduce_sum(ctx, P0, npv, &sums[0]));
+        }
         NPC_TRY(ctx->allreduce_sum(&sums[0], 1));
-        k_lz_beta<<<1, 1, 0, ctx->stream>>>(lz, betas, j, &sums[0]);
-        NPC_LAUNCH_CHECK();
-        k_lz_next<<<npv, 256, 0, ctx->stream>>>(lz, w, q, qp, &betas[j], n);
-        NPC_LAUNCH_CHECK();
+        {
+            TimedScope ts(ctx, T_REDUCE);
+            k_lz_beta<<<1, 1, 0, ctx->stream>>>(lz, betas, j, &sums[0]);
+            NPC_LAUNCH_CHECK();
+        }
+        {
+            TimedScope ts(ctx, T_VECTOR);
+            k_lz_next<<<npv, 256, 0, ctx->stream>>>(lz, w, q, qp, &betas[j], n);
+            NPC_LAUNCH_CHECK();
+        }
     }
     LzDev hl;
     std::vector<double> ha(m), hb(m);
@@ -677,6 +778,7 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, doub
     NPC_CUDA_TRY(cudaMemcpyAsync(ha.data(), alphas, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
     NPC_CUDA_TRY(cudaMemcpyAsync(hb.data(), betas, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
     NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ctx->timing) ctx->t_flush();
     const int sN = std::max(1, hl.steps);
     const double beta_last = hb[sN - 1];
     ha.resize(sN);
