@@ -111,6 +111,8 @@ class Operator {
     virtual double bytes_per_step(bool has_s2, bool has_r) const = 0;
     // Internal vector order differs from the caller's (SELL sigma-sort)?
     virtual bool permuted() const { return false; }
+    // May its steps be stream-captured into a CUDA graph? (user callbacks: no)
+    virtual bool capture_safe() const { return true; }
     // out[i] = in[perm[i]] (to internal) / out[perm[i]] = in[i] (to caller order).
     virtual npc_status to_internal(const double *in, double *out) { (void)in; (void)out; return NPC_SUCCESS; }
     virtual npc_status to_external(const double *in, double *out) { (void)in; (void)out; return NPC_SUCCESS; }
@@ -129,6 +131,8 @@ struct Context {
     cudaStream_t stream = nullptr;       // compute stream
     cudaStream_t comm_stream = nullptr;  // halo traffic (nranks > 1)
     bool own_stream = false;
+    cudaStream_t graph_stream = nullptr;  // CUDA-graph replay of PCG iterations
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ncclComm_t comm = nullptr;
     int num_sms = 148;
     // scratch for reductions: partial arrays + scalar slots

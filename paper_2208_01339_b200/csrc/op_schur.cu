@@ -4,14 +4,16 @@
 // This is the "global sparse product - local inverse - transposed product" shape of the
 // paper's S_u application (Alg. 3), with D standing in for
 // the block-diagonal A^{-1} and C = tridiag(-1, 2 + c, -1) for G^u.
-//   create: Bt = D^{-1/2} B (so S = C + Bt^T Bt, D is never read per application); the rows
-//           of Bt are reordered by length (2, 3, 4 entries) -- the order of B's rows is free
-//           since t = Bt v is internal -- and stored SELL-32 column-major: no padding except
-//           the tail chunk of each length class, every load coalesced.
-//   pass 1 (k_schur_bpass):   t_q = sum_p Bt_qp v_p ;  y[col_p] += Bt_qp t_q  (fp64 atomics
-//                              into y, which stays L2-resident)
-//   pass 2 (k_schur_tstep):   (S v)_i = (2 + c_i) v_i - v_{i-1} - v_{i+1} + y_i ; y_i = 0 ;
-//                              out = a (S v) + b v + c s2 + d r   (+ dot partial)
+//   create: Bt = D^{-1/2} B, so S = C + Bt^T Bt and D is never read per application.  The
+//           rows of Bt are reordered by length (4, 3, 2, 1 entries; the order of B's rows is
+//           free since t = Bt v is internal) and stored SELL-32 column-major (no padding but
+//           the tail chunk of each length class).  Bt^T is stored as CSR over the trace rows
+//           (column ids = positions of t), entries in ascending t position.
+//   pass 1 (k_schur_bpass):  t = Bt v            (coalesced slots, v gathered from L2)
+//   pass 2 (k_schur_tpass):  (S v)_i = (2 + c_i) v_i - v_{i-1} - v_{i+1} + (Bt^T t)_i and
+//                            out = a (S v) + b v + c s2 + d r   (+ dot partial), one CTA per
+//                            256 trace rows with the Bt^T segment staged by bulk TMA.
+// Deterministic (no atomics): every run gives the same bits.
 #include <algorithm>
 #include <numeric>
 
@@ -21,103 +23,171 @@
 namespace npc {
 
 static constexpr int SB_WARPS = 8;
-static constexpr int ST_T = 256;
+static constexpr int ST_TILE = 256;
+static constexpr int ST_MAX_SMEM = 200 * 1024;
 
 __global__ void __launch_bounds__(32 * SB_WARPS) k_schur_bpass(const int *__restrict__ chunk_off,
                                                                const int *__restrict__ chunk_len, int nchunks,
                                                                const int *__restrict__ cols,
-                                                               const double *__restrict__ vals, int nrows,
-                                                               const double *__restrict__ v, double *y,
+                                                               const double *__restrict__ vals,
+                                                               const double *__restrict__ v, double *__restrict__ t,
                                                                const int *done) {
     if (done && *done) return;
     const int lane = threadIdx.x & 31;
     const int ch = blockIdx.x * SB_WARPS + (threadIdx.x >> 5);
     if (ch >= nchunks) return;
-    const int row = ch * 32 + lane;
     const int len = chunk_len[ch];
     const long long base = (long long)chunk_off[ch] + lane;
     int c[4];
     double b[4];
-    double t = 0.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 4; ++j)
         if (j < len) {
             c[j] = __ldcs(cols + base + 32LL * j);
             b[j] = __ldcs(vals + base + 32LL * j);
-            t += b[j] * __ldg(v + c[j]);
         }
-    }
-    if (row >= nrows) return;
+    double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-        if (j < len) atomicAdd(y + c[j], b[j] * t);
+        if (j < len) acc += b[j] * __ldg(v + c[j]);
+    t[ch * 32 + lane] = acc;
 }
 
-template <bool HAS_S2, bool HAS_R, bool DOT>
-__global__ void __launch_bounds__(ST_T) k_schur_tstep(const double *__restrict__ cshift, double *y, int n, StepArgs s) {
+struct SchurTDev {
+    const int *rowptr;
+    const int *cols;  // positions in t
+    const double *vals;
+    const double *cshift;
+    const double *t;
+    int n;
+};
+
+template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT>
+__global__ void __launch_bounds__(ST_TILE) k_schur_tpass(SchurTDev T, StepArgs s, int vspan_max) {
     if (s.done && *s.done) return;
-    __shared__ double red[ST_T / 32];
-    double acc = 0.0;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t bar;
+    __shared__ double red[ST_TILE / 32];
+    const int row0 = blockIdx.x * ST_TILE;
+    const int nrows = min(ST_TILE, T.n - row0);
+    const int pb = T.rowptr[row0];
+    const int v0 = pb & ~1, c0 = pb & ~3;
+    double *sv = reinterpret_cast<double *>(smem);
+    int *sc = reinterpret_cast<int *>(smem + (size_t)vspan_max * 8);
+    if (STAGED) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int pe = T.rowptr[row0 + nrows];
+            const int v1 = (pe + 1) & ~1, c1 = (pe + 3) & ~3;
+            const uint32_t bv = (uint32_t)(v1 - v0) * 8u, bc = (uint32_t)(c1 - c0) * 4u;
+            mbar_arrive_expect_tx(&bar, bv + bc);
+            if (bv) {
+                const uint64_t pol = policy_evict_first();
+                bulk_g2s_evict_first(sv, T.vals + v0, bv, &bar, pol);
+                bulk_g2s_evict_first(sc, T.cols + c0, bc, &bar, pol);
+            }
+        }
+    }
+    const int i = row0 + threadIdx.x;
+    const bool active = threadIdx.x < nrows;
     const double *__restrict__ X = s.x;
-    for (int i = blockIdx.x * ST_T + threadIdx.x; i < n; i += gridDim.x * ST_T) {
-        const double xi = X[i];
-        double sv = (2.0 + cshift[i]) * xi;
-        if (i > 0) sv -= X[i - 1];
-        if (i < n - 1) sv -= X[i + 1];
-        sv += y[i];
-        y[i] = 0.0;
-        double o = s.a * sv + s.b * xi;
-        if (HAS_S2) o += s.c * s.s2[i];
-        if (HAS_R) o += s.d * s.r[i];
+    int rb = 0, re = 0;
+    double xi = 0.0, cv = 0.0, xl = 0.0, xr = 0.0, s2v = 0.0, rv = 0.0;
+    if (active) {
+        rb = T.rowptr[i];
+        re = T.rowptr[i + 1];
+        xi = X[i];
+        cv = T.cshift[i];
+        if (i > 0) xl = X[i - 1];
+        if (i < T.n - 1) xr = X[i + 1];
+        if (HAS_S2) s2v = s.s2[i];
+        if (HAS_R) rv = s.r[i];
+    }
+    if (STAGED) mbar_wait(&bar, 0);
+    double acc = 0.0;
+    if (active) {
+        double y = 0.0;
+        for (int p = rb; p < re; ++p) {
+            int c;
+            double v;
+            if (STAGED) {
+                c = sc[p - c0];
+                v = sv[p - v0];
+            } else {
+                c = __ldcs(T.cols + p);
+                v = __ldcs(T.vals + p);
+            }
+            y += v * __ldg(T.t + c);
+        }
+        const double svv = ((2.0 + cv) * xi - xl - xr) + y;
+        double o = s.a * svv + s.b * xi;
+        if (HAS_S2) o += s.c * s2v;
+        if (HAS_R) o += s.d * rv;
         s.out[i] = o;
-        if (DOT) acc += o * s.dotv[i];
+        if (DOT) acc = o * s.dotv[i];
     }
     if (DOT) {
-        acc = block_sum<ST_T>(acc, red);
+        acc = block_sum<ST_TILE>(acc, red);
         if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
     }
 }
 
 class SchurOperator : public Operator {
   public:
-    DevBuf cshift, chunk_off, chunk_len, cols, vals, y;
-    int nb = 0, nchunks = 0;
+    DevBuf cshift, chunk_off, chunk_len, bcols, bvals, t;
+    DevBuf trowptr, tcols, tvals;
+    int nbp = 0, nchunks = 0, ntiles = 0;
     long long nnz = 0, nslots = 0;
-    int grid2 = 1;
+    int vspan_max = 0, cspan_max = 0;
+    size_t smem_bytes = 0;
+    bool staged = true;
 
-    int num_partials() const override { return grid2; }
+    int num_partials() const override { return std::max(ntiles, 1); }
     double bytes_per_step(bool has_s2, bool has_r) const override {
-        // Bt slots once (D folded in), c once, x read once, y written (atomics) + read/reset,
-        // out written; s_{j-2}, r when present.  SURVEY §8(d) row 5 (the ~704 MB variant).
-        double b = (double)nslots * 12.0 + 8.0 * n_local /*c*/ + 2.0 * 8.0 * n_local /*x,out*/ +
-                   2.0 * 8.0 * n_local /*y*/;
+        // pass 1: Bt slots (12 B) + t written; pass 2: Bt^T (12 B/nnz + rowptr) + t read once +
+        // c + x + out (+ s_{j-2}, r).  v is gathered from L2 in pass 1 (read once in pass 2).
+        double b = (double)nslots * 12.0 + 8.0 * nbp + (double)nnz * 12.0 + 4.0 * (n_local + 1) + 8.0 * nbp +
+                   3.0 * 8.0 * n_local;
         if (has_s2) b += 8.0 * n_local;
         if (has_r) b += 8.0 * n_local;
         return b;
     }
-    template <bool H2, bool HR, bool DT>
+    template <bool ST, bool H2, bool HR, bool DT>
     npc_status launch2(const StepArgs &s) {
-        k_schur_tstep<H2, HR, DT><<<grid2, ST_T, 0, ctx->stream>>>(cshift.as<double>(), y.as<double>(), n_local, s);
+        SchurTDev T{trowptr.as<int>(), tcols.as<int>(), tvals.as<double>(), cshift.as<double>(), t.as<double>(),
+                    n_local};
+        auto kern = k_schur_tpass<ST, H2, HR, DT>;
+        const size_t sm = ST ? smem_bytes : 0;
+        if (sm > 48 * 1024) NPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kern<<<ntiles, ST_TILE, sm, ctx->stream>>>(T, s, vspan_max);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
+    }
+    template <bool H2, bool HR, bool DT>
+    npc_status launch2s(const StepArgs &s) {
+        return staged ? launch2<true, H2, HR, DT>(s) : launch2<false, H2, HR, DT>(s);
     }
     npc_status step(const StepArgs &s) override {
         if (n_local == 0) return NPC_SUCCESS;
         if (nchunks) {
             k_schur_bpass<<<ceil_div(nchunks, SB_WARPS), 32 * SB_WARPS, 0, ctx->stream>>>(
-                chunk_off.as<int>(), chunk_len.as<int>(), nchunks, cols.as<int>(), vals.as<double>(), nb, s.x,
-                y.as<double>(), s.done);
+                chunk_off.as<int>(), chunk_len.as<int>(), nchunks, bcols.as<int>(), bvals.as<double>(), s.x,
+                t.as<double>(), s.done);
             NPC_LAUNCH_CHECK();
         }
         const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
-        if (h2 && hr && dt) return launch2<true, true, true>(s);
-        if (h2 && hr) return launch2<true, true, false>(s);
-        if (h2 && dt) return launch2<true, false, true>(s);
-        if (h2) return launch2<true, false, false>(s);
-        if (hr && dt) return launch2<false, true, true>(s);
-        if (hr) return launch2<false, true, false>(s);
-        if (dt) return launch2<false, false, true>(s);
-        return launch2<false, false, false>(s);
+        if (h2 && hr && dt) return launch2s<true, true, true>(s);
+        if (h2 && hr) return launch2s<true, true, false>(s);
+        if (h2 && dt) return launch2s<true, false, true>(s);
+        if (h2) return launch2s<true, false, false>(s);
+        if (hr && dt) return launch2s<false, true, true>(s);
+        if (hr) return launch2s<false, true, false>(s);
+        if (dt) return launch2s<false, false, true>(s);
+        return launch2s<false, false, false>(s);
     }
 };
 
@@ -127,7 +197,7 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
         return NPC_ERR_UNSUPPORTED;
     }
     const int n = d->n_local, nb = d->b_n_local;
-    if (n < 0 || nb < 0 || !d->c || (nb > 0 && (!d->b_rowptr || !d->b_colidx || !d->b_vals || !d->d))) {
+    if (n < 0 || nb < 0 || (n > 0 && !d->c) || (nb > 0 && (!d->b_rowptr || !d->b_colidx || !d->b_vals || !d->d))) {
         set_error("SCHUR: invalid arrays");
         return NPC_ERR_INVALID_ARGUMENT;
     }
@@ -135,7 +205,7 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
         set_error("SCHUR: sizes disagree");
         return NPC_ERR_DIMENSION;
     }
-    if (d->b_rowptr[0] != 0) {
+    if (nb > 0 && d->b_rowptr[0] != 0) {
         set_error("SCHUR: b_rowptr[0] != 0");
         return NPC_ERR_DIMENSION;
     }
@@ -167,9 +237,8 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
     op->kind = NPC_OP_SCHUR;
     op->n_local = n;
     op->n_global = n;
-    op->nb = nb;
     op->nnz = nb ? d->b_rowptr[nb] : 0;
-    // order B rows by length (4, 3, 2, 1; empty rows dropped), chunks of 32 rows
+    // ---- Bt = D^{-1/2} B, rows ordered by length, SELL-32
     std::vector<int> order;
     std::vector<int> coff{0}, clen;
     for (int L = 4; L >= 1; --L) {
@@ -181,39 +250,73 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
         while (order.size() % 32) order.push_back(-1);  // pad the class tail
     }
     op->nchunks = (int)clen.size();
+    op->nbp = (int)order.size();
     op->nslots = coff.back();
     std::vector<int> scols((size_t)op->nslots, 0);
     std::vector<double> svals((size_t)op->nslots, 0.0);
+    std::vector<int> tcount(n + 1, 0);
     for (int ch = 0; ch < op->nchunks; ++ch)
         for (int l = 0; l < 32; ++l) {
-            int q = order[(size_t)ch * 32 + l];
+            const int q = order[(size_t)ch * 32 + l];
+            if (q < 0) continue;
+            const double sc = 1.0 / std::sqrt(d->d[q]);
             for (int j = 0; j < clen[ch]; ++j) {
-                size_t slot = (size_t)coff[ch] + (size_t)j * 32 + l;
-                if (q >= 0) {
-                    int p = d->b_rowptr[q] + j;
-                    scols[slot] = d->b_colidx[p];
-                    svals[slot] = d->b_vals[p] / std::sqrt(d->d[q]);
-                }
+                const size_t slot = (size_t)coff[ch] + (size_t)j * 32 + l;
+                const int p = d->b_rowptr[q] + j;
+                scols[slot] = d->b_colidx[p];
+                svals[slot] = d->b_vals[p] * sc;
+                tcount[d->b_colidx[p] + 1]++;
             }
         }
-    op->grid2 = vec_grid(n);
+    // ---- Bt^T as CSR over trace rows: column ids = positions in t (ascending)
+    std::vector<int> trp(n + 1, 0);
+    for (int i = 0; i < n; ++i) trp[i + 1] = trp[i] + tcount[i + 1];
+    std::vector<int> fill(trp.begin(), trp.end() - 1);
+    std::vector<int> tc((size_t)op->nnz + 8, 0);
+    std::vector<double> tv((size_t)op->nnz + 8, 0.0);
+    for (int pos = 0; pos < op->nbp; ++pos) {
+        const int q = order[pos];
+        if (q < 0) continue;
+        const int ch = pos / 32, l = pos % 32;
+        for (int j = 0; j < clen[ch]; ++j) {
+            const size_t slot = (size_t)coff[ch] + (size_t)j * 32 + l;
+            const int i = scols[slot];
+            tc[fill[i]] = pos;
+            tv[fill[i]] = svals[slot];
+            fill[i]++;
+        }
+    }
+    op->ntiles = std::max(1, ceil_div(n, ST_TILE));
+    for (int tt = 0; tt * ST_TILE < n; ++tt) {
+        const int r0 = tt * ST_TILE, r1 = std::min(n, r0 + ST_TILE);
+        const int pb = trp[r0], pe = trp[r1];
+        op->vspan_max = std::max(op->vspan_max, ((pe + 1) & ~1) - (pb & ~1));
+        op->cspan_max = std::max(op->cspan_max, ((pe + 3) & ~3) - (pb & ~3));
+    }
+    op->vspan_max = (op->vspan_max + 1) & ~1;
+    op->smem_bytes = (size_t)op->vspan_max * 8 + (size_t)op->cspan_max * 4 + 16;
+    op->staged = op->smem_bytes <= (size_t)ST_MAX_SMEM;
+    // ---- upload
     NPC_TRY(op->cshift.alloc(sizeof(double) * std::max(n, 1)));
-    NPC_TRY(op->y.alloc(sizeof(double) * std::max(n, 1)));
+    NPC_TRY(op->t.alloc(sizeof(double) * std::max(op->nbp, 1)));
     NPC_TRY(op->chunk_off.alloc(sizeof(int) * (op->nchunks + 1)));
     NPC_TRY(op->chunk_len.alloc(sizeof(int) * std::max(op->nchunks, 1)));
-    NPC_TRY(op->cols.alloc(sizeof(int) * std::max<long long>(op->nslots, 1)));
-    NPC_TRY(op->vals.alloc(sizeof(double) * std::max<long long>(op->nslots, 1)));
+    NPC_TRY(op->bcols.alloc(sizeof(int) * std::max<long long>(op->nslots, 1)));
+    NPC_TRY(op->bvals.alloc(sizeof(double) * std::max<long long>(op->nslots, 1)));
+    NPC_TRY(op->trowptr.alloc(sizeof(int) * (n + 1)));
+    NPC_TRY(op->tcols.alloc(sizeof(int) * tc.size()));
+    NPC_TRY(op->tvals.alloc(sizeof(double) * tv.size()));
     if (n) NPC_CUDA_TRY(cudaMemcpy(op->cshift.p, d->c, sizeof(double) * n, cudaMemcpyHostToDevice));
-    NPC_CUDA_TRY(cudaMemset(op->y.p, 0, op->y.bytes));
+    NPC_CUDA_TRY(cudaMemset(op->t.p, 0, op->t.bytes));
     NPC_CUDA_TRY(cudaMemcpy(op->chunk_off.p, coff.data(), sizeof(int) * coff.size(), cudaMemcpyHostToDevice));
     if (op->nchunks) {
         NPC_CUDA_TRY(cudaMemcpy(op->chunk_len.p, clen.data(), sizeof(int) * clen.size(), cudaMemcpyHostToDevice));
-        NPC_CUDA_TRY(cudaMemcpy(op->cols.p, scols.data(), sizeof(int) * scols.size(), cudaMemcpyHostToDevice));
-        NPC_CUDA_TRY(cudaMemcpy(op->vals.p, svals.data(), sizeof(double) * svals.size(), cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op->bcols.p, scols.data(), sizeof(int) * scols.size(), cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op->bvals.p, svals.data(), sizeof(double) * svals.size(), cudaMemcpyHostToDevice));
     }
-    // rows beyond nb inside padded chunks have value 0 (their atomics add 0.0): the kernel
-    // also skips them via the row index of the padded order
-    op->nb = (int)order.size();
+    NPC_CUDA_TRY(cudaMemcpy(op->trowptr.p, trp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemcpy(op->tcols.p, tc.data(), sizeof(int) * tc.size(), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemcpy(op->tvals.p, tv.data(), sizeof(double) * tv.size(), cudaMemcpyHostToDevice));
     out = std::move(op);
     return NPC_SUCCESS;
 }
@@ -224,6 +327,7 @@ class CallbackOperator : public Operator {
     npc_apply_fn fn = nullptr;
     void *user = nullptr;
     DevBuf y;
+    bool capture_safe() const override { return false; }
     int num_partials() const override { return vec_grid(n_local); }
     double bytes_per_step(bool has_s2, bool has_r) const override {
         double b = 3.0 * 8.0 * n_local;  // epilogue only: y, x, out (the user's A is opaque)
@@ -248,6 +352,7 @@ npc_status make_callback_operator(Context *ctx, const npc_operator_desc *d, std:
         set_error("CALLBACK: apply is NULL");
         return NPC_ERR_INVALID_ARGUMENT;
     }
+    // nranks > 1: the user's apply owns its halo traffic; the library allreduces the dots.
     auto op = std::make_unique<CallbackOperator>();
     op->ctx = ctx;
     op->kind = NPC_OP_CALLBACK;

@@ -73,6 +73,9 @@ void Context::t_flush() {
 }
 
 Context::~Context() {
+    if (graph_stream) cudaStreamDestroy(graph_stream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     for (auto &p : pending) {
         cudaEventDestroy(p.e0);
         if (p.e1) cudaEventDestroy(p.e1);
@@ -299,6 +302,67 @@ __global__ void k_cg_hist_multi(const CgDev *st, double *history) {
     if (history && st->iters > 0) history[st->iters] = sqrt(st->rr / st->bnorm2);
 }
 
+// Stream-captured replay of a fixed work block.  While active, ctx->stream points at the
+// library's graph stream (forked from the caller's stream); the destructor joins back.
+struct GraphRun {
+    static constexpr int ITERS = 4;
+    Context *c;
+    cudaStream_t orig;
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long kernels = 0;
+    bool forked = false;
+    explicit GraphRun(Context *ctx) : c(ctx), orig(ctx->stream) {}
+    template <class F>
+    npc_status capture(F &&body) {
+        if (!c->graph_stream) {
+            NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c->graph_stream, cudaStreamNonBlocking));
+            NPC_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+            NPC_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        }
+        NPC_CUDA_TRY(cudaEventRecord(c->ev_fork, orig));
+        NPC_CUDA_TRY(cudaStreamWaitEvent(c->graph_stream, c->ev_fork, 0));
+        c->stream = c->graph_stream;
+        forked = true;
+        const unsigned long long l0 = g_launches.load();
+        NPC_CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        npc_status st = NPC_SUCCESS;
+        for (int i = 0; i < ITERS && st == NPC_SUCCESS; ++i) st = body();
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+        kernels = g_launches.load() - l0;
+        g_launches.fetch_sub(kernels);  // captured, not launched
+        if (st != NPC_SUCCESS) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        if (ce != cudaSuccess) {
+            set_error("PCG graph capture failed: %s", cudaGetErrorString(ce));
+            return NPC_ERR_CUDA;
+        }
+        cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+            exec = nullptr;
+            set_error("PCG graph instantiate failed: %s", cudaGetErrorString(ie));
+            return NPC_ERR_CUDA;
+        }
+        return NPC_SUCCESS;
+    }
+    npc_status launch() {
+        NPC_CUDA_TRY(cudaGraphLaunch(exec, c->stream));
+        g_launches.fetch_add(kernels);
+        return NPC_SUCCESS;
+    }
+    ~GraphRun() {
+        if (forked) {
+            cudaEventRecord(c->ev_join, c->stream);
+            cudaStreamWaitEvent(orig, c->ev_join, 0);
+            c->stream = orig;
+        }
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
 static double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -453,8 +517,10 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     const int *dflag = &cg->done;
     int chunk = 4;
     int true_checks = 0;
-    for (;;) {
-        for (int it = 0; it < chunk; ++it) {
+    // One PCG iteration = k fused degree kernels (+ halo) + A u + reduce (+ allreduce) +
+    // scalars + update + ||r||^2; every kernel no-ops once the device flag says done.
+    auto iteration = [&]() -> npc_status {
+        {
             // u = p_k(A) r  with partials of gamma = <u, r>
             int npg = 0;
             if (P)
@@ -497,6 +563,19 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                 k_cg_rr<<<1, 1024, 0, ctx->stream>>>(cg, P2, np_vec, sums, dhist);
                 NPC_LAUNCH_CHECK();
             }
+        }
+        return NPC_SUCCESS;
+    };
+    // CUDA Graph of GRAPH_ITERS iterations (all pointers and coefficients are fixed for the
+    // solve), replayed on a library stream: one launch per 4 iterations instead of 4(k+5)
+    // launches; NCCL calls and the halo fork/join are captured too.  Off while timing.
+    GraphRun gr(ctx);
+    if (!ctx->timing && op->capture_safe() && !getenv("NPC_NO_GRAPH")) NPC_TRY(gr.capture(iteration));
+    for (;;) {
+        if (gr.exec) {
+            for (int it = 0; it < chunk; it += GraphRun::ITERS) NPC_TRY(gr.launch());
+        } else {
+            for (int it = 0; it < chunk; ++it) NPC_TRY(iteration());
         }
         NPC_CUDA_TRY(cudaMemcpyAsync(&h, cg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
