@@ -75,11 +75,11 @@ def matrix_bytes(w, kind):
     if kind == "stencil":
         return 0
     if kind == "schur":
-        # deterministic two-pass form (op_schur.cu): Bt = D^{-1/2} B streamed in pass 1, Bt^T
-        # (CSR) in pass 2, t = Bt v written once and read once, c once.  (The single-pass
-        # atomic form's floor, is nnz*12 + c + y = ~704 MB at config 5.)
-        nnz, nb = int(w["browptr"][-1]), int(w["nb"])
-        return 2 * nnz * 12 + 2 * nb * 8 + (n + 1) * 4 + n * 8
+        # atomic form (op_schur.cu default): Bt = D^{-1/2} B streamed once (12 B per entry),
+        # c once, y scattered then read/reset (SURVEY §8(d) floor, ~704 MB per degree at config 5
+        # with the four vector streams of poly_bytes)
+        nnz = int(w["browptr"][-1])
+        return nnz * 12 + n * 8 + 2 * n * 8
     raise ValueError(kind)
 
 

@@ -61,6 +61,12 @@ typedef struct npc_poly_s *npc_poly;
  * cuda_stream: a cudaStream_t to enqueue on, or NULL for a library-owned stream.        */
 NPC_API npc_status npc_context_create(int device, int nranks, int rank, const void *nccl_unique_id,
                               void *cuda_stream, npc_context *out);
+/* Testing/emulation transport: the nranks ranks are host threads of THIS process (each
+ * calls this with the same group name and its rank; COLLECTIVE).  Collectives go through
+ * host barriers and device-to-device copies, so several ranks may share one GPU; nothing is
+ * captured into CUDA graphs.  Same numerics as NCCL (sums in rank order).                */
+NPC_API npc_status npc_context_create_local(int device, int nranks, int rank, const char *group,
+                                    void *cuda_stream, npc_context *out);
 NPC_API npc_status npc_context_destroy(npc_context ctx);
 NPC_API npc_status npc_get_unique_id(void *out128);
 NPC_API const char *npc_last_error(void);

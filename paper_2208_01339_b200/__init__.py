@@ -85,6 +85,7 @@ def lib():
             "npc_halo_plan": [I, P, P, I, P, I, C.POINTER(I), P, P],
             "npc_poly_coefficients": [I, D, D, D, C.POINTER(D), C.POINTER(D), C.POINTER(D), P],
             "npc_context_set_timing": [P, I],
+            "npc_context_create_local": [I, I, I, C.c_char_p, P, C.POINTER(P)],
             "npc_context_get_timing": [P, P, P],
         }
         for name, args in sig.items():
@@ -163,6 +164,17 @@ def npc_context_create(device: int = 0, nranks: int = 1, rank: int = 0, unique_i
     # stream" in the C ABI, so pass cudaStreamLegacy (0x1) to enqueue on torch's stream.
     handle = stream.cuda_stream or 0x1
     _check(lib().npc_context_create(device, nranks, rank, uid, C.c_void_p(handle), C.byref(h)))
+    return Context(h, stream)
+
+
+def npc_context_create_local(device: int, nranks: int, rank: int, group: str, stream=None) -> Context:
+    """Rank `rank` of a local thread group (testing transport; see include/npc.h)."""
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    h = C.c_void_p()
+    handle = stream.cuda_stream or 0x1
+    _check(lib().npc_context_create_local(device, nranks, rank, group.encode(), C.c_void_p(handle), C.byref(h)))
     return Context(h, stream)
 
 

@@ -61,14 +61,14 @@ npc_status npc_get_unique_id(void *out128) {
     return NPC_SUCCESS;
 }
 
-npc_status npc_context_create(int device, int nranks, int rank, const void *nccl_unique_id, void *cuda_stream,
-                              npc_context *out) {
+}  // extern "C"
+
+static npc_status context_create(int device, int nranks, int rank, const void *nccl_unique_id,
+                                 const char *local_group, void *cuda_stream, npc_context *out) {
     NPC_GUARD(out, NPC_ERR_INVALID_ARGUMENT, "npc_context_create: null output");
     *out = nullptr;
     NPC_GUARD(nranks >= 1 && rank >= 0 && rank < nranks, NPC_ERR_INVALID_ARGUMENT, "npc_context_create: bad rank %d/%d",
               rank, nranks);
-    NPC_GUARD(nranks == 1 || nccl_unique_id, NPC_ERR_INVALID_ARGUMENT,
-              "npc_context_create: nranks > 1 needs an NCCL unique id");
     int ndev = 0;
     NPC_CUDA_TRY(cudaGetDeviceCount(&ndev));
     NPC_GUARD(device >= 0 && device < ndev, NPC_ERR_INVALID_ARGUMENT, "npc_context_create: device %d of %d", device, ndev);
@@ -92,13 +92,29 @@ npc_status npc_context_create(int device, int nranks, int rank, const void *nccl
     }
     if (nranks > 1) {
         NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking));
-        ncclUniqueId id;
-        memcpy(&id, nccl_unique_id, sizeof(id));
-        NPC_NCCL_TRY(ncclCommInitRank(&c.comm, nranks, id, rank));
+        if (local_group)
+            NPC_TRY(make_local_transport(&c, local_group, c.tr));
+        else
+            NPC_TRY(make_nccl_transport(&c, nccl_unique_id, c.tr));
     }
     NPC_TRY(c.ensure_partials(4096));
     *out = h.release();
     return NPC_SUCCESS;
+}
+
+extern "C" {
+
+npc_status npc_context_create(int device, int nranks, int rank, const void *nccl_unique_id, void *cuda_stream,
+                              npc_context *out) {
+    NPC_GUARD(nranks == 1 || nccl_unique_id, NPC_ERR_INVALID_ARGUMENT,
+              "npc_context_create: nranks > 1 needs an NCCL unique id");
+    return context_create(device, nranks, rank, nccl_unique_id, nullptr, cuda_stream, out);
+}
+
+npc_status npc_context_create_local(int device, int nranks, int rank, const char *group, void *cuda_stream,
+                                    npc_context *out) {
+    NPC_GUARD(group && group[0], NPC_ERR_INVALID_ARGUMENT, "npc_context_create_local: empty group name");
+    return context_create(device, nranks, rank, nullptr, group, cuda_stream, out);
 }
 
 npc_status npc_context_set_timing(npc_context ctx, int enable) {
@@ -127,7 +143,7 @@ npc_status npc_context_destroy(npc_context ctx) {
         DeviceScope ds(ctx->ctx.device);
         Context &c = ctx->ctx;
         if (c.stream) cudaStreamSynchronize(c.stream);
-        if (c.comm) ncclCommDestroy(c.comm);
+        c.tr.reset();
         if (c.comm_stream) cudaStreamDestroy(c.comm_stream);
         c.partials.release();
         c.scalars.release();

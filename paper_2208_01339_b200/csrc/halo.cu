@@ -5,7 +5,8 @@
 // column indices of the extra diagonal CSR blocks", overlapping the transfer with the local
 // block product.  Here: one GPU per rank, ghosts sorted by global id
 // (so the ghosts owned by one peer are contiguous in the ghost buffer and arrive with one
-// ncclRecv), send lists fixed at create time, transfers on a dedicated comm stream.
+// receive), send lists fixed at create time, transfers on a dedicated comm stream through
+// the context's transport (NCCL; or the local thread-group transport used for testing).
 #include <algorithm>
 
 #include "npc_internal.cuh"
@@ -54,45 +55,31 @@ npc_status halo_plan_local(int n_local, const int *rowptr, const int *colidx, in
     return NPC_SUCCESS;
 }
 
+// Turn every rank's recv lists (ghost ids, by owner) into the owners' send lists.
 npc_status halo_plan_exchange(Context *ctx, long long row_begin, HaloPlan &plan) {
     const int P = ctx->nranks;
-    // 1) counts: all-to-all of recv_count -> send_count (via allgather of the full matrix)
-    DevBuf cnt;
-    NPC_TRY(cnt.alloc(sizeof(int) * P * P));
-    NPC_CUDA_TRY(cudaMemcpyAsync(cnt.as<int>() + (size_t)ctx->rank * P, plan.recv_count.data(), sizeof(int) * P,
-                                 cudaMemcpyHostToDevice, ctx->stream));
-    NPC_NCCL_TRY(ncclAllGather(cnt.as<int>() + (size_t)ctx->rank * P, cnt.as<int>(), P, ncclInt32, ctx->comm, ctx->stream));
-    std::vector<int> all((size_t)P * P);
-    NPC_CUDA_TRY(cudaMemcpyAsync(all.data(), cnt.p, sizeof(int) * P * P, cudaMemcpyDeviceToHost, ctx->stream));
-    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::vector<int> all;
+    NPC_TRY(ctx->tr->allgather_i32v(ctx, plan.recv_count, all));
     plan.send_count.assign(P, 0);
     plan.send_off.assign(P, 0);
     for (int q = 0; q < P; ++q) plan.send_count[q] = all[(size_t)q * P + ctx->rank];
     for (int q = 1; q < P; ++q) plan.send_off[q] = plan.send_off[q - 1] + plan.send_count[q - 1];
     const int nsend = plan.send_off[P - 1] + plan.send_count[P - 1];
-    // 2) ids: send my ghost ids to their owners, receive the ids peers need from me
-    DevBuf gid, sid;
-    NPC_TRY(gid.alloc(sizeof(long long) * std::max(plan.n_ghost, 1)));
-    NPC_TRY(sid.alloc(sizeof(long long) * std::max(nsend, 1)));
-    if (plan.n_ghost)
-        NPC_CUDA_TRY(cudaMemcpyAsync(gid.p, plan.ghost_ids.data(), sizeof(long long) * plan.n_ghost,
-                                     cudaMemcpyHostToDevice, ctx->stream));
-    NPC_NCCL_TRY(ncclGroupStart());
-    for (int q = 0; q < P; ++q) {
-        if (q == ctx->rank) continue;
-        if (plan.recv_count[q])
-            NPC_NCCL_TRY(ncclSend(gid.as<long long>() + plan.recv_off[q], plan.recv_count[q], ncclInt64, q, ctx->comm,
-                                  ctx->stream));
-        if (plan.send_count[q])
-            NPC_NCCL_TRY(ncclRecv(sid.as<long long>() + plan.send_off[q], plan.send_count[q], ncclInt64, q, ctx->comm,
-                                  ctx->stream));
-    }
-    NPC_NCCL_TRY(ncclGroupEnd());
-    std::vector<long long> ids(std::max(nsend, 1));
-    NPC_CUDA_TRY(cudaMemcpyAsync(ids.data(), sid.p, sizeof(long long) * nsend, cudaMemcpyDeviceToHost, ctx->stream));
-    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    // my ghost ids go to their owners; I receive the ids the peers need from me
+    std::vector<long long> ids(nsend);
+    std::vector<long long> mine(plan.ghost_ids);
+    std::vector<int> rc(plan.recv_count), ro(plan.recv_off);
+    rc[ctx->rank] = 0;
+    NPC_TRY(ctx->tr->alltoallv_i64(ctx, mine, rc, ro, ids, plan.send_count, plan.send_off));
     plan.send_idx.resize(nsend);
-    for (int i = 0; i < nsend; ++i) plan.send_idx[i] = (int)(ids[i] - row_begin);
+    for (int i = 0; i < nsend; ++i) {
+        const long long li = ids[i] - row_begin;
+        if (li < 0 || li >= (1LL << 31)) {
+            set_error("halo plan: peer asked for row %lld not owned here", ids[i]);
+            return NPC_ERR_DIMENSION;
+        }
+        plan.send_idx[i] = (int)li;
+    }
     return NPC_SUCCESS;
 }
 
@@ -113,27 +100,24 @@ npc_status halo_setup(Context *ctx, const HaloPlan &plan, HaloRuntime &rt) {
     return NPC_SUCCESS;
 }
 
+// Pack x[send_idx] on the compute stream, then send/recv on the comm stream (overlapping the
+// interior kernels the caller enqueues next); halo_wait joins before the boundary kernels.
+// The local (testing) transport exchanges synchronously on the compute stream instead.
 npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const double *x) {
-    const int P = ctx->nranks;
     NPC_TRY(launch_gather(ctx, x, rt.send_idx.as<int>(), rt.send_buf.as<double>(), (int)plan.send_idx.size()));
+    if (!ctx->tr->capturable())
+        return ctx->tr->exchange(ctx, rt.send_buf.as<double>(), plan.send_count, plan.send_off,
+                                 rt.ghost_buf.as<double>(), plan.recv_count, plan.recv_off, ctx->stream);
     NPC_CUDA_TRY(cudaEventRecord(rt.packed, ctx->stream));
     NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, rt.packed, 0));
-    NPC_NCCL_TRY(ncclGroupStart());
-    for (int q = 0; q < P; ++q) {
-        if (q == ctx->rank) continue;
-        if (plan.send_count[q])
-            NPC_NCCL_TRY(ncclSend(rt.send_buf.as<double>() + plan.send_off[q], plan.send_count[q], ncclDouble, q,
-                                  ctx->comm, ctx->comm_stream));
-        if (plan.recv_count[q])
-            NPC_NCCL_TRY(ncclRecv(rt.ghost_buf.as<double>() + plan.recv_off[q], plan.recv_count[q], ncclDouble, q,
-                                  ctx->comm, ctx->comm_stream));
-    }
-    NPC_NCCL_TRY(ncclGroupEnd());
+    NPC_TRY(ctx->tr->exchange(ctx, rt.send_buf.as<double>(), plan.send_count, plan.send_off, rt.ghost_buf.as<double>(),
+                              plan.recv_count, plan.recv_off, ctx->comm_stream));
     NPC_CUDA_TRY(cudaEventRecord(rt.ready, ctx->comm_stream));
     return NPC_SUCCESS;
 }
 
 npc_status halo_wait(Context *ctx, HaloRuntime &rt) {
+    if (!ctx->tr->capturable()) return NPC_SUCCESS;
     NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, rt.ready, 0));
     return NPC_SUCCESS;
 }

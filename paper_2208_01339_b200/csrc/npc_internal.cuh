@@ -124,6 +124,27 @@ class Operator {
     long long row_begin = 0;
 };
 
+// ------------------------------------------------------------------ transport (transport.cu)
+struct Context;
+class Transport {
+  public:
+    virtual ~Transport() = default;
+    virtual bool capturable() const = 0;  // may its calls be captured into a CUDA graph?
+    // setup-time collectives on host data
+    virtual npc_status allgather_i64(Context *c, long long mine, std::vector<long long> &all) = 0;
+    virtual npc_status allgather_i32v(Context *c, const std::vector<int> &mine, std::vector<int> &all) = 0;
+    virtual npc_status alltoallv_i64(Context *c, const std::vector<long long> &sbuf, const std::vector<int> &scount,
+                                     const std::vector<int> &soff, std::vector<long long> &rbuf,
+                                     const std::vector<int> &rcount, const std::vector<int> &roff) = 0;
+    // per-application / per-iteration traffic on device buffers, enqueued on stream s
+    virtual npc_status exchange(Context *c, const double *sbuf, const std::vector<int> &scount,
+                                const std::vector<int> &soff, double *rbuf, const std::vector<int> &rcount,
+                                const std::vector<int> &roff, cudaStream_t s) = 0;
+    virtual npc_status allreduce_sum(Context *c, double *dev, int count, cudaStream_t s) = 0;
+};
+npc_status make_nccl_transport(Context *c, const void *uid, std::unique_ptr<Transport> &out);
+npc_status make_local_transport(Context *c, const char *group, std::unique_ptr<Transport> &out);
+
 // ------------------------------------------------------------------ context
 struct Context {
     int device = 0;
@@ -133,7 +154,7 @@ struct Context {
     bool own_stream = false;
     cudaStream_t graph_stream = nullptr;  // CUDA-graph replay of PCG iterations
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    ncclComm_t comm = nullptr;
+    std::unique_ptr<Transport> tr;       // nranks > 1: NCCL or a local thread group
     int num_sms = 148;
     // scratch for reductions: partial arrays + scalar slots
     DevBuf partials;        // 4 slots of partial_cap doubles

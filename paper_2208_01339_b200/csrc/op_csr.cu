@@ -230,17 +230,14 @@ npc_status localize_columns(Context *ctx, const npc_operator_desc *d, HaloPlan &
         return NPC_SUCCESS;
     }
     // partition: gather every rank's row_begin (collective)
-    DevBuf rs;
-    NPC_TRY(rs.alloc(sizeof(long long) * (ctx->nranks + 1)));
-    long long rb = d->row_begin;
-    NPC_CUDA_TRY(cudaMemcpyAsync(rs.as<long long>() + ctx->rank, &rb, sizeof(long long), cudaMemcpyHostToDevice,
-                                 ctx->stream));
-    NPC_NCCL_TRY(ncclAllGather(rs.as<long long>() + ctx->rank, rs.as<long long>(), 1, ncclInt64, ctx->comm, ctx->stream));
-    std::vector<long long> starts(ctx->nranks + 1);
-    NPC_CUDA_TRY(cudaMemcpyAsync(starts.data(), rs.as<long long>(), sizeof(long long) * ctx->nranks,
-                                 cudaMemcpyDeviceToHost, ctx->stream));
-    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    starts[ctx->nranks] = d->n_global;
+    std::vector<long long> starts;
+    NPC_TRY(ctx->tr->allgather_i64(ctx, d->row_begin, starts));
+    starts.push_back(d->n_global);
+    for (int q = 0; q < ctx->nranks; ++q)
+        if (starts[q + 1] < starts[q]) {
+            set_error("row blocks must be assigned to ranks in global row order");
+            return NPC_ERR_DIMENSION;
+        }
     NPC_TRY(halo_plan_local(n, d->rowptr, d->colidx, ctx->nranks, starts.data(), ctx->rank, plan));
     NPC_TRY(halo_plan_exchange(ctx, d->row_begin, plan));
     const long long r0 = d->row_begin, r1 = d->row_begin + n;

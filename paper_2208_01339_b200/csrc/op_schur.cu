@@ -7,13 +7,19 @@
 //   create: Bt = D^{-1/2} B, so S = C + Bt^T Bt and D is never read per application.  The
 //           rows of Bt are reordered by length (4, 3, 2, 1 entries; the order of B's rows is
 //           free since t = Bt v is internal) and stored SELL-32 column-major (no padding but
-//           the tail chunk of each length class).  Bt^T is stored as CSR over the trace rows
-//           (column ids = positions of t), entries in ascending t position.
-//   pass 1 (k_schur_bpass):  t = Bt v            (coalesced slots, v gathered from L2)
-//   pass 2 (k_schur_tpass):  (S v)_i = (2 + c_i) v_i - v_{i-1} - v_{i+1} + (Bt^T t)_i and
-//                            out = a (S v) + b v + c s2 + d r   (+ dot partial), one CTA per
-//                            256 trace rows with the Bt^T segment staged by bulk TMA.
-// Deterministic (no atomics): every run gives the same bits.
+//           the tail chunk of each length class).
+// Default (atomic) form, two kernels per application:
+//   k_schur_bpass_atomic:    t_q = (Bt v)_q in registers; y[col] += Bt_qj t_q (fp64 RED into
+//                            y, L2-resident: the random traffic -- v gather, y scatter --
+//                            stays in a 2 x 8n-byte L2 working set)
+//   k_schur_tstep:           (S v)_i = (2 + c_i) v_i - v_{i-1} - v_{i+1} + y_i ; y_i = 0 ;
+//                            out = a (S v) + b v + c s2 + d r   (+ dot partial)
+// Deterministic form (NPC_SCHUR_DETERMINISTIC=1 at create): Bt^T is also stored, as CSR over
+// the trace rows (column ids = positions of t, ascending), and
+//   pass 1 (k_schur_bpass):  t = Bt v written out (12 B x rows of B);
+//   pass 2 (k_schur_tpass):  (Bt^T t)_i gathered per trace row, tile-staged by bulk TMA, fused
+//                            with C and the epilogue.  Same bits every run, but t (8 x rows of
+//                            B bytes) is gathered at random and spills L2 at config 5 size.
 #include <algorithm>
 #include <numeric>
 
@@ -51,6 +57,66 @@ __global__ void __launch_bounds__(32 * SB_WARPS) k_schur_bpass(const int *__rest
     for (int j = 0; j < 4; ++j)
         if (j < len) acc += b[j] * __ldg(v + c[j]);
     t[ch * 32 + lane] = acc;
+}
+
+// Atomic form (default): t_q stays in a register and is scattered straight into y with fp64
+// reductions (RED.ADD.F64); y (8 n bytes) stays L2-resident, so the only random traffic is
+// the v gather and the y scatter, both inside L2.
+__global__ void __launch_bounds__(32 * SB_WARPS) k_schur_bpass_atomic(const int *__restrict__ chunk_off,
+                                                                      const int *__restrict__ chunk_len, int nchunks,
+                                                                      const int *__restrict__ cols,
+                                                                      const double *__restrict__ vals,
+                                                                      const double *__restrict__ v, double *y,
+                                                                      const int *done) {
+    if (done && *done) return;
+    const int lane = threadIdx.x & 31;
+    const int ch = blockIdx.x * SB_WARPS + (threadIdx.x >> 5);
+    if (ch >= nchunks) return;
+    const int len = chunk_len[ch];
+    const long long base = (long long)chunk_off[ch] + lane;
+    int c[4];
+    double b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (j < len) {
+            c[j] = __ldcs(cols + base + 32LL * j);
+            b[j] = __ldcs(vals + base + 32LL * j);
+        }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (j < len) acc += b[j] * __ldg(v + c[j]);
+    if (acc != 0.0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < len) atomicAdd(y + c[j], b[j] * acc);
+    }
+}
+
+template <bool HAS_S2, bool HAS_R, bool DOT>
+__global__ void __launch_bounds__(ST_TILE) k_schur_tstep(const double *__restrict__ cshift, double *y, int n,
+                                                         StepArgs s) {
+    if (s.done && *s.done) return;
+    __shared__ double red[ST_TILE / 32];
+    double acc = 0.0;
+    const double *__restrict__ X = s.x;
+    for (int i = blockIdx.x * ST_TILE + threadIdx.x; i < n; i += gridDim.x * ST_TILE) {
+        const double xi = X[i];
+        double sv = (2.0 + cshift[i]) * xi;
+        if (i > 0) sv -= X[i - 1];
+        if (i < n - 1) sv -= X[i + 1];
+        sv += y[i];
+        y[i] = 0.0;
+        double o = s.a * sv + s.b * xi;
+        if (HAS_S2) o += s.c * s.s2[i];
+        if (HAS_R) o += s.d * s.r[i];
+        s.out[i] = o;
+        if (DOT) acc += o * s.dotv[i];
+    }
+    if (DOT) {
+        acc = block_sum<ST_TILE>(acc, red);
+        if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
+    }
 }
 
 struct SchurTDev {
@@ -145,9 +211,18 @@ class SchurOperator : public Operator {
     int vspan_max = 0, cspan_max = 0;
     size_t smem_bytes = 0;
     bool staged = true;
+    bool deterministic = false;  // two-pass form (NPC_SCHUR_DETERMINISTIC=1 at create time)
+    int grid2 = 1;               // atomic form: grid of k_schur_tstep
 
-    int num_partials() const override { return std::max(ntiles, 1); }
+    int num_partials() const override { return deterministic ? std::max(ntiles, 1) : grid2; }
     double bytes_per_step(bool has_s2, bool has_r) const override {
+        if (!deterministic) {
+            // Bt slots once, c once, x read + out written, y scattered (L2) then read and reset
+            double b = (double)nslots * 12.0 + 8.0 * n_local + 2.0 * 8.0 * n_local + 2.0 * 8.0 * n_local;
+            if (has_s2) b += 8.0 * n_local;
+            if (has_r) b += 8.0 * n_local;
+            return b;
+        }
         // pass 1: Bt slots (12 B) + t written; pass 2: Bt^T (12 B/nnz + rowptr) + t read once +
         // c + x + out (+ s_{j-2}, r).  v is gathered from L2 in pass 1 (read once in pass 2).
         double b = (double)nslots * 12.0 + 8.0 * nbp + (double)nnz * 12.0 + 4.0 * (n_local + 1) + 8.0 * nbp +
@@ -171,8 +246,32 @@ class SchurOperator : public Operator {
     npc_status launch2s(const StepArgs &s) {
         return staged ? launch2<true, H2, HR, DT>(s) : launch2<false, H2, HR, DT>(s);
     }
+    template <bool H2, bool HR, bool DT>
+    npc_status launch_t(const StepArgs &s) {
+        k_schur_tstep<H2, HR, DT><<<grid2, ST_TILE, 0, ctx->stream>>>(cshift.as<double>(), t.as<double>(), n_local, s);
+        NPC_LAUNCH_CHECK();
+        return NPC_SUCCESS;
+    }
+    npc_status step_atomic(const StepArgs &s) {
+        if (nchunks) {
+            k_schur_bpass_atomic<<<ceil_div(nchunks, SB_WARPS), 32 * SB_WARPS, 0, ctx->stream>>>(
+                chunk_off.as<int>(), chunk_len.as<int>(), nchunks, bcols.as<int>(), bvals.as<double>(), s.x,
+                t.as<double>(), s.done);
+            NPC_LAUNCH_CHECK();
+        }
+        const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
+        if (h2 && hr && dt) return launch_t<true, true, true>(s);
+        if (h2 && hr) return launch_t<true, true, false>(s);
+        if (h2 && dt) return launch_t<true, false, true>(s);
+        if (h2) return launch_t<true, false, false>(s);
+        if (hr && dt) return launch_t<false, true, true>(s);
+        if (hr) return launch_t<false, true, false>(s);
+        if (dt) return launch_t<false, false, true>(s);
+        return launch_t<false, false, false>(s);
+    }
     npc_status step(const StepArgs &s) override {
         if (n_local == 0) return NPC_SUCCESS;
+        if (!deterministic) return step_atomic(s);
         if (nchunks) {
             k_schur_bpass<<<ceil_div(nchunks, SB_WARPS), 32 * SB_WARPS, 0, ctx->stream>>>(
                 chunk_off.as<int>(), chunk_len.as<int>(), nchunks, bcols.as<int>(), bvals.as<double>(), s.x,
@@ -268,6 +367,26 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
                 tcount[d->b_colidx[p] + 1]++;
             }
         }
+    op->deterministic = getenv("NPC_SCHUR_DETERMINISTIC") != nullptr;
+    op->grid2 = vec_grid(n);
+    if (!op->deterministic) {
+        NPC_TRY(op->cshift.alloc(sizeof(double) * std::max(n, 1)));
+        NPC_TRY(op->t.alloc(sizeof(double) * std::max(n, 1)));  // y accumulator
+        NPC_TRY(op->chunk_off.alloc(sizeof(int) * (op->nchunks + 1)));
+        NPC_TRY(op->chunk_len.alloc(sizeof(int) * std::max(op->nchunks, 1)));
+        NPC_TRY(op->bcols.alloc(sizeof(int) * std::max<long long>(op->nslots, 1)));
+        NPC_TRY(op->bvals.alloc(sizeof(double) * std::max<long long>(op->nslots, 1)));
+        if (n) NPC_CUDA_TRY(cudaMemcpy(op->cshift.p, d->c, sizeof(double) * n, cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemset(op->t.p, 0, op->t.bytes));
+        NPC_CUDA_TRY(cudaMemcpy(op->chunk_off.p, coff.data(), sizeof(int) * coff.size(), cudaMemcpyHostToDevice));
+        if (op->nchunks) {
+            NPC_CUDA_TRY(cudaMemcpy(op->chunk_len.p, clen.data(), sizeof(int) * clen.size(), cudaMemcpyHostToDevice));
+            NPC_CUDA_TRY(cudaMemcpy(op->bcols.p, scols.data(), sizeof(int) * scols.size(), cudaMemcpyHostToDevice));
+            NPC_CUDA_TRY(cudaMemcpy(op->bvals.p, svals.data(), sizeof(double) * svals.size(), cudaMemcpyHostToDevice));
+        }
+        out = std::move(op);
+        return NPC_SUCCESS;
+    }
     // ---- Bt^T as CSR over trace rows: column ids = positions in t (ascending)
     std::vector<int> trp(n + 1, 0);
     for (int i = 0; i < n; ++i) trp[i + 1] = trp[i] + tcount[i + 1];

@@ -27,8 +27,7 @@ npc_status Context::ensure_partials(size_t n) {
 npc_status Context::allreduce_sum(double *dev, int count) {
     if (nranks == 1) return NPC_SUCCESS;
     TimedScope ts(this, T_REDUCE);
-    NPC_NCCL_TRY(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, stream));
-    return NPC_SUCCESS;
+    return tr->allreduce_sum(this, dev, count, stream);
 }
 
 int Context::t_begin(int cls) {
@@ -570,7 +569,8 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     // solve), replayed on a library stream: one launch per 4 iterations instead of 4(k+5)
     // launches; NCCL calls and the halo fork/join are captured too.  Off while timing.
     GraphRun gr(ctx);
-    if (!ctx->timing && op->capture_safe() && !getenv("NPC_NO_GRAPH")) NPC_TRY(gr.capture(iteration));
+    if (!ctx->timing && op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH"))
+        NPC_TRY(gr.capture(iteration));
     for (;;) {
         if (gr.exec) {
             for (int it = 0; it < chunk; it += GraphRun::ITERS) NPC_TRY(gr.launch());

@@ -1,0 +1,228 @@
+// transport.cu -- the collectives the multi-rank path needs, behind one interface:
+//   * NcclTransport: one process per GPU, NCCL over NVLink/NVSwitch (the product path);
+//   * LocalTransport: ranks are host threads of ONE process (any GPUs, including one GPU
+//     shared by all ranks), exchanging through host barriers and device-to-device copies.
+//     It exists so the multi-rank code (partition, ghost remap, interior/boundary tiles,
+//     distributed Lanczos and PCG) can be run and checked on a single B200; ranks never wait
+//     on one another on the device (every wait is a host barrier after a stream sync), so it
+//     is safe to run several ranks on one GPU.  It is not captured into CUDA graphs.
+#include <condition_variable>
+#include <map>
+#include <mutex>
+
+#include "npc_internal.cuh"
+
+namespace npc {
+
+// ================================================================== NCCL
+class NcclTransport : public Transport {
+  public:
+    ncclComm_t comm = nullptr;
+    ~NcclTransport() override {
+        if (comm) ncclCommDestroy(comm);
+    }
+    bool capturable() const override { return true; }
+
+    npc_status allgather_i64(Context *c, long long mine, std::vector<long long> &all) override {
+        const int P = c->nranks;
+        DevBuf d;
+        NPC_TRY(d.alloc(sizeof(long long) * P));
+        NPC_CUDA_TRY(cudaMemcpyAsync(d.as<long long>() + c->rank, &mine, sizeof(long long), cudaMemcpyHostToDevice,
+                                     c->stream));
+        NPC_NCCL_TRY(ncclAllGather(d.as<long long>() + c->rank, d.as<long long>(), 1, ncclInt64, comm, c->stream));
+        all.resize(P);
+        NPC_CUDA_TRY(cudaMemcpyAsync(all.data(), d.p, sizeof(long long) * P, cudaMemcpyDeviceToHost, c->stream));
+        NPC_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return NPC_SUCCESS;
+    }
+    npc_status allgather_i32v(Context *c, const std::vector<int> &mine, std::vector<int> &all) override {
+        const int P = c->nranks, m = (int)mine.size();
+        DevBuf d;
+        NPC_TRY(d.alloc(sizeof(int) * (size_t)P * m));
+        NPC_CUDA_TRY(cudaMemcpyAsync(d.as<int>() + (size_t)c->rank * m, mine.data(), sizeof(int) * m,
+                                     cudaMemcpyHostToDevice, c->stream));
+        NPC_NCCL_TRY(ncclAllGather(d.as<int>() + (size_t)c->rank * m, d.as<int>(), m, ncclInt32, comm, c->stream));
+        all.resize((size_t)P * m);
+        NPC_CUDA_TRY(cudaMemcpyAsync(all.data(), d.p, sizeof(int) * P * m, cudaMemcpyDeviceToHost, c->stream));
+        NPC_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return NPC_SUCCESS;
+    }
+    npc_status alltoallv_i64(Context *c, const std::vector<long long> &sbuf, const std::vector<int> &scount,
+                             const std::vector<int> &soff, std::vector<long long> &rbuf,
+                             const std::vector<int> &rcount, const std::vector<int> &roff) override {
+        const int P = c->nranks;
+        DevBuf ds, dr;
+        NPC_TRY(ds.alloc(sizeof(long long) * std::max<size_t>(sbuf.size(), 1)));
+        NPC_TRY(dr.alloc(sizeof(long long) * std::max<size_t>(rbuf.size(), 1)));
+        if (!sbuf.empty())
+            NPC_CUDA_TRY(cudaMemcpyAsync(ds.p, sbuf.data(), sizeof(long long) * sbuf.size(), cudaMemcpyHostToDevice,
+                                         c->stream));
+        NPC_NCCL_TRY(ncclGroupStart());
+        for (int q = 0; q < P; ++q) {
+            if (q == c->rank) continue;
+            if (scount[q])
+                NPC_NCCL_TRY(ncclSend(ds.as<long long>() + soff[q], scount[q], ncclInt64, q, comm, c->stream));
+            if (rcount[q])
+                NPC_NCCL_TRY(ncclRecv(dr.as<long long>() + roff[q], rcount[q], ncclInt64, q, comm, c->stream));
+        }
+        NPC_NCCL_TRY(ncclGroupEnd());
+        if (!rbuf.empty())
+            NPC_CUDA_TRY(cudaMemcpyAsync(rbuf.data(), dr.p, sizeof(long long) * rbuf.size(), cudaMemcpyDeviceToHost,
+                                         c->stream));
+        NPC_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return NPC_SUCCESS;
+    }
+    npc_status exchange(Context *c, const double *sbuf, const std::vector<int> &scount, const std::vector<int> &soff,
+                        double *rbuf, const std::vector<int> &rcount, const std::vector<int> &roff,
+                        cudaStream_t s) override {
+        NPC_NCCL_TRY(ncclGroupStart());
+        for (int q = 0; q < c->nranks; ++q) {
+            if (q == c->rank) continue;
+            if (scount[q]) NPC_NCCL_TRY(ncclSend(sbuf + soff[q], scount[q], ncclDouble, q, comm, s));
+            if (rcount[q]) NPC_NCCL_TRY(ncclRecv(rbuf + roff[q], rcount[q], ncclDouble, q, comm, s));
+        }
+        NPC_NCCL_TRY(ncclGroupEnd());
+        return NPC_SUCCESS;
+    }
+    npc_status allreduce_sum(Context *c, double *dev, int count, cudaStream_t s) override {
+        (void)c;
+        NPC_NCCL_TRY(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, s));
+        return NPC_SUCCESS;
+    }
+};
+
+npc_status make_nccl_transport(Context *c, const void *uid, std::unique_ptr<Transport> &out) {
+    auto t = std::make_unique<NcclTransport>();
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    NPC_NCCL_TRY(ncclCommInitRank(&t->comm, c->nranks, id, c->rank));
+    out = std::move(t);
+    return NPC_SUCCESS;
+}
+
+// ================================================================== local thread group
+struct LocalGroup {
+    int nranks;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long generation = 0;
+    std::vector<const void *> slot;     // per-rank published pointer (host or device)
+    std::vector<const void *> slot2;    // second pointer (offsets / counts)
+    std::vector<int> slot_device;
+    explicit LocalGroup(int n) : nranks(n), slot(n, nullptr), slot2(n, nullptr), slot_device(n, 0) {}
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long gen = generation;
+        if (++arrived == nranks) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
+static std::mutex g_groups_mu;
+static std::map<std::string, std::weak_ptr<LocalGroup>> g_groups;
+
+class LocalTransport : public Transport {
+  public:
+    std::shared_ptr<LocalGroup> g;
+    bool capturable() const override { return false; }
+
+    npc_status allgather_i64(Context *c, long long mine, std::vector<long long> &all) override {
+        g->slot[c->rank] = &mine;
+        g->barrier();
+        all.resize(c->nranks);
+        for (int q = 0; q < c->nranks; ++q) all[q] = *static_cast<const long long *>(g->slot[q]);
+        g->barrier();
+        return NPC_SUCCESS;
+    }
+    npc_status allgather_i32v(Context *c, const std::vector<int> &mine, std::vector<int> &all) override {
+        g->slot[c->rank] = mine.data();
+        g->barrier();
+        const size_t m = mine.size();
+        all.resize((size_t)c->nranks * m);
+        for (int q = 0; q < c->nranks; ++q)
+            memcpy(all.data() + (size_t)q * m, g->slot[q], sizeof(int) * m);
+        g->barrier();
+        return NPC_SUCCESS;
+    }
+    npc_status alltoallv_i64(Context *c, const std::vector<long long> &sbuf, const std::vector<int> &scount,
+                             const std::vector<int> &soff, std::vector<long long> &rbuf,
+                             const std::vector<int> &rcount, const std::vector<int> &roff) override {
+        (void)scount;
+        g->slot[c->rank] = sbuf.data();
+        g->slot2[c->rank] = soff.data();
+        g->barrier();
+        for (int q = 0; q < c->nranks; ++q) {
+            if (q == c->rank || !rcount[q]) continue;
+            const long long *src = static_cast<const long long *>(g->slot[q]);
+            const int *qoff = static_cast<const int *>(g->slot2[q]);
+            memcpy(rbuf.data() + roff[q], src + qoff[c->rank], sizeof(long long) * rcount[q]);
+        }
+        g->barrier();
+        return NPC_SUCCESS;
+    }
+    npc_status exchange(Context *c, const double *sbuf, const std::vector<int> &scount, const std::vector<int> &soff,
+                        double *rbuf, const std::vector<int> &rcount, const std::vector<int> &roff,
+                        cudaStream_t s) override {
+        (void)scount;
+        NPC_CUDA_TRY(cudaStreamSynchronize(s));  // my packed send buffer is complete
+        g->slot[c->rank] = sbuf;
+        g->slot2[c->rank] = soff.data();
+        g->slot_device[c->rank] = c->device;
+        g->barrier();
+        for (int q = 0; q < c->nranks; ++q) {
+            if (q == c->rank || !rcount[q]) continue;
+            const double *src = static_cast<const double *>(g->slot[q]);
+            const int *qoff = static_cast<const int *>(g->slot2[q]);
+            if (g->slot_device[q] == c->device)
+                NPC_CUDA_TRY(cudaMemcpyAsync(rbuf + roff[q], src + qoff[c->rank], sizeof(double) * rcount[q],
+                                             cudaMemcpyDeviceToDevice, s));
+            else
+                NPC_CUDA_TRY(cudaMemcpyPeerAsync(rbuf + roff[q], c->device, src + qoff[c->rank], g->slot_device[q],
+                                                 sizeof(double) * rcount[q], s));
+        }
+        NPC_CUDA_TRY(cudaStreamSynchronize(s));
+        g->barrier();  // peers may now reuse their send buffers
+        return NPC_SUCCESS;
+    }
+    npc_status allreduce_sum(Context *c, double *dev, int count, cudaStream_t s) override {
+        std::vector<double> mine(count), sum(count, 0.0);
+        NPC_CUDA_TRY(cudaMemcpyAsync(mine.data(), dev, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+        NPC_CUDA_TRY(cudaStreamSynchronize(s));
+        g->slot[c->rank] = mine.data();
+        g->barrier();
+        for (int q = 0; q < c->nranks; ++q) {  // fixed rank order: identical bits on every rank
+            const double *v = static_cast<const double *>(g->slot[q]);
+            for (int i = 0; i < count; ++i) sum[i] += v[i];
+        }
+        g->barrier();
+        NPC_CUDA_TRY(cudaMemcpyAsync(dev, sum.data(), sizeof(double) * count, cudaMemcpyHostToDevice, s));
+        NPC_CUDA_TRY(cudaStreamSynchronize(s));
+        return NPC_SUCCESS;
+    }
+};
+
+npc_status make_local_transport(Context *c, const char *group, std::unique_ptr<Transport> &out) {
+    auto t = std::make_unique<LocalTransport>();
+    {
+        std::lock_guard<std::mutex> lk(g_groups_mu);
+        auto &w = g_groups[group];
+        t->g = w.lock();
+        if (!t->g) {
+            t->g = std::make_shared<LocalGroup>(c->nranks);
+            w = t->g;
+        } else if (t->g->nranks != c->nranks) {
+            set_error("local group '%s' has %d ranks, not %d", group, t->g->nranks, c->nranks);
+            return NPC_ERR_INVALID_ARGUMENT;
+        }
+    }
+    out = std::move(t);
+    return NPC_SUCCESS;
+}
+
+}  // namespace npc

@@ -1,0 +1,118 @@
+"""Multi-rank path on ONE B200: ranks are host threads sharing the GPU through the local
+thread-group transport (npc_context_create_local).  Everything but the NCCL calls runs as in
+the one-process-per-GPU deployment: the collective operator creation (row-start allgather,
+ghost discovery, id exchange -> send lists), interior/boundary tile lists and dot-partial
+offsets, the per-application halo, the distributed Lanczos and the single-reduction PCG with
+its one-iteration-late convergence test.  Results are compared with the CPU oracle.
+No rank ever waits on another on the device (host barriers after stream syncs only)."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import bench  # noqa: E402
+import paper_2208_01339_b200 as npc  # noqa: E402
+
+_group_id = [0]
+
+
+def run_ranks(ws, fn, timeout=240):
+    """Run fn(rank, ctx) on ws threads; return the per-rank results (re-raise failures)."""
+    _group_id[0] += 1
+    group = f"test-{_group_id[0]}"
+    out, err = [None] * ws, [None] * ws
+
+    def body(rank):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ctx = npc.npc_context_create_local(0, ws, rank, group, s)
+                out[rank] = fn(rank, ctx, s)
+                s.synchronize()
+        except BaseException as e:  # noqa: BLE001
+            err[rank] = e
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(ws)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout)
+    assert not any(t.is_alive() for t in th), "a rank hung"
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+CASES = [("c3", "csr", 2), ("c3", "csr", 4), ("c3", "sell", 3), ("c2", "stencil", 2), ("c2", "stencil", 4),
+         ("c4", "sell", 2), ("c4", "csr", 4)]
+WL = {"c3": lambda: W.config3(side=24), "c2": lambda: W.config2(side=20), "c4": lambda: W.config4(n=20_000)}
+CFG = {"c3": 3, "c2": 2, "c4": 4}
+
+
+@pytest.fixture(scope="module")
+def wl():
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache[name] = WL[name]()
+        return cache[name]
+    return get
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("name,kind,ws", CASES)
+def test_multirank_apply_poly_lanczos_pcg(wl, name, kind, ws):
+    w = wl(name)
+    orc = oracle.Operator(w)
+    n = w["n"]
+    lo_o, hi_o = oracle.estimate_spectrum(orc, 20, W.lanczos_start(n))
+    k = 12
+    r = np.random.default_rng(9).uniform(-1, 1, n)
+    x = np.random.default_rng(10).standard_normal(n)
+    ref_apply = orc.apply(x)
+    ref_poly = oracle.cheb_apply(orc, k, lo_o, hi_o, 1e-3, r)
+    _, st_o = oracle.pcg(orc, w["b"], k, lo_o, hi_o, 0.0, tol=w["tol"], maxit=5000)
+
+    def fn(rank, ctx, stream):
+        op, r0, r1 = bench.create_operator(npc, ctx, w, kind, ws, rank, CFG[name])
+        dev = lambda a: torch.tensor(np.ascontiguousarray(a[r0:r1]), device="cuda")  # noqa: E731
+        y = torch.empty(r1 - r0, dtype=torch.float64, device="cuda")
+        npc.npc_apply_operator(op, dev(x), y)
+        poly = npc.npc_set_poly(op, k, lo_o, hi_o, 1e-3)
+        z = torch.empty_like(y)
+        npc.npc_apply_poly(poly, dev(r), z)
+        lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+        p2 = npc.npc_set_poly(op, k, lo, hi, 0.0)
+        xs = torch.zeros_like(y)
+        st = npc.npc_pcg_solve(p2, op, dev(w["b"]), xs, w["tol"], 5000)
+        stream.synchronize()
+        return dict(r0=r0, r1=r1, y=y.cpu().numpy(), z=z.cpu().numpy(), lo=lo, hi=hi, st=st, x=xs.cpu().numpy())
+
+    res = run_ranks(ws, fn)
+    y = np.concatenate([q["y"] for q in res])
+    z = np.concatenate([q["z"] for q in res])
+    xs = np.concatenate([q["x"] for q in res])
+    assert [q["r0"] for q in res] == sorted(q["r0"] for q in res) and res[-1]["r1"] == n
+    assert np.linalg.norm(y - ref_apply) <= 1e-13 * np.linalg.norm(ref_apply)
+    assert np.linalg.norm(z - ref_poly) <= 1e-10 * np.linalg.norm(ref_poly)
+    # every rank holds the same global scalars
+    assert len({(q["lo"], q["hi"]) for q in res}) == 1
+    assert abs(res[0]["hi"] - hi_o) <= 1e-6 * hi_o
+    its = {q["st"]["iters"] for q in res}
+    assert len(its) == 1 and abs(its.pop() - st_o["iters"]) <= 2
+    assert all(q["st"]["converged"] and q["st"]["relres_true"] <= w["tol"] for q in res)
+    assert np.linalg.norm(w["b"] - orc.apply(xs)) / np.linalg.norm(w["b"]) <= w["tol"]
+    # multi-rank convergence is seen one iteration late: one extra (k+1) block is counted
+    st = res[0]["st"]
+    assert st["op_applications"] == (st["iters"] + 1) * (k + 1) + 1
