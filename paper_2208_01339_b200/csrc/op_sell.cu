@@ -5,10 +5,16 @@
 // defines a symmetric permutation of the rank's rows; every internal vector lives in that
 // order (the caller's vectors are permuted once on entry/exit of apply_poly / pcg_solve,
 // never per degree).  Chunks of 32 consecutive internal rows are stored column-major,
-// padded to the chunk's longest row (padding: value 0, column = the row itself).  One warp
-// per chunk: lane = row, each slot is one fully coalesced 256 B value + 128 B index load.
-// Entries keep their original (ascending original-column) order inside a row, so the
-// summation order equals the CSR oracle's.
+// padded to the chunk's longest row (padding: value 0, column = the row itself).  Entries
+// keep their original (ascending original-column) order inside a row, so the summation
+// order equals the CSR oracle's.
+//
+// Kernel: one CTA (4 warps) per tile of 4 consecutive chunks = 128 rows.  The tile's slots
+// are one contiguous, 256 B-aligned segment of the value and index arrays; thread 0 moves
+// both with 1D bulk TMA (cp.async.bulk + mbarrier, L2 evict-first) while the warps load
+// s_{j-2} and r, then warp w reads slot j of chunk w from shared memory (lane = row,
+// conflict-free) and gathers x through L1/L2.  Tiles too large for shared memory fall back
+// to direct coalesced loads.  Multi-rank: tiles touching a ghost column run after the halo.
 #include <algorithm>
 #include <numeric>
 
@@ -21,10 +27,11 @@ npc_status validate_csr_desc(Context *ctx, const npc_operator_desc *d);
 npc_status localize_columns(Context *ctx, const npc_operator_desc *d, HaloPlan &plan, std::vector<int> &local_cols);
 
 static constexpr int SELL_C = 32;
-static constexpr int SELL_WARPS = 8;
+static constexpr int SELL_TW = 4;  // chunks (warps) per tile
+static constexpr int SELL_MAX_SMEM = 160 * 1024;
 
 struct SellDev {
-    const int *chunk_off;  // slot offset of each chunk (in units of entries)
+    const int *chunk_off;  // slot offset of each chunk (entries); chunk_off[nchunks] = total
     const int *chunk_len;  // slots per row of each chunk
     const int *cols;
     const double *vals;
@@ -32,20 +39,56 @@ struct SellDev {
     const double *ghost;
 };
 
-template <bool HAS_S2, bool HAS_R, bool DOT, bool GHOST>
-__global__ void __launch_bounds__(SELL_C *SELL_WARPS) k_sell_step(SellDev A, StepArgs s, const int *__restrict__ chunks,
-                                                                  int nlist) {
+template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST>
+__global__ void __launch_bounds__(SELL_C *SELL_TW) k_sell_step(SellDev A, StepArgs s, const int *__restrict__ tiles,
+                                                               int span_max) {
     if (s.done && *s.done) return;
-    __shared__ double red[SELL_WARPS];
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t bar;
+    __shared__ double red[SELL_TW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int li = blockIdx.x * SELL_WARPS + warp;
+    const int tile = tiles ? tiles[blockIdx.x] : blockIdx.x;
+    const int ch0 = tile * SELL_TW;
+    const int ch1 = min(ch0 + SELL_TW, A.nchunks);
+    const int seg0 = A.chunk_off[ch0];
+    double *sv = reinterpret_cast<double *>(smem);
+    int *sc = reinterpret_cast<int *>(smem + (size_t)span_max * 8);
+    if (STAGED) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int seg1 = A.chunk_off[ch1];
+            const uint32_t nb = (uint32_t)(seg1 - seg0);
+            mbar_arrive_expect_tx(&bar, nb * 12u);
+            if (nb) {
+                const uint64_t pol = policy_evict_first();
+                bulk_g2s_evict_first(sv, A.vals + seg0, nb * 8u, &bar, pol);
+                bulk_g2s_evict_first(sc, A.cols + seg0, nb * 4u, &bar, pol);
+            }
+        }
+    }
+    const int ch = ch0 + warp;
+    const int row = ch * SELL_C + lane;
+    const bool active = ch < ch1 && row < A.n;
+    const double *__restrict__ X = s.x;
+    double xs = 0.0, s2v = 0.0, rv = 0.0;
+    int len = 0, off = 0;
+    if (ch < ch1) {
+        len = A.chunk_len[ch];
+        off = A.chunk_off[ch] - seg0 + lane;
+    }
+    if (active) {
+        xs = X[row];
+        if (HAS_S2) s2v = s.s2[row];
+        if (HAS_R) rv = s.r[row];
+    }
+    if (STAGED) mbar_wait(&bar, 0);
     double acc = 0.0;
-    if (li < nlist) {
-        const int ch = chunks ? chunks[li] : li;
-        const int row = ch * SELL_C + lane;
-        const int len = A.chunk_len[ch];
-        const long long base = (long long)A.chunk_off[ch] + lane;
-        const double *__restrict__ X = s.x;
+    if (ch < ch1) {
+        const long long gbase = (long long)seg0 + off;
         double y = 0.0;
         int j = 0;
         for (; j + 4 <= len; j += 4) {
@@ -53,8 +96,13 @@ __global__ void __launch_bounds__(SELL_C *SELL_WARPS) k_sell_step(SellDev A, Ste
             double v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                c[u] = __ldcs(A.cols + base + (long long)(j + u) * SELL_C);
-                v[u] = __ldcs(A.vals + base + (long long)(j + u) * SELL_C);
+                if (STAGED) {
+                    c[u] = sc[off + (j + u) * SELL_C];
+                    v[u] = sv[off + (j + u) * SELL_C];
+                } else {
+                    c[u] = __ldcs(A.cols + gbase + (long long)(j + u) * SELL_C);
+                    v[u] = __ldcs(A.vals + gbase + (long long)(j + u) * SELL_C);
+                }
             }
             double xv[4];
 #pragma unroll
@@ -63,21 +111,28 @@ __global__ void __launch_bounds__(SELL_C *SELL_WARPS) k_sell_step(SellDev A, Ste
             for (int u = 0; u < 4; ++u) y += v[u] * xv[u];
         }
         for (; j < len; ++j) {
-            int c = __ldcs(A.cols + base + (long long)j * SELL_C);
-            double v = __ldcs(A.vals + base + (long long)j * SELL_C);
-            double xv = (GHOST && c >= A.n) ? A.ghost[c - A.n] : __ldg(X + c);
+            int c;
+            double v;
+            if (STAGED) {
+                c = sc[off + j * SELL_C];
+                v = sv[off + j * SELL_C];
+            } else {
+                c = __ldcs(A.cols + gbase + (long long)j * SELL_C);
+                v = __ldcs(A.vals + gbase + (long long)j * SELL_C);
+            }
+            const double xv = (GHOST && c >= A.n) ? A.ghost[c - A.n] : __ldg(X + c);
             y += v * xv;
         }
-        if (row < A.n) {
-            double o = s.a * y + s.b * X[row];
-            if (HAS_S2) o += s.c * s.s2[row];
-            if (HAS_R) o += s.d * s.r[row];
+        if (active) {
+            double o = s.a * y + s.b * xs;
+            if (HAS_S2) o += s.c * s2v;
+            if (HAS_R) o += s.d * rv;
             s.out[row] = o;
             if (DOT) acc = o * s.dotv[row];
         }
     }
     if (DOT) {
-        acc = block_sum<SELL_C * SELL_WARPS>(acc, red);
+        acc = block_sum<SELL_C * SELL_TW>(acc, red);
         if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
     }
 }
@@ -85,9 +140,12 @@ __global__ void __launch_bounds__(SELL_C *SELL_WARPS) k_sell_step(SellDev A, Ste
 class SellOperator : public Operator {
   public:
     DevBuf chunk_off, chunk_len, cols, vals, perm;
-    DevBuf chunks_interior, chunks_boundary;
-    int nchunks = 0, n_interior = 0, n_boundary = 0;
+    DevBuf tiles_interior, tiles_boundary;
+    int nchunks = 0, ntiles = 0, n_interior = 0, n_boundary = 0;
     long long nslots = 0, nnz = 0;
+    int span_max = 0;
+    size_t smem_bytes = 0;
+    bool staged = true;
     bool multi = false;
     HaloPlan plan;
     HaloRuntime halo;
@@ -99,9 +157,8 @@ class SellOperator : public Operator {
     npc_status to_external(const double *in, double *out) override {
         return launch_scatter(ctx, in, perm.as<int>(), out, n_local);
     }
-    static int blocks(int nch) { return std::max(1, ceil_div(nch, SELL_WARPS)); }
     int num_partials() const override {
-        return multi ? blocks(n_interior) + blocks(n_boundary) : blocks(nchunks);
+        return multi ? std::max(n_interior, 1) + std::max(n_boundary, 1) : std::max(ntiles, 1);
     }
     double bytes_per_step(bool has_s2, bool has_r) const override {
         // stored slots (values + indices, padding included) + per-chunk metadata + vectors
@@ -111,7 +168,7 @@ class SellOperator : public Operator {
         return b;
     }
 
-    template <bool H2, bool HR, bool DT, bool GH>
+    template <bool ST, bool H2, bool HR, bool DT, bool GH>
     npc_status launch_t(const StepArgs &s, const int *list, int nlist, double *partials) {
         if (nlist <= 0) {
             if (partials && DT) NPC_TRY(launch_fill(ctx, partials, 0.0, 1));
@@ -121,30 +178,41 @@ class SellOperator : public Operator {
                   GH ? halo.ghost_buf.as<double>() : nullptr};
         StepArgs a = s;
         a.partials = partials;
-        k_sell_step<H2, HR, DT, GH><<<blocks(nlist), SELL_C * SELL_WARPS, 0, ctx->stream>>>(A, a, list, nlist);
+        auto kern = k_sell_step<ST, H2, HR, DT, GH>;
+        const size_t sm = ST ? smem_bytes : 0;
+        if (sm > 48 * 1024) NPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kern<<<nlist, SELL_C * SELL_TW, sm, ctx->stream>>>(A, a, list, span_max);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
-    template <bool GH>
-    npc_status launch_g(const StepArgs &s, const int *list, int nlist, double *p) {
+    template <bool H2, bool HR, bool DT>
+    npc_status launch_s(const StepArgs &s, const int *list, int nlist, double *p, bool ghost) {
+        if (staged) {
+            if (ghost) return launch_t<true, H2, HR, DT, true>(s, list, nlist, p);
+            return launch_t<true, H2, HR, DT, false>(s, list, nlist, p);
+        }
+        if (ghost) return launch_t<false, H2, HR, DT, true>(s, list, nlist, p);
+        return launch_t<false, H2, HR, DT, false>(s, list, nlist, p);
+    }
+    npc_status launch(const StepArgs &s, const int *list, int nlist, double *p, bool ghost) {
         const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
-        if (h2 && hr && dt) return launch_t<true, true, true, GH>(s, list, nlist, p);
-        if (h2 && hr) return launch_t<true, true, false, GH>(s, list, nlist, p);
-        if (h2 && dt) return launch_t<true, false, true, GH>(s, list, nlist, p);
-        if (h2) return launch_t<true, false, false, GH>(s, list, nlist, p);
-        if (hr && dt) return launch_t<false, true, true, GH>(s, list, nlist, p);
-        if (hr) return launch_t<false, true, false, GH>(s, list, nlist, p);
-        if (dt) return launch_t<false, false, true, GH>(s, list, nlist, p);
-        return launch_t<false, false, false, GH>(s, list, nlist, p);
+        if (h2 && hr && dt) return launch_s<true, true, true>(s, list, nlist, p, ghost);
+        if (h2 && hr) return launch_s<true, true, false>(s, list, nlist, p, ghost);
+        if (h2 && dt) return launch_s<true, false, true>(s, list, nlist, p, ghost);
+        if (h2) return launch_s<true, false, false>(s, list, nlist, p, ghost);
+        if (hr && dt) return launch_s<false, true, true>(s, list, nlist, p, ghost);
+        if (hr) return launch_s<false, true, false>(s, list, nlist, p, ghost);
+        if (dt) return launch_s<false, false, true>(s, list, nlist, p, ghost);
+        return launch_s<false, false, false>(s, list, nlist, p, ghost);
     }
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
-        if (!multi) return launch_g<false>(s, nullptr, nchunks, s.partials);
+        if (!multi) return launch(s, nullptr, ntiles, s.partials, false);
         NPC_TRY(halo_start(ctx, plan, halo, s.x));
-        NPC_TRY(launch_g<false>(s, chunks_interior.as<int>(), n_interior, s.partials));
+        NPC_TRY(launch(s, tiles_interior.as<int>(), n_interior, s.partials, false));
         NPC_TRY(halo_wait(ctx, halo));
-        return launch_g<true>(s, chunks_boundary.as<int>(), n_boundary,
-                              s.partials ? s.partials + blocks(n_interior) : nullptr);
+        return launch(s, tiles_boundary.as<int>(), n_boundary, s.partials ? s.partials + std::max(n_interior, 1) : nullptr,
+                      true);
     }
 };
 
@@ -198,9 +266,8 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
     op->nslots = coff[op->nchunks];
     std::vector<int> scols((size_t)op->nslots);
     std::vector<double> svals((size_t)op->nslots, 0.0);
-    std::vector<int> ti, tb;
+    std::vector<char> chunk_ghost(op->nchunks, 0);
     for (int ch = 0; ch < op->nchunks; ++ch) {
-        bool ghost = false;
         for (int l = 0; l < SELL_C; ++l) {
             int ir = ch * SELL_C + l;
             int orow = ir < n ? perm[ir] : -1;
@@ -210,7 +277,7 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
                 if (j < L) {
                     int p = d->rowptr[orow] + j;
                     int c = lcols[p];
-                    if (c >= n) ghost = true;
+                    if (c >= n) chunk_ghost[ch] = 1;
                     scols[slot] = c < n ? inv[c] : c;
                     svals[slot] = d->vals[p];
                 } else {
@@ -219,8 +286,19 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
                 }
             }
         }
-        (ghost ? tb : ti).push_back(ch);
     }
+    // tiles of SELL_TW chunks: largest contiguous slot segment -> shared memory size
+    op->ntiles = ceil_div(op->nchunks, SELL_TW);
+    std::vector<int> ti, tb;
+    for (int t = 0; t < op->ntiles; ++t) {
+        const int c0 = t * SELL_TW, c1 = std::min(op->nchunks, c0 + SELL_TW);
+        op->span_max = std::max(op->span_max, coff[c1] - coff[c0]);
+        bool ghost = false;
+        for (int c = c0; c < c1; ++c) ghost = ghost || chunk_ghost[c];
+        (ghost ? tb : ti).push_back(t);
+    }
+    op->smem_bytes = (size_t)op->span_max * 12 + 16;
+    op->staged = op->smem_bytes <= (size_t)SELL_MAX_SMEM;
     op->n_interior = (int)ti.size();
     op->n_boundary = (int)tb.size();
     NPC_TRY(op->chunk_off.alloc(sizeof(int) * (op->nchunks + 1)));
@@ -238,12 +316,12 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
     if (op->multi) {
         // pack list in internal order
         for (auto &i : op->plan.send_idx) i = inv[i];
-        NPC_TRY(op->chunks_interior.alloc(sizeof(int) * std::max<size_t>(ti.size(), 1)));
-        NPC_TRY(op->chunks_boundary.alloc(sizeof(int) * std::max<size_t>(tb.size(), 1)));
+        NPC_TRY(op->tiles_interior.alloc(sizeof(int) * std::max<size_t>(ti.size(), 1)));
+        NPC_TRY(op->tiles_boundary.alloc(sizeof(int) * std::max<size_t>(tb.size(), 1)));
         if (!ti.empty())
-            NPC_CUDA_TRY(cudaMemcpy(op->chunks_interior.p, ti.data(), sizeof(int) * ti.size(), cudaMemcpyHostToDevice));
+            NPC_CUDA_TRY(cudaMemcpy(op->tiles_interior.p, ti.data(), sizeof(int) * ti.size(), cudaMemcpyHostToDevice));
         if (!tb.empty())
-            NPC_CUDA_TRY(cudaMemcpy(op->chunks_boundary.p, tb.data(), sizeof(int) * tb.size(), cudaMemcpyHostToDevice));
+            NPC_CUDA_TRY(cudaMemcpy(op->tiles_boundary.p, tb.data(), sizeof(int) * tb.size(), cudaMemcpyHostToDevice));
         NPC_TRY(halo_setup(ctx, op->plan, op->halo));
     }
     out = std::move(op);

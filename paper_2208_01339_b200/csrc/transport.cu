@@ -110,44 +110,78 @@ struct LocalGroup {
     std::vector<const void *> slot;     // per-rank published pointer (host or device)
     std::vector<const void *> slot2;    // second pointer (offsets / counts)
     std::vector<int> slot_device;
+    bool aborted = false;
     explicit LocalGroup(int n) : nranks(n), slot(n, nullptr), slot2(n, nullptr), slot_device(n, 0) {}
-    void barrier() {
+    // false if the group was aborted (a rank left) or the wait timed out
+    bool barrier() {
         std::unique_lock<std::mutex> lk(mu);
+        if (aborted) return false;
         const long long gen = generation;
         if (++arrived == nranks) {
             arrived = 0;
             ++generation;
             cv.notify_all();
-        } else {
-            cv.wait(lk, [&] { return generation != gen; });
+            return true;
         }
+        const bool ok = cv.wait_for(lk, std::chrono::seconds(90), [&] { return generation != gen || aborted; });
+        if (generation != gen) return true;  // released normally (even if aborted since)
+        if (!ok) aborted = true;
+        if (aborted) cv.notify_all();
+        return !aborted;
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(mu);
+        aborted = true;
+        cv.notify_all();
     }
 };
+
+#define NPC_BARRIER(g)                                                                   \
+    do {                                                                                 \
+        if (!(g)->barrier()) {                                                           \
+            set_error("local group aborted (a rank failed, left, or timed out)");        \
+            return NPC_ERR_INVALID_ARGUMENT;                                             \
+        }                                                                                \
+    } while (0)
 
 static std::mutex g_groups_mu;
 static std::map<std::string, std::weak_ptr<LocalGroup>> g_groups;
 
+// A failing rank aborts the group so that its peers leave their barriers with an error.
+#define LT_CUDA_TRY(expr)                                                                          \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            g->abort();                                                                            \
+            npc::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_));    \
+            return NPC_ERR_CUDA;                                                                   \
+        }                                                                                          \
+    } while (0)
+
 class LocalTransport : public Transport {
   public:
     std::shared_ptr<LocalGroup> g;
+    ~LocalTransport() override {
+        if (g) g->abort();  // a rank leaving releases peers still waiting for it
+    }
     bool capturable() const override { return false; }
 
     npc_status allgather_i64(Context *c, long long mine, std::vector<long long> &all) override {
         g->slot[c->rank] = &mine;
-        g->barrier();
+        NPC_BARRIER(g);
         all.resize(c->nranks);
         for (int q = 0; q < c->nranks; ++q) all[q] = *static_cast<const long long *>(g->slot[q]);
-        g->barrier();
+        NPC_BARRIER(g);
         return NPC_SUCCESS;
     }
     npc_status allgather_i32v(Context *c, const std::vector<int> &mine, std::vector<int> &all) override {
         g->slot[c->rank] = mine.data();
-        g->barrier();
+        NPC_BARRIER(g);
         const size_t m = mine.size();
         all.resize((size_t)c->nranks * m);
         for (int q = 0; q < c->nranks; ++q)
             memcpy(all.data() + (size_t)q * m, g->slot[q], sizeof(int) * m);
-        g->barrier();
+        NPC_BARRIER(g);
         return NPC_SUCCESS;
     }
     npc_status alltoallv_i64(Context *c, const std::vector<long long> &sbuf, const std::vector<int> &scount,
@@ -156,53 +190,53 @@ class LocalTransport : public Transport {
         (void)scount;
         g->slot[c->rank] = sbuf.data();
         g->slot2[c->rank] = soff.data();
-        g->barrier();
+        NPC_BARRIER(g);
         for (int q = 0; q < c->nranks; ++q) {
             if (q == c->rank || !rcount[q]) continue;
             const long long *src = static_cast<const long long *>(g->slot[q]);
             const int *qoff = static_cast<const int *>(g->slot2[q]);
             memcpy(rbuf.data() + roff[q], src + qoff[c->rank], sizeof(long long) * rcount[q]);
         }
-        g->barrier();
+        NPC_BARRIER(g);
         return NPC_SUCCESS;
     }
     npc_status exchange(Context *c, const double *sbuf, const std::vector<int> &scount, const std::vector<int> &soff,
                         double *rbuf, const std::vector<int> &rcount, const std::vector<int> &roff,
                         cudaStream_t s) override {
         (void)scount;
-        NPC_CUDA_TRY(cudaStreamSynchronize(s));  // my packed send buffer is complete
+        LT_CUDA_TRY(cudaStreamSynchronize(s));  // my packed send buffer is complete
         g->slot[c->rank] = sbuf;
         g->slot2[c->rank] = soff.data();
         g->slot_device[c->rank] = c->device;
-        g->barrier();
+        NPC_BARRIER(g);
         for (int q = 0; q < c->nranks; ++q) {
             if (q == c->rank || !rcount[q]) continue;
             const double *src = static_cast<const double *>(g->slot[q]);
             const int *qoff = static_cast<const int *>(g->slot2[q]);
             if (g->slot_device[q] == c->device)
-                NPC_CUDA_TRY(cudaMemcpyAsync(rbuf + roff[q], src + qoff[c->rank], sizeof(double) * rcount[q],
+                LT_CUDA_TRY(cudaMemcpyAsync(rbuf + roff[q], src + qoff[c->rank], sizeof(double) * rcount[q],
                                              cudaMemcpyDeviceToDevice, s));
             else
-                NPC_CUDA_TRY(cudaMemcpyPeerAsync(rbuf + roff[q], c->device, src + qoff[c->rank], g->slot_device[q],
+                LT_CUDA_TRY(cudaMemcpyPeerAsync(rbuf + roff[q], c->device, src + qoff[c->rank], g->slot_device[q],
                                                  sizeof(double) * rcount[q], s));
         }
-        NPC_CUDA_TRY(cudaStreamSynchronize(s));
-        g->barrier();  // peers may now reuse their send buffers
+        LT_CUDA_TRY(cudaStreamSynchronize(s));
+        NPC_BARRIER(g);  // peers may now reuse their send buffers
         return NPC_SUCCESS;
     }
     npc_status allreduce_sum(Context *c, double *dev, int count, cudaStream_t s) override {
         std::vector<double> mine(count), sum(count, 0.0);
-        NPC_CUDA_TRY(cudaMemcpyAsync(mine.data(), dev, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
-        NPC_CUDA_TRY(cudaStreamSynchronize(s));
+        LT_CUDA_TRY(cudaMemcpyAsync(mine.data(), dev, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+        LT_CUDA_TRY(cudaStreamSynchronize(s));
         g->slot[c->rank] = mine.data();
-        g->barrier();
+        NPC_BARRIER(g);
         for (int q = 0; q < c->nranks; ++q) {  // fixed rank order: identical bits on every rank
             const double *v = static_cast<const double *>(g->slot[q]);
             for (int i = 0; i < count; ++i) sum[i] += v[i];
         }
-        g->barrier();
-        NPC_CUDA_TRY(cudaMemcpyAsync(dev, sum.data(), sizeof(double) * count, cudaMemcpyHostToDevice, s));
-        NPC_CUDA_TRY(cudaStreamSynchronize(s));
+        NPC_BARRIER(g);
+        LT_CUDA_TRY(cudaMemcpyAsync(dev, sum.data(), sizeof(double) * count, cudaMemcpyHostToDevice, s));
+        LT_CUDA_TRY(cudaStreamSynchronize(s));
         return NPC_SUCCESS;
     }
 };

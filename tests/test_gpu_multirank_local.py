@@ -32,6 +32,7 @@ def run_ranks(ws, fn, timeout=240):
     out, err = [None] * ws, [None] * ws
 
     def body(rank):
+        ctx = None
         try:
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
@@ -40,6 +41,8 @@ def run_ranks(ws, fn, timeout=240):
                 s.synchronize()
         except BaseException as e:  # noqa: BLE001
             err[rank] = e
+            if ctx is not None:
+                ctx.close()  # aborts the group: peers leave their barriers with an error
 
     th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(ws)]
     for t in th:
