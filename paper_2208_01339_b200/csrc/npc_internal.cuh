@@ -10,6 +10,7 @@
 
 #include <atomic>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -240,6 +241,15 @@ struct HaloRuntime {
 npc_status halo_setup(Context *ctx, const HaloPlan &plan, HaloRuntime &rt);
 npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const double *x);
 npc_status halo_wait(Context *ctx, HaloRuntime &rt);
+
+// Raise a kernel's dynamic shared memory limit to the device maximum once (thread-safe).
+// Setting it per launch to the launch's own size races when several host threads launch the
+// same kernel with different sizes; the limit does not change occupancy, the launch size does.
+npc_status allow_max_dynamic_smem_ptr(const void *kern);  // vec_kernels.cu
+template <class K>
+npc_status allow_max_dynamic_smem(K kern) {
+    return allow_max_dynamic_smem_ptr(reinterpret_cast<const void *>(kern));
+}
 
 // Device-side bit helpers
 __host__ __device__ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }

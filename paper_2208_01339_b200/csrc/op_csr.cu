@@ -142,7 +142,7 @@ class CsrOperator : public Operator {
         a.partials = partials;
         auto kern = k_csr_step<ST, H2, HR, DT, GH>;
         size_t sm = ST ? smem_bytes : 0;
-        if (sm > 48 * 1024) NPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        if (sm > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
         kern<<<nt, CSR_TILE, sm, ctx->stream>>>(A, a, tl, vspan_max);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;

@@ -100,7 +100,10 @@ __global__ void __launch_bounds__(ST_TILE) k_schur_tstep(const double *__restric
     __shared__ double red[ST_TILE / 32];
     double acc = 0.0;
     const double *__restrict__ X = s.x;
-    for (int i = blockIdx.x * ST_TILE + threadIdx.x; i < n; i += gridDim.x * ST_TILE) {
+    // one element per thread (grid = ceil(n / 256)): all loads of a thread are independent,
+    // so the whole grid's memory-level parallelism hides the HBM latency
+    const int i = blockIdx.x * ST_TILE + threadIdx.x;
+    if (i < n) {
         const double xi = X[i];
         double sv = (2.0 + cshift[i]) * xi;
         if (i > 0) sv -= X[i - 1];
@@ -237,7 +240,7 @@ class SchurOperator : public Operator {
                     n_local};
         auto kern = k_schur_tpass<ST, H2, HR, DT>;
         const size_t sm = ST ? smem_bytes : 0;
-        if (sm > 48 * 1024) NPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        if (sm > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
         kern<<<ntiles, ST_TILE, sm, ctx->stream>>>(T, s, vspan_max);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
@@ -368,7 +371,7 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
             }
         }
     op->deterministic = getenv("NPC_SCHUR_DETERMINISTIC") != nullptr;
-    op->grid2 = vec_grid(n);
+    op->grid2 = std::max(1, ceil_div(n, ST_TILE));
     if (!op->deterministic) {
         NPC_TRY(op->cshift.alloc(sizeof(double) * std::max(n, 1)));
         NPC_TRY(op->t.alloc(sizeof(double) * std::max(n, 1)));  // y accumulator

@@ -180,7 +180,7 @@ class SellOperator : public Operator {
         a.partials = partials;
         auto kern = k_sell_step<ST, H2, HR, DT, GH>;
         const size_t sm = ST ? smem_bytes : 0;
-        if (sm > 48 * 1024) NPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        if (sm > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
         kern<<<nlist, SELL_C * SELL_TW, sm, ctx->stream>>>(A, a, list, span_max);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;

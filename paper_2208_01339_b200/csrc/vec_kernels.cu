@@ -9,6 +9,22 @@ namespace npc {
 
 static constexpr int VT = 256;  // threads per block of the vector kernels
 
+npc_status allow_max_dynamic_smem_ptr(const void *kern) {
+    static std::mutex mu;
+    static std::vector<const void *> done;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const void *k : done)
+        if (k == kern) return NPC_SUCCESS;
+    int dev = 0, optin = 0;
+    cudaFuncAttributes fa{};
+    NPC_CUDA_TRY(cudaGetDevice(&dev));
+    NPC_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    NPC_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+    NPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+    done.push_back(kern);
+    return NPC_SUCCESS;
+}
+
 int vec_grid(int n) {
     // 4 elements per thread per pass; at most 8 blocks/SM * 148 SMs; fixed for a given n so
     // the number of partials (and the reduction order) never changes between calls.
