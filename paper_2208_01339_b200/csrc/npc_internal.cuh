@@ -254,6 +254,23 @@ npc_status allow_max_dynamic_smem(K kern) {
 // Device-side bit helpers
 __host__ __device__ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Per-(operator, poly) PCG state kept across solves: work vectors, device scalars and the
+// captured CUDA graph of the iteration (valid while none of the pointers it bakes in move).
+struct PcgCache {
+    DevBuf work, dev;
+    size_t work_n = 0;
+    long long dev_maxit = -1;
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long kernels = 0;  // kernels per graph launch
+    const void *key_partials = nullptr;
+    size_t key_cap = 0;
+    void invalidate() {
+        if (exec) cudaGraphExecDestroy(exec);
+        exec = nullptr;
+    }
+    ~PcgCache() { invalidate(); }
+};
+
 }  // namespace npc
 
 // Opaque handle structs of the C ABI.
@@ -266,6 +283,7 @@ struct npc_operator_s {
     npc_context owner = nullptr;
     int device = 0;
     std::unique_ptr<npc::Operator> op;
+    npc::PcgCache pcg;  // plain CG (poly == NULL)
 };
 struct npc_poly_s {
     npc_operator op = nullptr;
@@ -276,4 +294,5 @@ struct npc_poly_s {
     std::vector<double> coef;  // 4 * degree: a_j, b_j, c_j, d_j (j = 1..k)
     npc::DevBuf tmp;           // second recurrence buffer (internal order)
     npc::DevBuf rin, zout;     // internal-order copies when the operator is permuted
+    npc::PcgCache pcg;         // PCG work vectors + captured iteration graph
 };

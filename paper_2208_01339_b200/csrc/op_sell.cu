@@ -27,7 +27,7 @@ npc_status validate_csr_desc(Context *ctx, const npc_operator_desc *d);
 npc_status localize_columns(Context *ctx, const npc_operator_desc *d, HaloPlan &plan, std::vector<int> &local_cols);
 
 static constexpr int SELL_C = 32;
-static constexpr int SELL_TW = 4;  // chunks (warps) per tile
+static constexpr int SELL_TW = 8;  // chunks (warps) per tile
 static constexpr int SELL_MAX_SMEM = 160 * 1024;
 
 struct SellDev {
@@ -298,7 +298,10 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
         (ghost ? tb : ti).push_back(t);
     }
     op->smem_bytes = (size_t)op->span_max * 12 + 16;
-    op->staged = op->smem_bytes <= (size_t)SELL_MAX_SMEM;
+    // Direct coalesced loads by default: SELL slots are already full 128 B lines per warp, and
+    // staging limits occupancy (the x gather needs many warps in flight).  NPC_SELL_STAGED=1
+    // selects the bulk-TMA staged variant (measured slower on config 4: profiles/).
+    op->staged = getenv("NPC_SELL_STAGED") && op->smem_bytes <= (size_t)SELL_MAX_SMEM;
     op->n_interior = (int)ti.size();
     op->n_boundary = (int)tb.size();
     NPC_TRY(op->chunk_off.alloc(sizeof(int) * (op->nchunks + 1)));

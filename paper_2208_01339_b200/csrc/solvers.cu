@@ -306,11 +306,12 @@ __global__ void k_cg_hist_multi(const CgDev *st, double *history) {
 struct GraphRun {
     static constexpr int ITERS = 4;
     Context *c;
+    PcgCache &cache;
     cudaStream_t orig;
-    cudaGraphExec_t exec = nullptr;
+    cudaGraphExec_t exec = nullptr;  // owned by the cache
     unsigned long long kernels = 0;
     bool forked = false;
-    explicit GraphRun(Context *ctx) : c(ctx), orig(ctx->stream) {}
+    GraphRun(Context *ctx, PcgCache &pc) : c(ctx), cache(pc), orig(ctx->stream) {}
     template <class F>
     npc_status capture(F &&body) {
         if (!c->graph_stream) {
@@ -322,6 +323,11 @@ struct GraphRun {
         NPC_CUDA_TRY(cudaStreamWaitEvent(c->graph_stream, c->ev_fork, 0));
         c->stream = c->graph_stream;
         forked = true;
+        if (cache.exec) {  // replay the graph captured by an earlier solve
+            exec = cache.exec;
+            kernels = cache.kernels;
+            return NPC_SUCCESS;
+        }
         const unsigned long long l0 = g_launches.load();
         NPC_CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         npc_status st = NPC_SUCCESS;
@@ -345,6 +351,8 @@ struct GraphRun {
             set_error("PCG graph instantiate failed: %s", cudaGetErrorString(ie));
             return NPC_ERR_CUDA;
         }
+        cache.exec = exec;
+        cache.kernels = kernels;
         return NPC_SUCCESS;
     }
     npc_status launch() {
@@ -358,7 +366,6 @@ struct GraphRun {
             cudaStreamWaitEvent(orig, c->ev_join, 0);
             c->stream = orig;
         }
-        if (exec) cudaGraphExecDestroy(exec);
     }
 };
 
@@ -377,9 +384,14 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     npc_pcg_stats st{};
     double *host_hist = stats ? stats->history : nullptr;
     // work vectors (internal order): b, x, r, u, w, p, s
-    DevBuf work;
+    PcgCache &cache = P ? P->pcg : H->pcg;
     const size_t nn = std::max(n, 1);
-    NPC_TRY(work.alloc(sizeof(double) * nn * 7));
+    if (cache.work_n != nn) {
+        cache.invalidate();
+        NPC_TRY(cache.work.alloc(sizeof(double) * nn * 7));
+        cache.work_n = nn;
+    }
+    DevBuf &work = cache.work;
     double *b = work.as<double>(), *x = b + nn, *r = x + nn, *u = r + nn, *w = u + nn, *p = w + nn, *s = p + nn;
     if (op->permuted()) {
         NPC_TRY(op->to_internal(b_ext, b));
@@ -394,8 +406,17 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     const int np_vec = vec_grid(n);
     NPC_TRY(ctx->ensure_partials(std::max(np_op, np_vec)));
     double *P0 = ctx->partial_slot(0), *P1 = ctx->partial_slot(1), *P2 = ctx->partial_slot(2);
-    DevBuf dev;
-    NPC_TRY(dev.alloc(sizeof(CgDev) + sizeof(double) * (8 + (size_t)maxit + 1)));
+    if (cache.dev_maxit < maxit) {
+        cache.invalidate();
+        NPC_TRY(cache.dev.alloc(sizeof(CgDev) + sizeof(double) * (8 + (size_t)maxit + 1)));
+        cache.dev_maxit = maxit;
+    }
+    if (cache.key_partials != ctx->partials.p || cache.key_cap != ctx->partial_cap) {
+        cache.invalidate();
+        cache.key_partials = ctx->partials.p;
+        cache.key_cap = ctx->partial_cap;
+    }
+    DevBuf &dev = cache.dev;
     CgDev *cg = dev.as<CgDev>();
     double *sums = reinterpret_cast<double *>(cg + 1);
     double *dhist = sums + 8;
@@ -568,7 +589,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     // CUDA Graph of GRAPH_ITERS iterations (all pointers and coefficients are fixed for the
     // solve), replayed on a library stream: one launch per 4 iterations instead of 4(k+5)
     // launches; NCCL calls and the halo fork/join are captured too.  Off while timing.
-    GraphRun gr(ctx);
+    GraphRun gr(ctx, cache);
     if (!ctx->timing && op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH"))
         NPC_TRY(gr.capture(iteration));
     for (;;) {
