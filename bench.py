@@ -103,6 +103,14 @@ def solve_bytes(M, V, k, iters, lanczos_steps):
     return iters * per_iter + lz + setup + (M + 3 * V)     # + final true residual
 
 
+def config_dict(cfg, w, kind, k, xi, M, V):
+    """The workload description shared by both arms (same keys, same values)."""
+    return {"workload": f"config{cfg}: {w['name']}", "operator": kind, "n": w["n"], "k": k, "xi": xi,
+            "tol": w["tol"], "lanczos_steps": w.get("lanczos_steps", 20),
+            "l2": "inputs larger than L2 (matrix + vectors > 126 MB)" if (M + 4 * V) > 126e6
+            else "working set may be L2-resident (no flush)"}
+
+
 # ------------------------------------------------------------------ clocks sampling
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -356,10 +364,9 @@ def run_ours(args):
             "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads/, BASELINE.json config recipe)",
-            "config": {"workload": f"config{cfg}: {w['name']}", "operator": kind, "n": w["n"], "k": k, "xi": xi,
-                       "tol": tol, "lanczos_steps": lz_steps, "parallelism": f"row-block x{ws}" if ws > 1 else "1 GPU",
-                       "l2": "inputs larger than L2 (matrix + vectors > 126 MB)" if (M + 4 * V) > 126e6
-                       else "working set may be L2-resident (no flush)"},
+            "config": config_dict(cfg, w, kind, k, xi, M, V),
+            "parallelism": f"row-block x{ws} (z-slabs for grids), NCCL halo + 1 allreduce/iteration" if ws > 1
+            else "1 GPU",
             "pcg": {"iters": iters, "converged": stats[-1]["converged"], "relres_true": stats[-1]["relres_true"],
                     "op_applications": stats[-1]["op_applications"], "reductions": stats[-1]["reductions"],
                     "lmin": lo, "lmax": hi, "time_to_tol_ms": round(ms_step, 3),
@@ -431,7 +438,7 @@ def run_reference(args):
         "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded workloads/)",
-        "config": {"workload": f"config{cfg}: {w['name']}", "operator": kind, "n": w["n"], "k": k, "xi": args.xi},
+        "config": config_dict(cfg, w, kind, k, args.xi, M, V),
         "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
                          "sample": f"each step = one p_k(A) v application (k={k}) of the full workload, Alg. 2 verbatim"},
         "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

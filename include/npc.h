@@ -161,6 +161,13 @@ NPC_API npc_status npc_estimate_spectrum_ex(npc_operator op, int nsteps, const d
  * Coefficients are computed once on the host (Eq. rhocheb).                                */
 NPC_API npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, double xi,
                         npc_poly *out);
+/* Newton variant (Alg. 1): P_0 r = zeta_0 r, P_{j+1} r = zeta_{j+1}(2 P_j r
+ * - P_j A P_j r), degree 2^nlev - 1 (0 <= nlev <= 16), zeta_0 = 1/theta_bar and zeta_1 with
+ * alpha' = theta_bar - delta (reading A1; equal to Chebyshev of the same degree,
+ * PAPER.md:296-306).  Usable wherever an npc_poly is (apply, PCG); the recursion keeps
+ * 2 (nlev - 1) work vectors and is not fused across levels, so Chebyshev is the fast path.  */
+NPC_API npc_status npc_set_poly_newton(npc_operator op, int nlev, double lmin, double lmax, double xi,
+                               npc_poly *out);
 NPC_API npc_status npc_destroy_poly(npc_poly poly);
 /* z_dev = p_k(A) r_dev: exactly k operator applications, no reductions, no host sync.
  * z_dev must not alias r_dev.                                                              */

@@ -79,6 +79,7 @@ def lib():
             "npc_estimate_spectrum": [P, I, P, C.POINTER(D), C.POINTER(D)],
             "npc_estimate_spectrum_ex": [P, I, P, P],
             "npc_set_poly": [P, I, D, D, D, C.POINTER(P)],
+            "npc_set_poly_newton": [P, I, D, D, D, C.POINTER(P)],
             "npc_destroy_poly": [P],
             "npc_apply_poly": [P, P, P],
             "npc_pcg_solve": [P, P, P, P, D, I, C.POINTER(PcgStats)],
@@ -285,6 +286,13 @@ def npc_set_poly(op: Operator, degree: int, lmin: float, lmax: float, xi: float 
     h = C.c_void_p()
     _check(lib().npc_set_poly(op.h, int(degree), float(lmin), float(lmax), float(xi), C.byref(h)))
     return Poly(op, h, degree, lmin, lmax, xi)
+
+
+def npc_set_poly_newton(op: Operator, nlev: int, lmin: float, lmax: float, xi: float = 0.0) -> Poly:
+    """Newton variant (Alg. 1), degree 2^nlev - 1."""
+    h = C.c_void_p()
+    _check(lib().npc_set_poly_newton(op.h, int(nlev), float(lmin), float(lmax), float(xi), C.byref(h)))
+    return Poly(op, h, (1 << nlev) - 1, lmin, lmax, xi)
 
 
 def npc_apply_poly(poly: Poly, r, z):

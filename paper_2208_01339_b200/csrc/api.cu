@@ -22,6 +22,7 @@ npc_status apply_poly(npc_poly P, const double *r, double *z);
 npc_status apply_operator(Operator *op, const double *x, double *y, DevBuf &scratch);
 npc_status pcg(npc_poly P, npc_operator H, const double *b, double *x, double tol, int maxit, npc_pcg_stats *stats);
 npc_status lanczos(Operator *op, int m, const double *v0, double *lmin, double *lmax, double *out_ex);
+npc_status newton_zetas(int nlev, double lmin, double lmax, double xi, std::vector<double> &zeta);
 }  // namespace npc
 
 using namespace npc;
@@ -244,6 +245,33 @@ npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, d
     DeviceScope ds(op->owner->ctx.device);
     const size_t n = std::max(op->op->n_local, 1);
     NPC_TRY(P->tmp.alloc(sizeof(double) * n));
+    if (op->op->permuted()) {
+        NPC_TRY(P->rin.alloc(sizeof(double) * n));
+        NPC_TRY(P->zout.alloc(sizeof(double) * n));
+    }
+    *out = P.release();
+    return NPC_SUCCESS;
+}
+
+npc_status npc_set_poly_newton(npc_operator op, int nlev, double lmin, double lmax, double xi, npc_poly *out) {
+    NPC_GUARD(op && out, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly_newton: null argument");
+    *out = nullptr;
+    NPC_GUARD(nlev >= 0 && nlev <= 16, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly_newton: nlev %d not in [0, 16]", nlev);
+    auto P = std::make_unique<npc_poly_s>();
+    P->op = op;
+    P->device = op->device;
+    P->kind = 1;
+    P->nlev = nlev;
+    P->degree = (1 << nlev) - 1;
+    P->lmin = lmin;
+    P->lmax = lmax;
+    P->xi = xi;
+    NPC_TRY(newton_zetas(nlev, lmin, lmax, xi, P->zeta));
+    NPC_TRY(poly_coefficients(0, lmin, lmax, xi, &P->theta_bar, &P->delta, &P->sigma, nullptr));
+    DeviceScope ds(op->device);
+    const size_t n = std::max(op->op->n_local, 1);
+    NPC_TRY(P->tmp.alloc(sizeof(double) * n));
+    if (nlev >= 2) NPC_TRY(P->nbuf.alloc(sizeof(double) * n * 2 * (nlev - 1)));
     if (op->op->permuted()) {
         NPC_TRY(P->rin.alloc(sizeof(double) * n));
         NPC_TRY(P->zout.alloc(sizeof(double) * n));

@@ -288,6 +288,10 @@ struct npc_operator_s {
 struct npc_poly_s {
     npc_operator op = nullptr;
     int device = 0;
+    int kind = 0;              // 0 = Chebyshev (Alg. 2), 1 = Newton (Alg. 1)
+    int nlev = 0;              // Newton: number of levels (degree 2^nlev - 1)
+    std::vector<double> zeta;  // Newton: zeta_0 .. zeta_nlev
+    npc::DevBuf nbuf;          // Newton: 2 work vectors per level >= 2
     int degree = 0;
     double lmin = 0, lmax = 0, xi = 0;
     double theta_bar = 0, delta = 0, sigma = 0;

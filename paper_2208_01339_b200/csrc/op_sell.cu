@@ -91,6 +91,42 @@ __global__ void __launch_bounds__(SELL_C *SELL_TW) k_sell_step(SellDev A, StepAr
         const long long gbase = (long long)seg0 + off;
         double y = 0.0;
         int j = 0;
+        if (!STAGED) {
+            // software pipeline: the next group's slot loads are in flight while this group's
+            // x gathers wait (the kernel is bound by memory latency: long-scoreboard stalls)
+            const int *__restrict__ cp = A.cols + gbase;
+            const double *__restrict__ vp = A.vals + gbase;
+            int cn[4];
+            double vn[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (u < len) {
+                    cn[u] = __ldcs(cp + u * SELL_C);
+                    vn[u] = __ldcs(vp + u * SELL_C);
+                }
+            for (; j < len; j += 4) {
+                int c[4];
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    c[u] = cn[u];
+                    v[u] = vn[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (j + 4 + u < len) {
+                        cn[u] = __ldcs(cp + (j + 4 + u) * SELL_C);
+                        vn[u] = __ldcs(vp + (j + 4 + u) * SELL_C);
+                    }
+                double xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    xv[u] = (j + u < len) ? ((GHOST && c[u] >= A.n) ? A.ghost[c[u] - A.n] : __ldg(X + c[u])) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (j + u < len) y += v[u] * xv[u];
+            }
+        }
         for (; j + 4 <= len; j += 4) {
             int c[4];
             double v[4];

@@ -125,8 +125,93 @@ npc_status poly_coefficients(int k, double lmin, double lmax, double xi, double 
 // written over s_{j-2}.  j = 1 folds s_0 = r/theta_bar into the coefficients (reads only r),
 // j = 2 folds c_2 s_0 into the r term (no s_{j-2} read).  With dotv != null the last kernel
 // emits partials of <z, dotv> into 'partials' (count returned in *nparts).
+// ================================================================== Newton (Alg. 1)
+// zeta_0 = 1/theta_bar; zeta_1 = 2/(1 + 2 a' zeta_0 - (a' zeta_0)^2) with a' = theta_bar - delta
+// (reading A1: Newton on the interval shifted by xi*theta); zeta_i = 2/(1 + 2 zeta_{i-1} -
+// zeta_{i-1}^2) (Eq. zetaNewt).  P_0 r = zeta_0 r, P_{j+1} r = zeta_{j+1}
+// (2 P_j r - P_j A P_j r) (Alg. 1 step 4): 2^nlev - 1 applications of A.
+npc_status newton_zetas(int nlev, double lmin, double lmax, double xi, std::vector<double> &zeta) {
+    double tb, dl, sg;
+    NPC_TRY(poly_coefficients(0, lmin, lmax, xi, &tb, &dl, &sg, nullptr));
+    const double ap = tb - dl;
+    zeta.assign(nlev + 1, 0.0);
+    zeta[0] = 1.0 / tb;
+    if (nlev >= 1) zeta[1] = 2.0 / (1.0 + 2.0 * ap * zeta[0] - (ap * zeta[0]) * (ap * zeta[0]));
+    for (int i = 2; i <= nlev; ++i) zeta[i] = 2.0 / (1.0 + 2.0 * zeta[i - 1] - zeta[i - 1] * zeta[i - 1]);
+    return NPC_SUCCESS;
+}
+
+// out = zeta (2 t1 - out)  (+ partial <out, dotv>)
+template <bool DOT>
+__global__ void __launch_bounds__(256) k_newton_combine(double *out, const double *__restrict__ t1, double zeta,
+                                                        int n, const double *__restrict__ dotv, double *partials,
+                                                        const int *done) {
+    if (done && *done) return;
+    __shared__ double red[8];
+    double acc = 0.0;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const double o = zeta * (2.0 * t1[i] - out[i]);
+        out[i] = o;
+        if (DOT) acc += o * dotv[i];
+    }
+    if (DOT) {
+        acc = block_sum<256>(acc, red);
+        if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+    }
+}
+
+static npc_status newton_level(npc_poly P, int j, const double *in, double *out, const double *dotv,
+                               double *partials, int *nparts, const int *done) {
+    Operator *op = P->op->op.get();
+    Context *ctx = op->ctx;
+    const std::vector<double> &z = P->zeta;
+    if (j == 0) {
+        TimedScope ts(ctx, T_DEGREE);
+        return launch_scale(ctx, in, out, z[0], op->n_local, dotv, partials, nparts, done);
+    }
+    if (j == 1) {  // P_1 in = zeta_1 (2 zeta_0 in - zeta_0^2 A in): one fused step
+        StepArgs s;
+        s.x = in;
+        s.out = out;
+        s.a = -z[1] * z[0] * z[0];
+        s.b = 2.0 * z[1] * z[0];
+        s.done = done;
+        if (dotv) {
+            s.dotv = dotv;
+            s.partials = partials;
+            if (nparts) *nparts = op->num_partials();
+        }
+        TimedScope ts(ctx, T_DEGREE);
+        return op->step(s);
+    }
+    const size_t nn = std::max(op->n_local, 1);
+    double *t1 = P->nbuf.as<double>() + (size_t)2 * (j - 2) * nn, *t2 = t1 + nn;
+    NPC_TRY(newton_level(P, j - 1, in, t1, nullptr, nullptr, nullptr, done));
+    {
+        StepArgs s;  // t2 = A t1
+        s.x = t1;
+        s.out = t2;
+        s.a = 1.0;
+        s.done = done;
+        TimedScope ts(ctx, T_DEGREE);
+        NPC_TRY(op->step(s));
+    }
+    NPC_TRY(newton_level(P, j - 1, t2, out, nullptr, nullptr, nullptr, done));
+    const int g = vec_grid(op->n_local);
+    TimedScope ts(ctx, T_VECTOR);
+    if (dotv) {
+        if (nparts) *nparts = g;
+        k_newton_combine<true><<<g, 256, 0, ctx->stream>>>(out, t1, z[j], op->n_local, dotv, partials, done);
+    } else {
+        k_newton_combine<false><<<g, 256, 0, ctx->stream>>>(out, t1, z[j], op->n_local, nullptr, nullptr, done);
+    }
+    NPC_LAUNCH_CHECK();
+    return NPC_SUCCESS;
+}
+
 npc_status apply_poly_internal(npc_poly P, const double *r, double *z, const double *dotv, double *partials,
                                int *nparts, const int *done) {
+    if (P->kind == 1) return newton_level(P, P->nlev, r, z, dotv, partials, nparts, done);
     Operator *op = P->op->op.get();
     Context *ctx = op->ctx;
     const int k = P->degree;

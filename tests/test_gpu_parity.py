@@ -157,6 +157,38 @@ def test_pcg_parity(ctx, wl, name, kind, k, xi):
         assert np.max(np.abs(xg - 1.0)) < 1e-2
 
 
+@pytest.mark.parametrize("name,kind", [("c1", "csr"), ("c3", "sell"), ("c2", "stencil"), ("c5", "schur")])
+@pytest.mark.parametrize("nlev", [0, 1, 2, 3, 5])
+@pytest.mark.parametrize("xi", [0.0, 1e-3])
+def test_newton_variant(ctx, wl, name, kind, nlev, xi):
+    """Alg. 1 on the GPU == the oracle's Alg. 1 == GPU Chebyshev of degree 2^nlev - 1."""
+    w = wl(name)
+    orc = oracle.Operator(w)
+    lmin, lmax = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
+    op = npc.create_from_workload(ctx, w, kind)
+    r = np.random.default_rng(nlev).uniform(-1, 1, w["n"])
+    zn = torch.empty(w["n"], dtype=torch.float64, device="cuda")
+    zc = torch.empty_like(zn)
+    npc.npc_apply_poly(npc.npc_set_poly_newton(op, nlev, lmin, lmax, xi), dev(r), zn)
+    npc.npc_apply_poly(npc.npc_set_poly(op, 2 ** nlev - 1, lmin, lmax, xi), dev(r), zc)
+    ref = oracle.newton_apply(orc, nlev, lmin, lmax, xi, r)
+    assert rel(host(zn), ref) <= POLY_TOL
+    assert rel(host(zn), host(zc)) <= 1e-10
+
+
+def test_tab_epsil_newton_on_gpu(ctx):
+    """Table tab:epsil was produced with Newton, nlev = 6: the GPU Newton
+    variant inside PCG reproduces its iteration column (58, 57, 50, 34, 39, 62) +-1."""
+    w = W.tab_epsil_diag()
+    op = npc.create_from_workload(ctx, w)
+    for xi, it in [(0.0, 58), (1e-6, 57), (1e-5, 50), (1e-4, 34), (1e-3, 39), (1e-2, 62)]:
+        poly = npc.npc_set_poly_newton(op, 6, 1.0, 1e5, xi)
+        x = torch.zeros(w["n"], dtype=torch.float64, device="cuda")
+        st = npc.npc_pcg_solve(poly, op, dev(w["b"]), x, 1e-10, 500)
+        assert abs(st["iters"] - it) <= 1 and st["relres_true"] <= 1e-10
+        assert st["op_applications"] == st["iters"] * 64 + 1
+
+
 def test_schur_deterministic_mode(ctx, wl, monkeypatch):
     """NPC_SCHUR_DETERMINISTIC=1 selects the two-pass (no atomics) Schur form: same parity,
     and bit-identical results run to run."""
