@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnpc.so")
+LIB_PATH = os.environ.get("NPC_LIB_PATH") or os.path.join(_HERE, "libnpc.so")  # override: A/B variants
 
 NPC_OP_CSR, NPC_OP_SELL, NPC_OP_STENCIL, NPC_OP_SCHUR, NPC_OP_CALLBACK = range(5)
 STATUS = {0: "NPC_SUCCESS", 1: "NPC_ERR_INVALID_ARGUMENT", 2: "NPC_ERR_DIMENSION",

@@ -38,7 +38,28 @@ def _flags():
     inc, _ = nccl_dirs()
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I", INCLUDE,
                    "-I", CSRC, "-I", inc, "--expt-relaxed-constexpr", "-Xptxas", "-v"] + \
-        (["-DNPC_DEBUG"] if os.environ.get("NPC_DEBUG") else [])
+        (["-DNPC_DEBUG"] if os.environ.get("NPC_DEBUG") else []) + \
+        os.environ.get("NPC_EXTRA_FLAGS", "").split()
+
+
+def build_variant(name: str, defines: list[str]) -> str:
+    """Build an A/B variant of the library (tuning experiments only) to
+    paper_2208_01339_b200/variants/libnpc_<name>.so; load it with NPC_LIB_PATH=<path>."""
+    global LIB, OBJDIR
+    saved = (LIB, OBJDIR, os.environ.get("NPC_EXTRA_FLAGS"))
+    vdir = os.path.join(PKG, "variants")
+    os.makedirs(vdir, exist_ok=True)
+    LIB = os.path.join(vdir, f"libnpc_{name}.so")
+    OBJDIR = os.path.join(PKG, "build", f"variant_{name}")
+    os.environ["NPC_EXTRA_FLAGS"] = " ".join(defines)
+    try:
+        return build()
+    finally:
+        LIB, OBJDIR = saved[0], saved[1]
+        if saved[2] is None:
+            os.environ.pop("NPC_EXTRA_FLAGS", None)
+        else:
+            os.environ["NPC_EXTRA_FLAGS"] = saved[2]
 
 
 def _digest(paths, flags):

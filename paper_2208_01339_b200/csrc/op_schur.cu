@@ -334,6 +334,12 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
             }
         byl[L].push_back(q);
     }
+    // Within a length class, order B's rows by their first (smallest) column: the first-column
+    // gathers of v and scatters into y of a warp then fall on a few adjacent sectors, which
+    // cuts the L2 RED sector count (the kernel's bound) for one entry in every row.
+    for (int L = 1; L <= 4; ++L)
+        std::stable_sort(byl[L].begin(), byl[L].end(),
+                         [&](int a, int b) { return d->b_colidx[d->b_rowptr[a]] < d->b_colidx[d->b_rowptr[b]]; });
     auto op = std::make_unique<SchurOperator>();
     op->ctx = ctx;
     op->kind = NPC_OP_SCHUR;

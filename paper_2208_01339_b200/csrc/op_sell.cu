@@ -39,9 +39,13 @@ struct SellDev {
     const double *ghost;
 };
 
+#ifndef NPC_SELL_MINB
+#define NPC_SELL_MINB 1  // min resident CTAs per SM for the register allocator (A/B-tuned)
+#endif
+
 template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST>
-__global__ void __launch_bounds__(SELL_C *SELL_TW) k_sell_step(SellDev A, StepArgs s, const int *__restrict__ tiles,
-                                                               int span_max) {
+__global__ void __launch_bounds__(SELL_C *SELL_TW, NPC_SELL_MINB)
+    k_sell_step(SellDev A, StepArgs s, const int *__restrict__ tiles, int span_max) {
     if (s.done && *s.done) return;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t bar;
@@ -91,7 +95,11 @@ __global__ void __launch_bounds__(SELL_C *SELL_TW) k_sell_step(SellDev A, StepAr
         const long long gbase = (long long)seg0 + off;
         double y = 0.0;
         int j = 0;
+#ifdef NPC_SELL_NOPIPE
+        if (false) {
+#else
         if (!STAGED) {
+#endif
             // software pipeline: the next group's slot loads are in flight while this group's
             // x gathers wait (the kernel is bound by memory latency: long-scoreboard stalls)
             const int *__restrict__ cp = A.cols + gbase;

@@ -1,0 +1,60 @@
+#!/usr/bin/env python
+"""A/B timing of library build variants (tuning experiments; never a bench value).
+
+    python tools/ab_variants.py --config 4 --side 2000000 --k 60 --libs a.so,b.so
+
+Each variant library is loaded in a fresh subprocess (NPC_LIB_PATH) and times `reps`
+applications of p_k(A) r with CUDA events; prints one JSON line per variant.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, ROOT)
+import bench, paper_2208_01339_b200 as npc
+w = bench.make_workload(CFG, SIDE)
+kind = KIND or bench.op_kind(w, CFG)
+ctx = npc.npc_context_create(0)
+op = npc.create_from_workload(ctx, w, kind)
+lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+poly = npc.npc_set_poly(op, K, lo, hi, 0.0)
+b = torch.tensor(w["b"], device="cuda"); z = torch.empty_like(b)
+for _ in range(3): npc.npc_apply_poly(poly, b, z)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(REPS): npc.npc_apply_poly(poly, b, z)
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / REPS
+M, V = bench.matrix_bytes(w, kind), 8 * w["n"]
+print(json.dumps(dict(lib=npc.LIB_PATH, ms=ms, gbs=bench.poly_bytes(M, V, K) / (ms * 1e-3) / 1e9,
+                      znorm=float(torch.linalg.norm(z)))))
+"""
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--side", type=int, default=None)
+    ap.add_argument("--kind", default=None)
+    ap.add_argument("--k", type=int, default=60)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--libs", required=True)
+    a = ap.parse_args()
+    code = CHILD.replace("ROOT", repr(ROOT)).replace("CFG", str(a.config)).replace("SIDE", repr(a.side)) \
+        .replace("KIND", repr(a.kind)).replace("REPS", str(a.reps)).replace("K,", f"{a.k},") \
+        .replace("(M, V, K)", f"(M, V, {a.k})")
+    for lib in a.libs.split(","):
+        env = dict(os.environ, NPC_LIB_PATH=os.path.abspath(lib))
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        print(r.stdout.strip() or r.stderr[-2000:], flush=True)
+
+
+if __name__ == "__main__":
+    main()
