@@ -112,7 +112,11 @@ def test_lanczos_parity(ctx, wl, name, kind):
     for key in ("theta_min", "theta_max", "rho"):
         assert abs(ex0[key] - ex[key]) <= 1e-9 * abs(ex["theta_max"])
     lo, hi = npc.npc_estimate_spectrum(op, 20, None)
-    assert lo == ex["theta_min"] and hi == ex["theta_max"] + ex["rho"]
+    if kind != "schur":
+        assert lo == ex["theta_min"] and hi == ex["theta_max"] + ex["rho"]
+    else:  # a third run: same bar as ex0 vs ex above
+        assert abs(lo - ex["theta_min"]) <= 1e-9 * abs(ex["theta_max"])
+        assert abs(hi - (ex["theta_max"] + ex["rho"])) <= 2e-9 * abs(ex["theta_max"])
     # theta_max has converged after 20 steps: unique to rounding.  theta_min and rho have not,
     # and Lanczos without reorthogonalisation amplifies rounding once orthogonality is lost,
     # so their bar is the oracle's own sensitivity to a 1e-15 relative perturbation of v0 (x20).
