@@ -198,6 +198,17 @@ def create_operator(npc, ctx, w, kind, ws, rank, cfg):
                                      rowptr=(rp - rp[0]).astype(np.int32), colidx=w["colidx"][rp[0]:rp[-1]],
                                      vals=w["vals"][rp[0]:rp[-1]], sell_C=32, sell_sigma=256)
         return op, r0, r1
+    if kind == "schur":
+        # trace rows and B rows in contiguous blocks: the B pass needs
+        # all of v (allgather) and its partial B^T t covers all trace rows (reduce-scatter)
+        nb = w["nb"]
+        q0, q1 = nb * rank // ws, nb * (rank + 1) // ws
+        bp = w["browptr"][q0:q1 + 1]
+        op = npc.npc_create_operator(ctx, "schur", n_local=r1 - r0, n_global=w["n"], row_begin=r0,
+                                     c=w["c"][r0:r1], b_rows_global=nb, b_row_begin=q0, b_n_local=q1 - q0,
+                                     b_rowptr=(bp - bp[0]).astype(np.int32), b_colidx=w["bcolidx"][bp[0]:bp[-1]],
+                                     b_vals=w["bvals"][bp[0]:bp[-1]], d=w["d"][q0:q1])
+        return op, r0, r1
     raise SystemExit(f"config kind {kind} does not support --gpus > 1 in this version")
 
 

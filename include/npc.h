@@ -116,9 +116,11 @@ typedef struct {
      * y_i = diag*x_i + offdiag * sum of the existing neighbours (homogeneous Dirichlet). */
     int stencil_dim, nx, ny, nz_global, z_begin, nz_local;
     double diag, offdiag;
-    /* SCHUR: c[n_local] (diagonal shift of the tridiagonal block), B rows
-     * [b_row_begin, b_row_begin + b_n_local) as CSR with GLOBAL column ids (trace unknowns),
-     * d[b_n_local] > 0.  nranks > 1 is not supported in this version.                       */
+    /* SCHUR: c[n_local] (diagonal shift of the tridiagonal block over the rank's trace rows),
+     * B rows [b_row_begin, b_row_begin + b_n_local) as CSR with GLOBAL column ids (trace
+     * unknowns, 0..4 entries per row), d[b_n_local] > 0.  The B rows a rank owns are free
+     * (any block); with nranks > 1 each application all-gathers v, applies the rank's B rows
+     * and reduce-scatters B^T D^-1 B v to the trace-row owners.      */
     const double *c;
     long long b_rows_global;
     long long b_row_begin;

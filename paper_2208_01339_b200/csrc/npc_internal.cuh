@@ -142,6 +142,14 @@ class Transport {
                                 const std::vector<int> &soff, double *rbuf, const std::vector<int> &rcount,
                                 const std::vector<int> &roff, cudaStream_t s) = 0;
     virtual npc_status allreduce_sum(Context *c, double *dev, int count, cudaStream_t s) = 0;
+    // Padded-slot collectives of the Schur operator (slot q = [q m, q m + m) of a P*m buffer;
+    // rank q's valid entries are the first counts[q] of its slot):
+    //   allgather_slots: in place, every rank's slot is copied into every rank's buffer;
+    //   reduce_scatter_slots: mine[0..m) = sum over ranks of their full[rank*m .. +m).
+    virtual npc_status allgather_slots(Context *c, double *full, int m, const std::vector<int> &counts,
+                                       cudaStream_t s) = 0;
+    virtual npc_status reduce_scatter_slots(Context *c, const double *full, double *mine, int m,
+                                            cudaStream_t s) = 0;
 };
 npc_status make_nccl_transport(Context *c, const void *uid, std::unique_ptr<Transport> &out);
 npc_status make_local_transport(Context *c, const char *group, std::unique_ptr<Transport> &out);
@@ -207,6 +215,8 @@ npc_status launch_gather(Context *ctx, const double *in, const int *idx, double 
 npc_status launch_scatter(Context *ctx, const double *in, const int *idx, double *out, int n);
 npc_status launch_fill(Context *ctx, double *out, double v, int n);
 npc_status launch_hash_vector(Context *ctx, double *out, int n, long long offset, unsigned long long seed);
+// out[i] = sum_{q=0..P-1} rows[q*m + i] in q order (i < m), on stream s
+npc_status launch_sum_rows(Context *ctx, const double *rows, int P, int m, double *out, cudaStream_t s);
 
 // Grid size of the plain vector kernels for n entries (fixed: partial counts are static).
 int vec_grid(int n);

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(32 * SB_WARPS) k_schur_bpass_atomic(const int 
 
 template <bool HAS_S2, bool HAS_R, bool DOT>
 __global__ void __launch_bounds__(ST_TILE) k_schur_tstep(const double *__restrict__ cshift, double *y, int n,
-                                                         StepArgs s) {
+                                                         StepArgs s, const double *xl, const double *xr) {
     if (s.done && *s.done) return;
     __shared__ double red[ST_TILE / 32];
     double acc = 0.0;
@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(ST_TILE) k_schur_tstep(const double *__restric
         const double xi = X[i];
         double sv = (2.0 + cshift[i]) * xi;
         if (i > 0) sv -= X[i - 1];
+        else if (xl) sv -= *xl;  // multi-rank: last row of the previous rank
         if (i < n - 1) sv -= X[i + 1];
+        else if (xr) sv -= *xr;  // first row of the next rank
         sv += y[i];
         y[i] = 0.0;
         double o = s.a * sv + s.b * xi;
@@ -216,6 +218,13 @@ class SchurOperator : public Operator {
     bool staged = true;
     bool deterministic = false;  // two-pass form (NPC_SCHUR_DETERMINISTIC=1 at create time)
     int grid2 = 1;               // atomic form: grid of k_schur_tstep
+    // multi-rank (nranks > 1, atomic form): P slots of m entries; B column ids are remapped to
+    // slot positions.  Per application: own x -> my slot of xfull, allgather the slots, B pass
+    // of the rank's B rows into yfull, reduce-scatter yfull -> yown, reset yfull, C + epilogue.
+    bool multi = false;
+    int m = 0, xl_pos = -1, xr_pos = -1;
+    std::vector<int> counts;
+    DevBuf xfull, yfull, yown;
 
     int num_partials() const override { return deterministic ? std::max(ntiles, 1) : grid2; }
     double bytes_per_step(bool has_s2, bool has_r) const override {
@@ -251,16 +260,34 @@ class SchurOperator : public Operator {
     }
     template <bool H2, bool HR, bool DT>
     npc_status launch_t(const StepArgs &s) {
-        k_schur_tstep<H2, HR, DT><<<grid2, ST_TILE, 0, ctx->stream>>>(cshift.as<double>(), t.as<double>(), n_local, s);
+        const double *xl = multi && xl_pos >= 0 ? xfull.as<double>() + xl_pos : nullptr;
+        const double *xr = multi && xr_pos >= 0 ? xfull.as<double>() + xr_pos : nullptr;
+        double *y = multi ? yown.as<double>() : t.as<double>();
+        k_schur_tstep<H2, HR, DT><<<grid2, ST_TILE, 0, ctx->stream>>>(cshift.as<double>(), y, n_local, s, xl, xr);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
     npc_status step_atomic(const StepArgs &s) {
+        const double *v = s.x;
+        double *y = t.as<double>();
+        if (multi) {
+            double *xf = xfull.as<double>();
+            if (n_local)
+                NPC_CUDA_TRY(cudaMemcpyAsync(xf + (size_t)ctx->rank * m, s.x, sizeof(double) * n_local,
+                                             cudaMemcpyDeviceToDevice, ctx->stream));
+            NPC_TRY(ctx->tr->allgather_slots(ctx, xf, m, counts, ctx->stream));
+            v = xf;
+            y = yfull.as<double>();
+        }
         if (nchunks) {
             k_schur_bpass_atomic<<<ceil_div(nchunks, SB_WARPS), 32 * SB_WARPS, 0, ctx->stream>>>(
-                chunk_off.as<int>(), chunk_len.as<int>(), nchunks, bcols.as<int>(), bvals.as<double>(), s.x,
-                t.as<double>(), s.done);
+                chunk_off.as<int>(), chunk_len.as<int>(), nchunks, bcols.as<int>(), bvals.as<double>(), v, y,
+                s.done);
             NPC_LAUNCH_CHECK();
+        }
+        if (multi) {
+            NPC_TRY(ctx->tr->reduce_scatter_slots(ctx, yfull.as<double>(), yown.as<double>(), m, ctx->stream));
+            NPC_CUDA_TRY(cudaMemsetAsync(yfull.p, 0, yfull.bytes, ctx->stream));
         }
         const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
         if (h2 && hr && dt) return launch_t<true, true, true>(s);
@@ -273,7 +300,7 @@ class SchurOperator : public Operator {
         return launch_t<false, false, false>(s);
     }
     npc_status step(const StepArgs &s) override {
-        if (n_local == 0) return NPC_SUCCESS;
+        if (n_local == 0 && !multi) return NPC_SUCCESS;
         if (!deterministic) return step_atomic(s);
         if (nchunks) {
             k_schur_bpass<<<ceil_div(nchunks, SB_WARPS), 32 * SB_WARPS, 0, ctx->stream>>>(
@@ -294,16 +321,37 @@ class SchurOperator : public Operator {
 };
 
 npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out) {
-    if (ctx->nranks > 1) {
-        set_error("SCHUR: nranks > 1 is not supported in this version");
-        return NPC_ERR_UNSUPPORTED;
-    }
     const int n = d->n_local, nb = d->b_n_local;
+    const bool multi = ctx->nranks > 1;
     if (n < 0 || nb < 0 || (n > 0 && !d->c) || (nb > 0 && (!d->b_rowptr || !d->b_colidx || !d->b_vals || !d->d))) {
         set_error("SCHUR: invalid arrays");
         return NPC_ERR_INVALID_ARGUMENT;
     }
-    if ((d->n_global && d->n_global != n) || (d->b_rows_global && d->b_rows_global != nb)) {
+    if (multi && getenv("NPC_SCHUR_DETERMINISTIC")) {
+        set_error("SCHUR: the deterministic two-pass form is single-rank only");
+        return NPC_ERR_UNSUPPORTED;
+    }
+    // trace-row partition: every rank's (row_begin, n_local) -> slot layout
+    std::vector<long long> starts{0}, all_n;
+    long long n_global = n;
+    if (multi) {
+        NPC_TRY(ctx->tr->allgather_i64(ctx, n, all_n));
+        for (long long c : all_n) starts.push_back(starts.back() + c);
+        n_global = starts.back();
+        if (d->row_begin != starts[ctx->rank] || (d->n_global && d->n_global != n_global)) {
+            set_error("SCHUR: rank %d row_begin %lld / n_global %lld disagree with the partition", ctx->rank,
+                      d->row_begin, d->n_global);
+            return NPC_ERR_DIMENSION;
+        }
+        long long nbg = 0;
+        std::vector<long long> all_nb;
+        NPC_TRY(ctx->tr->allgather_i64(ctx, nb, all_nb));
+        for (long long c : all_nb) nbg += c;
+        if (d->b_rows_global && d->b_rows_global != nbg) {
+            set_error("SCHUR: b_rows_global disagrees with the sum of b_n_local");
+            return NPC_ERR_DIMENSION;
+        }
+    } else if ((d->n_global && d->n_global != n) || (d->b_rows_global && d->b_rows_global != nb)) {
         set_error("SCHUR: sizes disagree");
         return NPC_ERR_DIMENSION;
     }
@@ -328,7 +376,7 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
             return NPC_ERR_DIMENSION;
         }
         for (int p = d->b_rowptr[q]; p < d->b_rowptr[q + 1]; ++p)
-            if (d->b_colidx[p] < 0 || d->b_colidx[p] >= n || !std::isfinite(d->b_vals[p])) {
+            if (d->b_colidx[p] < 0 || d->b_colidx[p] >= n_global || !std::isfinite(d->b_vals[p])) {
                 set_error("SCHUR: bad B entry in row %d", q);
                 return NPC_ERR_DIMENSION;
             }
@@ -344,8 +392,20 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
     op->ctx = ctx;
     op->kind = NPC_OP_SCHUR;
     op->n_local = n;
-    op->n_global = n;
+    op->n_global = n_global;
+    op->row_begin = d->row_begin;
     op->nnz = nb ? d->b_rowptr[nb] : 0;
+    // global column id -> position in the slot layout (identity on one rank)
+    int m = n;
+    if (multi) {
+        m = 1;
+        for (long long c : all_n) m = std::max<long long>(m, c);
+    }
+    auto colpos = [&](int c) -> int {
+        if (!multi) return c;
+        const int q = (int)(std::upper_bound(starts.begin(), starts.end(), (long long)c) - starts.begin()) - 1;
+        return q * m + (int)(c - starts[q]);
+    };
     // ---- Bt = D^{-1/2} B, rows ordered by length, SELL-32
     std::vector<int> order;
     std::vector<int> coff{0}, clen;
@@ -371,9 +431,9 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
             for (int j = 0; j < clen[ch]; ++j) {
                 const size_t slot = (size_t)coff[ch] + (size_t)j * 32 + l;
                 const int p = d->b_rowptr[q] + j;
-                scols[slot] = d->b_colidx[p];
+                scols[slot] = colpos(d->b_colidx[p]);
                 svals[slot] = d->b_vals[p] * sc;
-                tcount[d->b_colidx[p] + 1]++;
+                if (!multi) tcount[d->b_colidx[p] + 1]++;
             }
         }
     op->deterministic = getenv("NPC_SCHUR_DETERMINISTIC") != nullptr;
@@ -392,6 +452,29 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
             NPC_CUDA_TRY(cudaMemcpy(op->chunk_len.p, clen.data(), sizeof(int) * clen.size(), cudaMemcpyHostToDevice));
             NPC_CUDA_TRY(cudaMemcpy(op->bcols.p, scols.data(), sizeof(int) * scols.size(), cudaMemcpyHostToDevice));
             NPC_CUDA_TRY(cudaMemcpy(op->bvals.p, svals.data(), sizeof(double) * svals.size(), cudaMemcpyHostToDevice));
+        }
+        if (multi) {
+            const int P = ctx->nranks, r = ctx->rank;
+            op->multi = true;
+            op->m = m;
+            op->counts.assign(all_n.begin(), all_n.end());
+            // neighbours of the rank's end rows in the tridiagonal block: last row of the
+            // nearest non-empty rank below, first row of the nearest non-empty rank above
+            for (int q = r - 1; q >= 0 && n > 0; --q)
+                if (all_n[q] > 0) {
+                    op->xl_pos = q * m + (int)all_n[q] - 1;
+                    break;
+                }
+            for (int q = r + 1; q < P && n > 0; ++q)
+                if (all_n[q] > 0) {
+                    op->xr_pos = q * m;
+                    break;
+                }
+            NPC_TRY(op->xfull.alloc(sizeof(double) * (size_t)P * m));
+            NPC_TRY(op->yfull.alloc(sizeof(double) * (size_t)P * m));
+            NPC_TRY(op->yown.alloc(sizeof(double) * (size_t)m));
+            NPC_CUDA_TRY(cudaMemset(op->xfull.p, 0, op->xfull.bytes));
+            NPC_CUDA_TRY(cudaMemset(op->yfull.p, 0, op->yfull.bytes));
         }
         out = std::move(op);
         return NPC_SUCCESS;

@@ -40,8 +40,12 @@ struct SellDev {
 };
 
 #ifndef NPC_SELL_MINB
-#define NPC_SELL_MINB 1  // min resident CTAs per SM for the register allocator (A/B-tuned)
+#define NPC_SELL_MINB 8  // min resident CTAs per SM for the register allocator (A/B-tuned)
 #endif
+#ifndef NPC_SELL_U
+#define NPC_SELL_U 4  // slots per load group of the direct path (A/B-tuned)
+#endif
+static constexpr int SELL_U = NPC_SELL_U;
 
 template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST>
 __global__ void __launch_bounds__(SELL_C *SELL_TW, NPC_SELL_MINB)
@@ -78,99 +82,67 @@ __global__ void __launch_bounds__(SELL_C *SELL_TW, NPC_SELL_MINB)
     const int row = ch * SELL_C + lane;
     const bool active = ch < ch1 && row < A.n;
     const double *__restrict__ X = s.x;
-    double xs = 0.0, s2v = 0.0, rv = 0.0;
-    int len = 0, off = 0;
-    if (ch < ch1) {
-        len = A.chunk_len[ch];
-        off = A.chunk_off[ch] - seg0 + lane;
-    }
-    if (active) {
-        xs = X[row];
-        if (HAS_S2) s2v = s.s2[row];
-        if (HAS_R) rv = s.r[row];
-    }
-    if (STAGED) mbar_wait(&bar, 0);
     double acc = 0.0;
-    if (ch < ch1) {
-        const long long gbase = (long long)seg0 + off;
-        double y = 0.0;
-        int j = 0;
-#ifdef NPC_SELL_NOPIPE
-        if (false) {
-#else
-        if (!STAGED) {
-#endif
-            // software pipeline: the next group's slot loads are in flight while this group's
-            // x gathers wait (the kernel is bound by memory latency: long-scoreboard stalls)
-            const int *__restrict__ cp = A.cols + gbase;
-            const double *__restrict__ vp = A.vals + gbase;
-            int cn[4];
-            double vn[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (u < len) {
-                    cn[u] = __ldcs(cp + u * SELL_C);
-                    vn[u] = __ldcs(vp + u * SELL_C);
-                }
-            for (; j < len; j += 4) {
-                int c[4];
-                double v[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    c[u] = cn[u];
-                    v[u] = vn[u];
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (j + 4 + u < len) {
-                        cn[u] = __ldcs(cp + (j + 4 + u) * SELL_C);
-                        vn[u] = __ldcs(vp + (j + 4 + u) * SELL_C);
-                    }
-                double xv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    xv[u] = (j + u < len) ? ((GHOST && c[u] >= A.n) ? A.ghost[c[u] - A.n] : __ldg(X + c[u])) : 0.0;
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (j + u < len) y += v[u] * xv[u];
-            }
-        }
-        for (; j + 4 <= len; j += 4) {
-            int c[4];
-            double v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (STAGED) {
-                    c[u] = sc[off + (j + u) * SELL_C];
-                    v[u] = sv[off + (j + u) * SELL_C];
-                } else {
-                    c[u] = __ldcs(A.cols + gbase + (long long)(j + u) * SELL_C);
-                    v[u] = __ldcs(A.vals + gbase + (long long)(j + u) * SELL_C);
-                }
-            }
-            double xv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) xv[u] = (GHOST && c[u] >= A.n) ? A.ghost[c[u] - A.n] : __ldg(X + c[u]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) y += v[u] * xv[u];
-        }
-        for (; j < len; ++j) {
-            int c;
-            double v;
-            if (STAGED) {
-                c = sc[off + j * SELL_C];
-                v = sv[off + j * SELL_C];
-            } else {
-                c = __ldcs(A.cols + gbase + (long long)j * SELL_C);
-                v = __ldcs(A.vals + gbase + (long long)j * SELL_C);
-            }
-            const double xv = (GHOST && c >= A.n) ? A.ghost[c - A.n] : __ldg(X + c);
-            y += v * xv;
+    if (STAGED) {
+        double xs = 0.0, s2v = 0.0, rv = 0.0;
+        int len = 0, off = 0;
+        if (ch < ch1) {
+            len = A.chunk_len[ch];
+            off = A.chunk_off[ch] - seg0 + lane;
         }
         if (active) {
-            double o = s.a * y + s.b * xs;
-            if (HAS_S2) o += s.c * s2v;
-            if (HAS_R) o += s.d * rv;
+            xs = X[row];
+            if (HAS_S2) s2v = s.s2[row];
+            if (HAS_R) rv = s.r[row];
+        }
+        mbar_wait(&bar, 0);
+        if (ch < ch1) {
+            double y = 0.0;
+            for (int j = 0; j < len; ++j) {
+                const int c = sc[off + j * SELL_C];
+                const double v = sv[off + j * SELL_C];
+                y += v * ((GHOST && c >= A.n) ? A.ghost[c - A.n] : __ldg(X + c));
+            }
+            if (active) {
+                double o = s.a * y + s.b * xs;
+                if (HAS_S2) o += s.c * s2v;
+                if (HAS_R) o += s.d * rv;
+                s.out[row] = o;
+                if (DOT) acc = o * s.dotv[row];
+            }
+        }
+    } else if (ch < ch1) {
+        // Direct coalesced slot loads (each slot of a warp is one 256 B value + 128 B index
+        // line), SELL_U slots per group.  The kernel is bound by memory latency (the x gathers
+        // depend on the index loads), so it is tuned for occupancy: few live registers, the
+        // epilogue operands loaded after the loop (A/B: profiles/r01_sell_ab.md).
+        const int len = A.chunk_len[ch];
+        const long long gbase = (long long)A.chunk_off[ch] + lane;
+        const int *__restrict__ cp = A.cols + gbase;
+        const double *__restrict__ vp = A.vals + gbase;
+        double y = 0.0;
+        int j = 0;
+        for (; j + SELL_U <= len; j += SELL_U) {
+            int c[SELL_U];
+            double v[SELL_U];
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u) {
+                c[u] = __ldcs(cp + (j + u) * SELL_C);
+                v[u] = __ldcs(vp + (j + u) * SELL_C);
+            }
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u)
+                y += v[u] * ((GHOST && c[u] >= A.n) ? A.ghost[c[u] - A.n] : __ldg(X + c[u]));
+        }
+        for (; j < len; ++j) {
+            const int c = __ldcs(cp + j * SELL_C);
+            const double v = __ldcs(vp + j * SELL_C);
+            y += v * ((GHOST && c >= A.n) ? A.ghost[c - A.n] : __ldg(X + c));
+        }
+        if (active) {
+            double o = s.a * y + s.b * X[row];
+            if (HAS_S2) o += s.c * s.s2[row];
+            if (HAS_R) o += s.d * s.r[row];
             s.out[row] = o;
             if (DOT) acc = o * s.dotv[row];
         }

@@ -89,6 +89,17 @@ class NcclTransport : public Transport {
         NPC_NCCL_TRY(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, s));
         return NPC_SUCCESS;
     }
+    npc_status allgather_slots(Context *c, double *full, int m, const std::vector<int> &counts,
+                               cudaStream_t s) override {
+        (void)counts;
+        NPC_NCCL_TRY(ncclAllGather(full + (size_t)c->rank * m, full, m, ncclDouble, comm, s));
+        return NPC_SUCCESS;
+    }
+    npc_status reduce_scatter_slots(Context *c, const double *full, double *mine, int m, cudaStream_t s) override {
+        (void)c;
+        NPC_NCCL_TRY(ncclReduceScatter(full, mine, m, ncclDouble, ncclSum, comm, s));
+        return NPC_SUCCESS;
+    }
 };
 
 npc_status make_nccl_transport(Context *c, const void *uid, std::unique_ptr<Transport> &out) {
@@ -161,6 +172,7 @@ static std::map<std::string, std::weak_ptr<LocalGroup>> g_groups;
 class LocalTransport : public Transport {
   public:
     std::shared_ptr<LocalGroup> g;
+    DevBuf stage;  // reduce_scatter_slots: the P contributions to this rank's slot
     ~LocalTransport() override {
         if (g) g->abort();  // a rank leaving releases peers still waiting for it
     }
@@ -222,6 +234,47 @@ class LocalTransport : public Transport {
         }
         LT_CUDA_TRY(cudaStreamSynchronize(s));
         NPC_BARRIER(g);  // peers may now reuse their send buffers
+        return NPC_SUCCESS;
+    }
+    npc_status allgather_slots(Context *c, double *full, int m, const std::vector<int> &counts,
+                               cudaStream_t s) override {
+        LT_CUDA_TRY(cudaStreamSynchronize(s));  // my slot is complete
+        g->slot[c->rank] = full;
+        g->slot_device[c->rank] = c->device;
+        NPC_BARRIER(g);
+        for (int q = 0; q < c->nranks; ++q) {
+            if (q == c->rank || !counts[q]) continue;
+            const double *src = static_cast<const double *>(g->slot[q]) + (size_t)q * m;
+            if (g->slot_device[q] == c->device)
+                LT_CUDA_TRY(cudaMemcpyAsync(full + (size_t)q * m, src, sizeof(double) * counts[q],
+                                            cudaMemcpyDeviceToDevice, s));
+            else
+                LT_CUDA_TRY(cudaMemcpyPeerAsync(full + (size_t)q * m, c->device, src, g->slot_device[q],
+                                                sizeof(double) * counts[q], s));
+        }
+        LT_CUDA_TRY(cudaStreamSynchronize(s));
+        NPC_BARRIER(g);  // peers may now overwrite their buffers
+        return NPC_SUCCESS;
+    }
+    npc_status reduce_scatter_slots(Context *c, const double *full, double *mine, int m, cudaStream_t s) override {
+        const int P = c->nranks;
+        if (stage.bytes < sizeof(double) * (size_t)P * m) NPC_TRY(stage.alloc(sizeof(double) * (size_t)P * m));
+        LT_CUDA_TRY(cudaStreamSynchronize(s));
+        g->slot[c->rank] = full;
+        g->slot_device[c->rank] = c->device;
+        NPC_BARRIER(g);
+        double *st = stage.as<double>();
+        for (int q = 0; q < P; ++q) {  // rank q's contribution to my slot -> stage row q
+            const double *src = static_cast<const double *>(g->slot[q]) + (size_t)c->rank * m;
+            if (g->slot_device[q] == c->device)
+                LT_CUDA_TRY(cudaMemcpyAsync(st + (size_t)q * m, src, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+            else
+                LT_CUDA_TRY(cudaMemcpyPeerAsync(st + (size_t)q * m, c->device, src, g->slot_device[q],
+                                                sizeof(double) * m, s));
+        }
+        NPC_TRY(launch_sum_rows(c, st, P, m, mine, s));  // fixed rank order
+        LT_CUDA_TRY(cudaStreamSynchronize(s));
+        NPC_BARRIER(g);
         return NPC_SUCCESS;
     }
     npc_status allreduce_sum(Context *c, double *dev, int count, cudaStream_t s) override {

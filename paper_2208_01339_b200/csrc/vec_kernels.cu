@@ -181,6 +181,22 @@ npc_status launch_fill(Context *ctx, double *out, double v, int n) {
     return NPC_SUCCESS;
 }
 
+__global__ void k_sum_rows(const double *__restrict__ rows, int P, int m, double *__restrict__ out) {
+    for (int i = blockIdx.x * VT + threadIdx.x; i < m; i += gridDim.x * VT) {
+        double a = 0.0;
+        for (int q = 0; q < P; ++q) a += rows[(size_t)q * m + i];
+        out[i] = a;
+    }
+}
+
+npc_status launch_sum_rows(Context *ctx, const double *rows, int P, int m, double *out, cudaStream_t s) {
+    (void)ctx;
+    if (m <= 0) return NPC_SUCCESS;
+    k_sum_rows<<<vec_grid(m), VT, 0, s>>>(rows, P, m, out);
+    NPC_LAUNCH_CHECK();
+    return NPC_SUCCESS;
+}
+
 // splitmix64 of (seed, global index) -> uniform [-1, 1): identical for any rank count.
 __global__ void k_hash(double *out, int n, long long offset, unsigned long long seed) {
     for (int i = blockIdx.x * VT + threadIdx.x; i < n; i += gridDim.x * VT) {
