@@ -63,7 +63,11 @@ def lib():
         _lib.orc_newton_zeta.argtypes = [D, D, D, C.c_int, P]
         _lib.orc_newton_apply.argtypes = [C.POINTER(_Op), C.c_int, D, D, D, P, P, P]
         _lib.orc_lanczos.argtypes = [C.POINTER(_Op), C.c_int, P, P, P, P]
-        _lib.orc_pcg.argtypes = [C.POINTER(_Op), C.c_int, D, D, D, P, P, D, C.c_int, P, C.POINTER(_Stats)]
+        _lib.orc_pcg.argtypes = [C.POINTER(_Op), C.c_int, D, D, D, P, P, D, C.c_int, P, C.POINTER(_Stats),
+                                 C.c_int, P, P]
+        _lib.orc_lowrank_setup.argtypes = [C.POINTER(_Op), C.c_int, P, P, P]
+        _lib.orc_lowrank_apply.argtypes = [C.POINTER(_Op), C.c_int, D, D, D, C.c_int, P, P, P, P, P]
+        _lib.orc_lanczos_full.argtypes = [C.POINTER(_Op), C.c_int, P, P, P, P, P]
         _lib.orc_num_threads.restype = C.c_int
     return _lib
 
@@ -199,17 +203,72 @@ def estimate_spectrum(op: Operator, m, v0):
     return lo, th + rho
 
 
+class LowRank:
+    """V (n x p) and the Cholesky factor L of V^T A V: the low-rank spectral correction
+    P = P_0 + V (V^T A V)^{-1} V^T of PAPER.md:483-508 (O8)."""
+
+    def __init__(self, op: Operator, V):
+        V = np.asarray(V, dtype=np.float64)
+        if V.ndim == 1:
+            V = V[:, None]
+        assert V.shape[0] == op.n
+        self.p = V.shape[1]
+        self.Vc = np.ascontiguousarray(V.T)  # column j contiguous (column-major n x p)
+        self.L = np.zeros((self.p, self.p))
+        work = np.empty(op.n)
+        if lib().orc_lowrank_setup(C.byref(op.op), self.p, _p(self.Vc), _p(self.L), _p(work)) != 0:
+            raise ValueError("V^T A V is not SPD")
+
+
+def lowrank_apply(op: Operator, m, alpha, beta, xi, lr: LowRank, r):
+    """(p_m(A) + V (V^T A V)^{-1} V^T) r  (O8)."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    out = np.empty(op.n)
+    work = np.empty(3 * op.n)
+    st = lib().orc_lowrank_apply(C.byref(op.op), m, alpha, beta, xi, lr.p, _p(lr.Vc), _p(lr.L), _p(r), _p(out),
+                                 _p(work))
+    if st:
+        raise ValueError(f"lowrank_apply failed ({st})")
+    return out
+
+
+def lanczos_full(op: Operator, m, v0):
+    """m-step Lanczos with full reorthogonalisation; returns (alphas, betas, Q) with Q the
+    n x (s+1) basis (s = steps taken; the last column is valid only if beta_s > 0)."""
+    v0 = np.ascontiguousarray(v0, dtype=np.float64)
+    a = np.zeros(m)
+    b = np.zeros(m)
+    Q = np.zeros((m + 1, op.n))
+    w = np.empty(op.n)
+    s = lib().orc_lanczos_full(C.byref(op.op), m, _p(v0), _p(a), _p(b), _p(Q), _p(w))
+    assert s >= 0
+    return a[:s], b[:s], Q[: s + 1].T
+
+
+def ritz_vectors(op: Operator, m, p, v0):
+    """(theta[p], V n x p): Ritz pairs of the p smallest Ritz values of the fully
+    reorthogonalised m-step Lanczos (the tridiagonal eigenproblem via LAPACK through scipy,
+    a library primitive)."""
+    from scipy.linalg import eigh_tridiagonal
+    a, b, Q = lanczos_full(op, m, v0)
+    s = len(a)
+    ev, S = eigh_tridiagonal(a, b[: s - 1])
+    return ev[:p], Q[:, :s] @ S[:, :p]
+
+
 def pcg(op: Operator, b, m, alpha=None, beta=None, xi=0.0, tol=1e-8, maxit=10000, x0=None,
-        history=False):
-    """Textbook PCG (O5) preconditioned by p_m(A) (m < 0: none).  Returns (x, stats dict)."""
+        history=False, lowrank: LowRank | None = None):
+    """Textbook PCG (O5) preconditioned by p_m(A) (m < 0: none), plus the low-rank
+    correction V (V^T A V)^{-1} V^T when `lowrank` is given (O8).  Returns (x, stats dict)."""
     b = np.ascontiguousarray(b, dtype=np.float64)
     x = np.zeros(op.n) if x0 is None else np.array(x0, dtype=np.float64)
     hist = np.zeros(maxit + 1) if history else None
     st = _Stats()
     if m >= 0:
         assert alpha is not None and beta is not None
+    lr_p, lr_V, lr_L = (lowrank.p, _p(lowrank.Vc), _p(lowrank.L)) if lowrank is not None else (0, None, None)
     lib().orc_pcg(C.byref(op.op), m, float(alpha or 0.0), float(beta or 0.0), float(xi), _p(b), _p(x),
-                  tol, maxit, _p(hist), C.byref(st))
+                  tol, maxit, _p(hist), C.byref(st), lr_p, lr_V, lr_L)
     out = dict(iters=st.iters, converged=bool(st.converged), breakdown=bool(st.breakdown),
                mvp=st.mvp, ddot=st.ddot, relres_recursive=st.relres_recursive,
                relres_true=st.relres_true)

@@ -22,7 +22,9 @@
  *   orc_cheb_apply       P1 (Table tab:epsil eigenvalues), P3, P4 (spectrum bound), P6
  *   orc_newton_apply     P5 (Newton == Chebyshev), P12 (Fig. 1 values)
  *   orc_lanczos          P9 (n steps reproduce the spectrum; config-1 Ritz bracket)
- *   orc_pcg              P2 (Table tab:epsil iterations), P6, P10 (counter laws), P11
+ *   orc_pcg              P2 (Table tab:epsil iterations), P6, P10 (counter laws), P11, P15
+ *   orc_lowrank_setup/apply  P14 (Eq. plusone on exact eigenvectors), P15 (dense P, symmetry)
+ *   orc_lanczos_full     P16 (n steps: exact spectrum and eigenvectors of a dense SPD matrix)
  */
 #include <math.h>
 #include <stdlib.h>
@@ -231,6 +233,92 @@ static double dot(long n, const double *a, const double *b) {
     return s;
 }
 
+/* ------------------------------------------------------------------------------------ */
+/* Low-rank spectral correction (O8), PAPER.md:483-508 (Sec. "Low-rank acceleration"):    */
+/*     P = P_0 + V (V^T A V)^{-1} V^T,   V = [v_1 .. v_p]  (n x p, column j at V + j n),  */
+/* P_0 = p_m(A) (Alg. 2).  Setup: G = V^T A V formed entry by entry (G_ab = <v_a, A v_b>),*/
+/* then its Cholesky factor G = L L^T (plain row-by-row algorithm, L lower, p x p         */
+/* row-major).  Apply: s = V^T r; solve L y = s, L^T c = y; out = p_m(A) r + V c.         */
+/* ------------------------------------------------------------------------------------ */
+int orc_lowrank_setup(const orc_op *A, int p, const double *V, double *L, double *work) {
+    const long n = A->n;
+    double *G = (double *)malloc(sizeof(double) * p * p);
+    for (int b = 0; b < p; b++) {
+        orc_op_apply(A, V + (long)b * n, work);
+        for (int a = 0; a < p; a++) G[a * p + b] = dot(n, V + (long)a * n, work);
+    }
+    for (int a = 0; a < p * p; a++) L[a] = 0.0;
+    for (int i = 0; i < p; i++) {            /* Cholesky: L_ii = sqrt(G_ii - sum_k L_ik^2) ... */
+        for (int j = 0; j <= i; j++) {
+            double t = G[i * p + j];
+            for (int k = 0; k < j; k++) t -= L[i * p + k] * L[j * p + k];
+            if (i == j) {
+                if (!(t > 0.0)) { free(G); return -1; }   /* V^T A V not SPD */
+                L[i * p + i] = sqrt(t);
+            } else {
+                L[i * p + j] = t / L[j * p + j];
+            }
+        }
+    }
+    free(G);
+    return 0;
+}
+
+/* c = (L L^T)^{-1} V^T r, out += V c.  c: p doubles of scratch. */
+static void lowrank_add(long n, int p, const double *V, const double *L, const double *r, double *out, double *c) {
+    for (int a = 0; a < p; a++) c[a] = dot(n, V + (long)a * n, r);          /* s = V^T r */
+    for (int i = 0; i < p; i++) {                                             /* L y = s */
+        double t = c[i];
+        for (int k = 0; k < i; k++) t -= L[i * p + k] * c[k];
+        c[i] = t / L[i * p + i];
+    }
+    for (int i = p - 1; i >= 0; i--) {                                        /* L^T c = y */
+        double t = c[i];
+        for (int k = i + 1; k < p; k++) t -= L[k * p + i] * c[k];
+        c[i] = t / L[i * p + i];
+    }
+    for (int a = 0; a < p; a++)                                               /* out += V c */
+        for (long i = 0; i < n; i++) out[i] += V[(long)a * n + i] * c[a];
+}
+
+int orc_lowrank_apply(const orc_op *A, int m, double alpha, double beta, double xi, int p, const double *V,
+                      const double *L, const double *r, double *out, double *work) {
+    int st = orc_cheb_apply(A, m, alpha, beta, xi, r, out, work);
+    if (st) return st;
+    double *c = (double *)malloc(sizeof(double) * (p > 0 ? p : 1));
+    lowrank_add(A->n, p, V, L, r, out, c);
+    free(c);
+    return 0;
+}
+
+/* Lanczos with full reorthogonalisation (classical Gram-Schmidt applied twice against all */
+/* previous basis vectors), keeping the basis Q (m+1 vectors, column j at Q + j n) for     */
+/* Ritz vectors (O8 helper: approximate leftmost eigenvectors for V).  Returns the steps.  */
+int orc_lanczos_full(const orc_op *A, int m, const double *v0, double *alphas, double *betas, double *Q,
+                     double *w) {
+    const long n = A->n;
+    double nv = sqrt(dot(n, v0, v0));
+    if (!(nv > 0.0)) return -1;
+    long i;
+    for (i = 0; i < n; i++) Q[i] = v0[i] / nv;
+    int j;
+    for (j = 0; j < m; j++) {
+        double *q = Q + (long)j * n;
+        orc_op_apply(A, q, w);
+        alphas[j] = dot(n, q, w);
+        for (int pass = 0; pass < 2; pass++)
+            for (int l = 0; l <= j; l++) {
+                const double h = dot(n, Q + (long)l * n, w);
+                for (i = 0; i < n; i++) w[i] -= h * Q[(long)l * n + i];
+            }
+        double bnext = sqrt(dot(n, w, w));
+        betas[j] = bnext;
+        if (bnext == 0.0) { j++; break; }
+        for (i = 0; i < n; i++) Q[(long)(j + 1) * n + i] = w[i] / bnext;
+    }
+    return j;
+}
+
 int orc_lanczos(const orc_op *A, int m, const double *v0, double *alphas, double *betas, double *work) {
     const long n = A->n;
     double *q = work, *q_prev = work + n, *w = work + 2 * n;
@@ -269,12 +357,14 @@ typedef struct {
 } orc_pcg_stats;
 
 int orc_pcg(const orc_op *A, int m, double alpha, double beta, double xi,
-            const double *b, double *x, double tol, int maxit, double *history, orc_pcg_stats *st) {
+            const double *b, double *x, double tol, int maxit, double *history, orc_pcg_stats *st,
+            int lr_p, const double *lr_V, const double *lr_L) {
     const long n = A->n;
     long i;
     double *r = (double *)malloc(sizeof(double) * n), *z = (double *)malloc(sizeof(double) * n);
     double *p = (double *)malloc(sizeof(double) * n), *q = (double *)malloc(sizeof(double) * n);
     double *work = (double *)malloc(sizeof(double) * 3 * n);
+    double *lr_c = (double *)malloc(sizeof(double) * (lr_p > 0 ? lr_p : 1));
     memset(st, 0, sizeof(*st));
     int true_done = 0;          /* true residual computed for the final x */
     double rr = 0.0, rz = 0.0;
@@ -302,6 +392,7 @@ int orc_pcg(const orc_op *A, int m, double alpha, double beta, double xi,
     do {                                                                               \
         if (m < 0) memcpy(dst, src, sizeof(double) * n);                               \
         else { orc_cheb_apply(A, m, alpha, beta, xi, src, dst, work); st->mvp += m; }   \
+        if (lr_p > 0) { lowrank_add(n, lr_p, lr_V, lr_L, src, dst, lr_c); st->ddot += lr_p; } \
     } while (0)
     APPLY_M(r, z);
     for (i = 0; i < n; i++) p[i] = z[i];
@@ -342,6 +433,6 @@ done:
         for (i = 0; i < n; i++) q[i] = b[i] - q[i];
         st->relres_true = sqrt(dot(n, q, q)) / bnorm; st->ddot++;
     }
-    free(r); free(z); free(p); free(q); free(work);
+    free(r); free(z); free(p); free(q); free(work); free(lr_c);
     return 0;
 }

@@ -381,3 +381,90 @@ def test_schur_operator_matches_dense():
     x = np.random.default_rng(0).standard_normal(n)
     assert np.allclose(op.apply(x), S @ x, rtol=1e-12, atol=1e-12)
     assert np.linalg.eigvalsh(S).min() > 0
+
+
+# ---------------------------------------------------------------- P14-P16: low-rank correction (O8)
+def _lap1d(n):
+    rowptr, colidx, vals = W.laplacian_1d_csr(n)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    i = np.arange(1, n + 1)
+    lam = 4 * np.sin(np.arange(1, n + 1) * np.pi / (2 * (n + 1))) ** 2
+    vec = lambda j: np.sin(i * j * np.pi / (n + 1)) * math.sqrt(2.0 / (n + 1))  # noqa: E731  unit norm
+    return op, lam, vec
+
+
+@pytest.mark.parametrize("k,xi,p", [(0, 0.0, 1), (10, 0.0, 5), (20, 1e-3, 3), (63, 1e-2, 8)])
+def test_P14_plusone_on_exact_eigenvectors(k, xi, p):
+    """PAPER.md:495-500 (Eq. plusone): with V = the p leftmost eigenvectors,
+    P A v_j = (mu_j + 1) v_j for j <= p and P A v_j = mu_j v_j for j > p, where
+    mu_j = lambda_j p_k(lambda_j) from the Chebyshev closed form (not the oracle's Alg. 2)."""
+    n = 150
+    op, lam, vec = _lap1d(n)
+    alpha, beta = lam[0], lam[-1]
+    V = np.column_stack([vec(j) for j in range(1, p + 1)])
+    lr = oracle.LowRank(op, V)
+    for j in [1, 2, p, p + 1, p + 2, 60, n]:
+        v = vec(j)
+        mu = lam[j - 1] * p_closed(lam[j - 1], k, alpha, beta, xi)
+        z = oracle.lowrank_apply(op, k, alpha, beta, xi, lr, op.apply(v))
+        expect = (mu + (1.0 if j <= p else 0.0)) * v
+        assert np.linalg.norm(z - expect) <= 1e-10 * max(1.0, abs(mu)), (j, k, p)
+
+
+@pytest.mark.parametrize("seed,p,k", [(0, 1, 3), (1, 4, 8), (2, 6, 0)])
+def test_P15_dense_lowrank_operator_and_pcg(seed, p, k):
+    """P = P_0 + V (V^T A V)^{-1} V^T for an arbitrary (non-eigen) V, built densely with numpy
+    from its definition (P_0 from the eigendecomposition closed form, as in P6), equals the
+    oracle column by column; P is symmetric; PCG with P converges to the dense solution."""
+    n = 32
+    A, _ = W.random_spd_dense(n, seed, cond=1e3)
+    rowptr, colidx, vals = W.dense_to_csr(A)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    ev, E = np.linalg.eigh(A)
+    alpha, beta, xi = 1.0, 1e3, 1e-3
+    V = np.random.default_rng(seed + 50).standard_normal((n, p))
+    P_def = (E * p_closed(ev, k, alpha, beta, xi)) @ E.T + V @ np.linalg.solve(V.T @ A @ V, V.T)
+    lr = oracle.LowRank(op, V)
+    P = np.column_stack([oracle.lowrank_apply(op, k, alpha, beta, xi, lr, e) for e in np.eye(n)])
+    assert np.linalg.norm(P - P_def) / np.linalg.norm(P_def) < 1e-10
+    assert np.linalg.norm(P - P.T) / np.linalg.norm(P) < 1e-12
+    b = np.random.default_rng(seed + 60).uniform(-1, 1, n)
+    x, st = oracle.pcg(op, b, k, alpha, beta, xi, tol=1e-10, maxit=400, lowrank=lr)
+    assert st["converged"]
+    xs = np.linalg.solve(A, b)
+    assert np.linalg.norm(x - xs) / np.linalg.norm(xs) <= 1e-10 * 1e3 * 10
+    # counter law (P10 + O8): one application of P per iteration, each with p extra inner
+    # products (V^T r): ddot = 3 iters + 3 + p iters
+    assert st["ddot"] == 3 * st["iters"] + 3 + p * st["iters"], st
+
+
+def test_P15_lowrank_cuts_pcg_iterations_on_laplacian():
+    """The paper's motivation: deflating the p leftmost eigenvalues
+    (shifted by +1) shrinks kappa(PA), so PCG needs fewer iterations.  Exact eigenvectors."""
+    n = 400
+    op, lam, vec = _lap1d(n)
+    b = np.random.default_rng(3).uniform(-1, 1, n)
+    k, alpha, beta = 10, lam[0], lam[-1]
+    _, st0 = oracle.pcg(op, b, k, alpha, beta, 0.0, tol=1e-10, maxit=2000)
+    lr = oracle.LowRank(op, np.column_stack([vec(j) for j in range(1, 9)]))
+    # with the 8 leftmost deflated, the interval may start at lambda_9
+    _, st1 = oracle.pcg(op, b, k, lam[8], beta, 0.0, tol=1e-10, maxit=2000, lowrank=lr)
+    assert st0["converged"] and st1["converged"] and st1["iters"] < 0.6 * st0["iters"], (st0["iters"], st1["iters"])
+
+
+def test_P16_full_lanczos_ritz_pairs():
+    """n-step Lanczos with full reorthogonalisation on a dense SPD matrix reproduces the
+    spectrum (dense eigensolve) and the leftmost eigenvectors up to sign."""
+    n = 24
+    A, _ = W.random_spd_dense(n, 5, cond=50.0)
+    rowptr, colidx, vals = W.dense_to_csr(A)
+    op = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    ev, E = np.linalg.eigh(A)
+    th, V = oracle.ritz_vectors(op, n, 4, np.random.default_rng(1).uniform(-1, 1, n))
+    assert np.allclose(th, ev[:4], rtol=1e-10)
+    for j in range(4):
+        assert abs(abs(V[:, j] @ E[:, j]) - 1.0) < 1e-8
+    # fewer steps: Ritz residual ||A y - theta y|| = beta_s |e_s^T s| (Kaniel-Paige setting)
+    th2, V2 = oracle.ritz_vectors(op, 10, 2, np.random.default_rng(2).uniform(-1, 1, n))
+    assert np.all(th2 >= ev[:2] - 1e-12)  # Ritz values from above (Cauchy interlacing)
+    assert np.allclose(np.linalg.norm(V2, axis=0), 1.0, atol=1e-12)
