@@ -170,6 +170,24 @@ NPC_API npc_status npc_set_poly(npc_operator op, int degree, double lmin, double
  * 2 (nlev - 1) work vectors and is not fused across levels, so Chebyshev is the fast path.  */
 NPC_API npc_status npc_set_poly_newton(npc_operator op, int nlev, double lmin, double lmax, double xi,
                                npc_poly *out);
+/* Low-rank spectral correction (Sec. "Low-rank acceleration"):
+ *     P = p_k(A) + V (V^T A V)^{-1} V^T,
+ * V_dev = p vectors of the rank's n_local rows, vector j at V_dev + j*n_local (caller-owned,
+ * copied), 0 <= p <= 16; p = 0 removes the correction.  Typically V holds approximate
+ * leftmost eigenvectors (npc_ritz_vectors): on an exact eigenvector the preconditioned
+ * eigenvalue mu_j becomes mu_j + 1 (Eq. plusone).  Setup applies A p times and forms
+ * V^T A V (Cholesky-inverted on the host): NPC_ERR_BREAKDOWN if it is not SPD.  Each later
+ * application of the poly adds one p-vector reduction (V^T r; one allreduce of p scalars when
+ * nranks > 1).  Applies to Chebyshev and Newton polys.  COLLECTIVE.                         */
+NPC_API npc_status npc_poly_set_lowrank(npc_poly poly, int p, const double *V_dev);
+/* Approximate leftmost eigenvectors: nsteps-step Lanczos with FULL reorthogonalisation
+ * (stores nsteps+1 basis vectors on the device) from v0_dev or, when NULL, the counter-hash
+ * start of npc_estimate_spectrum; the Ritz pairs of the p smallest Ritz values of T_nsteps
+ * are written to theta_out[p] (host, ascending) and V_dev (p vectors of n_local rows, vector
+ * j at V_dev + j*n_local, caller-owned, unit 2-norm).  1 <= p <= 16, p <= nsteps <= 4096.
+ * NPC_ERR_BREAKDOWN if the Krylov space is exhausted before p steps.  COLLECTIVE.          */
+NPC_API npc_status npc_ritz_vectors(npc_operator op, int nsteps, int p, const double *v0_dev, double *V_dev,
+                                    double *theta_out);
 NPC_API npc_status npc_destroy_poly(npc_poly poly);
 /* z_dev = p_k(A) r_dev: exactly k operator applications, no reductions, no host sync.
  * z_dev must not alias r_dev.                                                              */

@@ -88,6 +88,8 @@ def lib():
             "npc_context_set_timing": [P, I],
             "npc_context_create_local": [I, I, I, C.c_char_p, P, C.POINTER(P)],
             "npc_context_get_timing": [P, P, P],
+            "npc_poly_set_lowrank": [P, I, P],
+            "npc_ritz_vectors": [P, I, I, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -293,6 +295,27 @@ def npc_set_poly_newton(op: Operator, nlev: int, lmin: float, lmax: float, xi: f
     h = C.c_void_p()
     _check(lib().npc_set_poly_newton(op.h, int(nlev), float(lmin), float(lmax), float(xi), C.byref(h)))
     return Poly(op, h, (1 << nlev) - 1, lmin, lmax, xi)
+
+
+def npc_poly_set_lowrank(poly: Poly, V=None):
+    """Low-rank correction P = p_k(A) + V (V^T A V)^{-1} V^T.  V: fp64 CUDA tensor of shape
+    (p, n_local) (vector j = V[j]), or None / p = 0 to remove it."""
+    if V is None:
+        _check(lib().npc_poly_set_lowrank(poly.h, 0, None))
+        return
+    assert V.dim() == 2, "V must be (p, n_local)"
+    _check(lib().npc_poly_set_lowrank(poly.h, int(V.shape[0]), _ptr(V)))
+    poly._lowrank_V = V  # not needed by the library (it copies); kept for introspection
+
+
+def npc_ritz_vectors(op: Operator, nsteps: int, p: int, v0=None):
+    """-> (theta numpy[p], V CUDA tensor (p, n_local)): Ritz pairs of the p smallest Ritz values
+    of an nsteps-step fully reorthogonalised Lanczos."""
+    import torch
+    V = torch.empty((p, op.n_local), dtype=torch.float64, device="cuda")
+    th = (C.c_double * p)()
+    _check(lib().npc_ritz_vectors(op.h, int(nsteps), int(p), _ptr(v0), _ptr(V), th))
+    return np.array(th[:], dtype=np.float64), V
 
 
 def npc_apply_poly(poly: Poly, r, z):

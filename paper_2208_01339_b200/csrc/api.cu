@@ -280,6 +280,29 @@ npc_status npc_set_poly_newton(npc_operator op, int nlev, double lmin, double lm
     return NPC_SUCCESS;
 }
 
+npc_status npc_poly_set_lowrank(npc_poly poly, int p, const double *V_dev) {
+    NPC_GUARD(poly, NPC_ERR_INVALID_ARGUMENT, "npc_poly_set_lowrank: null poly");
+    NPC_GUARD(p >= 0 && p <= NPC_LOWRANK_MAX, NPC_ERR_INVALID_ARGUMENT, "npc_poly_set_lowrank: p %d not in [0, %d]", p,
+              NPC_LOWRANK_MAX);
+    NPC_GUARD(p == 0 || poly->op->op->n_local == 0 || V_dev, NPC_ERR_INVALID_ARGUMENT, "npc_poly_set_lowrank: null V");
+    NPC_GUARD(p <= poly->op->op->n_global, NPC_ERR_DIMENSION, "npc_poly_set_lowrank: p > n");
+    DeviceScope ds(poly->op->owner->ctx.device);
+    return set_lowrank(poly, p, V_dev);
+}
+
+npc_status npc_ritz_vectors(npc_operator op, int nsteps, int p, const double *v0_dev, double *V_dev,
+                            double *theta_out) {
+    NPC_GUARD(op && theta_out, NPC_ERR_INVALID_ARGUMENT, "npc_ritz_vectors: null argument");
+    NPC_GUARD(p >= 1 && p <= NPC_LOWRANK_MAX, NPC_ERR_INVALID_ARGUMENT, "npc_ritz_vectors: p %d not in [1, %d]", p,
+              NPC_LOWRANK_MAX);
+    NPC_GUARD(nsteps >= p && nsteps <= 4096, NPC_ERR_INVALID_ARGUMENT, "npc_ritz_vectors: nsteps %d not in [p, 4096]",
+              nsteps);
+    NPC_GUARD(op->op->n_local == 0 || V_dev, NPC_ERR_INVALID_ARGUMENT, "npc_ritz_vectors: null V");
+    NPC_GUARD(op->op->n_global >= nsteps, NPC_ERR_DIMENSION, "npc_ritz_vectors: nsteps > n");
+    DeviceScope ds(op->owner->ctx.device);
+    return ritz_vectors(op->op.get(), nsteps, p, v0_dev, V_dev, theta_out);
+}
+
 npc_status npc_destroy_poly(npc_poly poly) {
     if (!poly) return NPC_SUCCESS;
     {
@@ -288,6 +311,9 @@ npc_status npc_destroy_poly(npc_poly poly) {
         poly->tmp.release();
         poly->rin.release();
         poly->zout.release();
+        poly->lr_V.release();
+        poly->lr_Ginv.release();
+        poly->lr_scratch.release();
     }
     delete poly;
     return NPC_SUCCESS;

@@ -221,6 +221,9 @@ npc_status launch_sum_rows(Context *ctx, const double *rows, int P, int m, doubl
 // Grid size of the plain vector kernels for n entries (fixed: partial counts are static).
 int vec_grid(int n);
 
+// Low-rank correction and Ritz vectors (lowrank.cu)
+#define NPC_LOWRANK_MAX 16
+
 // Operator factories (op_*.cu)
 npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
 npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
@@ -309,4 +312,16 @@ struct npc_poly_s {
     npc::DevBuf tmp;           // second recurrence buffer (internal order)
     npc::DevBuf rin, zout;     // internal-order copies when the operator is permuted
     npc::PcgCache pcg;         // PCG work vectors + captured iteration graph
+    // low-rank spectral correction P = p_k(A) + V (V^T A V)^{-1} V^T (lowrank.cu)
+    int lr_p = 0;
+    npc::DevBuf lr_V;          // n_local x lr_p, internal order, column-major
+    npc::DevBuf lr_Ginv;       // lr_p x lr_p row-major
+    npc::DevBuf lr_scratch;    // multi-dot partials | sums | coefficients
 };
+
+namespace npc {
+npc_status set_lowrank(npc_poly P, int p, const double *V_ext);
+npc_status lowrank_pre(npc_poly P, const double *r, const int *done);
+npc_status lowrank_post(npc_poly P, double *z, const double *dotv, double *partials, int *nparts, const int *done);
+npc_status ritz_vectors(Operator *op, int m, int p, const double *v0_ext, double *V_ext, double *theta);
+}  // namespace npc

@@ -209,8 +209,21 @@ static npc_status newton_level(npc_poly P, int j, const double *in, double *out,
     return NPC_SUCCESS;
 }
 
+static npc_status apply_poly_core(npc_poly P, const double *r, double *z, const double *dotv, double *partials,
+                                  int *nparts, const int *done);
+
+// z = P r with P = p_k(A) (+ V (V^T A V)^{-1} V^T when a low-rank correction is set); the
+// partials of <z, dotv> come from the last kernel that writes z.
 npc_status apply_poly_internal(npc_poly P, const double *r, double *z, const double *dotv, double *partials,
                                int *nparts, const int *done) {
+    if (P->lr_p == 0) return apply_poly_core(P, r, z, dotv, partials, nparts, done);
+    NPC_TRY(lowrank_pre(P, r, done));
+    NPC_TRY(apply_poly_core(P, r, z, nullptr, nullptr, nullptr, done));
+    return lowrank_post(P, z, dotv, partials, nparts, done);
+}
+
+static npc_status apply_poly_core(npc_poly P, const double *r, double *z, const double *dotv, double *partials,
+                                  int *nparts, const int *done) {
     if (P->kind == 1) return newton_level(P, P->nlev, r, z, dotv, partials, nparts, done);
     Operator *op = P->op->op.get();
     Context *ctx = op->ctx;
@@ -735,6 +748,8 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     // convergence one block late (u, w of the next iteration are formed and discarded)
     st.op_applications += (long long)h.iters * (k + 1) + ((h.multi && h.converged) ? (k + 1) : 0);
     st.reductions += h.iters + ((h.multi && h.converged) ? 1 : 0);
+    if (P && P->lr_p > 0)  // V^T r inside every application of the preconditioner
+        st.reductions += h.iters + ((h.multi && h.converged) ? 1 : 0);
     if (host_hist && h.iters > 0)
         NPC_CUDA_TRY(cudaMemcpyAsync(host_hist + 1, dhist + 1, sizeof(double) * h.iters, cudaMemcpyDeviceToHost,
                                      ctx->stream));
@@ -875,6 +890,14 @@ static void tridiag_shift_solve(const std::vector<double> &a, const std::vector<
     x[m - 1] /= d[m - 1];
     if (m > 1) x[m - 2] = (x[m - 2] - du[m - 2] * x[m - 1]) / d[m - 2];
     for (int i = m - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / d[i];
+}
+
+double tridiag_eigenvalue(const std::vector<double> &a, const std::vector<double> &b, int idx) {
+    return tridiag_eig(a, b, idx);
+}
+void tridiag_inverse_iteration(const std::vector<double> &a, const std::vector<double> &b, double mu,
+                               std::vector<double> &x) {
+    tridiag_shift_solve(a, b, mu, x);
 }
 
 npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, double *lmax, double *out_ex) {
