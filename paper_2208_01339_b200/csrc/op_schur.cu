@@ -86,9 +86,26 @@ __global__ void __launch_bounds__(32 * SB_WARPS) k_schur_bpass_atomic(const int 
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         if (j < len) acc += b[j] * __ldg(v + c[j]);
+    // First entries: the chunk's rows are sorted by their first column, so lanes with equal
+    // c[0] are contiguous.  Sum their contributions with a segmented warp scan and issue one
+    // RED per distinct column (the L2 RED rate bounds this kernel: profiles/).
+    const unsigned full = 0xffffffffu;
+    // (padding lanes of a class tail carry column 0 and value 0: they add 0 to any segment)
+    const bool has0 = len > 0;
+    const int c0 = has0 ? c[0] : -1;
+    double part = has0 ? b[0] * acc : 0.0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double o = __shfl_up_sync(full, part, d);
+        const int oc = __shfl_up_sync(full, c0, d);
+        // lanes lane-d .. lane all share c0 iff the lane d below does (contiguous segments)
+        if (lane >= d && oc == c0) part += o;
+    }
+    const int next_c0 = __shfl_down_sync(full, c0, 1);
+    if (has0 && (lane == 31 || next_c0 != c0) && part != 0.0) atomicAdd(y + c0, part);
     if (acc != 0.0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 1; j < 4; ++j)
             if (j < len) atomicAdd(y + c[j], b[j] * acc);
     }
 }
