@@ -38,6 +38,14 @@ class _Op(C.Structure):
         ("c", C.c_void_p), ("nb", C.c_long),
         ("browptr", C.c_void_p), ("bcolidx", C.c_void_p), ("bvals", C.c_void_p), ("d", C.c_void_p),
         ("tmp", C.c_void_p),
+        ("nh", C.c_long), ("nblk", C.c_int), ("hblk", C.c_void_p),
+        ("Arp", C.c_void_p), ("Aci", C.c_void_p), ("Av", C.c_void_p),
+        ("Ghrp", C.c_void_p), ("Ghci", C.c_void_p), ("Ghv", C.c_void_p),
+        ("Crp", C.c_void_p), ("Cci", C.c_void_p), ("Cv", C.c_void_p),
+        ("Brp", C.c_void_p), ("Bci", C.c_void_p), ("Bv", C.c_void_p),
+        ("Gurp", C.c_void_p), ("Guci", C.c_void_p), ("Guv", C.c_void_p),
+        ("alpha", C.c_double), ("scaled", C.c_int),
+        ("Lfac", C.c_void_p), ("Loff", C.c_void_p), ("ds", C.c_void_p), ("dwork", C.c_void_p),
     ]
 
 
@@ -69,6 +77,8 @@ def lib():
         _lib.orc_lowrank_apply.argtypes = [C.POINTER(_Op), C.c_int, D, D, D, C.c_int, P, P, P, P, P]
         _lib.orc_lanczos_full.argtypes = [C.POINTER(_Op), C.c_int, P, P, P, P, P]
         _lib.orc_num_threads.restype = C.c_int
+        _lib.orc_dfn_setup.argtypes = [C.POINTER(_Op)]
+        _lib.orc_dfn_free.argtypes = [C.POINTER(_Op)]
     return _lib
 
 
@@ -79,8 +89,11 @@ def _p(a):
 class Operator:
     """Holds the numpy arrays alive and the C descriptor of an operator (O1)."""
 
-    def __init__(self, w: dict):
+    def __init__(self, w: dict, scaled: bool = True):
+        """scaled (DFN only): the operator is D_S^{-1/2} S_u D_S^{-1/2},
+        the one the polynomial is applied to; False gives S_u itself."""
         self.w = w
+        self._dfn = False
         op = _Op()
         kind = w["kind"]
         op.n = int(w["n"])
@@ -110,10 +123,37 @@ class Operator:
             op.bvals = arr(w["bvals"], np.float64)
             op.d = arr(w["d"], np.float64)
             op.tmp = arr(np.zeros(op.nb), np.float64)
+        elif kind == "dfn":
+            op.kind = 3
+            op.nh, op.nblk = int(w["nh"]), int(w["nf"])
+            op.hblk = arr(w["hblk"], np.int32)
+            for key, (rp, ci, v) in (("A", w["A"]), ("Gh", w["Gh"]), ("C", w["C"]), ("B", w["B"]),
+                                     ("Gu", w["Gu"])):
+                setattr(op, key + "rp", arr(rp, np.int32))
+                setattr(op, key + "ci", arr(ci, np.int32))
+                setattr(op, key + "v", arr(v, np.float64))
+            op.alpha = float(w["alpha"])
+            op.scaled = 1 if scaled else 0
         else:
             raise ValueError(kind)
         self.op = op
         self.n = op.n
+        if kind == "dfn":
+            st = lib().orc_dfn_setup(C.byref(op))
+            self._dfn = True
+            if st:
+                raise ValueError(f"orc_dfn_setup failed ({st}: -1 A block not SPD, -2 A not block-diagonal, "
+                                 f"-3 diag(S_u) <= 0)")
+
+    def dfn_diag(self):
+        """D_S = diag(S_u) by Alg. 4, computed at setup."""
+        assert self._dfn
+        return np.ctypeslib.as_array(C.cast(self.op.ds, C.POINTER(C.c_double)), shape=(self.n,)).copy()
+
+    def __del__(self):
+        if getattr(self, "_dfn", False) and _lib is not None:
+            _lib.orc_dfn_free(C.byref(self.op))
+            self._dfn = False
 
     def apply(self, x):
         """y = A x (O1)."""

@@ -25,6 +25,8 @@
  *   orc_pcg              P2 (Table tab:epsil iterations), P6, P10 (counter laws), P11, P15
  *   orc_lowrank_setup/apply  P14 (Eq. plusone on exact eigenvectors), P15 (dense P, symmetry)
  *   orc_lanczos_full     P16 (n steps: exact spectrum and eigenvectors of a dense SPD matrix)
+ *   orc_dfn_setup/apply  P17 (Alg. 3 == dense Eq. schur, symmetry, Alg. 4 == diag, unit
+ *                        diagonal after scaling, SPD), P18 (end-to-end block system residual)
  */
 #include <math.h>
 #include <stdlib.h>
@@ -52,6 +54,23 @@ typedef struct {
     const int *browptr, *bcolidx;
     const double *bvals, *d;  /* d: length nb */
     double *tmp;              /* length nb, scratch owned by the caller */
+    /* DFN Schur complement (kind 3): S_u = G^u - a B^T A^-1 C - a C^T A^-1 B + C^T A^-1 G^h A^-1 C
+     * (Eq. schur), n = n^u; A, G^h block-diagonal over nblk fracture blocks
+     * (hblk[nblk+1] row offsets into the n^h head unknowns); C, B are n^h x n^u.          */
+    long nh;
+    int nblk;
+    const int *hblk;
+    const int *Arp, *Aci;   const double *Av;
+    const int *Ghrp, *Ghci; const double *Ghv;
+    const int *Crp, *Cci;   const double *Cv;
+    const int *Brp, *Bci;   const double *Bv;
+    const int *Gurp, *Guci; const double *Guv;
+    double alpha;
+    int scaled;               /* 1: apply D_S^{-1/2} S_u D_S^{-1/2}    */
+    double *Lfac;             /* per-block dense Cholesky factors (orc_dfn_setup)          */
+    long *Loff;
+    double *ds;               /* D_S = diag(S_u) by Alg. 4 (orc_dfn_setup)                 */
+    double *dwork;            /* 7 n^h + n^u scratch                                       */
 } orc_op;
 
 int orc_num_threads(void) {
@@ -116,11 +135,151 @@ static void schur_apply(const orc_op *A, const double *x, double *y) {
         for (int p = A->browptr[q]; p < A->browptr[q + 1]; p++) y[A->bcolidx[p]] += A->bvals[p] * A->tmp[q];
 }
 
+/* ------------------------------------------------------------------------------------ */
+/* DFN Schur complement (O9).                                     */
+/* ------------------------------------------------------------------------------------ */
+/* y = M x for an m-row CSR matrix */
+static void csr_mv(long m, const int *rp, const int *ci, const double *v, const double *x, double *y) {
+    for (long i = 0; i < m; i++) {
+        double s = 0.0;
+        for (int p = rp[i]; p < rp[i + 1]; p++) s += v[p] * x[ci[p]];
+        y[i] = s;
+    }
+}
+/* y = M^T x (M: m rows, ncol columns), sequential scatter */
+static void csr_mtv(long m, long ncol, const int *rp, const int *ci, const double *v, const double *x, double *y) {
+    for (long j = 0; j < ncol; j++) y[j] = 0.0;
+    for (long i = 0; i < m; i++)
+        for (int p = rp[i]; p < rp[i + 1]; p++) y[ci[p]] += v[p] * x[i];
+}
+/* Solve L u = v (lower) then L^T t = u block by block with the dense per-block factors:
+ * t = (L_A L_A^T)^{-1} v (Alg. 3 steps 3-4, 5-6, 9-10). */
+static void dfn_solve(const orc_op *A, const double *v, double *t) {
+    for (int f = 0; f < A->nblk; f++) {
+        const long h0 = A->hblk[f], m = A->hblk[f + 1] - h0;
+        const double *L = A->Lfac + A->Loff[f];
+        for (long i = 0; i < m; i++) {                       /* L u = v */
+            double s = v[h0 + i];
+            for (long k = 0; k < i; k++) s -= L[i * m + k] * t[h0 + k];
+            t[h0 + i] = s / L[i * m + i];
+        }
+        for (long i = m - 1; i >= 0; i--) {                  /* L^T t = u */
+            double s = t[h0 + i];
+            for (long k = i + 1; k < m; k++) s -= L[k * m + i] * t[h0 + k];
+            t[h0 + i] = s / L[i * m + i];
+        }
+    }
+}
+/* Alg. 3 with the scalar alpha of Eq. schur (reading A8: the algorithm as
+ * printed omits alpha).  y = S_u r. */
+static void dfn_apply_unscaled(const orc_op *A, const double *r, double *y) {
+    const long nh = A->nh, nu = A->n;
+    double *v = A->dwork, *z = v + nh, *t = z + nh, *w = t + nh, *u = w + nh, *q = u + nh, *zu = q + nh;
+    csr_mv(nh, A->Crp, A->Cci, A->Cv, r, v);                  /* 1: v = C r            */
+    csr_mv(nh, A->Brp, A->Bci, A->Bv, r, z);                  /* 2: z = B r            */
+    dfn_solve(A, v, t);                                      /* 3-4: t = A^-1 v       */
+    dfn_solve(A, z, w);                                      /* 5-6: w = A^-1 z       */
+    csr_mv(nu, A->Gurp, A->Guci, A->Guv, r, zu);              /* 7: z = G^u r ...      */
+    csr_mtv(nh, nu, A->Brp, A->Bci, A->Bv, t, y);            /*    - a B^T t          */
+    for (long i = 0; i < nu; i++) zu[i] -= A->alpha * y[i];
+    csr_mtv(nh, nu, A->Crp, A->Cci, A->Cv, w, y);            /*    - a C^T w          */
+    for (long i = 0; i < nu; i++) zu[i] -= A->alpha * y[i];
+    csr_mv(nh, A->Ghrp, A->Ghci, A->Ghv, t, v);               /* 8: v = G^h t          */
+    dfn_solve(A, v, q);                                      /* 9-10: w = A^-1 v      */
+    csr_mtv(nh, nu, A->Crp, A->Cci, A->Cv, q, y);            /* 11: y = z + C^T w     */
+    for (long i = 0; i < nu; i++) y[i] += zu[i];
+}
+static void dfn_apply(const orc_op *A, const double *x, double *y) {
+    if (!A->scaled) { dfn_apply_unscaled(A, x, y); return; }
+    const long nu = A->n;
+    double *xs = A->dwork + 7 * A->nh;                        /* D^{-1/2} x            */
+    for (long i = 0; i < nu; i++) xs[i] = x[i] / sqrt(A->ds[i]);
+    dfn_apply_unscaled(A, xs, y);
+    for (long i = 0; i < nu; i++) y[i] /= sqrt(A->ds[i]);
+}
+
+/* Setup: dense Cholesky A_f = L_f L_f^T of every diagonal block of A (PAPER.md:782-785,
+ * "the exact Cholesky factorization of A"), then D_S = diag(S_u) by Alg. 4
+ * with alpha: Z = (L_A L_A^T)^{-1} C, T = G^h Z - 2 alpha B, (D_S)_i = G^u_ii + z_i^T t_i,
+ * one column at a time (z_i = A^{-1} c_i by dfn_solve on a dense n^h vector).
+ * Returns 0, -1 (A block not SPD), -2 (A not block-diagonal), -3 (D_S entry <= 0). */
+int orc_dfn_setup(orc_op *A) {
+    const long nh = A->nh, nu = A->n;
+    A->Loff = (long *)malloc(sizeof(long) * (A->nblk + 1));
+    A->Loff[0] = 0;
+    for (int f = 0; f < A->nblk; f++) {
+        const long m = A->hblk[f + 1] - A->hblk[f];
+        A->Loff[f + 1] = A->Loff[f] + m * m;
+    }
+    A->Lfac = (double *)calloc(A->Loff[A->nblk] > 0 ? A->Loff[A->nblk] : 1, sizeof(double));
+    A->ds = (double *)malloc(sizeof(double) * (nu > 0 ? nu : 1));
+    A->dwork = (double *)malloc(sizeof(double) * (7 * nh + nu + 1));
+    for (int f = 0; f < A->nblk; f++) {
+        const long h0 = A->hblk[f], m = A->hblk[f + 1] - h0;
+        double *L = A->Lfac + A->Loff[f];
+        for (long i = 0; i < m; i++)                          /* dense copy of A_f     */
+            for (int p = A->Arp[h0 + i]; p < A->Arp[h0 + i + 1]; p++) {
+                const long j = A->Aci[p] - h0;
+                if (j < 0 || j >= m) return -2;
+                L[i * m + j] = A->Av[p];
+            }
+        for (long j = 0; j < m; j++) {                        /* column Cholesky        */
+            double d = L[j * m + j];
+            for (long k = 0; k < j; k++) d -= L[j * m + k] * L[j * m + k];
+            if (!(d > 0.0)) return -1;
+            L[j * m + j] = sqrt(d);
+            for (long i = j + 1; i < m; i++) {
+                double s = L[i * m + j];
+                for (long k = 0; k < j; k++) s -= L[i * m + k] * L[j * m + k];
+                L[i * m + j] = s / L[j * m + j];
+            }
+            for (long i = 0; i < j; i++) L[i * m + j] = 0.0;  /* keep the strict upper part zero */
+        }
+    }
+    /* Alg. 4, column i of C and B: gather them from the CSR rows once (CSC by counting) */
+    int *ccnt = (int *)calloc(nu + 1, sizeof(int)), *bcnt = (int *)calloc(nu + 1, sizeof(int));
+    for (long p = 0; p < A->Crp[nh]; p++) ccnt[A->Cci[p] + 1]++;
+    for (long p = 0; p < A->Brp[nh]; p++) bcnt[A->Bci[p] + 1]++;
+    for (long i = 0; i < nu; i++) { ccnt[i + 1] += ccnt[i]; bcnt[i + 1] += bcnt[i]; }
+    int *crow = (int *)malloc(sizeof(int) * (A->Crp[nh] + 1)), *brow = (int *)malloc(sizeof(int) * (A->Brp[nh] + 1));
+    double *cval = (double *)malloc(sizeof(double) * (A->Crp[nh] + 1)), *bval = (double *)malloc(sizeof(double) * (A->Brp[nh] + 1));
+    int *cf = (int *)malloc(sizeof(int) * (nu + 1)), *bf = (int *)malloc(sizeof(int) * (nu + 1));
+    memcpy(cf, ccnt, sizeof(int) * (nu + 1)); memcpy(bf, bcnt, sizeof(int) * (nu + 1));
+    for (long i = 0; i < nh; i++) {
+        for (int p = A->Crp[i]; p < A->Crp[i + 1]; p++) { crow[cf[A->Cci[p]]] = (int)i; cval[cf[A->Cci[p]]++] = A->Cv[p]; }
+        for (int p = A->Brp[i]; p < A->Brp[i + 1]; p++) { brow[bf[A->Bci[p]]] = (int)i; bval[bf[A->Bci[p]]++] = A->Bv[p]; }
+    }
+    double *cz = A->dwork, *z = cz + nh, *gz = z + nh;
+    for (long i = 0; i < nh; i++) cz[i] = 0.0;
+    int st = 0;
+    for (long c = 0; c < nu && !st; c++) {
+        for (int p = ccnt[c]; p < ccnt[c + 1]; p++) cz[crow[p]] = cval[p];   /* c_i (dense)  */
+        dfn_solve(A, cz, z);                                                  /* z_i = A^-1 c_i */
+        csr_mv(nh, A->Ghrp, A->Ghci, A->Ghv, z, gz);                          /* G^h z_i      */
+        double zt = 0.0;                                                      /* z_i^T t_i    */
+        for (long i = 0; i < nh; i++) zt += z[i] * gz[i];
+        for (int p = bcnt[c]; p < bcnt[c + 1]; p++) zt -= 2.0 * A->alpha * z[brow[p]] * bval[p];
+        double gii = 0.0;
+        for (int p = A->Gurp[c]; p < A->Gurp[c + 1]; p++) if (A->Guci[p] == c) gii += A->Guv[p];
+        A->ds[c] = gii + zt;
+        if (!(A->ds[c] > 0.0)) st = -3;
+        for (int p = ccnt[c]; p < ccnt[c + 1]; p++) cz[crow[p]] = 0.0;
+    }
+    free(ccnt); free(bcnt); free(crow); free(brow); free(cval); free(bval); free(cf); free(bf);
+    return st;
+}
+
+void orc_dfn_free(orc_op *A) {
+    free(A->Lfac); free(A->Loff); free(A->ds); free(A->dwork);
+    A->Lfac = NULL; A->Loff = NULL; A->ds = NULL; A->dwork = NULL;
+}
+
 int orc_op_apply(const orc_op *A, const double *x, double *y) {
     switch (A->kind) {
         case 0: csr_apply(A, x, y); return 0;
         case 1: stencil_apply(A, x, y); return 0;
         case 2: schur_apply(A, x, y); return 0;
+        case 3: if (!A->Lfac) return -1; dfn_apply(A, x, y); return 0;
         default: return -1;
     }
 }

@@ -468,3 +468,70 @@ def test_P16_full_lanczos_ritz_pairs():
     th2, V2 = oracle.ritz_vectors(op, 10, 2, np.random.default_rng(2).uniform(-1, 1, n))
     assert np.all(th2 >= ev[:2] - 1e-12)  # Ritz values from above (Cauchy interlacing)
     assert np.allclose(np.linalg.norm(V2, axis=0), 1.0, atol=1e-12)
+
+
+# ---------------------------------------------------------------- P17-P18: DFN Schur complement (O9)
+def _dfn_dense(w):
+    import scipy.sparse as sp
+
+    def M(t, shape):
+        return sp.csr_matrix((t[2], t[1], t[0]), shape=shape).toarray()
+    nh, nu = w["nh"], w["n"]
+    return (M(w["A"], (nh, nh)), M(w["Gh"], (nh, nh)), M(w["C"], (nh, nu)), M(w["B"], (nh, nu)),
+            M(w["Gu"], (nu, nu)))
+
+
+@pytest.mark.parametrize("nf,seed,alpha", [(6, 0, None), (9, 1, None), (7, 2, 0.0)])
+def test_P17_dfn_schur_matches_dense(nf, seed, alpha):
+    """Alg. 3 (with alpha: reading A8) equals the dense closed form of
+    Eq. schur, S_u = G^u - a B^T A^-1 C - a C^T A^-1 B + C^T A^-1 G^h A^-1 C,
+    built with numpy's dense solve; S_u is symmetric and SPD; Alg. 4
+    equals diag(S_u); the Jacobi-scaled operator has unit diagonal."""
+    w = W.dfn(nf, seed=seed, alpha=alpha)
+    A, Gh, C, B, Gu = _dfn_dense(w)
+    a = w["alpha"]
+    Ai_C, Ai_B = np.linalg.solve(A, C), np.linalg.solve(A, B)
+    S = Gu - a * B.T @ Ai_C - a * C.T @ Ai_B + C.T @ np.linalg.solve(A, Gh @ Ai_C)
+    op = oracle.Operator(w, scaled=False)
+    n = w["n"]
+    cols = np.random.default_rng(seed).choice(n, 12, replace=False)
+    for j in cols:
+        e = np.zeros(n)
+        e[j] = 1.0
+        assert np.linalg.norm(op.apply(e) - S[:, j]) <= 1e-12 * np.linalg.norm(S[:, j])
+    x = np.random.default_rng(seed + 1).standard_normal(n)
+    assert np.linalg.norm(op.apply(x) - S @ x) <= 1e-13 * np.linalg.norm(S @ x)
+    assert np.linalg.norm(S - S.T) <= 1e-13 * np.linalg.norm(S)
+    assert np.linalg.eigvalsh(S)[0] > 0.0
+    D = op.dfn_diag()
+    assert np.allclose(D, np.diag(S), rtol=1e-13, atol=0)
+    ops = oracle.Operator(w, scaled=True)
+    Shat = np.column_stack([ops.apply(e) for e in np.eye(n)[:, :40].T])  # first 40 columns
+    assert np.allclose(np.diag(Shat[:40]), 1.0, rtol=1e-13)
+    assert np.allclose(Shat, (S / np.sqrt(np.outer(D, D)))[:, :40], rtol=1e-12, atol=1e-14)
+
+
+def test_P18_dfn_end_to_end_block_system():
+    """Solve the Schur system by the oracle's PCG + polynomial on the scaled operator, recover
+    h and p (with alpha) and check the original saddle-point system Eq. sys
+     with dense numpy: the paper's reformulation end to end."""
+    w = W.dfn(10, seed=3)
+    A, Gh, C, B, Gu = _dfn_dense(w)
+    a = w["alpha"]
+    nh, nu = w["nh"], w["n"]
+    q = np.random.default_rng(4).uniform(-1, 1, nh)
+    # r = W^T M^-1 f1 with f1 = [q; 0], M^-1 = [[A^-1, 0], [-A^-1 G^h A^-1, A^-1]], W = [a B; C]
+    Aq = np.linalg.solve(A, q)
+    r = a * B.T @ Aq - C.T @ np.linalg.solve(A, Gh @ Aq)
+    op = oracle.Operator(w, scaled=True)
+    D = op.dfn_diag()
+    lo, hi = oracle.estimate_spectrum(op, 20, W.lanczos_start(nu))
+    uh, st = oracle.pcg(op, r / np.sqrt(D), 10, lo, hi, 0.0, tol=1e-12, maxit=2000)
+    assert st["converged"]
+    u = uh / np.sqrt(D)
+    h = np.linalg.solve(A, q + C @ u)
+    p = np.linalg.solve(A, a * B @ u - Gh @ h)  # the paper's "B u" assumes alpha = 1 (reading A8)
+    K0 = np.block([[Gh, -a * B, A], [-a * B.T, Gu, -C.T], [A, -C, np.zeros((nh, nh))]])
+    x = np.concatenate([h, u, p])
+    f0 = np.concatenate([np.zeros(nh), np.zeros(nu), q])
+    assert np.linalg.norm(K0 @ x - f0) <= 1e-9 * np.linalg.norm(K0) * np.linalg.norm(x)

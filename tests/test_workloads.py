@@ -62,3 +62,31 @@ def test_config5_surrogate():
         c = w["bcolidx"][w["browptr"][q]:w["browptr"][q + 1]]
         assert np.all(np.diff(c) > 0)
     assert w["d"].min() >= 1 and w["d"].max() <= 100 and 1 <= w["c"].min() and w["c"].max() <= 2
+
+
+def test_dfn_generator_structure():
+    """Structure of the synthetic DFN system (PAPER.md:668-688 bullets; SPEC generate_synthetic)."""
+    w = W.dfn(40, seed=7)
+    w2 = W.dfn(40, seed=7)
+    for key in ("A", "Gh", "C", "B", "Gu"):  # deterministic
+        for a, b in zip(w[key], w2[key]):
+            assert np.array_equal(a, b)
+    hb = w["hblk"]
+    blk = np.searchsorted(hb, np.arange(w["nh"]), side="right") - 1
+    for key in ("A", "Gh"):  # block-diagonal
+        rp, ci, _ = w[key]
+        rows = np.repeat(np.arange(w["nh"]), np.diff(rp))
+        assert np.array_equal(blk[rows], blk[ci])
+    rp, ci, cv = w["C"]  # C fracture-local: every column in one fracture block
+    rows = np.repeat(np.arange(w["nh"]), np.diff(rp))
+    for j in np.unique(ci)[:200]:
+        assert len(set(blk[rows[ci == j]])) == 1
+    brp, bci, bv = w["B"]
+    assert brp[-1] >= rp[-1] and np.all(cv >= 0) and np.all(bv >= 0)
+    # G^h symmetric with zero row sums (SPSD, rank-deficient); G^u symmetric tridiagonal per trace
+    import scipy.sparse as sp
+    Gh = sp.csr_matrix((w["Gh"][2], w["Gh"][1], w["Gh"][0]), shape=(w["nh"], w["nh"]))
+    assert abs(Gh - Gh.T).max() == 0 and np.allclose(np.asarray(Gh.sum(axis=1)).ravel(), 0.0)
+    Gu = sp.csr_matrix((w["Gu"][2], w["Gu"][1], w["Gu"][0]), shape=(w["n"], w["n"]))
+    assert abs(Gu - Gu.T).max() == 0 and np.all(Gu.diagonal() == 2.0)
+    assert w["alpha"] > 0 and w["b"].shape == (w["n"],)

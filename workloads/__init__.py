@@ -17,7 +17,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = [
-    "config1", "config2", "config3", "config4", "config5",
+    "config1", "config2", "config3", "config4", "config5", "dfn",
     "tab_epsil_diag", "laplacian_1d_csr", "random_spd_dense", "dense_to_csr", "lanczos_start",
     "CONFIG_DEFAULTS",
 ]
@@ -229,6 +229,137 @@ def config5(n: int = 4_000_000, seed: int = 4, rows_per_trace: int = 3):
     b = rng.uniform(-1.0, 1.0, n)
     return dict(kind="schur", name=f"config5_{n}", n=n, nb=nb, c=c, browptr=browptr.astype(np.int32),
                 bcolidx=bcol.astype(np.int32), bvals=bval, d=D, b=b, **CONFIG_DEFAULTS[5])
+
+
+def dfn(nf: int = 2000, seed: int = 5, traces_per_fracture: int = 8, grid=(4, 8), trace_len=(8, 16),
+        alpha: float | None = None):
+    """Synthetic DFN block system (SPEC.md generate_synthetic), the
+    stand-in for the paper's DFN test cases (Table size; Frac32 has ~34
+    head unknowns per fracture and n^u / n^h ~ 2.8).  Structure follows the bullets of
+    Eq. algebraic_model (PAPER.md:668-688):
+
+    * nf fractures, fracture f a grid nx_f x ny_f (uniform in [grid[0], grid[1]]), head
+      unknowns h numbered fracture by fracture, x fastest (block-diagonal structure);
+    * A = block-diag(K_f L_f): L_f the 2D 5-point Dirichlet Laplacian of the fracture grid,
+      transmissivity K_f = exp(0.5 N(0,1)) -- SPD, "a 2-D discrete Laplacian" per block;
+    * traces: traces_per_fracture * nf pairs (f, g), f != g uniform; trace t carries L_t flux
+      unknowns u (L_t uniform in trace_len); the trace lies on a horizontal or vertical grid
+      line of each of its two fractures; u-dof k sits at s_k = (k + 1/2)/L_t along the line and
+      couples to its two nearest line nodes with hat weights (1 - th, th) / L_t;
+    * C: the owner fracture's (min(f, g)) couplings -- fracture-local rectangular blocks;
+      E: the other fracture's couplings (support disjoint from C's blocks); B = C + E;
+    * G^h = block-diag: for every trace on fracture f, the path-graph Laplacian of the nodes
+      of its line (SPSD, rank-deficient), summed;
+    * G^u = block-diag over traces of tridiag(-1, 2, -1) (1D Dirichlet, SPD; trace dofs tie
+      the two fractures of a trace: "global nature");
+    * alpha (PAPER.md:666 "usually on the order of 1"; SPD "by wisely selecting alpha",
+      PAPER.md:774-777): unless given, half the value that makes S_u(alpha) SPD by the norm
+      bound alpha ||B^T A^-1 C + C^T A^-1 B|| <= 2 alpha ||B|| ||C|| / lambda_min(A) <
+      lambda_min(G^u), with ||M||_2 <= sqrt(||M||_1 ||M||_inf) and the closed-form Laplacian
+      eigenvalues 4 sin^2(pi / (2(m+1))) -- input construction, no method arithmetic;
+    * b (the Schur right-hand side, u-space) = uniform(-1, 1, n^u).
+
+    Draw order (seed): grid dims (nf x 2), K_f (nf), trace pairs f (T), g (T), lengths (T),
+    line orientation + index for the owner then the other fracture (4 x T), b (n^u).
+    """
+    import scipy.sparse as sp
+    rng = np.random.default_rng(seed)
+    dims = rng.integers(grid[0], grid[1] + 1, size=(nf, 2))
+    nx, ny = dims[:, 0].astype(np.int64), dims[:, 1].astype(np.int64)
+    nblk = nx * ny
+    hoff = np.zeros(nf + 1, dtype=np.int64)
+    np.cumsum(nblk, out=hoff[1:])
+    nh = int(hoff[-1])
+    K = np.exp(0.5 * rng.standard_normal(nf))
+    T = traces_per_fracture * nf
+    f = rng.integers(0, nf, T)
+    g = rng.integers(0, nf - 1, T)
+    g = g + (g >= f)
+    L = rng.integers(trace_len[0], trace_len[1] + 1, T)
+    orient = rng.integers(0, 2, size=(2, T))          # 0: horizontal line (fixed y), 1: vertical
+    linepick = rng.random(size=(2, T))                # line index = floor(pick * lines)
+    owner, other = np.minimum(f, g), np.maximum(f, g)
+    uoff = np.zeros(T + 1, dtype=np.int64)
+    np.cumsum(L, out=uoff[1:])
+    nu = int(uoff[-1])
+    b = rng.uniform(-1.0, 1.0, nu)
+
+    # ---- A: block-diag K_f * 5-point Dirichlet Laplacian
+    rows, cols, vals = [], [], []
+    for (mx, my) in {(int(a), int(c)) for a, c in dims}:
+        sel = np.nonzero((nx == mx) & (ny == my))[0]
+        loc = np.arange(mx * my)
+        x, y = loc % mx, loc // mx
+        lr, lc, lv = [loc], [loc], [np.full(loc.size, 4.0)]
+        for dx, dy in ((-1, 0), (1, 0), (0, -1), (0, 1)):
+            ok = (x + dx >= 0) & (x + dx < mx) & (y + dy >= 0) & (y + dy < my)
+            lr.append(loc[ok]); lc.append(loc[ok] + dx + mx * dy); lv.append(np.full(ok.sum(), -1.0))
+        lr, lc, lv = np.concatenate(lr), np.concatenate(lc), np.concatenate(lv)
+        rows.append((hoff[sel][:, None] + lr[None, :]).ravel())
+        cols.append((hoff[sel][:, None] + lc[None, :]).ravel())
+        vals.append((K[sel][:, None] * lv[None, :]).ravel())
+    A = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(nh, nh))
+
+    # ---- trace lines on both fractures: node ids of each line
+    def line_nodes(fr, o, pick):
+        mx, my = nx[fr], ny[fr]
+        m = np.where(o == 0, mx, my)                      # nodes along the line
+        nlines = np.where(o == 0, my, mx)
+        li = np.minimum((pick * nlines).astype(np.int64), nlines - 1)
+        return m, li
+    cr, cc, cv, er, ec, ev = [], [], [], [], [], []
+    ghr, ghc, ghv = [], [], []
+    for side, fr in ((0, owner), (1, other)):
+        o, pick = orient[side], linepick[side]
+        m, li = line_nodes(fr, o, pick)
+        # u-dof k of trace t -> nodes j0 = floor(s), j0 + 1 along the line, s = (k+1/2)/L (m-1)
+        tt = np.repeat(np.arange(T), L)
+        kk = np.arange(nu) - uoff[tt]
+        s = (kk + 0.5) / L[tt] * (m[tt] - 1)
+        j0 = np.minimum(np.floor(s).astype(np.int64), m[tt] - 2)
+        th = s - j0
+        def node(j):
+            return np.where(o[tt] == 0, hoff[fr[tt]] + li[tt] * nx[fr[tt]] + j, hoff[fr[tt]] + j * nx[fr[tt]] + li[tt])
+        w0, w1 = (1.0 - th) / L[tt], th / L[tt]
+        tr, tc, tv = (cr, cc, cv) if side == 0 else (er, ec, ev)
+        tr += [node(j0), node(j0 + 1)]
+        tc += [np.arange(nu), np.arange(nu)]
+        tv += [w0, w1]
+        # G^h: path Laplacian along the line (edges j, j+1 for j < m-1)
+        te = np.repeat(np.arange(T), m - 1)
+        je = np.arange(int((m - 1).sum())) - np.repeat(np.cumsum(m - 1) - (m - 1), m - 1)
+        def node_t(j):
+            return np.where(o[te] == 0, hoff[fr[te]] + li[te] * nx[fr[te]] + j, hoff[fr[te]] + j * nx[fr[te]] + li[te])
+        a_, c_ = node_t(je), node_t(je + 1)
+        ghr += [a_, c_, a_, c_]; ghc += [a_, c_, c_, a_]
+        one = np.ones(a_.size)
+        ghv += [one, one, -one, -one]
+    C = sp.csr_matrix((np.concatenate(cv), (np.concatenate(cr), np.concatenate(cc))), shape=(nh, nu))
+    E = sp.csr_matrix((np.concatenate(ev), (np.concatenate(er), np.concatenate(ec))), shape=(nh, nu))
+    B = (C + E).tocsr()
+    Gh = sp.csr_matrix((np.concatenate(ghv), (np.concatenate(ghr), np.concatenate(ghc))), shape=(nh, nh))
+    # ---- G^u: per-trace tridiag(-1, 2, -1)
+    ku = np.arange(nu) - uoff[np.repeat(np.arange(T), L)]
+    Lr = np.repeat(L, L)
+    gr, gc, gv = [np.arange(nu)], [np.arange(nu)], [np.full(nu, 2.0)]
+    nxt = np.nonzero(ku < Lr - 1)[0]
+    gr += [nxt, nxt + 1]; gc += [nxt + 1, nxt]; gv += [-np.ones(nxt.size), -np.ones(nxt.size)]
+    Gu = sp.csr_matrix((np.concatenate(gv), (np.concatenate(gr), np.concatenate(gc))), shape=(nu, nu))
+    for M in (A, B, C, Gh, Gu):
+        M.sum_duplicates()
+        M.sort_indices()
+    if alpha is None:
+        def n2(M):
+            a = abs(M)
+            return float(np.sqrt(a.sum(axis=0).max() * a.sum(axis=1).max()))
+        lam_a = float(np.min(K * (4 * np.sin(np.pi / (2 * (nx + 1))) ** 2 + 4 * np.sin(np.pi / (2 * (ny + 1))) ** 2)))
+        lam_gu = float(4 * np.sin(np.pi / (2 * (L.max() + 1))) ** 2)
+        alpha = 0.5 * lam_gu * lam_a / (2.0 * n2(B) * n2(C))
+
+    def csr(M):
+        return (M.indptr.astype(np.int32), M.indices.astype(np.int32), M.data.astype(np.float64))
+    return dict(kind="dfn", name=f"dfn_{nf}", n=nu, nh=nh, nf=nf, hblk=hoff.astype(np.int32), alpha=float(alpha),
+                A=csr(A), Gh=csr(Gh), C=csr(C), B=csr(B), Gu=csr(Gu), b=b, k=30, tol=1e-8, lanczos_steps=20)
 
 
 def tab_epsil_diag(n: int = 100_000, seed: int = 42):
