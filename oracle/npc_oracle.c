@@ -154,8 +154,8 @@ static void csr_mtv(long m, long ncol, const int *rp, const int *ci, const doubl
 }
 /* Solve L u = v (lower) then L^T t = u block by block with the dense per-block factors:
  * t = (L_A L_A^T)^{-1} v (Alg. 3 steps 3-4, 5-6, 9-10). */
-static void dfn_solve(const orc_op *A, const double *v, double *t) {
-    for (int f = 0; f < A->nblk; f++) {
+static void dfn_solve_block(const orc_op *A, int f, const double *v, double *t) {
+    {
         const long h0 = A->hblk[f], m = A->hblk[f + 1] - h0;
         const double *L = A->Lfac + A->Loff[f];
         for (long i = 0; i < m; i++) {                       /* L u = v */
@@ -169,6 +169,9 @@ static void dfn_solve(const orc_op *A, const double *v, double *t) {
             t[h0 + i] = s / L[i * m + i];
         }
     }
+}
+static void dfn_solve(const orc_op *A, const double *v, double *t) {
+    for (int f = 0; f < A->nblk; f++) dfn_solve_block(A, f, v, t);
 }
 /* Alg. 3 with the scalar alpha of Eq. schur (reading A8: the algorithm as
  * printed omits alpha).  y = S_u r. */
@@ -249,22 +252,41 @@ int orc_dfn_setup(orc_op *A) {
         for (int p = A->Crp[i]; p < A->Crp[i + 1]; p++) { crow[cf[A->Cci[p]]] = (int)i; cval[cf[A->Cci[p]]++] = A->Cv[p]; }
         for (int p = A->Brp[i]; p < A->Brp[i + 1]; p++) { brow[bf[A->Bci[p]]] = (int)i; bval[bf[A->Bci[p]]++] = A->Bv[p]; }
     }
+    /* A is block-diagonal, so z_i = A^{-1} c_i vanishes outside the blocks that column i of C
+     * touches: only those blocks are solved and summed (the rest of z_i stays 0). */
     double *cz = A->dwork, *z = cz + nh, *gz = z + nh;
-    for (long i = 0; i < nh; i++) cz[i] = 0.0;
+    int *fblk = (int *)malloc(sizeof(int) * (nh > 0 ? nh : 1)), *touched = (int *)calloc(A->nblk + 1, sizeof(int));
+    for (int f = 0; f < A->nblk; f++) for (long i = A->hblk[f]; i < A->hblk[f + 1]; i++) fblk[i] = f;
+    for (long i = 0; i < nh; i++) { cz[i] = 0.0; z[i] = 0.0; }
     int st = 0;
     for (long c = 0; c < nu && !st; c++) {
         for (int p = ccnt[c]; p < ccnt[c + 1]; p++) cz[crow[p]] = cval[p];   /* c_i (dense)  */
-        dfn_solve(A, cz, z);                                                  /* z_i = A^-1 c_i */
-        csr_mv(nh, A->Ghrp, A->Ghci, A->Ghv, z, gz);                          /* G^h z_i      */
         double zt = 0.0;                                                      /* z_i^T t_i    */
-        for (long i = 0; i < nh; i++) zt += z[i] * gz[i];
+        for (int p = ccnt[c]; p < ccnt[c + 1]; p++) {
+            const int f = fblk[crow[p]];
+            if (touched[f]) continue;
+            touched[f] = 1;
+            dfn_solve_block(A, f, cz, z);                                     /* z_i = A^-1 c_i */
+            for (long i = A->hblk[f]; i < A->hblk[f + 1]; i++) {              /* G^h z_i      */
+                double g = 0.0;
+                for (int q = A->Ghrp[i]; q < A->Ghrp[i + 1]; q++) g += A->Ghv[q] * z[A->Ghci[q]];
+                zt += z[i] * g;
+            }
+        }
         for (int p = bcnt[c]; p < bcnt[c + 1]; p++) zt -= 2.0 * A->alpha * z[brow[p]] * bval[p];
         double gii = 0.0;
         for (int p = A->Gurp[c]; p < A->Gurp[c + 1]; p++) if (A->Guci[p] == c) gii += A->Guv[p];
         A->ds[c] = gii + zt;
         if (!(A->ds[c] > 0.0)) st = -3;
-        for (int p = ccnt[c]; p < ccnt[c + 1]; p++) cz[crow[p]] = 0.0;
+        for (int p = ccnt[c]; p < ccnt[c + 1]; p++) {                         /* reset z_i, c_i */
+            const int f = fblk[crow[p]];
+            cz[crow[p]] = 0.0;
+            if (!touched[f]) continue;
+            touched[f] = 0;
+            for (long i = A->hblk[f]; i < A->hblk[f + 1]; i++) z[i] = 0.0;
+        }
     }
+    free(fblk); free(touched); (void)gz;
     free(ccnt); free(bcnt); free(crow); free(brow); free(cval); free(bval); free(cf); free(bf);
     return st;
 }
