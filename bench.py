@@ -58,11 +58,14 @@ def make_workload(cfg: int, side: int | None):
         return W.config4(n=side or 8_000_000)
     if cfg == 5:
         return W.config5(n=side or 4_000_000)
+    if cfg == 6:  # the paper's DFN Schur operator, Frac32-sized
+        return W.dfn(nf=side or 29_370)
     raise ValueError(cfg)
 
 
 def op_kind(w, cfg):
-    return {1: "csr", 2: "stencil", 3: "csr", 4: "sell", 5: "schur"}[cfg] if w["kind"] != "stencil" else "stencil"
+    return {1: "csr", 2: "stencil", 3: "csr", 4: "sell", 5: "schur", 6: "dfn"}[cfg] if w["kind"] != "stencil" \
+        else "stencil"
 
 
 def matrix_bytes(w, kind):
@@ -80,6 +83,21 @@ def matrix_bytes(w, kind):
         # with the four vector streams of poly_bytes)
         nnz = int(w["browptr"][-1])
         return nnz * 12 + n * 8 + 2 * n * 8
+    if kind == "dfn":
+        # op_dfn.cu: C, B and their transposes, G^h, G^u once (12 B/nnz + row pointers), the band
+        # factor of A (8 B/entry; band = bandwidth + 1 per row, nx for a grid block), and the
+        # internal vectors t, u2 (written and read) plus the second read of x
+        nh = w["nh"]
+        nnz = lambda key: int(w[key][0][-1])  # noqa: E731
+        hb = w["hblk"]
+        rp, ci, _ = w["A"]
+        band = 0
+        for f in range(len(hb) - 1):
+            r0, r1 = int(hb[f]), int(hb[f + 1])
+            rows = np.repeat(np.arange(r0, r1), np.diff(rp[r0:r1 + 1]))
+            band += (r1 - r0) * (int(np.max(np.abs(rows - ci[rp[r0]:rp[r1]]))) + 1)
+        return int(12 * (2 * nnz("C") + 2 * nnz("B") + nnz("Gh") + nnz("Gu")) + 4 * (5 * nh + 3 * n) + 8 * band
+                   + 8 * (4 * nh + n))
     raise ValueError(kind)
 
 

@@ -92,7 +92,9 @@ typedef enum {
     NPC_OP_SELL = 1,     /* general sparse given as CSR, stored as SELL-C-sigma (config 4)  */
     NPC_OP_STENCIL = 2,  /* constant-coefficient 2D 5-point / 3D 7-point Dirichlet (config 2)*/
     NPC_OP_SCHUR = 3,    /* S = tridiag(-1, 2 + c, -1) + B^T D^{-1} B, never assembled (cfg 5)*/
-    NPC_OP_CALLBACK = 4  /* user y = A x on the device; recurrence in a separate kernel      */
+    NPC_OP_CALLBACK = 4, /* user y = A x on the device; recurrence in a separate kernel      */
+    NPC_OP_DFN = 5       /* the paper's DFN Schur complement S_u (Alg. 3), optionally Jacobi-
+                            scaled by D_S (Alg. 4); single rank in this version              */
 } npc_op_kind;
 
 /* User operator: y_dev = A x_dev for this rank's n_local rows, enqueued on cuda_stream.
@@ -132,6 +134,31 @@ typedef struct {
     /* CALLBACK */
     npc_apply_fn apply;
     void *user;
+    /* DFN (§4.2, Eq. schur):  S_u = G^u - a B^T A^-1 C - a C^T A^-1 B
+     *                                        + C^T A^-1 G^h A^-1 C,   n_local = n^u.
+     * A (n^h x n^h) SPD and G^h (n^h x n^h) SPSD must be block-diagonal over the dfn_nblk
+     * fracture blocks [dfn_hblk[f], dfn_hblk[f+1]) (dfn_hblk[0] = 0, dfn_hblk[nblk] = n^h,
+     * at most 8192 rows per block); C and B (n^h x n^u), G^u (n^u x n^u), all CSR with
+     * column ids ascending or not (copied).  The library factorises every block of A
+     * (banded Cholesky, band = the block's bandwidth in the given ordering).  dfn_scaled = 1
+     * makes the operator D_S^{-1/2} S_u D_S^{-1/2}, D_S = diag(S_u) by Alg. 4 (PAPER.md:
+     * 812-841), computed at create; NPC_ERR_DIMENSION if a block of A is not SPD or an entry
+     * of D_S is not positive.  nranks must be 1.                                            */
+    long long dfn_nh;
+    int dfn_nblk;
+    const int *dfn_hblk;
+    const int *a_rowptr, *a_colidx;
+    const double *a_vals;
+    const int *gh_rowptr, *gh_colidx;
+    const double *gh_vals;
+    const int *c_rowptr, *c_colidx;
+    const double *c_vals;
+    const int *bm_rowptr, *bm_colidx;
+    const double *bm_vals;
+    const int *gu_rowptr, *gu_colidx;
+    const double *gu_vals;
+    double dfn_alpha;
+    int dfn_scaled;
 } npc_operator_desc;
 
 /* Create an operator (COLLECTIVE when nranks > 1: builds the halo plan).  Validates the

@@ -19,12 +19,12 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NPC_LIB_PATH") or os.path.join(_HERE, "libnpc.so")  # override: A/B variants
 
-NPC_OP_CSR, NPC_OP_SELL, NPC_OP_STENCIL, NPC_OP_SCHUR, NPC_OP_CALLBACK = range(5)
+NPC_OP_CSR, NPC_OP_SELL, NPC_OP_STENCIL, NPC_OP_SCHUR, NPC_OP_CALLBACK, NPC_OP_DFN = range(6)
 STATUS = {0: "NPC_SUCCESS", 1: "NPC_ERR_INVALID_ARGUMENT", 2: "NPC_ERR_DIMENSION",
           3: "NPC_ERR_DEGENERATE_INTERVAL", 4: "NPC_ERR_NOT_CONVERGED", 5: "NPC_ERR_BREAKDOWN",
           6: "NPC_ERR_CUDA", 7: "NPC_ERR_NCCL", 8: "NPC_ERR_OUT_OF_MEMORY", 9: "NPC_ERR_UNSUPPORTED"}
 KIND = {"csr": NPC_OP_CSR, "sell": NPC_OP_SELL, "stencil": NPC_OP_STENCIL, "schur": NPC_OP_SCHUR,
-        "callback": NPC_OP_CALLBACK}
+        "callback": NPC_OP_CALLBACK, "dfn": NPC_OP_DFN}
 
 
 class NpcError(RuntimeError):
@@ -48,6 +48,13 @@ class OperatorDesc(C.Structure):
         ("b_n_local", C.c_int), ("b_rowptr", C.c_void_p), ("b_colidx", C.c_void_p),
         ("b_vals", C.c_void_p), ("d", C.c_void_p),
         ("apply", APPLY_FN), ("user", C.c_void_p),
+        ("dfn_nh", C.c_longlong), ("dfn_nblk", C.c_int), ("dfn_hblk", C.c_void_p),
+        ("a_rowptr", C.c_void_p), ("a_colidx", C.c_void_p), ("a_vals", C.c_void_p),
+        ("gh_rowptr", C.c_void_p), ("gh_colidx", C.c_void_p), ("gh_vals", C.c_void_p),
+        ("c_rowptr", C.c_void_p), ("c_colidx", C.c_void_p), ("c_vals", C.c_void_p),
+        ("bm_rowptr", C.c_void_p), ("bm_colidx", C.c_void_p), ("bm_vals", C.c_void_p),
+        ("gu_rowptr", C.c_void_p), ("gu_colidx", C.c_void_p), ("gu_vals", C.c_void_p),
+        ("dfn_alpha", C.c_double), ("dfn_scaled", C.c_int),
     ]
 
 
@@ -216,7 +223,7 @@ def npc_create_operator(ctx: Context, kind, *, n_local, n_global=0, row_begin=0,
                         vals=None, sell_C=0, sell_sigma=0, dim=3, nx=0, ny=0, nz_global=1, z_begin=0,
                         nz_local=None, diag=0.0, offdiag=0.0, c=None, b_rows_global=0, b_row_begin=0,
                         b_n_local=0, b_rowptr=None, b_colidx=None, b_vals=None, d=None, apply=None,
-                        user=None) -> Operator:
+                        user=None, dfn=None) -> Operator:
     """Host arrays (numpy) are copied by the library.  `apply` (callback kind) is a Python
     callable (x_ptr, y_ptr, stream_ptr) -> int, kept alive by the returned Operator."""
     desc = OperatorDesc()
@@ -241,6 +248,16 @@ def npc_create_operator(ctx: Context, kind, *, n_local, n_global=0, row_begin=0,
     desc.b_rows_global, desc.b_row_begin, desc.b_n_local = int(b_rows_global), int(b_row_begin), int(b_n_local)
     desc.b_rowptr, desc.b_colidx = arr(b_rowptr, np.int32), arr(b_colidx, np.int32)
     desc.b_vals, desc.d = arr(b_vals, np.float64), arr(d, np.float64)
+    if dfn is not None:
+        # dfn = dict(nh, nblk, hblk, A=(rowptr, colidx, vals), Gh=..., C=..., B=..., Gu=..., alpha, scaled)
+        desc.dfn_nh, desc.dfn_nblk = int(dfn["nh"]), int(dfn["nblk"])
+        desc.dfn_hblk = arr(dfn["hblk"], np.int32)
+        for key, pre in (("A", "a"), ("Gh", "gh"), ("C", "c"), ("B", "bm"), ("Gu", "gu")):
+            rp, ci, v = dfn[key]
+            setattr(desc, pre + "_rowptr", arr(rp, np.int32))
+            setattr(desc, pre + "_colidx", arr(ci, np.int32))
+            setattr(desc, pre + "_vals", arr(v, np.float64))
+        desc.dfn_alpha, desc.dfn_scaled = float(dfn["alpha"]), int(dfn.get("scaled", 1))
     if apply is not None:
         cb = APPLY_FN(lambda u, x, y, s: int(apply(x, y, s)))
         keep.append(cb)
@@ -382,4 +399,8 @@ def create_from_workload(ctx: Context, w: dict, kind: str | None = None) -> Oper
         return npc_create_operator(ctx, "schur", n_local=w["n"], n_global=w["n"], c=w["c"], b_rows_global=w["nb"],
                                    b_n_local=w["nb"], b_rowptr=w["browptr"], b_colidx=w["bcolidx"],
                                    b_vals=w["bvals"], d=w["d"])
+    if k == "dfn":
+        return npc_create_operator(ctx, "dfn", n_local=w["n"], n_global=w["n"],
+                                   dfn=dict(nh=w["nh"], nblk=w["nf"], hblk=w["hblk"], A=w["A"], Gh=w["Gh"], C=w["C"],
+                                            B=w["B"], Gu=w["Gu"], alpha=w["alpha"], scaled=w.get("scaled", 1)))
     raise ValueError(k)

@@ -174,6 +174,7 @@ npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, n
         case NPC_OP_STENCIL: NPC_TRY(make_stencil_operator(&ctx->ctx, &d, op)); break;
         case NPC_OP_SCHUR: NPC_TRY(make_schur_operator(&ctx->ctx, &d, op)); break;
         case NPC_OP_CALLBACK: NPC_TRY(make_callback_operator(&ctx->ctx, &d, op)); break;
+        case NPC_OP_DFN: NPC_TRY(make_dfn_operator(&ctx->ctx, &d, op)); break;
         default: NPC_GUARD(false, NPC_ERR_INVALID_ARGUMENT, "npc_create_operator: unknown kind %d", (int)d.kind);
     }
     NPC_TRY(ctx->ctx.ensure_partials(op->num_partials()));

@@ -230,6 +230,7 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
 npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
 npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
 npc_status make_callback_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
+npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out);
 
 // Host halo plan (halo.cu)
 struct HaloPlan {

@@ -21,7 +21,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2208_01339_b200 as npc  # noqa: E402
 
-KS = {1: [10], 2: [30], 3: [20, 50, 100], 4: [60], 5: [10, 50, 100, 200]}
+KS = {1: [10], 2: [30], 3: [20, 50, 100], 4: [60], 5: [10, 50, 100, 200], 6: [30]}
 
 
 def run(cfg, reps, ctx, kinds=None):
