@@ -246,6 +246,12 @@ npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, d
     DeviceScope ds(op->owner->ctx.device);
     const size_t n = std::max(op->op->n_local, 1);
     NPC_TRY(P->tmp.alloc(sizeof(double) * n));
+    if (degree >= 4 && op->op->supports_step2()) NPC_TRY(P->tmp2.alloc(sizeof(double) * n * 2));
+    if (degree >= 1 && op->op->supports_fused_poly()) {
+        NPC_TRY(P->coef_dev.alloc(sizeof(double) * 4 * (size_t)degree));
+        NPC_CUDA_TRY(cudaMemcpy(P->coef_dev.p, P->coef.data(), sizeof(double) * 4 * (size_t)degree,
+                                cudaMemcpyHostToDevice));
+    }
     if (op->op->permuted()) {
         NPC_TRY(P->rin.alloc(sizeof(double) * n));
         NPC_TRY(P->zout.alloc(sizeof(double) * n));
@@ -310,6 +316,8 @@ npc_status npc_destroy_poly(npc_poly poly) {
         DeviceScope ds(poly->device);
         cudaDeviceSynchronize();
         poly->tmp.release();
+        poly->tmp2.release();
+        poly->coef_dev.release();
         poly->rin.release();
         poly->zout.release();
         poly->lr_V.release();

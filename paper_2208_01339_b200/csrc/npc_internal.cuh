@@ -110,6 +110,25 @@ class Operator {
     virtual int num_partials() const = 0;
     // Algorithmic bytes of one application + recurrence, for reporting.
     virtual double bytes_per_step(bool has_s2, bool has_r) const = 0;
+    // Two consecutive degrees in one pass (temporal blocking, stencils): s1 produces s_j from
+    // s_{j-1} = s1.x, s_{j-2} = s1.s2, r = s1.r into s1.out; s2 produces s_{j+1} into s2.out
+    // (s2.x = s1.out, s2.s2 = s1.x implied) with the optional dot of s2.  Outputs must not
+    // alias the inputs.
+    virtual bool supports_step2() const { return false; }
+    virtual npc_status step2(const StepArgs &s1, const StepArgs &s2) {
+        (void)s1; (void)s2;
+        return NPC_ERR_UNSUPPORTED;
+    }
+    virtual int num_partials2() const { return num_partials(); }
+    // The whole polynomial in one launch (small CSR operators: csr_cluster.cu).  coef_dev is the
+    // 4k table of npc_poly_coefficients; writes nparts partials of <z, dotv> when dotv != null.
+    virtual bool supports_fused_poly() const { return false; }
+    virtual npc_status apply_poly_fused(const double *r, double *z, const double *coef_dev, int k, double tb,
+                                        const double *dotv, double *partials, int *nparts, const int *done) {
+        (void)r; (void)z; (void)coef_dev; (void)k; (void)tb; (void)dotv; (void)partials; (void)nparts; (void)done;
+        return NPC_ERR_UNSUPPORTED;
+    }
+    virtual double bytes_per_step2() const { return 0.0; }
     // Internal vector order differs from the caller's (SELL sigma-sort)?
     virtual bool permuted() const { return false; }
     // May its steps be stream-captured into a CUDA graph? (user callbacks: no)
@@ -221,6 +240,22 @@ npc_status launch_sum_rows(Context *ctx, const double *rows, int P, int m, doubl
 // Grid size of the plain vector kernels for n entries (fixed: partial counts are static).
 int vec_grid(int n);
 
+// Cluster-resident polynomial for small CSR operators (csr_cluster.cu)
+struct SmallCsrDev {
+    const int *rowptr;
+    const int *cols;
+    const double *vals;
+    int n, R, nnz_cta;
+};
+struct SmallCsrPlan {
+    int cl_size = 0, R = 0, nnz_cta = 0, threads = 0;
+    size_t smem = 0;
+};
+bool plan_csr_poly_cluster(int n, const int *rowptr, SmallCsrPlan &pl);
+npc_status launch_csr_poly_cluster(Context *ctx, const SmallCsrDev &A, int cl_size, int threads, size_t smem,
+                                   const double *r, double *z, const double *coef, int k, double tb,
+                                   const double *dotv, double *partials, const int *done);
+
 // Low-rank correction and Ritz vectors (lowrank.cu)
 #define NPC_LOWRANK_MAX 16
 
@@ -310,7 +345,9 @@ struct npc_poly_s {
     double lmin = 0, lmax = 0, xi = 0;
     double theta_bar = 0, delta = 0, sigma = 0;
     std::vector<double> coef;  // 4 * degree: a_j, b_j, c_j, d_j (j = 1..k)
+    npc::DevBuf coef_dev;      // the same table on the device (cluster-resident polynomial)
     npc::DevBuf tmp;           // second recurrence buffer (internal order)
+    npc::DevBuf tmp2;          // two more buffers when the operator fuses two degrees (step2)
     npc::DevBuf rin, zout;     // internal-order copies when the operator is permuted
     npc::PcgCache pcg;         // PCG work vectors + captured iteration graph
     // low-rank spectral correction P = p_k(A) + V (V^T A V)^{-1} V^T (lowrank.cu)

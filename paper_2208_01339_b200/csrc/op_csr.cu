@@ -170,6 +170,18 @@ class CsrOperator : public Operator {
         return launch_g<false, false, false>(s, tl, nt, partials, ghost);
     }
 
+    SmallCsrPlan small;  // cluster-resident polynomial (single rank, n <= 16384)
+    bool supports_fused_poly() const override {
+        return small.cl_size > 0 && !getenv("NPC_NO_CLUSTER");
+    }
+    npc_status apply_poly_fused(const double *r, double *z, const double *coef_dev, int k, double tb,
+                                const double *dotv, double *partials, int *nparts, const int *done) override {
+        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local, small.R, small.nnz_cta};
+        if (dotv && nparts) *nparts = small.cl_size;
+        return launch_csr_poly_cluster(ctx, A, small.cl_size, small.threads, small.smem, r, z, coef_dev, k, tb, dotv,
+                                       partials, done);
+    }
+
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
         if (!multi) return launch(s, nullptr, ntiles, s.partials, false);
@@ -296,6 +308,7 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
         NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
         NPC_CUDA_TRY(cudaMemcpy(op->vals.p, d->vals, sizeof(double) * nnz, cudaMemcpyHostToDevice));
     }
+    if (!op->multi && !plan_csr_poly_cluster(n, d->rowptr, op->small)) op->small = SmallCsrPlan{};
     if (op->multi) {
         NPC_TRY(op->tiles_interior.alloc(sizeof(int) * std::max<size_t>(ti.size(), 1)));
         NPC_TRY(op->tiles_boundary.alloc(sizeof(int) * std::max<size_t>(tb.size(), 1)));

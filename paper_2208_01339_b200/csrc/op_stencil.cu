@@ -74,6 +74,121 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
     }
 }
 
+// ---------------------------------------------------------------- temporal blocking
+// Two consecutive degrees in one pass (goes beyond the paper):
+//     s_j     = a1 A s_{j-1} + b1 s_{j-1} + c1 s_{j-2} + d1 r
+//     s_{j+1} = a2 A s_j     + b2 s_j     + c2 s_{j-1} + d2 r
+// A CTA owns a TBX x TBY tile of a z-chunk and marches z.  s_{j-1} is staged in shared
+// memory with a halo of 2 (ring of 3 planes), s_j is computed on the tile + a halo of 1
+// (ring of 3 planes, zero outside the domain: Dirichlet), and s_{j+1} on the tile.  Per
+// interior point and two degrees the pass reads s_{j-1}, s_{j-2}, r and writes s_j, s_{j+1}:
+// 5 vector streams instead of 8 (the halo re-reads hit L2).  Outputs go to two buffers that
+// are not inputs (neighbouring tiles still read s_{j-1} and s_{j-2} near the tile border).
+static constexpr int TBX = 32, TBY = 8, TB_ZC = 16;
+static constexpr int TPX = TBX + 4, TPY = TBY + 4;  // s_{j-1} plane with halo 2
+static constexpr int TQX = TBX + 2, TQY = TBY + 2;  // s_j plane with halo 1
+
+struct Step2Args {
+    const double *x1;   // s_{j-1}
+    const double *x2;   // s_{j-2} (nullable: c1 = 0)
+    const double *r;
+    double *o1, *o2;    // s_j, s_{j+1}
+    const double *dotv; // partial <s_{j+1}, dotv> (nullable)
+    double *partials;
+    const int *done;
+    double a1, b1, c1, d1, a2, b2, c2, d2;
+};
+
+template <bool DOT>
+__global__ void __launch_bounds__(TBX *TBY) k_stencil_step2(int nx, int ny, int nz, double diag, double off,
+                                                           Step2Args S) {
+    if (S.done && *S.done) return;
+    __shared__ double P[3][TPY][TPX];  // s_{j-1}
+    __shared__ double Q[3][TQY][TQX];  // s_j
+    __shared__ double red[TBX * TBY / 32];
+    const int tid = threadIdx.y * TBX + threadIdx.x;
+    const int gx0 = blockIdx.x * TBX, gy0 = blockIdx.y * TBY;
+    const int z0 = blockIdx.z * TB_ZC, z1 = min(z0 + TB_ZC, nz);
+    const long long plane = (long long)nx * ny;
+    auto loadP = [&](int zz) {  // s_{j-1} plane zz (zero outside the domain) -> P[zz % 3]
+        double(*Pp)[TPX] = P[(zz + 3) % 3];
+        for (int e = tid; e < TPX * TPY; e += TBX * TBY) {
+            const int ly = e / TPX, lx = e % TPX;
+            const int gx = gx0 + lx - 2, gy = gy0 + ly - 2;
+            double v = 0.0;
+            if (zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny)
+                v = S.x1[gx + (long long)nx * gy + plane * zz];
+            Pp[ly][lx] = v;
+        }
+    };
+    // prologue: s_{j-1} planes z0-2 .. z0 (z0-2 is never used as a centre, only z0-1's below)
+    loadP(z0 - 2);
+    loadP(z0 - 1);
+    double acc = 0.0;
+    for (int zz = z0 - 1; zz <= z1; ++zz) {
+        // s_j at plane zz needs s_{j-1} at zz-1, zz, zz+1
+        loadP(zz + 1);
+        __syncthreads();
+        double(*Qz)[TQX] = Q[(zz + 3) % 3];
+        const double(*Pm)[TPX] = P[(zz + 2) % 3];
+        const double(*P0)[TPX] = P[(zz + 3) % 3];
+        const double(*Pp)[TPX] = P[(zz + 4) % 3];
+        for (int e = tid; e < TQX * TQY; e += TBX * TBY) {
+            const int ly = e / TQX, lx = e % TQX;
+            const int gx = gx0 + lx - 1, gy = gy0 + ly - 1;
+            double v = 0.0;
+            if (zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny) {
+                const int px = lx + 1, py = ly + 1;  // position in P
+                const double cur = P0[py][px];
+                double nb = Pm[py][px];
+                nb += P0[py - 1][px];
+                nb += P0[py][px - 1];
+                nb += P0[py][px + 1];
+                nb += P0[py + 1][px];
+                nb += Pp[py][px];
+                const double ax = diag * cur + off * nb;
+                const long long i = gx + (long long)nx * gy + plane * zz;
+                v = S.a1 * ax + S.b1 * cur;
+                if (S.x2) v += S.c1 * S.x2[i];
+                v += S.d1 * S.r[i];
+            }
+            Qz[ly][lx] = v;
+        }
+        __syncthreads();
+        // s_{j+1} at plane zz-1 (interior tile) from s_j planes zz-2, zz-1, zz
+        const int zo = zz - 1;
+        if (zo >= z0 && zo < z1) {
+            const int gx = gx0 + threadIdx.x, gy = gy0 + threadIdx.y;
+            if (gx < nx && gy < ny) {
+                const double(*Qm)[TQX] = Q[(zo + 2) % 3];
+                const double(*Q0)[TQX] = Q[(zo + 3) % 3];
+                const double(*Qp)[TQX] = Q[(zo + 4) % 3];
+                const int qx = threadIdx.x + 1, qy = threadIdx.y + 1;
+                const double cur = Q0[qy][qx];
+                double nb = Qm[qy][qx];
+                nb += Q0[qy - 1][qx];
+                nb += Q0[qy][qx - 1];
+                nb += Q0[qy][qx + 1];
+                nb += Q0[qy + 1][qx];
+                nb += Qp[qy][qx];
+                const double ax = diag * cur + off * nb;
+                const long long i = gx + (long long)nx * gy + plane * zo;
+                const double sjm1 = P[(zo + 3) % 3][threadIdx.y + 2][threadIdx.x + 2];
+                const double o = S.a2 * ax + S.b2 * cur + S.c2 * sjm1 + S.d2 * S.r[i];
+                S.o1[i] = cur;
+                S.o2[i] = o;
+                if (DOT) acc += o * S.dotv[i];
+            }
+        }
+        // the next iteration overwrites P[(zz+2) % 3] = plane zz-1: nobody needs it any more
+        __syncthreads();
+    }
+    if (DOT) {
+        acc = block_sum<TBX * TBY>(acc, red);
+        if (tid == 0) S.partials[linear_bid()] = acc;
+    }
+}
+
 class StencilOperator : public Operator {
   public:
     int dim = 3, nx = 0, ny = 0, nzg = 1, zb = 0, nzl = 1;
@@ -129,6 +244,28 @@ class StencilOperator : public Operator {
     }
     npc_status launch(const StepArgs &s, int z_lo, int z_hi, int zc, double *p) {
         return dim == 3 ? launch_d<3>(s, z_lo, z_hi, zc, p) : launch_d<2>(s, z_lo, z_hi, zc, p);
+    }
+
+    dim3 grid2() const { return dim3(ceil_div(nx, TBX), ceil_div(ny, TBY), std::max(1, ceil_div(nzl, TB_ZC))); }
+    bool supports_step2() const override { return dim == 3 && !multi && n_local > 0 && !getenv("NPC_NO_STEP2"); }
+    int num_partials2() const override {
+        dim3 g = grid2();
+        return (int)(g.x * g.y * g.z);
+    }
+    double bytes_per_step2() const override { return 5.0 * 8.0 * n_local; }
+    npc_status step2(const StepArgs &s1, const StepArgs &s2) override {
+        Step2Args S{s1.x, s1.s2, s1.r, s1.out, s2.out, s2.dotv, s2.partials, s1.done,
+                    s1.a, s1.b, s1.c, s1.d, s2.a, s2.b, s2.c, s2.d};
+        if (!S.r) {
+            set_error("stencil step2: r is required");
+            return NPC_ERR_INVALID_ARGUMENT;
+        }
+        if (s2.dotv)
+            k_stencil_step2<true><<<grid2(), dim3(TBX, TBY), 0, ctx->stream>>>(nx, ny, nzl, diag, off, S);
+        else
+            k_stencil_step2<false><<<grid2(), dim3(TBX, TBY), 0, ctx->stream>>>(nx, ny, nzl, diag, off, S);
+        NPC_LAUNCH_CHECK();
+        return NPC_SUCCESS;
     }
 
     npc_status step(const StepArgs &s) override {

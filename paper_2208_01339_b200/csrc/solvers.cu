@@ -234,6 +234,100 @@ static npc_status apply_poly_core(npc_poly P, const double *r, double *z, const 
         return launch_scale(ctx, r, z, 1.0 / tb, op->n_local, dotv, partials, nparts, done);
     }
     double *tmp = P->tmp.as<double>();
+    if (op->supports_fused_poly() && P->coef_dev.p) {  // all k degrees in one cluster launch
+        TimedScope ts(ctx, T_DEGREE);
+        return op->apply_poly_fused(r, z, P->coef_dev.as<double>(), k, tb, dotv, partials, nparts, done);
+    }
+    if (k >= 4 && op->supports_step2() && P->tmp2.p) {
+        // Temporal blocking: degrees 1, 2 single, then pairs (j, j+1) in one pass, a single tail
+        // step if k is odd.  A pair's outputs must not alias its inputs (neighbouring tiles still
+        // read them), so four buffers rotate; labels are assigned forward and renamed at the end
+        // so that s_k lands in z.
+        struct Act {
+            int j, pair, in1, in2, o1, o2;
+        };
+        std::vector<Act> plan;
+        int cur = 0, prev = -1;  // labels of s_{j-1}, s_{j-2}
+        plan.push_back({1, 0, -1, -1, 0, -1});
+        plan.push_back({2, 0, 0, -1, 1, -1});
+        prev = 0;
+        cur = 1;
+        int j = 3;
+        for (; j + 1 <= k; j += 2) {
+            int o[2], c = 0;
+            for (int l = 0; l < 4 && c < 2; ++l)
+                if (l != cur && l != prev) o[c++] = l;
+            plan.push_back({j, 1, cur, prev, o[0], o[1]});
+            prev = o[0];
+            cur = o[1];
+        }
+        if (j == k) {
+            plan.push_back({k, 0, cur, prev, prev, -1});
+            prev = cur;
+            cur = plan.back().o1;
+        }
+        double *phys[4];
+        const size_t nn = std::max(op->n_local, 1);
+        double *spare[3] = {tmp, P->tmp2.as<double>(), P->tmp2.as<double>() + nn};
+        for (int l = 0, q = 0; l < 4; ++l) phys[l] = (l == cur) ? z : spare[q++];
+        auto coefs = [&](int jj, StepArgs &st) {
+            const double *cf = &P->coef[4 * (jj - 1)];
+            st.a = cf[0];
+            st.b = cf[1];
+            st.c = cf[2];
+            st.d = cf[3];
+        };
+        for (const Act &a : plan) {
+            const bool last = a.pair ? (a.j + 1 == k) : (a.j == k);
+            if (!a.pair) {
+                StepArgs st;
+                st.done = done;
+                st.out = phys[a.o1];
+                const double *cf = &P->coef[4 * (a.j - 1)];
+                if (a.j == 1) {
+                    st.x = r;
+                    st.a = cf[0] / tb;
+                    st.b = cf[1] / tb + cf[3];
+                } else if (a.j == 2) {
+                    st.x = phys[a.in1];
+                    st.r = r;
+                    st.a = cf[0];
+                    st.b = cf[1];
+                    st.d = cf[2] / tb + cf[3];
+                } else {
+                    st.x = phys[a.in1];
+                    st.s2 = phys[a.in2];
+                    st.r = r;
+                    coefs(a.j, st);
+                }
+                if (last && dotv) {
+                    st.dotv = dotv;
+                    st.partials = partials;
+                    if (nparts) *nparts = op->num_partials();
+                }
+                TimedScope ts(ctx, T_DEGREE);
+                NPC_TRY(op->step(st));
+            } else {
+                StepArgs s1, s2;
+                s1.done = s2.done = done;
+                s1.x = phys[a.in1];
+                s1.s2 = phys[a.in2];
+                s1.r = s2.r = r;
+                s1.out = phys[a.o1];
+                s2.out = phys[a.o2];
+                coefs(a.j, s1);
+                coefs(a.j + 1, s2);
+                if (last && dotv) {
+                    s2.dotv = dotv;
+                    s2.partials = partials;
+                    if (nparts) *nparts = op->num_partials2();
+                }
+                TimedScope ts(ctx, T_DEGREE);
+                NPC_TRY(op->step2(s1, s2));
+            }
+        }
+        return NPC_SUCCESS;
+    }
     auto buf = [&](int j) { return ((k - j) % 2 == 0) ? z : tmp; };
     for (int j = 1; j <= k; ++j) {
         const double *cf = &P->coef[4 * (j - 1)];

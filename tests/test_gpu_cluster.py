@@ -1,0 +1,73 @@
+"""Cluster-resident polynomial for small CSR operators (csr_cluster.cu): all k degrees of
+Alg. 2 in one thread-block-cluster launch with DSMEM gathers.  Same bits as the launch-per-
+degree path (same per-row operation order) and the oracle's result within the north-star bar;
+PCG through it keeps iteration parity."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2208_01339_b200 as npc  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = npc.npc_context_create(0)
+    yield c
+    torch.cuda.synchronize()
+
+
+def run(ctx, w, k, lo, hi, xi, r, cluster):
+    if cluster:
+        os.environ.pop("NPC_NO_CLUSTER", None)
+    else:
+        os.environ["NPC_NO_CLUSTER"] = "1"
+    try:
+        op = npc.create_from_workload(ctx, w, "csr")
+        poly = npc.npc_set_poly(op, k, lo, hi, xi)
+        z = torch.empty(w["n"], dtype=torch.float64, device="cuda")
+        npc.npc_apply_poly(poly, torch.tensor(r, device="cuda"), z)
+        return z.cpu().numpy()
+    finally:
+        os.environ.pop("NPC_NO_CLUSTER", None)
+
+
+CASES = {"c1": lambda: W.config1(), "c1_ragged": lambda: W.config1(side=37), "c3_20": lambda: W.config3(side=20),
+         "c4_16k": lambda: W.config4(n=16_384), "tiny": lambda: W.config1(side=5)}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("k,xi", [(1, 0.0), (2, 1e-3), (3, 0.0), (10, 1e-3), (63, 0.0)])
+def test_cluster_poly_bitwise_and_oracle(ctx, name, k, xi):
+    w = CASES[name]()
+    orc = oracle.Operator(w)
+    lo, hi = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
+    r = np.random.default_rng(k).uniform(-1, 1, w["n"])
+    zc = run(ctx, w, k, lo, hi, xi, r, True)
+    zl = run(ctx, w, k, lo, hi, xi, r, False)
+    assert np.array_equal(zc, zl), np.max(np.abs(zc - zl))
+    ref = oracle.cheb_apply(orc, k, lo, hi, xi, r)
+    assert np.linalg.norm(zc - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_cluster_pcg_config1(ctx):
+    w = W.config1()
+    orc = oracle.Operator(w)
+    lo_o, hi_o = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
+    _, st_o = oracle.pcg(orc, w["b"], 10, lo_o, hi_o, 0.0, tol=w["tol"])
+    op = npc.create_from_workload(ctx, w, "csr")
+    lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+    poly = npc.npc_set_poly(op, 10, lo, hi, 0.0)
+    x = torch.zeros(w["n"], dtype=torch.float64, device="cuda")
+    st = npc.npc_pcg_solve(poly, op, torch.tensor(w["b"], device="cuda"), x, w["tol"], 1000)
+    assert st["converged"] and abs(st["iters"] - st_o["iters"]) <= 2 and st["relres_true"] <= w["tol"]
+    assert st["op_applications"] == st["iters"] * 11 + 1
