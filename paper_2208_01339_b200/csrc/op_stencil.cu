@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
 }
 
 // ---------------------------------------------------------------- temporal blocking
-// Two consecutive degrees in one pass (goes beyond the paper):
+// Two consecutive degrees in one pass (goes beyond the paper), used
+// for stencils whose vectors do not fit L2 (see supports_step2):
 //     s_j     = a1 A s_{j-1} + b1 s_{j-1} + c1 s_{j-2} + d1 r
 //     s_{j+1} = a2 A s_j     + b2 s_j     + c2 s_{j-1} + d2 r
 // A CTA owns a TBX x TBY tile of a z-chunk and marches z.  s_{j-1} is staged in shared
@@ -84,9 +85,10 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
 // interior point and two degrees the pass reads s_{j-1}, s_{j-2}, r and writes s_j, s_{j+1}:
 // 5 vector streams instead of 8 (the halo re-reads hit L2).  Outputs go to two buffers that
 // are not inputs (neighbouring tiles still read s_{j-1} and s_{j-2} near the tile border).
-static constexpr int TBX = 32, TBY = 8, TB_ZC = 16;
+static constexpr int TBX = 32, TBY = 8, TBT = TBX * TBY;
 static constexpr int TPX = TBX + 4, TPY = TBY + 4;  // s_{j-1} plane with halo 2
 static constexpr int TQX = TBX + 2, TQY = TBY + 2;  // s_j plane with halo 1
+static constexpr int NPE = (TPX * TPY + TBT - 1) / TBT, NQE = (TQX * TQY + TBT - 1) / TBT;
 
 struct Step2Args {
     const double *x1;   // s_{j-1}
@@ -99,92 +101,136 @@ struct Step2Args {
     double a1, b1, c1, d1, a2, b2, c2, d2;
 };
 
+// Software-pipelined: while plane zz is computed, the loads of s_{j-1} at plane zz+2 and of
+// s_{j-2}, r at plane zz+1 are in flight in registers.  Rings of 4 (s_{j-1}, s_j) and 3 (r)
+// planes let two barriers per plane suffice.
 template <bool DOT>
-__global__ void __launch_bounds__(TBX *TBY) k_stencil_step2(int nx, int ny, int nz, double diag, double off,
-                                                           Step2Args S) {
+__global__ void __launch_bounds__(TBT) k_stencil_step2(int nx, int ny, int nz, int zc, double diag, double off,
+                                                      Step2Args S) {
     if (S.done && *S.done) return;
-    __shared__ double P[3][TPY][TPX];  // s_{j-1}
-    __shared__ double Q[3][TQY][TQX];  // s_j
-    __shared__ double red[TBX * TBY / 32];
+    __shared__ double P[4][TPY * TPX];  // s_{j-1}
+    __shared__ double Q[4][TQY * TQX];  // s_j
+    __shared__ double Rr[3][TQY * TQX]; // r at the s_j points
+    __shared__ double red[TBT / 32];
     const int tid = threadIdx.y * TBX + threadIdx.x;
     const int gx0 = blockIdx.x * TBX, gy0 = blockIdx.y * TBY;
-    const int z0 = blockIdx.z * TB_ZC, z1 = min(z0 + TB_ZC, nz);
+    const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, nz);
     const long long plane = (long long)nx * ny;
-    auto loadP = [&](int zz) {  // s_{j-1} plane zz (zero outside the domain) -> P[zz % 3]
-        double(*Pp)[TPX] = P[(zz + 3) % 3];
-        for (int e = tid; e < TPX * TPY; e += TBX * TBY) {
-            const int ly = e / TPX, lx = e % TPX;
-            const int gx = gx0 + lx - 2, gy = gy0 + ly - 2;
-            double v = 0.0;
-            if (zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny)
-                v = S.x1[gx + (long long)nx * gy + plane * zz];
-            Pp[ly][lx] = v;
+    // this thread's P and Q elements: global (x, y) offsets, or -1 outside the domain
+    long long pidx[NPE], qidx[NQE];
+#pragma unroll
+    for (int u = 0; u < NPE; ++u) {
+        const int e = tid + u * TBT;
+        const int gx = gx0 + e % TPX - 2, gy = gy0 + e / TPX - 2;
+        pidx[u] = (e < TPX * TPY && gx >= 0 && gx < nx && gy >= 0 && gy < ny) ? gx + (long long)nx * gy : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < NQE; ++u) {
+        const int e = tid + u * TBT;
+        const int gx = gx0 + e % TQX - 1, gy = gy0 + e / TQX - 1;
+        qidx[u] = (e < TQX * TQY && gx >= 0 && gx < nx && gy >= 0 && gy < ny) ? gx + (long long)nx * gy : -1;
+    }
+    auto ldP = [&](int u, int zz) -> double {
+        return (pidx[u] >= 0 && zz >= 0 && zz < nz) ? S.x1[pidx[u] + plane * zz] : 0.0;
+    };
+    auto ldQ = [&](const double *v, int u, int zz) -> double {
+        return (v && qidx[u] >= 0 && zz >= 0 && zz < nz) ? v[qidx[u] + plane * zz] : 0.0;
+    };
+    auto stP = [&](int zz, const double *vals) {
+#pragma unroll
+        for (int u = 0; u < NPE; ++u) {
+            const int e = tid + u * TBT;
+            if (e < TPX * TPY) P[(zz + 4) & 3][e] = vals[u];
         }
     };
-    // prologue: s_{j-1} planes z0-2 .. z0 (z0-2 is never used as a centre, only z0-1's below)
-    loadP(z0 - 2);
-    loadP(z0 - 1);
+    // prologue: s_{j-1} planes z0-2, z0-1 stored; plane z0 and s_{j-2}, r of plane z0-1 loaded
+    double pn[NPE], s2c[NQE], rc[NQE], s2n[NQE], rn[NQE];
+    {
+        double t[NPE];
+#pragma unroll
+        for (int u = 0; u < NPE; ++u) t[u] = ldP(u, z0 - 2);
+        stP(z0 - 2, t);
+#pragma unroll
+        for (int u = 0; u < NPE; ++u) t[u] = ldP(u, z0 - 1);
+        stP(z0 - 1, t);
+    }
+#pragma unroll
+    for (int u = 0; u < NPE; ++u) pn[u] = ldP(u, z0);
+#pragma unroll
+    for (int u = 0; u < NQE; ++u) {
+        s2c[u] = ldQ(S.x2, u, z0 - 1);
+        rc[u] = ldQ(S.r, u, z0 - 1);
+    }
     double acc = 0.0;
     for (int zz = z0 - 1; zz <= z1; ++zz) {
-        // s_j at plane zz needs s_{j-1} at zz-1, zz, zz+1
-        loadP(zz + 1);
+        stP(zz + 1, pn);  // s_{j-1} plane zz+1 (prefetched in the previous iteration)
         __syncthreads();
-        double(*Qz)[TQX] = Q[(zz + 3) % 3];
-        const double(*Pm)[TPX] = P[(zz + 2) % 3];
-        const double(*P0)[TPX] = P[(zz + 3) % 3];
-        const double(*Pp)[TPX] = P[(zz + 4) % 3];
-        for (int e = tid; e < TQX * TQY; e += TBX * TBY) {
-            const int ly = e / TQX, lx = e % TQX;
-            const int gx = gx0 + lx - 1, gy = gy0 + ly - 1;
-            double v = 0.0;
-            if (zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny) {
-                const int px = lx + 1, py = ly + 1;  // position in P
-                const double cur = P0[py][px];
-                double nb = Pm[py][px];
-                nb += P0[py - 1][px];
-                nb += P0[py][px - 1];
-                nb += P0[py][px + 1];
-                nb += P0[py + 1][px];
-                nb += Pp[py][px];
-                const double ax = diag * cur + off * nb;
-                const long long i = gx + (long long)nx * gy + plane * zz;
-                v = S.a1 * ax + S.b1 * cur;
-                if (S.x2) v += S.c1 * S.x2[i];
-                v += S.d1 * S.r[i];
+        // next loads in flight during this plane's compute
+#pragma unroll
+        for (int u = 0; u < NPE; ++u) pn[u] = ldP(u, zz + 2);
+#pragma unroll
+        for (int u = 0; u < NQE; ++u) {
+            s2n[u] = ldQ(S.x2, u, zz + 1);
+            rn[u] = ldQ(S.r, u, zz + 1);
+        }
+        // s_j at plane zz on the tile + halo 1
+        const double *Pm = P[(zz + 3) & 3], *P0 = P[(zz + 4) & 3], *Pp = P[(zz + 5) & 3];
+        double *Qz = Q[(zz + 4) & 3], *Rz = Rr[(zz + 3) % 3];
+#pragma unroll
+        for (int u = 0; u < NQE; ++u) {
+            const int e = tid + u * TBT;
+            if (e < TQX * TQY) {
+                double v = 0.0;
+                if (qidx[u] >= 0 && zz >= 0 && zz < nz) {
+                    const int pe = (e / TQX + 1) * TPX + e % TQX + 1;  // position in P
+                    const double cur = P0[pe];
+                    double nb = Pm[pe];
+                    nb += P0[pe - TPX];
+                    nb += P0[pe - 1];
+                    nb += P0[pe + 1];
+                    nb += P0[pe + TPX];
+                    nb += Pp[pe];
+                    const double ax = diag * cur + off * nb;
+                    v = S.a1 * ax + S.b1 * cur;
+                    if (S.x2) v += S.c1 * s2c[u];
+                    v += S.d1 * rc[u];
+                }
+                Qz[e] = v;
+                Rz[e] = rc[u];
             }
-            Qz[ly][lx] = v;
         }
         __syncthreads();
-        // s_{j+1} at plane zz-1 (interior tile) from s_j planes zz-2, zz-1, zz
+        // s_{j+1} at plane zz-1 on the tile, from s_j planes zz-2, zz-1, zz
         const int zo = zz - 1;
         if (zo >= z0 && zo < z1) {
             const int gx = gx0 + threadIdx.x, gy = gy0 + threadIdx.y;
             if (gx < nx && gy < ny) {
-                const double(*Qm)[TQX] = Q[(zo + 2) % 3];
-                const double(*Q0)[TQX] = Q[(zo + 3) % 3];
-                const double(*Qp)[TQX] = Q[(zo + 4) % 3];
-                const int qx = threadIdx.x + 1, qy = threadIdx.y + 1;
-                const double cur = Q0[qy][qx];
-                double nb = Qm[qy][qx];
-                nb += Q0[qy - 1][qx];
-                nb += Q0[qy][qx - 1];
-                nb += Q0[qy][qx + 1];
-                nb += Q0[qy + 1][qx];
-                nb += Qp[qy][qx];
+                const double *Qm = Q[(zo + 3) & 3], *Q0 = Q[(zo + 4) & 3], *Qp = Q[(zo + 5) & 3];
+                const int qe = (threadIdx.y + 1) * TQX + threadIdx.x + 1;
+                const double cur = Q0[qe];
+                double nb = Qm[qe];
+                nb += Q0[qe - TQX];
+                nb += Q0[qe - 1];
+                nb += Q0[qe + 1];
+                nb += Q0[qe + TQX];
+                nb += Qp[qe];
                 const double ax = diag * cur + off * nb;
+                const double sjm1 = P[(zo + 4) & 3][(threadIdx.y + 2) * TPX + threadIdx.x + 2];
+                const double o = S.a2 * ax + S.b2 * cur + S.c2 * sjm1 + S.d2 * Rr[(zo + 3) % 3][qe];
                 const long long i = gx + (long long)nx * gy + plane * zo;
-                const double sjm1 = P[(zo + 3) % 3][threadIdx.y + 2][threadIdx.x + 2];
-                const double o = S.a2 * ax + S.b2 * cur + S.c2 * sjm1 + S.d2 * S.r[i];
                 S.o1[i] = cur;
                 S.o2[i] = o;
                 if (DOT) acc += o * S.dotv[i];
             }
         }
-        // the next iteration overwrites P[(zz+2) % 3] = plane zz-1: nobody needs it any more
-        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < NQE; ++u) {
+            s2c[u] = s2n[u];
+            rc[u] = rn[u];
+        }
     }
     if (DOT) {
-        acc = block_sum<TBX * TBY>(acc, red);
+        acc = block_sum<TBT>(acc, red);
         if (tid == 0) S.partials[linear_bid()] = acc;
     }
 }
@@ -246,8 +292,26 @@ class StencilOperator : public Operator {
         return dim == 3 ? launch_d<3>(s, z_lo, z_hi, zc, p) : launch_d<2>(s, z_lo, z_hi, zc, p);
     }
 
-    dim3 grid2() const { return dim3(ceil_div(nx, TBX), ceil_div(ny, TBY), std::max(1, ceil_div(nzl, TB_ZC))); }
-    bool supports_step2() const override { return dim == 3 && !multi && n_local > 0 && !getenv("NPC_NO_STEP2"); }
+    // z-chunk of the fused pass: about 4 CTAs per SM (the register-limited residency) in one
+    // wave; each chunk recomputes s_j on its two boundary planes, so chunks are not made shorter
+    int zc2() const {
+        const long long tiles = (long long)ceil_div(nx, TBX) * ceil_div(ny, TBY);
+        const long long want = 4LL * ctx->num_sms;
+        return std::max(4, ceil_div((long long)nzl * tiles, std::max(want, 1LL)));
+    }
+    dim3 grid2() const { return dim3(ceil_div(nx, TBX), ceil_div(ny, TBY), std::max(1, ceil_div(nzl, zc2()))); }
+    // Measured (profiles/r01_temporal_blocking.md): the fused pass is ~10 % faster per degree
+    // when the four vector streams exceed L2 (HBM-bound: 200^3, 256^3) and 1.6x slower when
+    // they are L2-resident (128^3, config 2), so it is used only above ~3/4 of the L2 size.
+    // NPC_STEP2=1 forces it on, NPC_NO_STEP2=1 off.
+    bool supports_step2() const override {
+        if (dim != 3 || multi || n_local == 0 || getenv("NPC_NO_STEP2")) return false;
+        if (getenv("NPC_STEP2")) return true;
+        int l2 = 0;
+        if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device) != cudaSuccess || l2 <= 0)
+            l2 = 126 << 20;
+        return 4.0 * 8.0 * n_local > 0.75 * l2;
+    }
     int num_partials2() const override {
         dim3 g = grid2();
         return (int)(g.x * g.y * g.z);
@@ -260,10 +324,11 @@ class StencilOperator : public Operator {
             set_error("stencil step2: r is required");
             return NPC_ERR_INVALID_ARGUMENT;
         }
+        const int zc = zc2();
         if (s2.dotv)
-            k_stencil_step2<true><<<grid2(), dim3(TBX, TBY), 0, ctx->stream>>>(nx, ny, nzl, diag, off, S);
+            k_stencil_step2<true><<<grid2(), dim3(TBX, TBY), 0, ctx->stream>>>(nx, ny, nzl, zc, diag, off, S);
         else
-            k_stencil_step2<false><<<grid2(), dim3(TBX, TBY), 0, ctx->stream>>>(nx, ny, nzl, diag, off, S);
+            k_stencil_step2<false><<<grid2(), dim3(TBX, TBY), 0, ctx->stream>>>(nx, ny, nzl, zc, diag, off, S);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }

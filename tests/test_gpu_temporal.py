@@ -32,9 +32,11 @@ def ctx():
 
 
 def apply(ctx, w, k, lo, hi, xi, r, step2):
-    if step2:
+    if step2:  # small grids are L2-resident: force the fused pass on
         os.environ.pop("NPC_NO_STEP2", None)
+        os.environ["NPC_STEP2"] = "1"
     else:
+        os.environ.pop("NPC_STEP2", None)
         os.environ["NPC_NO_STEP2"] = "1"
     try:
         op = npc.create_from_workload(ctx, w, "stencil")
@@ -44,6 +46,7 @@ def apply(ctx, w, k, lo, hi, xi, r, step2):
         return z.cpu().numpy()
     finally:
         os.environ.pop("NPC_NO_STEP2", None)
+        os.environ.pop("NPC_STEP2", None)
 
 
 @pytest.mark.parametrize("dims", [(24, 24, 24), (37, 13, 29), (33, 9, 17), (8, 8, 40)])
@@ -60,7 +63,8 @@ def test_step2_bitwise_and_oracle(ctx, dims, k):
     assert np.linalg.norm(z2 - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
-def test_step2_pcg(ctx):
+def test_step2_pcg(ctx, monkeypatch):
+    monkeypatch.setenv("NPC_STEP2", "1")
     w = W.config2(side=30)
     orc = oracle.Operator(w)
     lo_o, hi_o = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
