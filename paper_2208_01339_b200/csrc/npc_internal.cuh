@@ -100,6 +100,7 @@ struct StepArgs {
 };
 
 struct Context;
+struct ClusterPcgOut;
 
 class Operator {
   public:
@@ -123,6 +124,14 @@ class Operator {
     // The whole polynomial in one launch (small CSR operators: csr_cluster.cu).  coef_dev is the
     // 4k table of npc_poly_coefficients; writes nparts partials of <z, dotv> when dotv != null.
     virtual bool supports_fused_poly() const { return false; }
+    // The whole PCG solve in one launch (small CSR operators, single rank).
+    virtual bool supports_fused_pcg() const { return false; }
+    virtual npc_status pcg_fused(const double *b, double *x, const double *coef_dev, int k, double tb, int use_poly,
+                                 double tol2b, int maxit, ClusterPcgOut *out, double *history) {
+        (void)b; (void)x; (void)coef_dev; (void)k; (void)tb; (void)use_poly; (void)tol2b; (void)maxit; (void)out;
+        (void)history;
+        return NPC_ERR_UNSUPPORTED;
+    }
     virtual npc_status apply_poly_fused(const double *r, double *z, const double *coef_dev, int k, double tb,
                                         const double *dotv, double *partials, int *nparts, const int *done) {
         (void)r; (void)z; (void)coef_dev; (void)k; (void)tb; (void)dotv; (void)partials; (void)nparts; (void)done;
@@ -249,8 +258,17 @@ struct SmallCsrDev {
 };
 struct SmallCsrPlan {
     int cl_size = 0, R = 0, nnz_cta = 0, threads = 0;
-    size_t smem = 0;
+    size_t smem = 0;      // polynomial kernel
+    size_t smem_pcg = 0;  // whole-PCG kernel (0: does not fit)
 };
+struct ClusterPcgOut {
+    int iters, converged, breakdown, pad;
+    long long applications, reductions;
+    double rr, relres_true, bnorm2;
+};
+npc_status launch_csr_pcg_cluster(Context *ctx, const SmallCsrDev &A, const SmallCsrPlan &pl, const double *b,
+                                  double *x, const double *coef, int k, double tb, int use_poly, double tol2b,
+                                  int maxit, ClusterPcgOut *out, double *history);
 bool plan_csr_poly_cluster(int n, const int *rowptr, SmallCsrPlan &pl);
 npc_status launch_csr_poly_cluster(Context *ctx, const SmallCsrDev &A, int cl_size, int threads, size_t smem,
                                    const double *r, double *z, const double *coef, int k, double tb,

@@ -182,6 +182,15 @@ class CsrOperator : public Operator {
                                        partials, done);
     }
 
+    bool supports_fused_pcg() const override {
+        return supports_fused_poly() && small.smem_pcg > 0;
+    }
+    npc_status pcg_fused(const double *b, double *x, const double *coef_dev, int k, double tb, int use_poly,
+                         double tol2b, int maxit, ClusterPcgOut *out, double *history) override {
+        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local, small.R, small.nnz_cta};
+        return launch_csr_pcg_cluster(ctx, A, small, b, x, coef_dev, k, tb, use_poly, tol2b, maxit, out, history);
+    }
+
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
         if (!multi) return launch(s, nullptr, ntiles, s.partials, false);

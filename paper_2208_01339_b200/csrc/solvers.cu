@@ -577,6 +577,53 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     double *host_hist = stats ? stats->history : nullptr;
     // work vectors (internal order): b, x, r, u, w, p, s
     PcgCache &cache = P ? P->pcg : H->pcg;
+    if (op->supports_fused_pcg() && ctx->nranks == 1 && (!P || (P->kind == 0 && P->lr_p == 0 &&
+                                                                (P->degree == 0 || P->coef_dev.p)))) {
+        // small operator: the whole solve in one cluster launch (csr_cluster.cu)
+        if (cache.dev_maxit < maxit) {
+            cache.invalidate();
+            NPC_TRY(cache.dev.alloc(sizeof(CgDev) + sizeof(double) * (8 + (size_t)maxit + 1)));
+            cache.dev_maxit = maxit;
+        }
+        ClusterPcgOut *dout = reinterpret_cast<ClusterPcgOut *>(cache.dev.p);
+        double *dhist = reinterpret_cast<double *>(cache.dev.as<char>() + sizeof(CgDev)) + 8;
+        // tol2b = tol^2 ||b||^2 needs ||b||: the kernel forms ||b||^2 itself, so pass tol^2 and
+        // let it scale (encoded as a negative number: -tol^2)
+        {
+            TimedScope ts(ctx, T_DEGREE);
+            NPC_TRY(op->pcg_fused(b_ext, x_ext, P ? P->coef_dev.as<double>() : nullptr, k,
+                                  P ? P->theta_bar : 1.0, P ? 1 : 0, -tol * tol, maxit, dout,
+                                  host_hist ? dhist : nullptr));
+        }
+        ClusterPcgOut h;
+        NPC_CUDA_TRY(cudaMemcpyAsync(&h, dout, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        if (host_hist && h.iters >= 0)
+            NPC_CUDA_TRY(cudaMemcpyAsync(host_hist, dhist, sizeof(double) * ((size_t)maxit + 1),
+                                         cudaMemcpyDeviceToHost, ctx->stream));
+        NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (ctx->timing) ctx->t_flush();
+        st.iters = h.iters;
+        st.converged = h.converged;
+        st.op_applications = h.applications;
+        st.reductions = h.reductions;
+        st.relres_recursive = h.bnorm2 > 0.0 ? sqrt(h.rr / h.bnorm2) : 0.0;
+        st.relres_true = h.relres_true;
+        st.solve_seconds = now_s() - t0;
+        if (stats) {
+            double *hh = stats->history;
+            *stats = st;
+            stats->history = hh;
+        }
+        if (h.breakdown) {
+            set_error("PCG breakdown (%s <= 0) at iteration %d", h.breakdown == 1 ? "<r,z>" : "<p,Ap>", h.iters);
+            return NPC_ERR_BREAKDOWN;
+        }
+        if (!h.converged) {
+            set_error("PCG did not converge in %d iterations (true relres %.3e)", maxit, h.relres_true);
+            return NPC_ERR_NOT_CONVERGED;
+        }
+        return NPC_SUCCESS;
+    }
     const size_t nn = std::max(n, 1);
     if (cache.work_n != nn) {
         cache.invalidate();
