@@ -400,6 +400,83 @@ __global__ void k_csr_pcg_cluster(SmallCsrDev A, const double *__restrict__ b, d
     }
 }
 
+// ================================================================== Lanczos in one cluster
+// The m-step Lanczos of solvers.cu (same recurrence and operation order: q = v0 / ||v0||;
+// w = A q - beta_{j-1} q_prev; alpha_j = <q, w>; w -= alpha_j q; beta_j = ||w||; stop when
+// beta_j = 0) for small CSR operators, all steps in one launch.  Writes alpha, beta and the
+// number of steps taken; the host then forms the Ritz values exactly as for the grid path.
+__global__ void k_csr_lanczos_cluster(SmallCsrDev A, const double *__restrict__ v0, int m, double *alphas,
+                                      double *betas, int *steps_out) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int c = (int)cl.block_rank();
+    const int R = A.R;
+    const int row0 = c * R, row1 = min(A.n, row0 + R), nr = max(0, row1 - row0);
+    extern __shared__ __align__(16) double sm[];
+    double *Q = sm, *Qp = sm + R, *Wv = sm + 2 * R;
+    double *vs = sm + 9 * R;  // same layout as the PCG kernel (fits whenever it does)
+    int *cs = reinterpret_cast<int *>(vs + A.nnz_cta);
+    int *rp = cs + A.nnz_cta;
+    __shared__ double slots[2 * 48];
+    __shared__ double red[100];
+    ClusterReduce cr{slots, 0};
+    const int p0 = A.rowptr[row0 < A.n ? row0 : A.n], p1 = A.rowptr[row1 < A.n ? row1 : A.n];
+    for (int e = threadIdx.x; e < p1 - p0; e += blockDim.x) {
+        vs[e] = A.vals[p0 + e];
+        cs[e] = A.cols[p0 + e];
+    }
+    if (nr > 0)
+        for (int i = threadIdx.x; i <= nr; i += blockDim.x) rp[i] = A.rowptr[row0 + i] - p0;
+    double vn = 0.0, u1 = 0.0, u2 = 0.0;
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+        const double v = v0[row0 + i];
+        Wv[i] = v;
+        vn += v * v;
+    }
+    cluster_sums3(cl, cr, red, vn, u1, u2);
+    const double inv0 = 1.0 / sqrt(vn);
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+        Q[i] = Wv[i] * inv0;
+        Qp[i] = 0.0;
+    }
+    cl.sync();
+    double beta_prev = 0.0;
+    int steps = 0;
+    for (int j = 0; j < m; ++j) {
+        double a = 0.0, t1 = 0.0, t2 = 0.0;
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+            double wi = row_apply(cl, c, R, row0, rp, cs, vs, Q, i);
+            if (j) wi -= beta_prev * Qp[i];
+            Wv[i] = wi;
+            a += Q[i] * wi;
+        }
+        cluster_sums3(cl, cr, red, a, t1, t2);
+        double bb = 0.0;
+        t1 = t2 = 0.0;
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+            const double wi = Wv[i] - a * Q[i];
+            Wv[i] = wi;
+            bb += wi * wi;
+        }
+        cluster_sums3(cl, cr, red, bb, t1, t2);
+        const double bj = sqrt(bb);
+        if (c == 0 && threadIdx.x == 0) {
+            alphas[j] = a;
+            betas[j] = bj;
+        }
+        steps = j + 1;
+        if (bj == 0.0) break;
+        const double inv = 1.0 / bj;
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+            Qp[i] = Q[i];
+            Q[i] = Wv[i] * inv;
+        }
+        beta_prev = bj;
+        cl.sync();  // new q visible before the next gathers
+    }
+    cl.sync();
+    if (c == 0 && threadIdx.x == 0) *steps_out = steps;
+}
+
 // Non-portable cluster size (16) and the dynamic shared memory limit, set once per process.
 static cudaError_t cluster_attrs() {
     static std::once_flag once;
@@ -412,6 +489,11 @@ static cudaError_t cluster_attrs() {
             err = cudaFuncSetAttribute(k_csr_pcg_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (err == cudaSuccess)
             err = cudaFuncSetAttribute(k_csr_pcg_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(k_csr_lanczos_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(k_csr_lanczos_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024);
     });
     return err;
 }
@@ -515,6 +597,30 @@ npc_status launch_csr_pcg_cluster(Context *ctx, const SmallCsrDev &A, const Smal
     cfg.numAttrs = 1;
     NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_csr_pcg_cluster, A, b, x, coef, k, tb, use_poly, tol2b, maxit, out,
                                     history));
+    NPC_LAUNCH_CHECK();
+    return NPC_SUCCESS;
+}
+
+}  // namespace npc
+
+namespace npc {
+
+npc_status launch_csr_lanczos_cluster(Context *ctx, const SmallCsrDev &A, const SmallCsrPlan &pl, const double *v0,
+                                      int m, double *alphas, double *betas, int *steps) {
+    NPC_CUDA_TRY(cluster_attrs());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.cl_size, 1, 1);
+    cfg.blockDim = dim3(pl.threads, 1, 1);
+    cfg.dynamicSmemBytes = pl.smem_pcg;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = pl.cl_size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_csr_lanczos_cluster, A, v0, m, alphas, betas, steps));
     NPC_LAUNCH_CHECK();
     return NPC_SUCCESS;
 }

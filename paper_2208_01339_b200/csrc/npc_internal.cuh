@@ -124,6 +124,13 @@ class Operator {
     // The whole polynomial in one launch (small CSR operators: csr_cluster.cu).  coef_dev is the
     // 4k table of npc_poly_coefficients; writes nparts partials of <z, dotv> when dotv != null.
     virtual bool supports_fused_poly() const { return false; }
+    // All steps of the Lanczos estimate in one launch (small CSR operators, single rank);
+    // v0 in internal order; writes alphas[m], betas[m] and the steps taken (device).
+    virtual bool supports_fused_lanczos() const { return false; }
+    virtual npc_status lanczos_fused(const double *v0, int m, double *alphas, double *betas, int *steps) {
+        (void)v0; (void)m; (void)alphas; (void)betas; (void)steps;
+        return NPC_ERR_UNSUPPORTED;
+    }
     // The whole PCG solve in one launch (small CSR operators, single rank).
     virtual bool supports_fused_pcg() const { return false; }
     virtual npc_status pcg_fused(const double *b, double *x, const double *coef_dev, int k, double tb, int use_poly,
@@ -266,6 +273,8 @@ struct ClusterPcgOut {
     long long applications, reductions;
     double rr, relres_true, bnorm2;
 };
+npc_status launch_csr_lanczos_cluster(Context *ctx, const SmallCsrDev &A, const SmallCsrPlan &pl, const double *v0,
+                                      int m, double *alphas, double *betas, int *steps);
 npc_status launch_csr_pcg_cluster(Context *ctx, const SmallCsrDev &A, const SmallCsrPlan &pl, const double *b,
                                   double *x, const double *coef, int k, double tb, int use_poly, double tol2b,
                                   int maxit, ClusterPcgOut *out, double *history);

@@ -182,6 +182,11 @@ class CsrOperator : public Operator {
                                        partials, done);
     }
 
+    bool supports_fused_lanczos() const override { return supports_fused_pcg(); }
+    npc_status lanczos_fused(const double *v0, int m, double *alphas, double *betas, int *steps) override {
+        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local, small.R, small.nnz_cta};
+        return launch_csr_lanczos_cluster(ctx, A, small, v0, m, alphas, betas, steps);
+    }
     bool supports_fused_pcg() const override {
         return supports_fused_poly() && small.smem_pcg > 0;
     }

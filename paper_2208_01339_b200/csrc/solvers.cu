@@ -1078,6 +1078,10 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, doub
         set_error("estimate_spectrum: start vector is zero");
         return NPC_ERR_INVALID_ARGUMENT;
     }
+    if (op->supports_fused_lanczos() && ctx->nranks == 1) {  // small operator: one cluster launch
+        TimedScope ts(ctx, T_OPERATOR);
+        NPC_TRY(op->lanczos_fused(v0, m, alphas, betas, &lz->steps));
+    } else {
     k_lz_scale_init<<<npv, 256, 0, ctx->stream>>>(v0, q, qp, n, &lz->vn2);
     NPC_LAUNCH_CHECK();
     for (int j = 0; j < m; ++j) {
@@ -1120,6 +1124,7 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, doub
             k_lz_next<<<npv, 256, 0, ctx->stream>>>(lz, w, q, qp, &betas[j], n);
             NPC_LAUNCH_CHECK();
         }
+    }
     }
     LzDev hl;
     std::vector<double> ha(m), hb(m);
