@@ -58,8 +58,9 @@ def make_workload(cfg: int, side: int | None):
         return W.config4(n=side or 8_000_000)
     if cfg == 5:
         return W.config5(n=side or 4_000_000)
-    if cfg == 6:  # the paper's DFN Schur operator, Frac32-sized
-        return W.dfn(nf=side or 29_370)
+    if cfg == 6:  # the paper's DFN Schur operator, Frac32-sized, u in
+        # owner order so that --gpus N can use the DSMat fracture-block partition
+        return W.dfn_owner_order(W.dfn(nf=side or 29_370))
     raise ValueError(cfg)
 
 
@@ -227,6 +228,24 @@ def create_operator(npc, ctx, w, kind, ws, rank, cfg):
                                      b_rowptr=(bp - bp[0]).astype(np.int32), b_colidx=w["bcolidx"][bp[0]:bp[-1]],
                                      b_vals=w["bvals"][bp[0]:bp[-1]], d=w["d"][q0:q1])
         return op, r0, r1
+    if kind == "dfn":
+        # DSMat partition: consecutive whole fracture blocks per rank, u rows
+        # by owning fracture (w must be in owner order: workloads.dfn_owner_order)
+        nf = w["nf"]
+        f0, f1 = nf * rank // ws, nf * (rank + 1) // ws
+        hb = np.asarray(w["hblk"], dtype=np.int64)
+        h0, h1 = int(hb[f0]), int(hb[f1])
+        u0, u1 = int(w["uoff"][f0]), int(w["uoff"][f1])
+
+        def rows(t, a, b):
+            rp, ci, v = t
+            return ((rp[a:b + 1] - rp[a]).astype(np.int32), ci[rp[a]:rp[b]], v[rp[a]:rp[b]])
+        op = npc.npc_create_operator(
+            ctx, "dfn", n_local=u1 - u0, n_global=w["n"], row_begin=u0,
+            dfn=dict(nh=h1 - h0, nblk=f1 - f0, hblk=(hb[f0:f1 + 1] - h0).astype(np.int32), A=rows(w["A"], h0, h1),
+                     Gh=rows(w["Gh"], h0, h1), C=rows(w["C"], h0, h1), B=rows(w["B"], h0, h1),
+                     Gu=rows(w["Gu"], u0, u1), alpha=w["alpha"], scaled=w.get("scaled", 1)))
+        return op, u0, u1
     raise SystemExit(f"config kind {kind} does not support --gpus > 1 in this version")
 
 

@@ -55,6 +55,34 @@ npc_status halo_plan_local(int n_local, const int *rowptr, const int *colidx, in
     return NPC_SUCCESS;
 }
 
+// Plan from an arbitrary list of referenced global ids (any row space; duplicates and owned
+// ids allowed): ghosts = the sorted distinct ids outside [row_starts[rank], row_starts[rank+1]).
+npc_status halo_plan_from_ids(std::vector<long long> ids, int nranks, const long long *row_starts, int rank,
+                              HaloPlan &plan) {
+    const long long r0 = row_starts[rank], r1 = row_starts[rank + 1], nglob = row_starts[nranks];
+    std::vector<long long> g;
+    for (long long c : ids) {
+        if (c < 0 || c >= nglob) {
+            set_error("halo_plan: id %lld out of range", c);
+            return NPC_ERR_DIMENSION;
+        }
+        if (c < r0 || c >= r1) g.push_back(c);
+    }
+    std::sort(g.begin(), g.end());
+    g.erase(std::unique(g.begin(), g.end()), g.end());
+    plan.ghost_ids = g;
+    plan.n_ghost = (int)g.size();
+    plan.recv_count.assign(nranks, 0);
+    plan.recv_off.assign(nranks, 0);
+    int q = 0;
+    for (size_t i = 0; i < g.size(); ++i) {
+        while (g[i] >= row_starts[q + 1]) ++q;
+        plan.recv_count[q]++;
+    }
+    for (int k = 1; k < nranks; ++k) plan.recv_off[k] = plan.recv_off[k - 1] + plan.recv_count[k - 1];
+    return NPC_SUCCESS;
+}
+
 // Turn every rank's recv lists (ghost ids, by owner) into the owners' send lists.
 npc_status halo_plan_exchange(Context *ctx, long long row_begin, HaloPlan &plan) {
     const int P = ctx->nranks;

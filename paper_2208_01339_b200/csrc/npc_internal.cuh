@@ -305,6 +305,8 @@ struct HaloPlan {
 };
 npc_status halo_plan_local(int n_local, const int *rowptr, const int *colidx, int nranks,
                            const long long *row_starts, int rank, HaloPlan &plan);
+npc_status halo_plan_from_ids(std::vector<long long> ids, int nranks, const long long *row_starts, int rank,
+                              HaloPlan &plan);
 // Exchange ghost-id lists with the owners (NCCL, collective) to fill send lists.
 npc_status halo_plan_exchange(Context *ctx, long long row_begin, HaloPlan &plan);
 // Per-step exchange: pack x[send_idx] -> send buffer, ncclSend/Recv to the ghost buffer,

@@ -30,10 +30,13 @@
 //     w2 = A^-1 v2; write t and u2 = w2 - a w.
 //   k_dfn_out: one thread per u row: y = GuS x - a BsT t + CsT u2  (Alg. 3 steps 7 and 11),
 //     fused with the Chebyshev epilogue out = a_j y + b_j x + c_j s2 + d_j r (+ PCG partial).
-// Single rank in this version (the paper's DSMat partitions by whole fracture blocks; B and
-// G^u would need a halo).
+// Multi-rank: the paper's DSMat partition -- whole fracture blocks per rank,
+// u rows grouped by owning fracture (C is fracture-local, so Alg. 4 stays rank-local); per
+// application a u-space halo of x (B's E part, G^u) and an h-space halo of t and u2 (rows of
+// B^T held by other ranks' fractures, gathered once at setup).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <thread>
 #include <vector>
 
@@ -275,6 +278,7 @@ struct DfnOutDev {
     const int *ctrp, *ctci;
     const double *ctv;
     const double *t, *u2;
+    const double *xg;  // x for the G^u gathers (owned rows + ghosts when multi-rank)
     double alpha;
     int n;
 };
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(DFN_OUT_T) k_dfn_out(DfnOutDev O, StepArgs s) 
     if (i < O.n) {
         const double *__restrict__ X = s.x;
         double g = 0.0, bt = 0.0, ct = 0.0;
-        for (int p = O.gurp[i]; p < O.gurp[i + 1]; ++p) g += O.guv[p] * __ldg(X + O.guci[p]);
+        for (int p = O.gurp[i]; p < O.gurp[i + 1]; ++p) g += O.guv[p] * __ldg(O.xg + O.guci[p]);
         for (int p = O.btrp[i]; p < O.btrp[i + 1]; ++p) bt += O.btv[p] * __ldg(O.t + O.btci[p]);
         for (int p = O.ctrp[i]; p < O.ctrp[i + 1]; ++p) ct += O.ctv[p] * __ldg(O.u2 + O.ctci[p]);
         const double y = g - O.alpha * bt + ct;
@@ -355,7 +359,15 @@ class DfnOperator : public Operator {
     DevBuf t, u2;
     DevBuf ainv, dense_info, band_list, perm;
     bool perm_dev_needed = false;
-    bool permuted() const override { return true; }
+    // multi-rank (the paper's DSMat partition): whole fracture blocks per
+    // rank, u rows by owning fracture; per application a u-space halo of x (columns of B's E
+    // part and of G^u) and an h-space halo of t and u2 (rows of B^T from other ranks' fractures)
+    bool multi = false;
+    int ngu = 0, ngh = 0;
+    HaloPlan uplan, hplan;
+    HaloRuntime urt, trt, u2rt;
+    DevBuf xg;  // x of the owned u rows followed by the u ghosts
+    bool permuted() const override { return !multi; }
     npc_status to_internal(const double *in, double *out) override {
         return launch_gather(ctx, in, perm.as<int>(), out, n_local);
     }
@@ -411,23 +423,45 @@ class DfnOperator : public Operator {
     npc_status launch_out(const StepArgs &s) {
         DfnOutDev O{gurp.as<int>(), guci.as<int>(), guv.as<double>(), btrp.as<int>(), btci.as<int>(),
                     btv.as<double>(), ctrp.as<int>(), ctci.as<int>(), ctv.as<double>(), t.as<double>(),
-                    u2.as<double>(), alpha, n_local};
+                    u2.as<double>(), multi ? xg.as<double>() : s.x, alpha, n_local};
         k_dfn_out<H2, HR, DT><<<num_partials(), DFN_OUT_T, 0, ctx->stream>>>(O, s);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
+    // ghosts of a halo -> the tail of a local+ghost buffer
+    npc_status halo_into(const HaloPlan &plan, HaloRuntime &rt, const double *src, double *full, int nown) {
+        NPC_TRY(halo_start(ctx, plan, rt, src));
+        NPC_TRY(halo_wait(ctx, rt));
+        if (plan.n_ghost)
+            NPC_CUDA_TRY(cudaMemcpyAsync(full + nown, rt.ghost_buf.p, sizeof(double) * plan.n_ghost,
+                                         cudaMemcpyDeviceToDevice, ctx->stream));
+        return NPC_SUCCESS;
+    }
     npc_status step(const StepArgs &s) override {
-        if (n_local == 0) return NPC_SUCCESS;
+        if (n_local == 0 && !multi) return NPC_SUCCESS;
+        const double *xin = s.x;
+        if (multi) {
+            if (n_local)
+                NPC_CUDA_TRY(cudaMemcpyAsync(xg.p, s.x, sizeof(double) * n_local, cudaMemcpyDeviceToDevice,
+                                             ctx->stream));
+            NPC_TRY(halo_into(uplan, urt, s.x, xg.as<double>(), n_local));
+            xin = xg.as<double>();
+        }
         if (n_dense > 0) {  // rows per lane
-            if (dense_nt == 32) NPC_TRY(launch_dense<1>(s.x, s.done));
-            else if (dense_nt == 64) NPC_TRY(launch_dense<2>(s.x, s.done));
-            else NPC_TRY(launch_dense<4>(s.x, s.done));
+            if (dense_nt == 32) NPC_TRY(launch_dense<1>(xin, s.done));
+            else if (dense_nt == 64) NPC_TRY(launch_dense<2>(xin, s.done));
+            else NPC_TRY(launch_dense<4>(xin, s.done));
         }
         if (n_band > 0) {
-            if (lanes == 4) NPC_TRY(launch_block<4>(s.x, s.done));
-            else if (lanes == 8) NPC_TRY(launch_block<8>(s.x, s.done));
-            else if (lanes == 16) NPC_TRY(launch_block<16>(s.x, s.done));
-            else NPC_TRY(launch_block<32>(s.x, s.done));
+            if (lanes == 4) NPC_TRY(launch_block<4>(xin, s.done));
+            else if (lanes == 8) NPC_TRY(launch_block<8>(xin, s.done));
+            else if (lanes == 16) NPC_TRY(launch_block<16>(xin, s.done));
+            else NPC_TRY(launch_block<32>(xin, s.done));
+        }
+        if (multi) {
+            NPC_TRY(halo_into(hplan, trt, t.as<double>(), t.as<double>(), nh));
+            NPC_TRY(halo_into(hplan, u2rt, u2.as<double>(), u2.as<double>(), nh));
+            if (n_local == 0) return NPC_SUCCESS;
         }
         const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
         if (h2 && hr && dt) return launch_out<true, true, true>(s);
@@ -448,11 +482,84 @@ static npc_status upload(DevBuf &b, const T *src, size_t n) {
     return NPC_SUCCESS;
 }
 
-npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out) {
-    if (ctx->nranks > 1) {
-        set_error("DFN: nranks > 1 is not supported in this version");
-        return NPC_ERR_UNSUPPORTED;
+npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d0, std::unique_ptr<Operator> &out) {
+    const bool multi = ctx->nranks > 1;
+    const int P = ctx->nranks, me = ctx->rank;
+    // ---- partition (multi-rank): u rows [U0, U0 + n_local), h rows [H0, H0 + n^h_local) in rank
+    // order; the desc's A / G^h columns are GLOBAL h ids, C / B / G^u columns GLOBAL u ids.
+    std::vector<long long> u_starts{0}, h_starts{0};
+    if (multi) {
+        std::vector<long long> all_nu, all_nh;
+        NPC_TRY(ctx->tr->allgather_i64(ctx, d0->n_local, all_nu));
+        NPC_TRY(ctx->tr->allgather_i64(ctx, d0->dfn_nh, all_nh));
+        for (int q = 0; q < P; ++q) {
+            u_starts.push_back(u_starts.back() + all_nu[q]);
+            h_starts.push_back(h_starts.back() + all_nh[q]);
+        }
+        if (d0->row_begin != u_starts[me] || (d0->n_global && d0->n_global != u_starts[P])) {
+            set_error("DFN: row_begin / n_global disagree with the rank-ordered u partition");
+            return NPC_ERR_DIMENSION;
+        }
+    } else {
+        u_starts.push_back(d0->n_local);
+        h_starts.push_back(d0->dfn_nh);
     }
+    const long long U0 = u_starts[me], H0 = h_starts[me], NU = u_starts[P], NH = h_starts[P];
+    npc_operator_desc dl = *d0;  // localized copy: the rest works in local ids
+    const npc_operator_desc *d = &dl;
+    const int nh0 = (int)std::max(0LL, std::min(d0->dfn_nh, (long long)INT32_MAX));
+    std::vector<int> a_ci, gh_ci, c_ci, b_ci, gu_ci;
+    HaloPlan uplan;
+    std::vector<long long> b_glob;  // B column ids (global) for the multi-rank B^T exchange
+    if (multi) {
+        if (d0->dfn_nh < 0 || !d0->a_rowptr || !d0->gh_rowptr || !d0->c_rowptr || !d0->bm_rowptr ||
+            !d0->gu_rowptr) {
+            set_error("DFN: missing arrays");
+            return NPC_ERR_INVALID_ARGUMENT;
+        }
+        NPC_TRY(check_csr("A", nh0, (int)std::min(NH, (long long)INT32_MAX), d0->a_rowptr, d0->a_colidx, d0->a_vals));
+        NPC_TRY(check_csr("G^h", nh0, (int)std::min(NH, (long long)INT32_MAX), d0->gh_rowptr, d0->gh_colidx,
+                          d0->gh_vals));
+        NPC_TRY(check_csr("C", nh0, (int)NU, d0->c_rowptr, d0->c_colidx, d0->c_vals));
+        NPC_TRY(check_csr("B", nh0, (int)NU, d0->bm_rowptr, d0->bm_colidx, d0->bm_vals));
+        NPC_TRY(check_csr("G^u", d0->n_local, (int)NU, d0->gu_rowptr, d0->gu_colidx, d0->gu_vals));
+        auto shift = [&](const int *rp, const int *ci, int nrows, long long base, std::vector<int> &o) {
+            o.assign(ci, ci + rp[nrows]);
+            for (int &c : o) c = (int)(c - base);  // block checks below reject foreign columns
+        };
+        shift(d0->a_rowptr, d0->a_colidx, nh0, H0, a_ci);
+        shift(d0->gh_rowptr, d0->gh_colidx, nh0, H0, gh_ci);
+        c_ci.assign(d0->c_colidx, d0->c_colidx + d0->c_rowptr[nh0]);
+        for (int &c : c_ci) {
+            if (c < U0 || c >= U0 + d0->n_local) {
+                set_error("DFN: rank %d: column %d of C is not an owned u row (the u partition must follow "
+                          "fracture ownership: C is fracture-local)", me, c);
+                return NPC_ERR_UNSUPPORTED;
+            }
+            c = (int)(c - U0);
+        }
+        std::vector<long long> ids;
+        for (int p = 0; p < d0->bm_rowptr[nh0]; ++p) ids.push_back(d0->bm_colidx[p]);
+        for (int p = 0; p < d0->gu_rowptr[d0->n_local]; ++p) ids.push_back(d0->gu_colidx[p]);
+        b_glob.assign(d0->bm_colidx, d0->bm_colidx + d0->bm_rowptr[nh0]);
+        NPC_TRY(halo_plan_from_ids(ids, P, u_starts.data(), me, uplan));
+        NPC_TRY(halo_plan_exchange(ctx, U0, uplan));
+        auto uloc = [&](long long c) -> int {
+            if (c >= U0 && c < U0 + d0->n_local) return (int)(c - U0);
+            return d0->n_local +
+                   (int)(std::lower_bound(uplan.ghost_ids.begin(), uplan.ghost_ids.end(), c) - uplan.ghost_ids.begin());
+        };
+        b_ci.resize(d0->bm_rowptr[nh0]);
+        for (int p = 0; p < d0->bm_rowptr[nh0]; ++p) b_ci[p] = uloc(d0->bm_colidx[p]);
+        gu_ci.resize(d0->gu_rowptr[d0->n_local]);
+        for (int p = 0; p < d0->gu_rowptr[d0->n_local]; ++p) gu_ci[p] = uloc(d0->gu_colidx[p]);
+        dl.a_colidx = a_ci.data();
+        dl.gh_colidx = gh_ci.data();
+        dl.c_colidx = c_ci.data();
+        dl.bm_colidx = b_ci.data();
+        dl.gu_colidx = gu_ci.data();
+    }
+    const int ngu = multi ? uplan.n_ghost : 0;
     const int nu = d->n_local, nblk = d->dfn_nblk;
     const long long nhl = d->dfn_nh;
     if (nhl < 0 || nhl >= (1LL << 31) || nblk < 0 || (nblk > 0 && !d->dfn_hblk) || !(std::isfinite(d->dfn_alpha))) {
@@ -472,13 +579,16 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     NPC_TRY(check_csr("A", nh, nh, d->a_rowptr, d->a_colidx, d->a_vals));
     NPC_TRY(check_csr("G^h", nh, nh, d->gh_rowptr, d->gh_colidx, d->gh_vals));
     NPC_TRY(check_csr("C", nh, nu, d->c_rowptr, d->c_colidx, d->c_vals));
-    NPC_TRY(check_csr("B", nh, nu, d->bm_rowptr, d->bm_colidx, d->bm_vals));
-    NPC_TRY(check_csr("G^u", nu, nu, d->gu_rowptr, d->gu_colidx, d->gu_vals));
+    NPC_TRY(check_csr("B", nh, nu + ngu, d->bm_rowptr, d->bm_colidx, d->bm_vals));
+    NPC_TRY(check_csr("G^u", nu, nu + ngu, d->gu_rowptr, d->gu_colidx, d->gu_vals));
     auto op = std::make_unique<DfnOperator>();
     op->ctx = ctx;
     op->kind = NPC_OP_DFN;
     op->n_local = nu;
-    op->n_global = nu;
+    op->n_global = multi ? NU : nu;
+    op->row_begin = U0;
+    op->multi = multi;
+    op->ngu = ngu;
     op->nblk = nblk;
     op->nh = nh;
     op->alpha = d->dfn_alpha;
@@ -549,7 +659,7 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     const double *bvals = d->bm_vals;
     if (d->dfn_scaled) {
         HostCsr CT = transpose(nh, nu, d->c_rowptr, d->c_colidx, d->c_vals);
-        HostCsr BT = transpose(nh, nu, brp, bci, bvals);
+        HostCsr BT = transpose(nh, nu + ngu, brp, bci, bvals);  // ghost columns are never visited
         std::vector<int> blk_of(std::max(nh, 1));
         for (int f = 0; f < nblk; ++f)
             for (int i = hb[f]; i < hb[f + 1]; ++i) blk_of[i] = f;
@@ -605,13 +715,31 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::uniq
             }
         for (int c = 0; c < nu; ++c) dscale[c] = 1.0 / std::sqrt(ds[c]);
     }
+    // ---- multi-rank: D_S^{-1/2} of the ghost u columns (B's E part, G^u) from their owners
+    dscale.resize(std::max(nu + ngu, 1), 1.0);
+    if (multi) {
+        op->uplan = uplan;
+        NPC_TRY(halo_setup(ctx, op->uplan, op->urt));
+        if (d->dfn_scaled) {
+            DevBuf dd;
+            NPC_TRY(dd.alloc(sizeof(double) * std::max(nu, 1)));
+            if (nu) NPC_CUDA_TRY(cudaMemcpy(dd.p, dscale.data(), sizeof(double) * nu, cudaMemcpyHostToDevice));
+            NPC_TRY(halo_start(ctx, op->uplan, op->urt, dd.as<double>()));
+            NPC_TRY(halo_wait(ctx, op->urt));
+            NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            if (ngu)
+                NPC_CUDA_TRY(cudaMemcpy(dscale.data() + nu, op->urt.ghost_buf.p, sizeof(double) * ngu,
+                                        cudaMemcpyDeviceToHost));
+        }
+    }
     // ---- internal order of the u unknowns: grouped by the fracture block that owns them (the
     // block of the first row of their column of C), stable.  A symmetric permutation (PCG and
     // p_k are unchanged; vectors are permuted once on entry/exit): the C part of a block's rows
     // then gathers a contiguous range of x, and consecutive u rows of the output pass gather t
     // and u2 from the same fracture -- the random L2 gathers bound both kernels.
-    std::vector<int> perm(std::max(nu, 1)), inv(std::max(nu, 1));
-    {
+    std::vector<int> perm(std::max(nu, 1)), inv(std::max(nu + ngu, 1));
+    for (int i = 0; i < nu + ngu; ++i) inv[i] = i;  // ghosts keep their slots
+    if (!multi) {  // multi-rank: the caller's order (halos index owned rows directly)
         std::vector<int> own(std::max(nu, 1), nblk);
         std::vector<int> blk_of(std::max(nh, 1), 0);
         for (int f = 0; f < nblk; ++f)
@@ -621,6 +749,8 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::uniq
         for (int i = 0; i < nu; ++i) perm[i] = i;
         std::stable_sort(perm.begin(), perm.begin() + nu, [&](int a, int b) { return own[a] < own[b]; });
         for (int i = 0; i < nu; ++i) inv[perm[i]] = i;
+    } else {
+        for (int i = 0; i < nu; ++i) perm[i] = i;
     }
     op->perm_dev_needed = true;
     // ---- scaled matrices, u columns / rows renumbered to the internal order
@@ -646,9 +776,78 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::uniq
         }
     }
     HostCsr CsT = transpose(nh, nu, d->c_rowptr, cci_i.data(), cs.data());
-    HostCsr BsT = transpose(nh, nu, brp, bci_i.data(), bs.data());
+    HostCsr BsT;
+    if (!multi) {
+        BsT = transpose(nh, nu, brp, bci_i.data(), bs.data());
+    } else {
+        // rows of B^T for the owned u columns: the owned B rows' entries plus the entries other
+        // ranks' fractures hold for these columns (B's E part), exchanged once at setup as
+        // (u global, h global, value bits) triples; then an h-space halo plan for t and u2
+        std::vector<std::vector<long long>> out_t(P);
+        std::vector<std::vector<std::pair<long long, double>>> rows(nu);
+        for (int h = 0; h < nh; ++h)
+            for (int q = brp[h]; q < brp[h + 1]; ++q) {
+                const long long cg = b_glob[q];
+                if (cg >= U0 && cg < U0 + nu) {
+                    rows[cg - U0].push_back({H0 + h, bs[q]});
+                } else {
+                    const int owner = (int)(std::upper_bound(u_starts.begin(), u_starts.end(), cg) - u_starts.begin()) - 1;
+                    long long bits;
+                    memcpy(&bits, &bs[q], 8);
+                    out_t[owner].insert(out_t[owner].end(), {cg, H0 + h, bits});
+                }
+            }
+        std::vector<int> scount(P), soff(P, 0), all;
+        for (int q = 0; q < P; ++q) scount[q] = (int)out_t[q].size();
+        for (int q = 1; q < P; ++q) soff[q] = soff[q - 1] + scount[q - 1];
+        NPC_TRY(ctx->tr->allgather_i32v(ctx, scount, all));
+        std::vector<int> rcount(P), roff(P, 0);
+        for (int q = 0; q < P; ++q) rcount[q] = all[(size_t)q * P + me];
+        for (int q = 1; q < P; ++q) roff[q] = roff[q - 1] + rcount[q - 1];
+        std::vector<long long> sbuf, rbuf((size_t)roff[P - 1] + rcount[P - 1]);
+        for (int q = 0; q < P; ++q) sbuf.insert(sbuf.end(), out_t[q].begin(), out_t[q].end());
+        rcount[me] = 0;  // nothing to myself
+        NPC_TRY(ctx->tr->alltoallv_i64(ctx, sbuf, scount, soff, rbuf, rcount, roff));
+        for (size_t e = 0; e + 2 < rbuf.size(); e += 3) {
+            double v;
+            memcpy(&v, &rbuf[e + 2], 8);
+            const long long cg = rbuf[e];
+            if (cg < U0 || cg >= U0 + nu) {
+                set_error("DFN: received a B^T entry for u row %lld not owned here", cg);
+                return NPC_ERR_DIMENSION;
+            }
+            rows[cg - U0].push_back({rbuf[e + 1], v});
+        }
+        std::vector<long long> hids;
+        for (auto &r : rows) {
+            std::sort(r.begin(), r.end());  // ascending global h: the same order on any partition
+            for (auto &e : r) hids.push_back(e.first);
+        }
+        NPC_TRY(halo_plan_from_ids(hids, P, h_starts.data(), me, op->hplan));
+        NPC_TRY(halo_plan_exchange(ctx, H0, op->hplan));
+        op->ngh = op->hplan.n_ghost;
+        const auto &gh = op->hplan.ghost_ids;
+        BsT.rp.assign(nu + 1, 0);
+        for (int c = 0; c < nu; ++c) {
+            BsT.rp[c + 1] = BsT.rp[c] + (int)rows[c].size();
+            for (auto &e : rows[c]) {
+                const long long hg = e.first;
+                BsT.ci.push_back(hg >= H0 && hg < H0 + nh
+                                     ? (int)(hg - H0)
+                                     : nh + (int)(std::lower_bound(gh.begin(), gh.end(), hg) - gh.begin()));
+                BsT.v.push_back(e.second);
+            }
+        }
+        if (BsT.ci.empty()) {
+            BsT.ci.push_back(0);
+            BsT.v.push_back(0.0);
+        }
+        NPC_TRY(halo_setup(ctx, op->hplan, op->trt));
+        NPC_TRY(halo_setup(ctx, op->hplan, op->u2rt));
+        NPC_TRY(op->xg.alloc(sizeof(double) * std::max(nu + ngu, 1)));
+    }
     op->nnz_c = d->c_rowptr[nh];
-    op->nnz_b = brp[nh];
+    op->nnz_b = multi ? BsT.rp[nu] : brp[nh];
     op->nnz_gh = d->gh_rowptr[nh];
     op->nnz_gu = d->gu_rowptr[nu];
     // ---- small blocks: explicit inverse A_f^-1 = L^-T L^-1 (column j = banded solve of e_j),
@@ -737,8 +936,8 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     NPC_TRY(upload(op->perm, perm.data(), (size_t)nu));
     NPC_TRY(upload(op->guv, gus.data(), gus.size()));
     NPC_TRY(upload(op->btrp, BsT.rp.data(), BsT.rp.size()));
-    NPC_TRY(upload(op->btci, BsT.ci.data(), (size_t)brp[nh]));
-    NPC_TRY(upload(op->btv, BsT.v.data(), (size_t)brp[nh]));
+    NPC_TRY(upload(op->btci, BsT.ci.data(), (size_t)BsT.rp[nu]));
+    NPC_TRY(upload(op->btv, BsT.v.data(), (size_t)BsT.rp[nu]));
     NPC_TRY(upload(op->ctrp, CsT.rp.data(), CsT.rp.size()));
     NPC_TRY(upload(op->ctci, CsT.ci.data(), (size_t)d->c_rowptr[nh]));
     NPC_TRY(upload(op->ctv, CsT.v.data(), (size_t)d->c_rowptr[nh]));
@@ -758,8 +957,8 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     }
     NPC_TRY(upload(op->dense_info, dinfo.data(), dinfo.size()));
     NPC_TRY(upload(op->band_list, blist.data(), blist.size()));
-    NPC_TRY(op->t.alloc(sizeof(double) * std::max(nh, 1)));
-    NPC_TRY(op->u2.alloc(sizeof(double) * std::max(nh, 1)));
+    NPC_TRY(op->t.alloc(sizeof(double) * std::max(nh + op->ngh, 1)));   // owned h rows + h ghosts
+    NPC_TRY(op->u2.alloc(sizeof(double) * std::max(nh + op->ngh, 1)));
     out = std::move(op);
     return NPC_SUCCESS;
 }

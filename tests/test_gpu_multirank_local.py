@@ -57,10 +57,11 @@ def run_ranks(ws, fn, timeout=240):
 
 
 CASES = [("c3", "csr", 2), ("c3", "csr", 4), ("c3", "sell", 3), ("c2", "stencil", 2), ("c2", "stencil", 4),
-         ("c4", "sell", 2), ("c4", "csr", 4), ("c5", "schur", 2), ("c5", "schur", 3)]
+         ("c4", "sell", 2), ("c4", "csr", 4), ("c5", "schur", 2), ("c5", "schur", 3), ("c6", "dfn", 2),
+         ("c6", "dfn", 3)]
 WL = {"c3": lambda: W.config3(side=24), "c2": lambda: W.config2(side=20), "c4": lambda: W.config4(n=20_000),
-      "c5": lambda: W.config5(n=20_011)}
-CFG = {"c3": 3, "c2": 2, "c4": 4, "c5": 5}
+      "c5": lambda: W.config5(n=20_011), "c6": lambda: W.dfn_owner_order(W.dfn(61, seed=7))}
+CFG = {"c3": 3, "c2": 2, "c4": 4, "c5": 5, "c6": 6}
 
 
 @pytest.fixture(scope="module")
@@ -108,8 +109,9 @@ def test_multirank_apply_poly_lanczos_pcg(wl, name, kind, ws):
     z = np.concatenate([q["z"] for q in res])
     xs = np.concatenate([q["x"] for q in res])
     assert [q["r0"] for q in res] == sorted(q["r0"] for q in res) and res[-1]["r1"] == n
-    # Schur: fp64 atomics + a reduce-scatter change the summation order (rounding only)
-    assert np.linalg.norm(y - ref_apply) <= (1e-13 if kind != "schur" else 1e-12) * np.linalg.norm(ref_apply)
+    # Schur: fp64 atomics + a reduce-scatter; DFN: explicit block inverses vs the oracle's
+    # triangular solves -- summation order only
+    assert np.linalg.norm(y - ref_apply) <= (1e-12 if kind in ("schur", "dfn") else 1e-13) * np.linalg.norm(ref_apply)
     assert np.linalg.norm(z - ref_poly) <= 1e-10 * np.linalg.norm(ref_poly)
     # every rank holds the same global scalars
     assert len({(q["lo"], q["hi"]) for q in res}) == 1

