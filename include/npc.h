@@ -94,7 +94,7 @@ typedef enum {
     NPC_OP_SCHUR = 3,    /* S = tridiag(-1, 2 + c, -1) + B^T D^{-1} B, never assembled (cfg 5)*/
     NPC_OP_CALLBACK = 4, /* user y = A x on the device; recurrence in a separate kernel      */
     NPC_OP_DFN = 5       /* the paper's DFN Schur complement S_u (Alg. 3), optionally Jacobi-
-                            scaled by D_S (Alg. 4); single rank in this version              */
+                            scaled by D_S (Alg. 4)                                           */
 } npc_op_kind;
 
 /* User operator: y_dev = A x_dev for this rank's n_local rows, enqueued on cuda_stream.
@@ -143,7 +143,14 @@ typedef struct {
      * (banded Cholesky, band = the block's bandwidth in the given ordering).  dfn_scaled = 1
      * makes the operator D_S^{-1/2} S_u D_S^{-1/2}, D_S = diag(S_u) by Alg. 4 (PAPER.md:
      * 812-841), computed at create; NPC_ERR_DIMENSION if a block of A is not SPD or an entry
-     * of D_S is not positive.  nranks must be 1.                                            */
+     * of D_S is not positive.
+     * nranks > 1 (COLLECTIVE; the paper's DSMat partition): each rank passes
+     * its consecutive whole fracture blocks -- dfn_nh / dfn_nblk / dfn_hblk local, h rows in
+     * rank order, the column ids of A and G^h GLOBAL h ids -- and the u rows [row_begin,
+     * row_begin + n_local) those fractures own: every column of C in its rows must be an owned
+     * u row (C is fracture-local), else NPC_ERR_UNSUPPORTED.  B and G^u columns are GLOBAL u
+     * ids of any rank; the library gathers the B^T entries and D_S of other ranks at create
+     * and exchanges halos of x (u space) and of A^-1-products (h space) per application.     */
     long long dfn_nh;
     int dfn_nblk;
     const int *dfn_hblk;
