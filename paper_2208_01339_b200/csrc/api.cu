@@ -51,7 +51,7 @@ extern "C" {
 
 const char *npc_last_error(void) { return g_err; }
 unsigned long long npc_launch_count(void) { return g_launches.load(); }
-const char *npc_version(void) { return "npc 0.1 sm_100a (fp64, CSR/SELL/stencil/Schur/callback)"; }
+const char *npc_version(void) { return "npc 0.2 sm_100a (fp64, CSR/SELL/stencil/Schur/DFN/callback)"; }
 
 npc_status npc_get_unique_id(void *out128) {
     NPC_GUARD(out128, NPC_ERR_INVALID_ARGUMENT, "npc_get_unique_id: null output");

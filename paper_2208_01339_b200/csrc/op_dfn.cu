@@ -358,7 +358,6 @@ class DfnOperator : public Operator {
     DevBuf gurp, guci, guv, btrp, btci, btv, ctrp, ctci, ctv;
     DevBuf t, u2;
     DevBuf ainv, dense_info, band_list, perm;
-    bool perm_dev_needed = false;
     // multi-rank (the paper's DSMat partition): whole fracture blocks per
     // rank, u rows by owning fracture; per application a u-space halo of x (columns of B's E
     // part and of G^u) and an h-space halo of t and u2 (rows of B^T from other ranks' fractures)
@@ -752,7 +751,6 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d0, std::uni
     } else {
         for (int i = 0; i < nu; ++i) perm[i] = i;
     }
-    op->perm_dev_needed = true;
     // ---- scaled matrices, u columns / rows renumbered to the internal order
     std::vector<double> cs(d->c_vals, d->c_vals + d->c_rowptr[nh]), bs(bvals, bvals + brp[nh]);
     std::vector<int> cci_i(d->c_colidx, d->c_colidx + d->c_rowptr[nh]), bci_i(bci, bci + brp[nh]);
