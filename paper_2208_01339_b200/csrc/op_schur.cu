@@ -8,18 +8,20 @@
 //           rows of Bt are reordered by length (4, 3, 2, 1 entries; the order of B's rows is
 //           free since t = Bt v is internal) and stored SELL-32 column-major (no padding but
 //           the tail chunk of each length class).
-// Default (atomic) form, two kernels per application:
+// Atomic form (NPC_SCHUR_ATOMIC=1; always across ranks), two kernels per application:
 //   k_schur_bpass_atomic:    t_q = (Bt v)_q in registers; y[col] += Bt_qj t_q (fp64 RED into
 //                            y, L2-resident: the random traffic -- v gather, y scatter --
 //                            stays in a 2 x 8n-byte L2 working set)
 //   k_schur_tstep:           (S v)_i = (2 + c_i) v_i - v_{i-1} - v_{i+1} + y_i ; y_i = 0 ;
 //                            out = a (S v) + b v + c s2 + d r   (+ dot partial)
-// Deterministic form (NPC_SCHUR_DETERMINISTIC=1 at create): Bt^T is also stored, as CSR over
-// the trace rows (column ids = positions of t, ascending), and
+// Deterministic form (default on one rank): Bt^T is also stored, as CSR over the trace rows
+// (column ids = positions of t, ascending), split into K position ranges, and
 //   pass 1 (k_schur_bpass):  t = Bt v written out (12 B x rows of B);
-//   pass 2 (k_schur_tpass):  (Bt^T t)_i gathered per trace row, tile-staged by bulk TMA, fused
-//                            with C and the epilogue.  Same bits every run, but t (8 x rows of
-//                            B bytes) is gathered at random and spills L2 at config 5 size.
+//   pass 2 (k_schur_tpass):  (Bt^T t)_i gathered per trace row, tile-staged by bulk TMA, one
+//                            launch per t range carrying the row sums, the last fused with C
+//                            and the epilogue.  Same bits every run; each launch gathers from a
+//                            t range small enough to stay L2-resident (unsplit, the 96 MB t
+//                            spills beside the 432 MB Bt^T stream and the pass is 2x slower).
 #include <algorithm>
 #include <numeric>
 
@@ -150,8 +152,12 @@ struct SchurTDev {
     int n;
 };
 
-template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT>
-__global__ void __launch_bounds__(ST_TILE) k_schur_tpass(SchurTDev T, StepArgs s, int vspan_max) {
+// PARTIAL: the t-position range of this pass is one of several (see SchurOperator::parts):
+// yout = yin + the partial row sums, no epilogue.  The last pass adds yin and finishes.  The
+// per-row summation sequence is the same as one unsplit pass (bitwise).
+template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool PARTIAL>
+__global__ void __launch_bounds__(ST_TILE) k_schur_tpass(SchurTDev T, StepArgs s, int vspan_max,
+                                                         const double *__restrict__ yin, double *__restrict__ yout) {
     if (s.done && *s.done) return;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t bar;
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(ST_TILE) k_schur_tpass(SchurTDev T, StepArgs s
     if (STAGED) mbar_wait(&bar, 0);
     double acc = 0.0;
     if (active) {
-        double y = 0.0;
+        double y = yin ? yin[i] : 0.0;
         for (int p = rb; p < re; ++p) {
             int c;
             double v;
@@ -210,6 +216,10 @@ __global__ void __launch_bounds__(ST_TILE) k_schur_tpass(SchurTDev T, StepArgs s
                 v = __ldcs(T.vals + p);
             }
             y += v * __ldg(T.t + c);
+        }
+        if (PARTIAL) {
+            yout[i] = y;
+            return;  // no block reduction in partial passes
         }
         const double svv = ((2.0 + cv) * xi - xl - xr) + y;
         double o = s.a * svv + s.b * xi;
@@ -228,12 +238,23 @@ class SchurOperator : public Operator {
   public:
     DevBuf cshift, chunk_off, chunk_len, bcols, bvals, t;
     DevBuf trowptr, tcols, tvals;
+    // Deterministic form, t split into K position ranges (NPC_SCHUR_SPLIT, default 3) so the
+    // t range each pass gathers (96 MB / K) stays L2-resident beside its entry stream; pass k
+    // carries the row sums of passes < k in yacc.
+    struct Part {
+        DevBuf rowptr, cols, vals;
+        int vspan = 0, cspan = 0;
+        size_t smem = 0;
+        bool staged = true;
+    };
+    std::vector<std::unique_ptr<Part>> parts;
+    DevBuf yacc;
     int nbp = 0, nchunks = 0, ntiles = 0;
     long long nnz = 0, nslots = 0;
     int vspan_max = 0, cspan_max = 0;
     size_t smem_bytes = 0;
     bool staged = true;
-    bool deterministic = false;  // two-pass form (NPC_SCHUR_DETERMINISTIC=1 at create time)
+    bool deterministic = false;  // split two-pass form (default on one rank; NPC_SCHUR_ATOMIC=1 off)
     int grid2 = 1;               // atomic form: grid of k_schur_tstep
     // multi-rank (nranks > 1, atomic form): P slots of m entries; B column ids are remapped to
     // slot positions.  Per application: own x -> my slot of xfull, allgather the slots, B pass
@@ -254,26 +275,40 @@ class SchurOperator : public Operator {
         }
         // pass 1: Bt slots (12 B) + t written; pass 2: Bt^T (12 B/nnz + rowptr) + t read once +
         // c + x + out (+ s_{j-2}, r).  v is gathered from L2 in pass 1 (read once in pass 2).
-        double b = (double)nslots * 12.0 + 8.0 * nbp + (double)nnz * 12.0 + 4.0 * (n_local + 1) + 8.0 * nbp +
-                   3.0 * 8.0 * n_local;
+        const double K = (double)std::max<size_t>(parts.size(), 1);
+        double b = (double)nslots * 12.0 + 8.0 * nbp + (double)nnz * 12.0 + 4.0 * K * (n_local + 1) + 8.0 * nbp +
+                   3.0 * 8.0 * n_local + (K - 1.0) * 2.0 * 8.0 * n_local;
         if (has_s2) b += 8.0 * n_local;
         if (has_r) b += 8.0 * n_local;
         return b;
     }
-    template <bool ST, bool H2, bool HR, bool DT>
-    npc_status launch2(const StepArgs &s) {
-        SchurTDev T{trowptr.as<int>(), tcols.as<int>(), tvals.as<double>(), cshift.as<double>(), t.as<double>(),
-                    n_local};
-        auto kern = k_schur_tpass<ST, H2, HR, DT>;
-        const size_t sm = ST ? smem_bytes : 0;
+    template <bool ST, bool H2, bool HR, bool DT, bool PA>
+    npc_status launch_part(const StepArgs &s, const Part &pt, const double *yin, double *yout) {
+        SchurTDev T{pt.rowptr.as<int>(), pt.cols.as<int>(), pt.vals.as<double>(), cshift.as<double>(),
+                    t.as<double>(), n_local};
+        auto kern = k_schur_tpass<ST, H2, HR, DT, PA>;
+        const size_t sm = ST ? pt.smem : 0;
         if (sm > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
-        kern<<<ntiles, ST_TILE, sm, ctx->stream>>>(T, s, vspan_max);
+        kern<<<ntiles, ST_TILE, sm, ctx->stream>>>(T, s, pt.vspan, yin, yout);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
     template <bool H2, bool HR, bool DT>
     npc_status launch2s(const StepArgs &s) {
-        return staged ? launch2<true, H2, HR, DT>(s) : launch2<false, H2, HR, DT>(s);
+        const int K = (int)parts.size();
+        double *ya = yacc.as<double>();
+        for (int k = 0; k + 1 < K; ++k) {
+            const Part &pt = *parts[k];
+            const double *yin = k ? ya : nullptr;
+            if (pt.staged)
+                NPC_TRY((launch_part<true, false, false, false, true>(s, pt, yin, ya)));
+            else
+                NPC_TRY((launch_part<false, false, false, false, true>(s, pt, yin, ya)));
+        }
+        const Part &pl = *parts[K - 1];
+        const double *yin = K > 1 ? ya : nullptr;
+        return pl.staged ? launch_part<true, H2, HR, DT, false>(s, pl, yin, nullptr)
+                         : launch_part<false, H2, HR, DT, false>(s, pl, yin, nullptr);
     }
     template <bool H2, bool HR, bool DT>
     npc_status launch_t(const StepArgs &s) {
@@ -344,10 +379,7 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
         set_error("SCHUR: invalid arrays");
         return NPC_ERR_INVALID_ARGUMENT;
     }
-    if (multi && getenv("NPC_SCHUR_DETERMINISTIC")) {
-        set_error("SCHUR: the deterministic two-pass form is single-rank only");
-        return NPC_ERR_UNSUPPORTED;
-    }
+
     // trace-row partition: every rank's (row_begin, n_local) -> slot layout
     std::vector<long long> starts{0}, all_n;
     long long n_global = n;
@@ -453,7 +485,10 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
                 if (!multi) tcount[d->b_colidx[p] + 1]++;
             }
         }
-    op->deterministic = getenv("NPC_SCHUR_DETERMINISTIC") != nullptr;
+    // Single rank: the deterministic split two-pass form (faster, and bitwise reproducible;
+    // profiles/r01_schur_scatter_microbench.md).  NPC_SCHUR_ATOMIC=1 selects the fp64-RED form,
+    // which is also the form used across ranks (its partial B^T t is reduce-scattered).
+    op->deterministic = !multi && getenv("NPC_SCHUR_ATOMIC") == nullptr;
     op->grid2 = std::max(1, ceil_div(n, ST_TILE));
     if (!op->deterministic) {
         NPC_TRY(op->cshift.alloc(sizeof(double) * std::max(n, 1)));
@@ -515,15 +550,45 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
         }
     }
     op->ntiles = std::max(1, ceil_div(n, ST_TILE));
-    for (int tt = 0; tt * ST_TILE < n; ++tt) {
-        const int r0 = tt * ST_TILE, r1 = std::min(n, r0 + ST_TILE);
-        const int pb = trp[r0], pe = trp[r1];
-        op->vspan_max = std::max(op->vspan_max, ((pe + 1) & ~1) - (pb & ~1));
-        op->cspan_max = std::max(op->cspan_max, ((pe + 3) & ~3) - (pb & ~3));
+    // split the t positions into K ranges; part k keeps each row's entries with positions in
+    // range k (rows' entries are in ascending position order, so parts are row sub-ranges)
+    int K = 2;  // measured best at config 5 (96 MB of t): 1 -> 718, 2 -> 349, 3 -> 392, 4 -> 384 us/degree
+    if (const char *e = getenv("NPC_SCHUR_SPLIT")) K = std::max(1, std::min(16, atoi(e)));
+    const long long P = std::max(1LL, ((long long)op->nbp + K - 1) / K);
+    for (int k = 0; k < K; ++k) op->parts.push_back(std::make_unique<SchurOperator::Part>());
+    for (int k = 0; k < K; ++k) {
+        SchurOperator::Part &pt = *op->parts[k];
+        std::vector<int> rp(n + 1, 0), pc;
+        std::vector<double> pv;
+        for (int i = 0; i < n; ++i) {
+            for (int q = trp[i]; q < trp[i + 1]; ++q)
+                if (tc[q] / P == k) {
+                    pc.push_back(tc[q]);
+                    pv.push_back(tv[q]);
+                }
+            rp[i + 1] = (int)pc.size();
+        }
+        for (int pad = 0; pad < 8; ++pad) {  // aligned bulk copies may read past the last entry
+            pc.push_back(0);
+            pv.push_back(0.0);
+        }
+        for (int tt = 0; tt * ST_TILE < n; ++tt) {
+            const int r0 = tt * ST_TILE, r1 = std::min(n, r0 + ST_TILE);
+            const int pb = rp[r0], pe = rp[r1];
+            pt.vspan = std::max(pt.vspan, ((pe + 1) & ~1) - (pb & ~1));
+            pt.cspan = std::max(pt.cspan, ((pe + 3) & ~3) - (pb & ~3));
+        }
+        pt.vspan = (pt.vspan + 1) & ~1;
+        pt.smem = (size_t)pt.vspan * 8 + (size_t)pt.cspan * 4 + 16;
+        pt.staged = pt.smem <= (size_t)ST_MAX_SMEM;
+        NPC_TRY(pt.rowptr.alloc(sizeof(int) * (n + 1)));
+        NPC_TRY(pt.cols.alloc(sizeof(int) * pc.size()));
+        NPC_TRY(pt.vals.alloc(sizeof(double) * pv.size()));
+        NPC_CUDA_TRY(cudaMemcpy(pt.rowptr.p, rp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(pt.cols.p, pc.data(), sizeof(int) * pc.size(), cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(pt.vals.p, pv.data(), sizeof(double) * pv.size(), cudaMemcpyHostToDevice));
     }
-    op->vspan_max = (op->vspan_max + 1) & ~1;
-    op->smem_bytes = (size_t)op->vspan_max * 8 + (size_t)op->cspan_max * 4 + 16;
-    op->staged = op->smem_bytes <= (size_t)ST_MAX_SMEM;
+    NPC_TRY(op->yacc.alloc(sizeof(double) * std::max(n, 1)));
     // ---- upload
     NPC_TRY(op->cshift.alloc(sizeof(double) * std::max(n, 1)));
     NPC_TRY(op->t.alloc(sizeof(double) * std::max(op->nbp, 1)));
@@ -531,9 +596,7 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
     NPC_TRY(op->chunk_len.alloc(sizeof(int) * std::max(op->nchunks, 1)));
     NPC_TRY(op->bcols.alloc(sizeof(int) * std::max<long long>(op->nslots, 1)));
     NPC_TRY(op->bvals.alloc(sizeof(double) * std::max<long long>(op->nslots, 1)));
-    NPC_TRY(op->trowptr.alloc(sizeof(int) * (n + 1)));
-    NPC_TRY(op->tcols.alloc(sizeof(int) * tc.size()));
-    NPC_TRY(op->tvals.alloc(sizeof(double) * tv.size()));
+
     if (n) NPC_CUDA_TRY(cudaMemcpy(op->cshift.p, d->c, sizeof(double) * n, cudaMemcpyHostToDevice));
     NPC_CUDA_TRY(cudaMemset(op->t.p, 0, op->t.bytes));
     NPC_CUDA_TRY(cudaMemcpy(op->chunk_off.p, coff.data(), sizeof(int) * coff.size(), cudaMemcpyHostToDevice));
@@ -542,9 +605,7 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
         NPC_CUDA_TRY(cudaMemcpy(op->bcols.p, scols.data(), sizeof(int) * scols.size(), cudaMemcpyHostToDevice));
         NPC_CUDA_TRY(cudaMemcpy(op->bvals.p, svals.data(), sizeof(double) * svals.size(), cudaMemcpyHostToDevice));
     }
-    NPC_CUDA_TRY(cudaMemcpy(op->trowptr.p, trp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-    NPC_CUDA_TRY(cudaMemcpy(op->tcols.p, tc.data(), sizeof(int) * tc.size(), cudaMemcpyHostToDevice));
-    NPC_CUDA_TRY(cudaMemcpy(op->tvals.p, tv.data(), sizeof(double) * tv.size(), cudaMemcpyHostToDevice));
+
     out = std::move(op);
     return NPC_SUCCESS;
 }

@@ -194,27 +194,47 @@ def test_tab_epsil_newton_on_gpu(ctx):
 
 
 def test_schur_deterministic_mode(ctx, wl, monkeypatch):
-    """NPC_SCHUR_DETERMINISTIC=1 selects the two-pass (no atomics) Schur form: same parity,
-    and bit-identical results run to run."""
+    """The default single-rank Schur form is the split two-pass (no atomics) form: parity, and
+    bit-identical results run to run and for any number of t ranges (the per-row summation
+    sequence does not depend on the split)."""
     w = wl("c5")
-    monkeypatch.setenv("NPC_SCHUR_DETERMINISTIC", "1")
-    op = npc.create_from_workload(ctx, w, "schur")
-    monkeypatch.delenv("NPC_SCHUR_DETERMINISTIC")
     orc = oracle.Operator(w)
     lmin, lmax = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
     r = np.random.default_rng(4).uniform(-1, 1, w["n"])
     outs = []
-    for _ in range(2):
+    for split in ("1", "2", "3", "2"):
+        monkeypatch.setenv("NPC_SCHUR_SPLIT", split)
+        op = npc.create_from_workload(ctx, w, "schur")
+        monkeypatch.delenv("NPC_SCHUR_SPLIT")
         poly = npc.npc_set_poly(op, 30, lmin, lmax, 0.0)
         z = torch.empty(w["n"], dtype=torch.float64, device="cuda")
         npc.npc_apply_poly(poly, dev(r), z)
         outs.append(host(z))
-    assert np.array_equal(outs[0], outs[1])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
     assert rel(outs[0], oracle.cheb_apply(orc, 30, lmin, lmax, 0.0, r)) <= POLY_TOL
     x = torch.zeros(w["n"], dtype=torch.float64, device="cuda")
     st = npc.npc_pcg_solve(npc.npc_set_poly(op, 10, lmin, lmax, 0.0), op, dev(w["b"]), x, 1e-8, 100)
     _, st_o = oracle.pcg(orc, w["b"], 10, lmin, lmax, 0.0, tol=1e-8)
     assert abs(st["iters"] - st_o["iters"]) <= 2
+
+
+def test_schur_atomic_mode(ctx, wl, monkeypatch):
+    """NPC_SCHUR_ATOMIC=1 selects the fp64-RED form (the one used across ranks): parity."""
+    w = wl("c5")
+    monkeypatch.setenv("NPC_SCHUR_ATOMIC", "1")
+    op = npc.create_from_workload(ctx, w, "schur")
+    monkeypatch.delenv("NPC_SCHUR_ATOMIC")
+    orc = oracle.Operator(w)
+    lmin, lmax = oracle.estimate_spectrum(orc, 20, W.lanczos_start(w["n"]))
+    r = np.random.default_rng(5).uniform(-1, 1, w["n"])
+    z = torch.empty(w["n"], dtype=torch.float64, device="cuda")
+    npc.npc_apply_poly(npc.npc_set_poly(op, 40, lmin, lmax, 1e-3), dev(r), z)
+    assert rel(host(z), oracle.cheb_apply(orc, 40, lmin, lmax, 1e-3, r)) <= POLY_TOL
+    x = torch.zeros(w["n"], dtype=torch.float64, device="cuda")
+    st = npc.npc_pcg_solve(npc.npc_set_poly(op, 10, lmin, lmax, 0.0), op, dev(w["b"]), x, 1e-8, 100)
+    _, st_o = oracle.pcg(orc, w["b"], 10, lmin, lmax, 0.0, tol=1e-8)
+    assert st["converged"] and abs(st["iters"] - st_o["iters"]) <= 2
 
 
 def test_unpreconditioned_cg(ctx, wl):

@@ -84,7 +84,7 @@ def main():
         rows += run(c, a.reps, ctx, kinds)
     if a.md:
         with open(a.md, "w") as f:
-            f.write("| config | operator | n | k | p_k(A)v ms | GB/s (alg.) | frac of 6533 | applications/s | "
+            f.write("| config | operator | n | k | p_k(A)v ms | GB/s (alg.) | frac of measured HBM | applications/s | "
                     "PCG iters | time-to-tol s | solve GB/s | true relres |\n|---|---|---|---|---|---|---|---|---|---|---|---|\n")
             for r in rows:
                 f.write(f"| {r['name']} | {r['operator']} | {r['n']} | {r['k']} | {r['apply_ms']} | {r['apply_gbs']} | "
