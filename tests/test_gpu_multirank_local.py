@@ -123,3 +123,53 @@ def test_multirank_apply_poly_lanczos_pcg(wl, name, kind, ws):
     # multi-rank convergence is seen one iteration late: one extra (k+1) block is counted
     st = res[0]["st"]
     assert st["op_applications"] == (st["iters"] + 1) * (k + 1) + 1
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("kind", ["csr", "sell", "schur"])
+def test_multirank_with_an_empty_rank(kind):
+    """Edge case: a rank that owns no rows still takes part in every collective (halo plans,
+    allreduces, the Schur allgather / reduce-scatter) and the result matches the oracle."""
+    w = W.config5(n=9_000) if kind == "schur" else W.config3(side=14)
+    orc = oracle.Operator(w)
+    n = w["n"]
+    cuts = [0, n // 2, n // 2, n]  # rank 1 owns nothing
+    lo_o, hi_o = oracle.estimate_spectrum(orc, 20, W.lanczos_start(n))
+    r = np.random.default_rng(12).uniform(-1, 1, n)
+    ref = oracle.cheb_apply(orc, 8, lo_o, hi_o, 0.0, r)
+    _, st_o = oracle.pcg(orc, w["b"], 8, lo_o, hi_o, 0.0, tol=w["tol"], maxit=5000)
+
+    def fn(rank, ctx, stream):
+        r0, r1 = cuts[rank], cuts[rank + 1]
+        if kind == "schur":
+            nb = w["nb"]
+            q0, q1 = nb * rank // 3, nb * (rank + 1) // 3
+            bp = w["browptr"][q0:q1 + 1]
+            op = npc.npc_create_operator(ctx, "schur", n_local=r1 - r0, n_global=n, row_begin=r0, c=w["c"][r0:r1],
+                                         b_rows_global=nb, b_row_begin=q0, b_n_local=q1 - q0,
+                                         b_rowptr=(bp - bp[0]).astype(np.int32),
+                                         b_colidx=w["bcolidx"][bp[0]:bp[-1]], b_vals=w["bvals"][bp[0]:bp[-1]],
+                                         d=w["d"][q0:q1])
+        else:
+            rp = w["rowptr"][r0:r1 + 1]
+            op = npc.npc_create_operator(ctx, kind, n_local=r1 - r0, n_global=n, row_begin=r0,
+                                         rowptr=(rp - rp[0]).astype(np.int32), colidx=w["colidx"][rp[0]:rp[-1]],
+                                         vals=w["vals"][rp[0]:rp[-1]], sell_C=32, sell_sigma=256)
+        dev = lambda a: torch.tensor(np.ascontiguousarray(a[r0:r1]), device="cuda")  # noqa: E731
+        poly = npc.npc_set_poly(op, 8, lo_o, hi_o, 0.0)
+        z = torch.empty(r1 - r0, dtype=torch.float64, device="cuda")
+        npc.npc_apply_poly(poly, dev(r), z)
+        lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+        p2 = npc.npc_set_poly(op, 8, lo, hi, 0.0)
+        xs = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+        st = npc.npc_pcg_solve(p2, op, dev(w["b"]), xs, w["tol"], 5000)
+        stream.synchronize()
+        return dict(z=z.cpu().numpy(), x=xs.cpu().numpy(), st=st)
+
+    res = run_ranks(3, fn)
+    z = np.concatenate([q["z"] for q in res])
+    assert np.linalg.norm(z - ref) <= 1e-10 * np.linalg.norm(ref)
+    its = {q["st"]["iters"] for q in res}
+    assert len(its) == 1 and abs(its.pop() - st_o["iters"]) <= 2
+    xs = np.concatenate([q["x"] for q in res])
+    assert np.linalg.norm(w["b"] - orc.apply(xs)) / np.linalg.norm(w["b"]) <= w["tol"]
