@@ -427,8 +427,11 @@ def run_ours(args):
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / peak, 4),
                          "frac_vs_8TBs_nominal": round(ach / 8000.0, 4), "traffic": traffic,
                          "bytes_per_launch": apply_bytes / max(k, 1), "launch_ms": round(per_launch_ms, 5),
-                         "timed": "library CUDA events around every fused degree launch inside the timed region"
-                         if in_step else f"{R} x npc_apply_poly (k={k} launches each), CUDA events on the library stream",
+                         "timed": "library CUDA events on the launching stream inside the timed region: one event "
+                         "pair around each p_k(A) r application (its k fused degree launches, replayed in the PCG "
+                         "CUDA graph as event-record nodes); achieved = algorithmic bytes of the degree steps / their "
+                         "summed device time" if in_step
+                         else f"{R} x npc_apply_poly (k={k} launches each), CUDA events on the library stream",
                          "isolated_achieved": round(ach_isolated, 1),
                          "isolated": f"{R} x npc_apply_poly back to back after the timed region",
                          "step_breakdown": in_step},

@@ -215,26 +215,39 @@ struct Context {
     struct Pending {
         int cls;
         cudaEvent_t e0, e1;
+        int count;  // launches (degree applications) the interval covers
     };
     bool timing = false;
+    int timing_suppress = 0;         // > 0: inside a scope that times a whole group of launches
+    bool capturing = false;          // a PCG iteration is being stream-captured (timing on)
     std::vector<cudaEvent_t> ev_free;
     std::vector<Pending> pending;
+    std::vector<Pending> captured;   // events recorded as graph nodes during the capture
     double t_ms[NPC_TIMING_CLASSES] = {0};
     long long t_cnt[NPC_TIMING_CLASSES] = {0};
-    int t_begin(int cls);
+    int t_begin(int cls, int count = 1);
     void t_end(int idx);
     void t_flush();  // caller has synchronised the stream
+    void t_flush_graph(const std::vector<Pending> &ev);  // a timed graph replay has completed
     ~Context();
 };
 
 // RAII bracket of a launch (or a multi-kernel step) for the timing classes above.
+// A scope nested inside a group scope (timing_suppress > 0) records nothing; a group scope
+// (count > 1) brackets several launches with one event pair and credits them all.
 struct TimedScope {
     Context *c;
     int idx;
-    TimedScope(Context *ctx, int cls) : c(ctx), idx(ctx->timing ? ctx->t_begin(cls) : -1) {}
+    TimedScope(Context *ctx, int cls, int count = 1)
+        : c(ctx), idx(ctx->timing && ctx->timing_suppress == 0 ? ctx->t_begin(cls, count) : -1) {}
     ~TimedScope() {
         if (idx >= 0) c->t_end(idx);
     }
+};
+struct TimingGroup {  // suppresses the per-launch scopes inside a group scope
+    Context *c;
+    explicit TimingGroup(Context *ctx) : c(ctx) { ++c->timing_suppress; }
+    ~TimingGroup() { --c->timing_suppress; }
 };
 enum { T_DEGREE = 0, T_OPERATOR = 1, T_UPDATE = 2, T_REDUCE = 3, T_VECTOR = 4 };
 
@@ -342,9 +355,20 @@ struct PcgCache {
     unsigned long long kernels = 0;  // kernels per graph launch
     const void *key_partials = nullptr;
     size_t key_cap = 0;
+    bool timed = false;                         // captured with timing event nodes
+    std::vector<Context::Pending> timing_events;  // owned by the graph (re-recorded per replay)
+    void release_events() {
+        for (auto &p : timing_events) {
+            if (p.e0) cudaEventDestroy(p.e0);
+            if (p.e1) cudaEventDestroy(p.e1);
+        }
+        timing_events.clear();
+    }
     void invalidate() {
         if (exec) cudaGraphExecDestroy(exec);
         exec = nullptr;
+        release_events();
+        timed = false;
     }
     ~PcgCache() { invalidate(); }
 };

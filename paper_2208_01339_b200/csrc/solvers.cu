@@ -30,29 +30,54 @@ npc_status Context::allreduce_sum(double *dev, int count) {
     return tr->allreduce_sum(this, dev, count, stream);
 }
 
-int Context::t_begin(int cls) {
+// While a PCG iteration is being stream-captured (timing on), the events become event-record
+// nodes of the graph (cudaEventRecordExternal) and are collected in `captured`: the graph owns
+// them and every replay re-records them, so the solver reads them after each replay.
+static void record_timing_event(Context *c, cudaEvent_t e) {
+    if (c->capturing)
+        cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
+    else
+        cudaEventRecord(e, c->stream);
+}
+
+int Context::t_begin(int cls, int count) {
     cudaEvent_t e0;
-    if (ev_free.empty()) {
+    if (capturing || ev_free.empty()) {
         if (cudaEventCreate(&e0) != cudaSuccess) return -1;
     } else {
         e0 = ev_free.back();
         ev_free.pop_back();
     }
-    cudaEventRecord(e0, stream);
-    pending.push_back({cls, e0, nullptr});
-    return (int)pending.size() - 1;
+    record_timing_event(this, e0);
+    auto &list = capturing ? captured : pending;
+    list.push_back({cls, e0, nullptr, count});
+    return (capturing ? (1 << 30) : 0) + (int)list.size() - 1;
 }
 
 void Context::t_end(int idx) {
     cudaEvent_t e1;
-    if (ev_free.empty()) {
+    if (capturing || ev_free.empty()) {
         if (cudaEventCreate(&e1) != cudaSuccess) return;
     } else {
         e1 = ev_free.back();
         ev_free.pop_back();
     }
-    cudaEventRecord(e1, stream);
-    pending[idx].e1 = e1;
+    record_timing_event(this, e1);
+    if (idx >= (1 << 30))
+        captured[idx - (1 << 30)].e1 = e1;
+    else
+        pending[idx].e1 = e1;
+}
+
+// Accumulate the intervals of a replayed graph's timing events (the replay has completed).
+void Context::t_flush_graph(const std::vector<Pending> &ev) {
+    for (const auto &p : ev) {
+        float ms = 0.f;
+        if (p.e1 && cudaEventElapsedTime(&ms, p.e0, p.e1) == cudaSuccess) {
+            t_ms[p.cls] += ms;
+            t_cnt[p.cls] += p.count;
+        }
+    }
 }
 
 void Context::t_flush() {
@@ -62,7 +87,7 @@ void Context::t_flush() {
             cudaEventSynchronize(p.e1);
             if (cudaEventElapsedTime(&ms, p.e0, p.e1) == cudaSuccess) {
                 t_ms[p.cls] += ms;
-                t_cnt[p.cls] += 1;
+                t_cnt[p.cls] += p.count;
             }
             ev_free.push_back(p.e1);
         }
@@ -216,6 +241,11 @@ static npc_status apply_poly_core(npc_poly P, const double *r, double *z, const 
 // partials of <z, dotv> come from the last kernel that writes z.
 npc_status apply_poly_internal(npc_poly P, const double *r, double *z, const double *dotv, double *partials,
                                int *nparts, const int *done) {
+    // timing: ONE event pair around the k degree launches (credited as k launches) -- per-launch
+    // events inside a graph replay perturb short kernels by several microseconds each
+    Context *ctx = P->op->op->ctx;
+    TimedScope ts(ctx, T_DEGREE, std::max(P->degree, 1));
+    TimingGroup grp(ctx);
     if (P->lr_p == 0) return apply_poly_core(P, r, z, dotv, partials, nparts, done);
     NPC_TRY(lowrank_pre(P, r, done));
     NPC_TRY(apply_poly_core(P, r, z, nullptr, nullptr, nullptr, done));
@@ -522,8 +552,14 @@ struct GraphRun {
         }
         const unsigned long long l0 = g_launches.load();
         NPC_CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        c->capturing = c->timing;
+        c->captured.clear();
         npc_status st = NPC_SUCCESS;
         for (int i = 0; i < ITERS && st == NPC_SUCCESS; ++i) st = body();
+        c->capturing = false;
+        cache.release_events();
+        cache.timing_events.swap(c->captured);
+        cache.timed = c->timing;
         cudaGraph_t g = nullptr;
         cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
         kernels = g_launches.load() - l0;
@@ -828,12 +864,26 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     // CUDA Graph of GRAPH_ITERS iterations (all pointers and coefficients are fixed for the
     // solve), replayed on a library stream: one launch per 4 iterations instead of 4(k+5)
     // launches; NCCL calls and the halo fork/join are captured too.  Off while timing.
+    // With timing on, the captured graph carries event-record nodes around every launch and is
+    // replayed one graph per host sync so that its events can be read after each replay.
+    if (cache.exec && cache.timed != ctx->timing) cache.invalidate();
     GraphRun gr(ctx, cache);
-    if (!ctx->timing && op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH"))
+    if (op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH"))
         NPC_TRY(gr.capture(iteration));
     for (;;) {
         if (gr.exec) {
-            for (int it = 0; it < chunk; it += GraphRun::ITERS) NPC_TRY(gr.launch());
+            if (ctx->timing) {  // read the events after every replay; stop replaying once done
+                for (int it = 0; it < chunk; it += GraphRun::ITERS) {
+                    NPC_TRY(gr.launch());
+                    int dflag_h = 0;
+                    NPC_CUDA_TRY(cudaMemcpyAsync(&dflag_h, dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+                    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+                    ctx->t_flush_graph(cache.timing_events);
+                    if (dflag_h) break;
+                }
+            } else {
+                for (int it = 0; it < chunk; it += GraphRun::ITERS) NPC_TRY(gr.launch());
+            }
         } else {
             for (int it = 0; it < chunk; ++it) NPC_TRY(iteration());
         }

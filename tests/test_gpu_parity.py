@@ -404,3 +404,30 @@ def test_closed_form_eigenvector_stencil(ctx):
     z = torch.empty(w["n"], dtype=torch.float64, device="cuda")
     npc.npc_apply_poly(poly, dev(v), z)
     assert rel(host(z), p * v) < 1e-10
+
+
+def test_in_library_timing_with_graphs(ctx, wl):
+    """npc_context_set_timing: the PCG iteration graph carries event-record nodes, is replayed
+    one graph per sync, and the per-class device times are collected; the solve is the same
+    (iterations, solution) as without timing."""
+    w = W.config3(side=32)  # 32,768 rows: above the cluster-resident size, so graphs are used
+    op = npc.create_from_workload(ctx, w, "csr")
+    lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+    k = 12
+    res = {}
+    for timing in (False, True):
+        poly = npc.npc_set_poly(op, k, lo, hi, 0.0)
+        npc.npc_context_set_timing(ctx, timing)
+        npc.npc_context_get_timing(ctx)  # reset
+        x = torch.zeros(w["n"], dtype=torch.float64, device="cuda")
+        st = npc.npc_pcg_solve(poly, op, dev(w["b"]), x, 1e-8, 2000)
+        tm = npc.npc_context_get_timing(ctx)
+        npc.npc_context_set_timing(ctx, False)
+        res[timing] = (st, host(x), tm)
+    (s0, x0, _), (s1, x1, tm) = res[False], res[True]
+    assert s0["iters"] == s1["iters"] and np.array_equal(x0, x1)
+    ms, n = tm["degree"]
+    # every degree launch of every replayed iteration is timed (the last graph replay may run
+    # up to 3 no-op iterations after convergence)
+    assert s1["iters"] * k <= n <= (s1["iters"] + 3) * k and ms > 0.0
+    assert tm["operator"][1] >= s1["iters"] and tm["update"][1] >= s1["iters"]
