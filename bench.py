@@ -447,6 +447,31 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def host_info():
+    """CPU model and a STREAM-triad bandwidth (numpy a = b + s c on 3 x 256 MB, one thread) of
+    the host the oracle runs on (record nproc, the CPU model, a triad GB/s)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    n = 32 * 1024 * 1024
+    b, c = np.ones(n), np.full(n, 2.0)
+    a = np.empty(n)
+    best = 0.0
+    for _ in range(3):
+        t0 = time.perf_counter()
+        np.multiply(c, 3.0, out=a)
+        np.add(a, b, out=a)
+        dt = time.perf_counter() - t0
+        best = max(best, 4 * 8 * n / dt / 1e9)  # two passes: read c, write a, read a+b, write a
+    return {"cpu_model": model, "nproc": os.cpu_count(), "stream_triad_gbs_1thread": round(best, 1)}
+
+
 def cpu_baseline(w, k, lo, hi, xi, M, V, max_seconds=30.0):
     """The oracle as it stands, one p_k(A) v application of the same workload on the host cores."""
     try:
@@ -462,7 +487,7 @@ def cpu_baseline(w, k, lo, hi, xi, M, V, max_seconds=30.0):
     byts = poly_bytes(M, V, kk)
     return {"value": round(byts / dt / 1e9, 3), "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"one p_k(A) v application (k={kk}) of {w['name']} by Alg. 2 verbatim (oracle/npc_oracle.c)",
-            "seconds": round(dt, 3)}
+            "seconds": round(dt, 3), **host_info()}
 
 
 # ------------------------------------------------------------------ reference arm (the oracle)
@@ -495,6 +520,7 @@ def run_reference(args):
         "data": "synthetic (seeded workloads/)",
         "config": config_dict(cfg, w, kind, k, args.xi, M, V),
         "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
+                         **host_info(),
                          "sample": f"each step = one p_k(A) v application (k={k}) of the full workload, Alg. 2 verbatim"},
         "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
