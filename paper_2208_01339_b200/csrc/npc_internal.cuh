@@ -8,8 +8,10 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 #include <memory>
+#include <thread>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -340,6 +342,24 @@ npc_status allow_max_dynamic_smem_ptr(const void *kern);  // vec_kernels.cu
 template <class K>
 npc_status allow_max_dynamic_smem(K kern) {
     return allow_max_dynamic_smem_ptr(reinterpret_cast<const void *>(kern));
+}
+
+// Host-side parallel loop over [0, n) in contiguous chunks (operator setup: validation and
+// format conversion of 10^7-10^8 entries).  fn(begin, end, thread_index).
+template <class F>
+void host_parallel_for(long long n, F &&fn) {
+    const int hw = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const int nt = n < 200000 ? 1 : hw;
+    if (nt == 1) {
+        fn(0LL, n, 0);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+        const long long b = n * t / nt, e = n * (t + 1) / nt;
+        th.emplace_back([&fn, b, e, t]() { fn(b, e, t); });
+    }
+    for (auto &x : th) x.join();
 }
 
 // Device-side bit helpers

@@ -214,26 +214,34 @@ static npc_status validate_csr(int n, long long ncols, const int *rowptr, const 
         set_error("CSR: rowptr[0] = %d (must be 0)", rowptr[0]);
         return NPC_ERR_DIMENSION;
     }
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < n; ++i)  // monotone first: the row ranges below are then valid
         if (rowptr[i + 1] < rowptr[i]) {
             set_error("CSR: rowptr not monotone at row %d", i);
             return NPC_ERR_DIMENSION;
         }
-        for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
-            if (colidx[p] < 0 || colidx[p] >= ncols) {
-                set_error("CSR: column %d out of range at row %d", colidx[p], i);
-                return NPC_ERR_DIMENSION;
+    // rows checked in parallel chunks; the first offending row (lowest index) is reported
+    std::vector<long long> bad(64, -1);
+    std::vector<int> why(64, 0);
+    host_parallel_for(n, [&](long long b, long long e, int t) {
+        for (long long i = b; i < e; ++i)
+            for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+                int w = 0;
+                if (colidx[p] < 0 || colidx[p] >= ncols) w = 1;
+                else if (p > rowptr[i] && colidx[p] <= colidx[p - 1]) w = 2;
+                else if (!std::isfinite(vals[p])) w = 3;
+                if (w) {
+                    bad[t] = i;
+                    why[t] = w;
+                    return;
+                }
             }
-            if (p > rowptr[i] && colidx[p] <= colidx[p - 1]) {
-                set_error("CSR: columns not strictly ascending in row %d", i);
-                return NPC_ERR_DIMENSION;
-            }
-            if (!std::isfinite(vals[p])) {
-                set_error("CSR: non-finite value at row %d", i);
-                return NPC_ERR_DIMENSION;
-            }
+    });
+    for (int t = 0; t < 64; ++t)
+        if (bad[t] >= 0) {
+            const char *msg[] = {"", "column out of range", "columns not strictly ascending", "non-finite value"};
+            set_error("CSR: %s in row %lld", msg[why[t]], bad[t]);
+            return NPC_ERR_DIMENSION;
         }
-    }
     return NPC_SUCCESS;
 }
 

@@ -413,30 +413,70 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
             set_error("SCHUR: non-finite c");
             return NPC_ERR_DIMENSION;
         }
-    std::vector<int> byl[5];
-    for (int q = 0; q < nb; ++q) {
-        int L = d->b_rowptr[q + 1] - d->b_rowptr[q];
-        if (L < 0 || L > 4) {
-            set_error("SCHUR: B rows must have 0..4 entries (row %d has %d)", q, L);
-            return L < 0 ? NPC_ERR_DIMENSION : NPC_ERR_UNSUPPORTED;
-        }
-        if (!(d->d[q] > 0.0) || !std::isfinite(d->d[q])) {
-            set_error("SCHUR: D must be positive and finite (row %d)", q);
-            return NPC_ERR_DIMENSION;
-        }
-        for (int p = d->b_rowptr[q]; p < d->b_rowptr[q + 1]; ++p)
-            if (d->b_colidx[p] < 0 || d->b_colidx[p] >= n_global || !std::isfinite(d->b_vals[p])) {
-                set_error("SCHUR: bad B entry in row %d", q);
+    // validation in parallel row chunks (first offending row reported)
+    {
+        std::vector<long long> bad(64, -1);
+        std::vector<int> why(64, 0);
+        host_parallel_for(nb, [&](long long b, long long e, int t) {
+            for (long long q = b; q < e; ++q) {
+                const int L = d->b_rowptr[q + 1] - d->b_rowptr[q];
+                int w = 0;
+                if (L < 0) w = 1;
+                else if (L > 4) w = 2;
+                else if (!(d->d[q] > 0.0) || !std::isfinite(d->d[q])) w = 3;
+                else
+                    for (int p = d->b_rowptr[q]; p < d->b_rowptr[q + 1] && !w; ++p)
+                        if (d->b_colidx[p] < 0 || d->b_colidx[p] >= n_global || !std::isfinite(d->b_vals[p])) w = 4;
+                if (w) {
+                    bad[t] = q;
+                    why[t] = w;
+                    return;
+                }
+            }
+        });
+        for (int t = 0; t < 64; ++t)
+            if (bad[t] >= 0) {
+                const long long q = bad[t];
+                if (why[t] <= 2) {
+                    set_error("SCHUR: B rows must have 0..4 entries (row %lld has %d)", q,
+                              d->b_rowptr[q + 1] - d->b_rowptr[q]);
+                    return why[t] == 1 ? NPC_ERR_DIMENSION : NPC_ERR_UNSUPPORTED;
+                }
+                set_error(why[t] == 3 ? "SCHUR: D must be positive and finite (row %lld)"
+                                      : "SCHUR: bad B entry in row %lld", q);
                 return NPC_ERR_DIMENSION;
             }
-        byl[L].push_back(q);
     }
-    // Within a length class, order B's rows by their first (smallest) column: the first-column
-    // gathers of v and scatters into y of a warp then fall on a few adjacent sectors, which
-    // cuts the L2 RED sector count (the kernel's bound) for one entry in every row.
-    for (int L = 1; L <= 4; ++L)
-        std::stable_sort(byl[L].begin(), byl[L].end(),
-                         [&](int a, int b) { return d->b_colidx[d->b_rowptr[a]] < d->b_colidx[d->b_rowptr[b]]; });
+    // Rows grouped by length; within a length class ordered by their first (smallest) column
+    // (stable counting sort): the first-column gathers of v and scatters into y of a warp then
+    // fall on a few adjacent sectors, cutting the random L2 sector count for one entry per row.
+    std::vector<int> byl[5];
+    {
+        std::vector<int> key(std::max(nb, 1));
+        std::vector<long long> cnt((size_t)5 * ((size_t)n_global + 1) + 1, 0);
+        auto slot = [&](int L, long long c) { return (size_t)L * ((size_t)n_global + 1) + (size_t)c; };
+        for (int q = 0; q < nb; ++q) {
+            const int L = d->b_rowptr[q + 1] - d->b_rowptr[q];
+            const long long c = L ? d->b_colidx[d->b_rowptr[q]] : 0;
+            key[q] = L;
+            cnt[slot(L, c) + 1]++;
+        }
+        for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+        std::vector<int> sorted(std::max(nb, 1));
+        for (int q = 0; q < nb; ++q) {
+            const int L = key[q];
+            const long long c = L ? d->b_colidx[d->b_rowptr[q]] : 0;
+            sorted[cnt[slot(L, c)]++] = q;
+        }
+        // sorted is ordered by (L, first column, q); split into the length classes
+        long long at = 0;
+        for (int L = 0; L <= 4; ++L) {
+            long long len = 0;
+            for (int q = 0; q < nb; ++q) len += key[q] == L;  // class sizes
+            byl[L].assign(sorted.begin() + at, sorted.begin() + at + len);
+            at += len;
+        }
+    }
     auto op = std::make_unique<SchurOperator>();
     op->ctx = ctx;
     op->kind = NPC_OP_SCHUR;
@@ -472,19 +512,22 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
     std::vector<int> scols((size_t)op->nslots, 0);
     std::vector<double> svals((size_t)op->nslots, 0.0);
     std::vector<int> tcount(n + 1, 0);
-    for (int ch = 0; ch < op->nchunks; ++ch)
-        for (int l = 0; l < 32; ++l) {
-            const int q = order[(size_t)ch * 32 + l];
-            if (q < 0) continue;
-            const double sc = 1.0 / std::sqrt(d->d[q]);
-            for (int j = 0; j < clen[ch]; ++j) {
-                const size_t slot = (size_t)coff[ch] + (size_t)j * 32 + l;
-                const int p = d->b_rowptr[q] + j;
-                scols[slot] = colpos(d->b_colidx[p]);
-                svals[slot] = d->b_vals[p] * sc;
-                if (!multi) tcount[d->b_colidx[p] + 1]++;
+    host_parallel_for(op->nchunks, [&](long long cb, long long ce, int) {
+        for (long long ch = cb; ch < ce; ++ch)
+            for (int l = 0; l < 32; ++l) {
+                const int q = order[(size_t)ch * 32 + l];
+                if (q < 0) continue;
+                const double sc = 1.0 / std::sqrt(d->d[q]);
+                for (int j = 0; j < clen[ch]; ++j) {
+                    const size_t slot = (size_t)coff[ch] + (size_t)j * 32 + l;
+                    const int p = d->b_rowptr[q] + j;
+                    scols[slot] = colpos(d->b_colidx[p]);
+                    svals[slot] = d->b_vals[p] * sc;
+                }
             }
-        }
+    });
+    if (!multi)
+        for (long long p = 0; p < op->nnz; ++p) tcount[d->b_colidx[p] + 1]++;
     // Single rank: the deterministic split two-pass form (faster, and bitwise reproducible;
     // profiles/r01_schur_scatter_microbench.md).  NPC_SCHUR_ATOMIC=1 selects the fp64-RED form,
     // which is also the form used across ranks (its partial B^T t is reduce-scattered).
@@ -556,22 +599,27 @@ npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::un
     if (const char *e = getenv("NPC_SCHUR_SPLIT")) K = std::max(1, std::min(16, atoi(e)));
     const long long P = std::max(1LL, ((long long)op->nbp + K - 1) / K);
     for (int k = 0; k < K; ++k) op->parts.push_back(std::make_unique<SchurOperator::Part>());
+    // per-row entry counts of every part, then each part's CSR filled in parallel row chunks
+    std::vector<std::vector<int>> prp(K, std::vector<int>(n + 1, 0));
+    for (int i = 0; i < n; ++i)
+        for (int q = trp[i]; q < trp[i + 1]; ++q) prp[tc[q] / P][i + 1]++;
+    for (int k = 0; k < K; ++k)
+        for (int i = 0; i < n; ++i) prp[k][i + 1] += prp[k][i];
     for (int k = 0; k < K; ++k) {
         SchurOperator::Part &pt = *op->parts[k];
-        std::vector<int> rp(n + 1, 0), pc;
-        std::vector<double> pv;
-        for (int i = 0; i < n; ++i) {
-            for (int q = trp[i]; q < trp[i + 1]; ++q)
-                if (tc[q] / P == k) {
-                    pc.push_back(tc[q]);
-                    pv.push_back(tv[q]);
-                }
-            rp[i + 1] = (int)pc.size();
-        }
-        for (int pad = 0; pad < 8; ++pad) {  // aligned bulk copies may read past the last entry
-            pc.push_back(0);
-            pv.push_back(0.0);
-        }
+        std::vector<int> &rp = prp[k];
+        std::vector<int> pc((size_t)rp[n] + 8, 0);  // + pad: aligned bulk copies may read past the end
+        std::vector<double> pv((size_t)rp[n] + 8, 0.0);
+        host_parallel_for(n, [&](long long b, long long e, int) {
+            for (long long i = b; i < e; ++i) {
+                int o = rp[i];
+                for (int q = trp[i]; q < trp[i + 1]; ++q)
+                    if (tc[q] / P == k) {
+                        pc[o] = tc[q];
+                        pv[o++] = tv[q];
+                    }
+            }
+        });
         for (int tt = 0; tt * ST_TILE < n; ++tt) {
             const int r0 = tt * ST_TILE, r1 = std::min(n, r0 + ST_TILE);
             const int pb = rp[r0], pe = rp[r1];

@@ -283,7 +283,8 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
     std::vector<int> scols((size_t)op->nslots);
     std::vector<double> svals((size_t)op->nslots, 0.0);
     std::vector<char> chunk_ghost(op->nchunks, 0);
-    for (int ch = 0; ch < op->nchunks; ++ch) {
+    host_parallel_for(op->nchunks, [&](long long cb, long long ce, int) {
+    for (int ch = (int)cb; ch < (int)ce; ++ch) {
         for (int l = 0; l < SELL_C; ++l) {
             int ir = ch * SELL_C + l;
             int orow = ir < n ? perm[ir] : -1;
@@ -303,6 +304,7 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
             }
         }
     }
+    });
     // tiles of SELL_TW chunks: largest contiguous slot segment -> shared memory size
     op->ntiles = ceil_div(op->nchunks, SELL_TW);
     std::vector<int> ti, tb;
