@@ -107,3 +107,10 @@ def test_config4_1m(ctx):
     w = W.config4(n=1_000_000)
     orc, op = _poly_parity(ctx, w, "sell", [60])
     _pcg_parity(ctx, w, "sell", 60, op=op, orc=orc)
+
+
+def test_config6_dfn_full(ctx):
+    """The Frac32-sized synthetic DFN system (config 6 of tools/bench_all.py, NEXT row 2)."""
+    w = W.dfn_owner_order(W.dfn(29_370))
+    orc, op = _poly_parity(ctx, w, "dfn", [30])
+    _pcg_parity(ctx, w, "dfn", 30, op=op, orc=orc)
