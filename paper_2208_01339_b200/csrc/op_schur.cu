@@ -158,7 +158,6 @@ struct SchurTDev {
 template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool PARTIAL>
 __global__ void __launch_bounds__(ST_TILE) k_schur_tpass(SchurTDev T, StepArgs s, int vspan_max,
                                                          const double *__restrict__ yin, double *__restrict__ yout) {
-    if (s.done && *s.done) return;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t bar;
     __shared__ double red[ST_TILE / 32];
@@ -201,7 +200,9 @@ __global__ void __launch_bounds__(ST_TILE) k_schur_tpass(SchurTDev T, StepArgs s
         if (HAS_S2) s2v = s.s2[i];
         if (HAS_R) rv = s.r[i];
     }
+    const bool is_done = s.done && *s.done;  // the PCG's flag, read while the bulk copy is in flight
     if (STAGED) mbar_wait(&bar, 0);
+    if (is_done) return;
     double acc = 0.0;
     if (active) {
         double y = yin ? yin[i] : 0.0;

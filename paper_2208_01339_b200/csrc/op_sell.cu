@@ -50,7 +50,6 @@ static constexpr int SELL_U = NPC_SELL_U;
 template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST>
 __global__ void __launch_bounds__(SELL_C *SELL_TW, NPC_SELL_MINB)
     k_sell_step(SellDev A, StepArgs s, const int *__restrict__ tiles, int span_max) {
-    if (s.done && *s.done) return;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t bar;
     __shared__ double red[SELL_TW];
@@ -95,7 +94,9 @@ __global__ void __launch_bounds__(SELL_C *SELL_TW, NPC_SELL_MINB)
             if (HAS_S2) s2v = s.s2[row];
             if (HAS_R) rv = s.r[row];
         }
+        const bool is_done = s.done && *s.done;  // read while the bulk copy is in flight
         mbar_wait(&bar, 0);
+        if (is_done) return;
         if (ch < ch1) {
             double y = 0.0;
             for (int j = 0; j < len; ++j) {
@@ -111,13 +112,19 @@ __global__ void __launch_bounds__(SELL_C *SELL_TW, NPC_SELL_MINB)
                 if (DOT) acc = o * s.dotv[row];
             }
         }
-    } else if (ch < ch1) {
+    } else {
         // Direct coalesced slot loads (each slot of a warp is one 256 B value + 128 B index
         // line), SELL_U slots per group.  The kernel is bound by memory latency (the x gathers
         // depend on the index loads), so it is tuned for occupancy: few live registers, the
         // epilogue operands loaded after the loop (A/B: profiles/r01_sell_ab.md).
-        const int len = A.chunk_len[ch];
-        const long long gbase = (long long)A.chunk_off[ch] + lane;
+        const bool is_done = s.done && *s.done;  // the PCG's flag, read beside the chunk metadata
+        int len = 0;
+        long long gbase = lane;
+        if (ch < ch1) {
+            len = A.chunk_len[ch];
+            gbase += A.chunk_off[ch];
+        }
+        if (is_done) return;  // uniform over the CTA (before the block reduction)
         const int *__restrict__ cp = A.cols + gbase;
         const double *__restrict__ vp = A.vals + gbase;
         double y = 0.0;

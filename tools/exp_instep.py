@@ -1,7 +1,8 @@
 import sys, time, json
 sys.path.insert(0, '/root/repo')
 import numpy as np, torch, bench, paper_2208_01339_b200 as npc
-w = bench.make_workload(3, None); kind = 'csr'; k = 50
+import os
+CFG = int(os.environ.get("EXP_CFG", "3")); w = bench.make_workload(CFG, None); kind = bench.op_kind(w, CFG); k = w["k"]
 ctx = npc.npc_context_create(0)
 op = npc.create_from_workload(ctx, w, kind)
 b = torch.tensor(w['b'], device='cuda'); x = torch.zeros_like(b); z = torch.empty_like(b)
