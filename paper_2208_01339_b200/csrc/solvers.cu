@@ -811,6 +811,12 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     NPC_CUDA_TRY(cudaMemcpyAsync(sums + 2, &h.rr, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     const int *dflag = &cg->done;
     int chunk = 4;
+    // Iterations between host checks grow 4, 8, ..., 64 for short iterations; when one chunk of
+    // 4 already takes >= 2 ms the host checks after every graph replay instead (a few µs per
+    // check), so at most 3 iterations run past convergence -- no-op kernels still stream some
+    // data (the CSR kernel issues its tile copy before reading the flag).
+    int chunk_max = 64;
+    double t_chunk = now_s();
     int true_checks = 0;
     // One PCG iteration = k fused degree kernels (+ halo) + A u + reduce (+ allreduce) +
     // scalars + update + ||r||^2; every kernel no-ops once the device flag says done.
@@ -870,6 +876,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     GraphRun gr(ctx, cache);
     if (op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH"))
         NPC_TRY(gr.capture(iteration));
+    t_chunk = now_s();  // the first chunk's clock starts after the capture
     for (;;) {
         if (gr.exec) {
             if (ctx->timing) {  // read the events after every replay; stop replaying once done
@@ -891,7 +898,9 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         if (ctx->timing) ctx->t_flush();
         if (!h.done) {
-            chunk = std::min(chunk * 2, 64);
+            if (chunk_max == 64 && now_s() - t_chunk >= 2e-3) chunk_max = GraphRun::ITERS;
+            chunk = std::min(chunk * 2, chunk_max);
+            t_chunk = now_s();
             continue;
         }
         st.iters = h.iters;
