@@ -52,15 +52,18 @@ def main():
     ap.add_argument("--kind", default=None)
     ap.add_argument("--k", type=int, default=60)
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--libs", required=True)
+    ap.add_argument("--libs", default="paper_2208_01339_b200/libnpc.so")
+    ap.add_argument("--envs", default="", help="'|'-separated env variants, e.g. '|NPC_DFN_M=1'")
     a = ap.parse_args()
     code = CHILD.replace("ROOT", repr(ROOT)).replace("CFG", str(a.config)).replace("SIDE", repr(a.side)) \
         .replace("KIND", repr(a.kind)).replace("REPS", str(a.reps)).replace("K,", f"{a.k},") \
         .replace("(M, V, K)", f"(M, V, {a.k})")
     for lib in a.libs.split(","):
-        env = dict(os.environ, NPC_LIB_PATH=os.path.abspath(lib))
-        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
-        print(r.stdout.strip() or r.stderr[-2000:], flush=True)
+        for ev in a.envs.split("|"):
+            env = dict(os.environ, NPC_LIB_PATH=os.path.abspath(lib))
+            env.update(kv.split("=", 1) for kv in ev.split(",") if kv)
+            r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+            print(ev or "-", r.stdout.strip() or r.stderr[-2000:], flush=True)
 
 
 if __name__ == "__main__":
