@@ -208,7 +208,7 @@ def partition_rows(w, cfg, ws, rank):
 
 
 def create_operator(npc, ctx, w, kind, ws, rank, cfg):
-    if ws == 1:
+    if ws == 1 and not getattr(ctx, "distributed", False):
         return npc.create_from_workload(ctx, w, kind), 0, w["n"]
     r0, r1, zs = partition_rows(w, cfg, ws, rank)
     if kind == "stencil":
@@ -277,6 +277,8 @@ def run_ours(args):
             t.copy_(torch.frombuffer(bytearray(npc.npc_get_unique_id()), dtype=torch.uint8))
         dist.broadcast(t, 0)
         uid = bytes(t.cpu().numpy().tobytes())
+    elif args.distributed:
+        uid = npc.npc_get_unique_id()
     stream = torch.cuda.current_stream()
     ctx = npc.npc_context_create(local, ws, rank, uid, stream)
     op, r0, r1 = create_operator(npc, ctx, w, kind, ws, rank, cfg)
@@ -421,7 +423,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads/, BASELINE.json config recipe)",
             "config": config_dict(cfg, w, kind, k, xi, M, V),
             "parallelism": f"row-block x{ws} (z-slabs for grids), NCCL halo + 1 allreduce/iteration" if ws > 1
-            else "1 GPU",
+            else "1 GPU, multi-rank path on a 1-rank NCCL communicator" if args.distributed else "1 GPU",
             "pcg": {"iters": iters, "converged": stats[-1]["converged"], "relres_true": stats[-1]["relres_true"],
                     "op_applications": stats[-1]["op_applications"], "reductions": stats[-1]["reductions"],
                     "lmin": lo, "lmax": hi, "time_to_tol_ms": round(ms_step, 3),
@@ -445,7 +447,7 @@ def run_ours(args):
             "clocks": clk,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if ws > 1:
         dist.destroy_process_group()
 
@@ -527,10 +529,26 @@ def run_reference(args):
                          "sample": f"each step = one p_k(A) v application (k={k}) of the full workload, Alg. 2 verbatim"},
         "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_json_out = None
+
+
+def emit(line):
+    """The one JSON line, on the process's real stdout."""
+    out = _json_out or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _json_out
+    # stdout carries exactly one JSON line: anything else written to fd 1 (native libraries,
+    # e.g. NCCL's version banner) goes to stderr
+    sys.stdout.flush()
+    _json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -546,6 +564,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=30.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--distributed", action="store_true",
+                    help="at --gpus 1: a 1-rank NCCL context, i.e. the multi-rank path (include/npc.h)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="do not bracket launches with library CUDA events in the timed region")

@@ -58,6 +58,12 @@ typedef struct npc_poly_s *npc_poly;
  * device: CUDA ordinal.  nranks/rank: 1/0 for a single GPU; for nranks > 1,
  * nccl_unique_id points to the 128-byte ncclUniqueId produced by npc_get_unique_id on rank
  * 0 and broadcast by the caller (e.g. torch.distributed); COLLECTIVE in that case.
+ * A context created with a transport -- any nccl_unique_id, or npc_context_create_local --
+ * is DISTRIBUTED even at nranks == 1: operators take the multi-rank descriptor contract
+ * (global column ids, row_begin/n_global) and every operator and solver runs its multi-rank
+ * path (halo plans, NCCL collectives captured into the PCG graphs, ||r||^2 allreduced on a
+ * side stream overlapping the next p_k(A) r), with empty halos on one rank.  nranks == 1 without a unique id is the
+ * single-GPU path (device-side convergence test, fused small-operator kernels).
  * cuda_stream: a cudaStream_t to enqueue on, or NULL for a library-owned stream.        */
 NPC_API npc_status npc_context_create(int device, int nranks, int rank, const void *nccl_unique_id,
                               void *cuda_stream, npc_context *out);
@@ -237,8 +243,14 @@ NPC_API npc_status npc_apply_poly(npc_poly poly, const double *r_dev, double *z_
 typedef struct {
     int iters;                   /* x updates                                               */
     int converged;
-    long long op_applications;   /* every A application, including those inside p_k       */
-    long long reductions;        /* global reduction points (allreduces when nranks > 1)    */
+    long long op_applications;   /* every A application, including those inside p_k: k+1
+                                    per iteration, +1 if x0 != 0, +1 per true residual; a
+                                    distributed solve's application cut short by the
+                                    overlapped convergence check is not counted             */
+    long long reductions;        /* global reduction points (allreduces when distributed):
+                                    1 per iteration (2 when distributed: gamma/delta, and
+                                    ||r||^2 on the side stream) + 1 per V^T r of a low-rank
+                                    correction, +1 each for ||b||, ||r_0||, true residual   */
     double relres_recursive;     /* ||r_iters|| / ||b|| (recursive residual)                */
     double relres_true;          /* ||b - A x|| / ||b|| of the returned x                   */
     double solve_seconds;        /* wall time of the call                                   */

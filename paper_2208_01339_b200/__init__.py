@@ -146,6 +146,7 @@ class Context:
     def __init__(self, handle, stream):
         self.h = handle
         self.stream = stream
+        self.distributed = False
 
     def close(self):
         if self.h:
@@ -174,7 +175,9 @@ def npc_context_create(device: int = 0, nranks: int = 1, rank: int = 0, unique_i
     # stream" in the C ABI, so pass cudaStreamLegacy (0x1) to enqueue on torch's stream.
     handle = stream.cuda_stream or 0x1
     _check(lib().npc_context_create(device, nranks, rank, uid, C.c_void_p(handle), C.byref(h)))
-    return Context(h, stream)
+    c = Context(h, stream)
+    c.distributed = unique_id is not None  # include/npc.h: a transport makes the context distributed
+    return c
 
 
 def npc_context_create_local(device: int, nranks: int, rank: int, group: str, stream=None) -> Context:
@@ -185,7 +188,9 @@ def npc_context_create_local(device: int, nranks: int, rank: int, group: str, st
     h = C.c_void_p()
     handle = stream.cuda_stream or 0x1
     _check(lib().npc_context_create_local(device, nranks, rank, group.encode(), C.c_void_p(handle), C.byref(h)))
-    return Context(h, stream)
+    c = Context(h, stream)
+    c.distributed = True
+    return c
 
 
 TIMING_CLASSES = ("degree", "operator", "update", "reduce", "vector")

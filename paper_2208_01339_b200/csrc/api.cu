@@ -91,7 +91,7 @@ static npc_status context_create(int device, int nranks, int rank, const void *n
         NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         c.own_stream = true;
     }
-    if (nranks > 1) {
+    if (nranks > 1 || local_group || nccl_unique_id) {
         NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking));
         if (local_group)
             NPC_TRY(make_local_transport(&c, local_group, c.tr));
@@ -158,7 +158,7 @@ npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, n
     NPC_GUARD(ctx && desc && out, NPC_ERR_INVALID_ARGUMENT, "npc_create_operator: null argument");
     *out = nullptr;
     NPC_GUARD(desc->n_local >= 0 && desc->row_begin >= 0, NPC_ERR_DIMENSION, "npc_create_operator: negative size");
-    if (ctx->ctx.nranks == 1)
+    if (!ctx->ctx.distributed())
         NPC_GUARD(desc->row_begin == 0 && (desc->n_global == 0 || desc->n_global == desc->n_local), NPC_ERR_DIMENSION,
                   "npc_create_operator: single rank must own all rows");
     else

@@ -179,6 +179,11 @@ class Transport {
                                 const std::vector<int> &soff, double *rbuf, const std::vector<int> &rcount,
                                 const std::vector<int> &roff, cudaStream_t s) = 0;
     virtual npc_status allreduce_sum(Context *c, double *dev, int count, cudaStream_t s) = 0;
+    // Same sum on an auxiliary channel that may run CONCURRENTLY with the transport's other
+    // calls (NCCL: a split communicator); issued in the same order on every rank.
+    virtual npc_status allreduce_sum_aux(Context *c, double *dev, int count, cudaStream_t s) {
+        return allreduce_sum(c, dev, count, s);
+    }
     // Padded-slot collectives of the Schur operator (slot q = [q m, q m + m) of a P*m buffer;
     // rank q's valid entries are the first counts[q] of its slot):
     //   allgather_slots: in place, every rank's slot is copied into every rank's buffer;
@@ -196,11 +201,16 @@ struct Context {
     int device = 0;
     int nranks = 1, rank = 0;
     cudaStream_t stream = nullptr;       // compute stream
-    cudaStream_t comm_stream = nullptr;  // halo traffic (nranks > 1)
+    cudaStream_t comm_stream = nullptr;  // halo traffic (distributed contexts)
     bool own_stream = false;
     cudaStream_t graph_stream = nullptr;  // CUDA-graph replay of PCG iterations
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    std::unique_ptr<Transport> tr;       // nranks > 1: NCCL or a local thread group
+    cudaEvent_t ev_rr0 = nullptr, ev_rr1 = nullptr;  // PCG side-stream ||r||^2 allreduce (distributed)
+    std::unique_ptr<Transport> tr;       // distributed contexts: NCCL or a local thread group
+    // Distributed context: created with a transport (any nranks >= 1, see include/npc.h). Every
+    // operator and solver takes its multi-rank path (halo plans, collectives) iff this holds; a
+    // 1-rank distributed context runs that path with empty halos and 1-rank collectives.
+    bool distributed() const { return tr != nullptr; }
     int num_sms = 148;
     // scratch for reductions: partial arrays + scalar slots
     DevBuf partials;        // 4 slots of partial_cap doubles

@@ -201,7 +201,9 @@ class CsrOperator : public Operator {
 
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
-        if (!multi) return launch(s, nullptr, ntiles, s.partials, false);
+        // single rank, or a 1-rank distributed context (no halo; with more ranks the exchange
+        // is collective for the local transport even when this rank's plan is empty)
+        if (!multi || ctx->nranks == 1) return launch(s, nullptr, ntiles, s.partials, false);
         // halo of x -> ghost slots on the comm stream, interior tiles meanwhile
         NPC_TRY(halo_start(ctx, plan, halo, s.x));
         NPC_TRY(launch(s, tiles_interior.as<int>(), n_interior, s.partials, false));
@@ -262,7 +264,7 @@ npc_status localize_columns(Context *ctx, const npc_operator_desc *d, HaloPlan &
     const int n = d->n_local;
     const long long nnz = d->rowptr[n];
     local_cols.resize((size_t)nnz);
-    if (ctx->nranks == 1) {
+    if (!ctx->distributed()) {
         for (long long p = 0; p < nnz; ++p) local_cols[p] = d->colidx[p];
         return NPC_SUCCESS;
     }
@@ -303,7 +305,7 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     op->nnz = nnz;
     std::vector<int> lcols;
     NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
-    op->multi = ctx->nranks > 1;
+    op->multi = ctx->distributed();
     // tiles, spans, interior/boundary split
     op->ntiles = ceil_div(n, CSR_TILE);
     std::vector<int> ti, tb;

@@ -482,7 +482,7 @@ static npc_status upload(DevBuf &b, const T *src, size_t n) {
 }
 
 npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d0, std::unique_ptr<Operator> &out) {
-    const bool multi = ctx->nranks > 1;
+    const bool multi = ctx->distributed();
     const int P = ctx->nranks, me = ctx->rank;
     // ---- partition (multi-rank): u rows [U0, U0 + n_local), h rows [H0, H0 + n^h_local) in rank
     // order; the desc's A / G^h columns are GLOBAL h ids, C / B / G^u columns GLOBAL u ids.

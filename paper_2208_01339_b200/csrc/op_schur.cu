@@ -375,7 +375,7 @@ class SchurOperator : public Operator {
 
 npc_status make_schur_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out) {
     const int n = d->n_local, nb = d->b_n_local;
-    const bool multi = ctx->nranks > 1;
+    const bool multi = ctx->distributed();
     if (n < 0 || nb < 0 || (n > 0 && !d->c) || (nb > 0 && (!d->b_rowptr || !d->b_colidx || !d->b_vals || !d->d))) {
         set_error("SCHUR: invalid arrays");
         return NPC_ERR_INVALID_ARGUMENT;

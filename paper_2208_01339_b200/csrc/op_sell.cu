@@ -181,7 +181,7 @@ class SellOperator : public Operator {
         return launch_scatter(ctx, in, perm.as<int>(), out, n_local);
     }
     int num_partials() const override {
-        return multi ? std::max(n_interior, 1) + std::max(n_boundary, 1) : std::max(ntiles, 1);
+        return multi && ctx->nranks > 1 ? std::max(n_interior, 1) + std::max(n_boundary, 1) : std::max(ntiles, 1);
     }
     double bytes_per_step(bool has_s2, bool has_r) const override {
         // stored slots (values + indices, padding included) + per-chunk metadata + vectors
@@ -230,7 +230,9 @@ class SellOperator : public Operator {
     }
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
-        if (!multi) return launch(s, nullptr, ntiles, s.partials, false);
+        // single rank, or a 1-rank distributed context (no halo; with more ranks the exchange
+        // is collective for the local transport even when this rank's plan is empty)
+        if (!multi || ctx->nranks == 1) return launch(s, nullptr, ntiles, s.partials, false);
         NPC_TRY(halo_start(ctx, plan, halo, s.x));
         NPC_TRY(launch(s, tiles_interior.as<int>(), n_interior, s.partials, false));
         NPC_TRY(halo_wait(ctx, halo));
@@ -257,7 +259,7 @@ npc_status make_sell_operator(Context *ctx, const npc_operator_desc *d, std::uni
     op->n_local = n;
     op->n_global = d->n_global;
     op->row_begin = d->row_begin;
-    op->multi = ctx->nranks > 1;
+    op->multi = ctx->distributed();
     std::vector<int> lcols;
     NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
     op->nnz = d->rowptr[n];

@@ -250,9 +250,29 @@ class StencilOperator : public Operator {
         dim3 g = grid_for(nplanes, zc);
         return (int)(g.x * g.y * g.z);
     }
+    // multi-rank launch segments: the planes that need no ghost (launched while the halo is in
+    // flight) and then the boundary planes next to a neighbour rank (after the halo wait); a
+    // side without a neighbour (the global z boundary) is part of the first segment
+    struct Seg {
+        int z0, z1, zc;
+        bool after_wait;
+    };
+    int segments(Seg *o) const {
+        if (nzl <= 0) return 0;
+        int n = 0;
+        const int lo_i = has_lo ? 1 : 0, hi_i = std::max(lo_i, has_hi ? nzl - 1 : nzl);
+        if (hi_i > lo_i) o[n++] = {lo_i, hi_i, ST_ZC, false};
+        if (lo_i == 1) o[n++] = {0, 1, 1, true};
+        if (hi_i < nzl) o[n++] = {hi_i, nzl, 1, true};
+        return n;
+    }
     int num_partials() const override {
         if (!multi) return blocks_for(nzl, ST_ZC);
-        return blocks_for(std::max(nzl - 2, 0), ST_ZC) + 2 * blocks_for(1, 1);
+        Seg sg[3];
+        const int ns = segments(sg);
+        int tot = 0;
+        for (int i = 0; i < ns; ++i) tot += blocks_for(sg[i].z1 - sg[i].z0, sg[i].zc);
+        return std::max(tot, 1);
     }
     double bytes_per_step(bool has_s2, bool has_r) const override {
         double b = 2.0 * 8.0 * n_local;  // read x once, write out
@@ -305,7 +325,9 @@ class StencilOperator : public Operator {
     // they are L2-resident (128^3, config 2), so it is used only above ~3/4 of the L2 size.
     // NPC_STEP2=1 forces it on, NPC_NO_STEP2=1 off.
     bool supports_step2() const override {
-        if (dim != 3 || multi || n_local == 0 || getenv("NPC_NO_STEP2")) return false;
+        // multi-rank: only in a 1-rank distributed context -- a neighbour's plane would be
+        // needed two degrees deep
+        if (dim != 3 || (multi && ctx->nranks > 1) || n_local == 0 || getenv("NPC_NO_STEP2")) return false;
         if (getenv("NPC_STEP2")) return true;
         int l2 = 0;
         if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device) != cudaSuccess || l2 <= 0)
@@ -336,15 +358,21 @@ class StencilOperator : public Operator {
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
         if (!multi) return launch(s, 0, nzl, ST_ZC, s.partials);
-        NPC_TRY(halo_start(ctx, plan, halo, s.x));
+        Seg sg[3];
+        const int ns = segments(sg);
         double *p = s.partials;
-        const int nin = blocks_for(std::max(nzl - 2, 0), ST_ZC), nb1 = blocks_for(1, 1);
-        if (nzl > 2) NPC_TRY(launch(s, 1, nzl - 1, ST_ZC, p));
-        NPC_TRY(halo_wait(ctx, halo));
-        NPC_TRY(launch(s, 0, 1, 1, p ? p + nin : nullptr));
-        if (nzl > 1) NPC_TRY(launch(s, nzl - 1, nzl, 1, p ? p + nin + nb1 : nullptr));
-        else if (p) NPC_TRY(launch_fill(ctx, p + nin + nb1, 0.0, nb1));
-        if (p && nzl <= 2 && nin > 0) NPC_TRY(launch_fill(ctx, p, 0.0, nin));
+        if (ns == 0) return p ? launch_fill(ctx, p, 0.0, 1) : NPC_SUCCESS;
+        const bool need_halo = ctx->nranks > 1;  // collective for the local transport
+        if (need_halo) NPC_TRY(halo_start(ctx, plan, halo, s.x));
+        bool waited = !need_halo;
+        for (int i = 0; i < ns; ++i) {
+            if (sg[i].after_wait && !waited) {
+                NPC_TRY(halo_wait(ctx, halo));
+                waited = true;
+            }
+            NPC_TRY(launch(s, sg[i].z0, sg[i].z1, sg[i].zc, p));
+            if (p) p += blocks_for(sg[i].z1 - sg[i].z0, sg[i].zc);
+        }
         return NPC_SUCCESS;
     }
 };
@@ -386,7 +414,7 @@ npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::
         set_error("stencil: n_local/n_global disagree with the grid");
         return NPC_ERR_DIMENSION;
     }
-    if (ctx->nranks > 1) {
+    if (ctx->distributed()) {
         if (op->dim != 3) {
             set_error("stencil: multi-rank needs dim 3 (z-slabs)");
             return NPC_ERR_UNSUPPORTED;

@@ -25,7 +25,7 @@ npc_status Context::ensure_partials(size_t n) {
 }
 
 npc_status Context::allreduce_sum(double *dev, int count) {
-    if (nranks == 1) return NPC_SUCCESS;
+    if (!distributed()) return NPC_SUCCESS;
     TimedScope ts(this, T_REDUCE);
     return tr->allreduce_sum(this, dev, count, stream);
 }
@@ -100,6 +100,8 @@ Context::~Context() {
     if (graph_stream) cudaStreamDestroy(graph_stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_rr0) cudaEventDestroy(ev_rr0);
+    if (ev_rr1) cudaEventDestroy(ev_rr1);
     for (auto &p : pending) {
         cudaEventDestroy(p.e0);
         if (p.e1) cudaEventDestroy(p.e1);
@@ -430,22 +432,11 @@ struct CgDev {
     int done, iters, maxit, breakdown, converged, first, multi, pad;
 };
 
-// sums[0] = <r, u> (gamma), sums[1] = <u, A u> (delta), sums[2] = ||r||^2 (multi-rank: of
-// the current r, reduced together with gamma and delta -- one allreduce per iteration).
+// sums[0] = <r, u> (gamma), sums[1] = <u, A u> (delta) -- the one allreduce of the iteration.
+// (Distributed contexts reduce ||r_{i+1}||^2 separately, overlapped with the next p_k(A) r:
+// k_cg_rrcheck.)
 __global__ void k_cg_scalars(CgDev *st, const double *sums) {
     if (st->done) return;
-    if (st->multi) {
-        st->rr = sums[2];
-        if (st->iters > 0 && st->rr <= st->tol2) {  // r_i converged: u_i, w_i are discarded
-            st->converged = 1;
-            st->done = 1;
-            return;
-        }
-        if (st->iters >= st->maxit) {
-            st->done = 1;
-            return;
-        }
-    }
     const double g = sums[0], dl = sums[1];
     if (!(g > 0.0)) {
         st->breakdown = 1;
@@ -504,7 +495,7 @@ __global__ void __launch_bounds__(1024) k_cg_rr(CgDev *st, const double *__restr
     t = block_sum<1024>(t, red);
     if (threadIdx.x == 0) {
         st->iters += 1;
-        sums[2] = t;
+        sums[st->multi ? 4 : 2] = t;  // multi: the local partial, allreduced on the side stream
         if (!st->multi) {
             st->rr = t;
             if (history) history[st->iters] = sqrt(t / st->bnorm2);
@@ -518,9 +509,21 @@ __global__ void __launch_bounds__(1024) k_cg_rr(CgDev *st, const double *__restr
     }
 }
 
-__global__ void k_cg_hist_multi(const CgDev *st, double *history) {
-    // multi-rank: the global ||r_i||^2 becomes known in k_cg_scalars of iteration i+1
-    if (history && st->iters > 0) history[st->iters] = sqrt(st->rr / st->bnorm2);
+// Distributed contexts: the global ||r_i||^2 arrives from an allreduce on
+// the side stream that overlaps the next p_k(A) r; on convergence the flag is raised while
+// that application is in flight, so its remaining degree kernels and w = A u no-op (the
+// discarded work is about one allreduce latency, not a whole (k+1)-application block).
+__global__ void k_cg_rrcheck(CgDev *st, const double *rr_glob, double *history) {
+    if (st->done) return;
+    const double t = *rr_glob;
+    st->rr = t;
+    if (history) history[st->iters] = sqrt(t / st->bnorm2);
+    if (t <= st->tol2) {
+        st->converged = 1;
+        st->done = 1;
+    } else if (st->iters >= st->maxit) {
+        st->done = 1;
+    }
 }
 
 // Stream-captured replay of a fixed work block.  While active, ctx->stream points at the
@@ -613,7 +616,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     double *host_hist = stats ? stats->history : nullptr;
     // work vectors (internal order): b, x, r, u, w, p, s
     PcgCache &cache = P ? P->pcg : H->pcg;
-    if (op->supports_fused_pcg() && ctx->nranks == 1 && (!P || (P->kind == 0 && P->lr_p == 0 &&
+    if (op->supports_fused_pcg() && !ctx->distributed() && (!P || (P->kind == 0 && P->lr_p == 0 &&
                                                                 (P->degree == 0 || P->coef_dev.p)))) {
         // small operator: the whole solve in one cluster launch (csr_cluster.cu)
         if (cache.dev_maxit < maxit) {
@@ -785,7 +788,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     h.tol2 = tol * tol * bnorm2;
     h.maxit = maxit;
     h.first = 1;
-    h.multi = ctx->nranks > 1;
+    h.multi = ctx->distributed();
     bool done = rr0 <= h.tol2;
     st.relres_recursive = sqrt(rr0 / bnorm2);
     if (done) {
@@ -818,6 +821,19 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     int chunk_max = 64;
     double t_chunk = now_s();
     int true_checks = 0;
+    bool rr_pending = false;
+    long long iter_calls = 0;
+    auto join_rr = [&]() -> npc_status {
+        if (rr_pending) {
+            NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_rr1, 0));
+            rr_pending = false;
+        }
+        return NPC_SUCCESS;
+    };
+    if (h.multi && !ctx->ev_rr0) {
+        NPC_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_rr0, cudaEventDisableTiming));
+        NPC_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_rr1, cudaEventDisableTiming));
+    }
     // One PCG iteration = k fused degree kernels (+ halo) + A u + reduce (+ allreduce) +
     // scalars + update + ||r||^2; every kernel no-ops once the device flag says done.
     auto iteration = [&]() -> npc_status {
@@ -844,14 +860,11 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                 TimedScope ts(ctx, T_REDUCE);
                 NPC_TRY(launch_reduce_sum(ctx, P0, npg, sums + 0, 1, P1, np_op, sums + 1));
             }
-            NPC_TRY(ctx->allreduce_sum(sums, 3));  // the single global reduction
+            NPC_TRY(ctx->allreduce_sum(sums, 2));  // the single global reduction
+            NPC_TRY(join_rr());  // ||r_i||^2 of the previous update is known (and checked)
             {
                 TimedScope ts(ctx, T_REDUCE);
                 k_cg_scalars<<<1, 1, 0, ctx->stream>>>(cg, sums);
-                NPC_LAUNCH_CHECK();
-            }
-            if (h.multi) {
-                k_cg_hist_multi<<<1, 1, 0, ctx->stream>>>(cg, dhist);
                 NPC_LAUNCH_CHECK();
             }
             {
@@ -863,6 +876,17 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                 TimedScope ts(ctx, T_REDUCE);
                 k_cg_rr<<<1, 1024, 0, ctx->stream>>>(cg, P2, np_vec, sums, dhist);
                 NPC_LAUNCH_CHECK();
+            }
+            if (h.multi) {  // ||r_{i+1}||^2: allreduce + check on the side stream
+                NPC_CUDA_TRY(cudaEventRecord(ctx->ev_rr0, ctx->stream));
+                NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_rr0, 0));
+                NPC_TRY(ctx->tr->allreduce_sum_aux(ctx, sums + 4, 1, ctx->comm_stream));
+                k_cg_rrcheck<<<1, 1, 0, ctx->comm_stream>>>(cg, sums + 4, dhist);
+                NPC_LAUNCH_CHECK();
+                NPC_CUDA_TRY(cudaEventRecord(ctx->ev_rr1, ctx->comm_stream));
+                rr_pending = true;
+                // a captured block of GraphRun::ITERS iterations ends joined
+                if (++iter_calls % GraphRun::ITERS == 0) NPC_TRY(join_rr());
             }
         }
         return NPC_SUCCESS;
@@ -893,6 +917,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
             }
         } else {
             for (int it = 0; it < chunk; ++it) NPC_TRY(iteration());
+            NPC_TRY(join_rr());
         }
         NPC_CUDA_TRY(cudaMemcpyAsync(&h, cg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -944,12 +969,13 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         result = NPC_ERR_NOT_CONVERGED;
         break;
     }
-    // counters: k+1 applications per x-update (Table tab11 law); multi-rank detects
-    // convergence one block late (u, w of the next iteration are formed and discarded)
-    st.op_applications += (long long)h.iters * (k + 1) + ((h.multi && h.converged) ? (k + 1) : 0);
-    st.reductions += h.iters + ((h.multi && h.converged) ? 1 : 0);
+    // counters: k+1 applications per x-update (Table tab11 law); distributed contexts reduce
+    // ||r||^2 in a second (overlapped) allreduce per iteration.  Not counted: the application
+    // in flight when the overlapped check raises the done flag (its remaining kernels no-op).
+    st.op_applications += (long long)h.iters * (k + 1);
+    st.reductions += h.iters * (h.multi ? 2 : 1);
     if (P && P->lr_p > 0)  // V^T r inside every application of the preconditioner
-        st.reductions += h.iters + ((h.multi && h.converged) ? 1 : 0);
+        st.reductions += h.iters;
     if (host_hist && h.iters > 0)
         NPC_CUDA_TRY(cudaMemcpyAsync(host_hist + 1, dhist + 1, sizeof(double) * h.iters, cudaMemcpyDeviceToHost,
                                      ctx->stream));
@@ -1137,7 +1163,7 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, doub
         set_error("estimate_spectrum: start vector is zero");
         return NPC_ERR_INVALID_ARGUMENT;
     }
-    if (op->supports_fused_lanczos() && ctx->nranks == 1) {  // small operator: one cluster launch
+    if (op->supports_fused_lanczos() && !ctx->distributed()) {  // small operator: one cluster launch
         TimedScope ts(ctx, T_OPERATOR);
         NPC_TRY(op->lanczos_fused(v0, m, alphas, betas, &lz->steps));
     } else {

@@ -18,7 +18,9 @@ namespace npc {
 class NcclTransport : public Transport {
   public:
     ncclComm_t comm = nullptr;
+    ncclComm_t comm_aux = nullptr;  // split of comm: the PCG ||r||^2 allreduce on the side stream
     ~NcclTransport() override {
+        if (comm_aux) ncclCommDestroy(comm_aux);
         if (comm) ncclCommDestroy(comm);
     }
     bool capturable() const override { return true; }
@@ -89,6 +91,11 @@ class NcclTransport : public Transport {
         NPC_NCCL_TRY(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, s));
         return NPC_SUCCESS;
     }
+    npc_status allreduce_sum_aux(Context *c, double *dev, int count, cudaStream_t s) override {
+        (void)c;
+        NPC_NCCL_TRY(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm_aux, s));
+        return NPC_SUCCESS;
+    }
     npc_status allgather_slots(Context *c, double *full, int m, const std::vector<int> &counts,
                                cudaStream_t s) override {
         (void)counts;
@@ -107,6 +114,7 @@ npc_status make_nccl_transport(Context *c, const void *uid, std::unique_ptr<Tran
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));
     NPC_NCCL_TRY(ncclCommInitRank(&t->comm, c->nranks, id, c->rank));
+    NPC_NCCL_TRY(ncclCommSplit(t->comm, 0, c->rank, &t->comm_aux, nullptr));
     out = std::move(t);
     return NPC_SUCCESS;
 }
