@@ -422,7 +422,7 @@ class DfnOperator : public Operator {
     npc_status launch_out(const StepArgs &s) {
         DfnOutDev O{gurp.as<int>(), guci.as<int>(), guv.as<double>(), btrp.as<int>(), btci.as<int>(),
                     btv.as<double>(), ctrp.as<int>(), ctci.as<int>(), ctv.as<double>(), t.as<double>(),
-                    u2.as<double>(), multi ? xg.as<double>() : s.x, alpha, n_local};
+                    u2.as<double>(), multi && ctx->nranks > 1 ? xg.as<double>() : s.x, alpha, n_local};
         k_dfn_out<H2, HR, DT><<<num_partials(), DFN_OUT_T, 0, ctx->stream>>>(O, s);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
@@ -439,7 +439,8 @@ class DfnOperator : public Operator {
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
         const double *xin = s.x;
-        if (multi) {
+        const bool halo = multi && ctx->nranks > 1;  // a 1-rank distributed context has no ghosts
+        if (halo) {
             if (n_local)
                 NPC_CUDA_TRY(cudaMemcpyAsync(xg.p, s.x, sizeof(double) * n_local, cudaMemcpyDeviceToDevice,
                                              ctx->stream));
@@ -457,7 +458,7 @@ class DfnOperator : public Operator {
             else if (lanes == 16) NPC_TRY(launch_block<16>(xin, s.done));
             else NPC_TRY(launch_block<32>(xin, s.done));
         }
-        if (multi) {
+        if (halo) {
             NPC_TRY(halo_into(hplan, trt, t.as<double>(), t.as<double>(), nh));
             NPC_TRY(halo_into(hplan, u2rt, u2.as<double>(), u2.as<double>(), nh));
             if (n_local == 0) return NPC_SUCCESS;

@@ -898,8 +898,15 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     // replayed one graph per host sync so that its events can be read after each replay.
     if (cache.exec && cache.timed != ctx->timing) cache.invalidate();
     GraphRun gr(ctx, cache);
-    if (op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH"))
+    const bool graph_ok = op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH");
+    // Distributed: capturing the NCCL calls costs milliseconds per new graph (measured 16 ms
+    // for a DFN block of 4 iterations), so a solve without a cached graph runs its first chunk
+    // eagerly and captures only if it needs a second one.
+    bool deferred = graph_ok && h.multi && !cache.exec;
+    if (graph_ok && !deferred) {
+        iter_calls = 0;
         NPC_TRY(gr.capture(iteration));
+    }
     t_chunk = now_s();  // the first chunk's clock starts after the capture
     for (;;) {
         if (gr.exec) {
@@ -923,6 +930,11 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         if (ctx->timing) ctx->t_flush();
         if (!h.done) {
+            if (deferred) {
+                deferred = false;
+                iter_calls = 0;
+                NPC_TRY(gr.capture(iteration));
+            }
             if (chunk_max == 64 && now_s() - t_chunk >= 2e-3) chunk_max = GraphRun::ITERS;
             chunk = std::min(chunk * 2, chunk_max);
             t_chunk = now_s();

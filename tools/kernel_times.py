@@ -25,12 +25,13 @@ def main():
     ap.add_argument("--kind", default=None)
     ap.add_argument("--k", type=int, default=10)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--distributed", action="store_true", help="1-rank NCCL context (multi-rank path)")
     ap.add_argument("--interval", default=None, help="lo,hi instead of the Lanczos estimate (A/B of broken variants)")
     a = ap.parse_args()
     w = bench.make_workload(a.config, a.side)
     kind = a.kind or bench.op_kind(w, a.config)
-    ctx = npc.npc_context_create(0)
-    op = npc.create_from_workload(ctx, w, kind)
+    ctx = npc.npc_context_create(0, 1, 0, npc.npc_get_unique_id() if a.distributed else None)
+    op, _, _ = bench.create_operator(npc, ctx, w, kind, 1, 0, a.config)
     lo, hi = (map(float, a.interval.split(","))) if a.interval else npc.npc_estimate_spectrum(op, 20, None)
     poly = npc.npc_set_poly(op, a.k, lo, hi, 0.0)
     b = torch.tensor(w["b"], device="cuda")
