@@ -140,10 +140,20 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
+    # Started before the warm-up: nvidia-smi's NVML start-up stalls CUDA calls of this process
+    # for tens to hundreds of ms (measured), so it must not fall inside the timed region; only
+    # the samples that arrive between mark_begin() and mark_end() are summarised.
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
+
+    def mark_begin(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def start(self):
         try:
@@ -157,7 +167,7 @@ class ClockSampler:
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.time(), ln.strip()))
 
     def stop(self):
         if not self.proc:
@@ -169,7 +179,8 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for t, ln in self.lines if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+        for ln in inside or [ln for _, ln in self.lines[-3:]]:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 7:
                 continue
@@ -302,11 +313,12 @@ def run_ours(args):
         st["lmin"], st["lmax"] = lo, hi
         return st
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         st = step(b, x)
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark_begin()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = npc.npc_launch_count()
     if not args.no_kernel_timing:
@@ -314,9 +326,14 @@ def run_ours(args):
         npc.npc_context_get_timing(ctx)  # reset
     barrier()
     ev0.record(stream)
-    stats = [step(b, x) for _ in range(args.steps)]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stats = []
+    for i in range(args.steps):
+        stats.append(step(b, x))
+        evs[i].record(stream)
     ev1.record(stream)
     barrier()
+    clocks.mark_end()
     launches = npc.npc_launch_count() - launches0
     ktime = None
     if not args.no_kernel_timing:
@@ -324,6 +341,8 @@ def run_ours(args):
         npc.npc_context_set_timing(ctx, False)
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    step_ms = [round(ev0.elapsed_time(evs[0]), 3)] + [round(evs[i - 1].elapsed_time(evs[i]), 3)
+                                                      for i in range(1, args.steps)]
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -418,7 +437,7 @@ def run_ours(args):
         line = {
             "metric": METRIC,
             "value": round(gbs, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "ms_per_step": round(ms_step, 3), "step_ms": step_ms, "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads/, BASELINE.json config recipe)",
             "config": config_dict(cfg, w, kind, k, xi, M, V),

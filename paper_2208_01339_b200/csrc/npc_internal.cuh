@@ -56,6 +56,15 @@ extern std::atomic<unsigned long long> g_launches;
     } while (0)
 
 // ------------------------------------------------------------------ device buffers
+// Device memory pool (pool.cu): blocks of >= 1 MiB are rounded up to a size class (1/8
+// steps per power of two) and, when released, kept per device for reuse instead of being
+// unmapped -- cudaMalloc/cudaFree of the PCG work vectors and Lanczos bases cost ~1 ms per
+// solve on the bench configs.  A release first waits for the device (as cudaFree does), so a
+// block is never handed out while a kernel may still touch it.  The cache is bounded
+// (NPC_POOL_MB, default 16384) and flushed when cudaMalloc reports out-of-memory.
+cudaError_t pool_alloc(void **p, size_t bytes);
+void pool_free(void *p, size_t bytes);  // bytes as passed to pool_alloc
+
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
@@ -64,14 +73,14 @@ struct DevBuf {
     DevBuf &operator=(const DevBuf &) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) pool_free(p, bytes);
         p = nullptr;
         bytes = 0;
     }
     npc_status alloc(size_t nbytes) {
         release();
         if (nbytes == 0) nbytes = 16;
-        cudaError_t e = cudaMalloc(&p, nbytes);
+        cudaError_t e = pool_alloc(&p, nbytes);
         if (e != cudaSuccess) {
             p = nullptr;
             set_error("cudaMalloc(%zu) failed: %s", nbytes, cudaGetErrorString(e));

@@ -10,7 +10,7 @@ for raw in sys.stdin:
     line = json.loads(raw)
     rf = line.get("roofline") or {}
     pc = line.get("pcg") or {}
-    out = {k: line.get(k) for k in ("value", "ms_per_step", "parallelism")}
+    out = {k: line.get(k) for k in ("value", "ms_per_step", "step_ms", "parallelism", "clocks")}
     out.update(iters=pc.get("iters"), apps=pc.get("op_applications"), red=pc.get("reductions"), frac=rf.get("frac"))
     br = rf.get("step_breakdown") or {}
     if br:
