@@ -56,9 +56,8 @@ extern std::atomic<unsigned long long> g_launches;
     } while (0)
 
 // ------------------------------------------------------------------ device buffers
-// Device memory pool (pool.cu): blocks of >= 1 MiB are rounded up to a size class (1/8
-// steps per power of two) and, when released, kept per device for reuse instead of being
-// unmapped -- cudaMalloc/cudaFree of the PCG work vectors and Lanczos bases cost ~1 ms per
+// Device memory pool (pool.cu): blocks of >= 1 MiB are, when released, kept per device
+// (keyed by their exact size) for reuse instead of being unmapped -- cudaMalloc/cudaFree of the PCG work vectors and Lanczos bases cost ~1 ms per
 // solve on the bench configs.  A release first waits for the device (as cudaFree does), so a
 // block is never handed out while a kernel may still touch it.  The cache is bounded
 // (NPC_POOL_MB, default 16384) and flushed when cudaMalloc reports out-of-memory.

@@ -54,6 +54,14 @@ static constexpr int DFN_DENSE_MAX = 128;  // blocks up to this size use the exp
 #ifndef NPC_DFN_WARPS
 #define NPC_DFN_WARPS 8  // blocks (warps) per CTA of the dense kernel (A/B-tuned)
 #endif
+// NPC_DFN_MINB (A/B builds only): min resident CTAs per SM of the dense kernel.  Left unset
+// on purpose: ptxas then settles at 64 registers; an explicit 1 lets it take 108 and cost
+// 20 % (8.9 -> 10.7 ms per p_30 on config 6).
+#ifdef NPC_DFN_MINB
+#define NPC_DFN_LB(t) __launch_bounds__(t, NPC_DFN_MINB)
+#else
+#define NPC_DFN_LB(t) __launch_bounds__(t)
+#endif
 static constexpr int DFN_WARPS = NPC_DFN_WARPS;
 static constexpr int DFN_UNROLL = NPC_DFN_UNROLL;
 
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(256) k_dfn_block(DfnDev D, const int *__restri
 // its issue slots at __syncthreads; a bulk-TMA-staged variant cut residency to 12 warps/SM
 // and ran 2.3x slower).
 template <int RPL>
-__global__ void __launch_bounds__(32 * DFN_WARPS) k_dfn_dense(DfnDev D, const int4 *__restrict__ binfo, int nlist,
+__global__ void NPC_DFN_LB(32 * DFN_WARPS) k_dfn_dense(DfnDev D, const int4 *__restrict__ binfo, int nlist,
                                                    const double *__restrict__ Ainv, const double *__restrict__ x,
                                                    double *__restrict__ t_out, double *__restrict__ u2_out,
                                                    const int *done) {

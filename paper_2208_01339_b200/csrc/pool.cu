@@ -36,12 +36,9 @@ Pool &pool() {
     return *p;
 }
 
-size_t size_class(size_t n) {
-    if (n < POOL_MIN) return n;
-    int lg = 63 - __builtin_clzll((unsigned long long)n);
-    const size_t step = (size_t)1 << (lg - 3);
-    return (n + step - 1) / step * step;
-}
+// Exact sizes (to 256 B): the repeated solves this pool serves ask for the same sizes, and
+// nothing is wasted on rounding.
+size_t size_class(size_t n) { return n < POOL_MIN ? n : (n + 255) / 256 * 256; }
 
 }  // namespace
 

@@ -19,7 +19,9 @@ import sys, json, numpy as np, torch
 sys.path.insert(0, ROOT)
 import bench, paper_2208_01339_b200 as npc
 import os, pickle
-cache = f"/tmp/npc_ab_workload_{CFG}_{SIDE}.pkl"  # generated once per box, shared by the variants
+import hashlib
+_wh = hashlib.sha1(open(os.path.join(ROOT, "workloads", "__init__.py"), "rb").read()).hexdigest()[:12]
+cache = f"/tmp/npc_ab_workload_{CFG}_{SIDE}_{_wh}.pkl"  # per box and generator version, shared by the variants
 if os.path.exists(cache):
     w = pickle.load(open(cache, "rb"))
 else:
