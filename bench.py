@@ -372,7 +372,11 @@ def run_ours(args):
     e1.record(stream)
     barrier()
     t_apply = e0.elapsed_time(e1) / R  # ms per p_k(A) r (k launches)
-    apply_bytes = poly_bytes(M, V, k) / ws
+    # roofline numerator: the bytes the kernels stream in the library's stored format (a coded
+    # CSR streams 9 B per nonzero, not 12), this rank's share
+    Mf = npc.npc_operator_matrix_bytes(op)
+    Vf = 8 * nl
+    apply_bytes = poly_bytes(Mf, Vf, k)
     per_launch_ms = t_apply / max(k, 1)
     peak, peak_src = hbm_peak()
     ach_isolated = apply_bytes / max(k, 1) / (per_launch_ms * 1e-3) / 1e9
@@ -382,7 +386,7 @@ def run_ours(args):
         # the fused degree kernels as they ran inside the timed region (library CUDA events
         # on the launching stream): bytes of every degree launch / their summed device time
         n_deg = ktime["degree"][1]
-        deg_bytes = sum(s["iters"] for s in stats) * poly_bytes(M, V, k) / ws
+        deg_bytes = sum(s["iters"] for s in stats) * poly_bytes(Mf, Vf, k)
         ach = deg_bytes / (ktime["degree"][0] * 1e-3) / 1e9
         per_launch_ms = ktime["degree"][0] / n_deg
         in_step = {c: {"ms": round(v[0], 3), "launches": v[1], "share": round(v[0] / (ms_step * args.steps), 4)}
@@ -455,6 +459,9 @@ def run_ours(args):
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / peak, 4),
                          "frac_vs_8TBs_nominal": round(ach / 8000.0, 4), "traffic": traffic,
                          "bytes_per_launch": apply_bytes / max(k, 1), "launch_ms": round(per_launch_ms, 5),
+                         "bytes_basis": "operator data in the stored format (npc_operator_matrix_bytes: "
+                         f"{Mf / 1e6:.1f} MB per application) + the recurrence's vector streams; `value` uses the "
+                         f"format-independent SURVEY §8(d) bytes ({M / ws / 1e6:.1f} MB), the reference arm's basis",
                          "timed": "library CUDA events on the launching stream inside the timed region: one event "
                          "pair around each p_k(A) r application (its k fused degree launches, replayed in the PCG "
                          "CUDA graph as event-record nodes); achieved = algorithmic bytes of the degree steps / their "

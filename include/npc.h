@@ -175,10 +175,15 @@ typedef struct {
 } npc_operator_desc;
 
 /* Create an operator (COLLECTIVE when nranks > 1: builds the halo plan).  Validates the
- * CSR invariants (NPC_ERR_DIMENSION), uploads and converts (CSR -> tile metadata;
- * CSR -> sigma-sorted SELL-32; B -> D^{-1/2} B).                                            */
+ * CSR invariants (NPC_ERR_DIMENSION), uploads and converts (CSR -> tile metadata and, when
+ * every 256-row tile has <= 256 distinct column offsets, 1-byte dictionary codes for the
+ * column ids; CSR -> sigma-sorted SELL-32; B -> D^{-1/2} B).                                */
 NPC_API npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, npc_operator *out);
 NPC_API npc_status npc_destroy_operator(npc_operator op);
+/* Bytes of operator data one application streams in the format the library stored (e.g. a
+ * CSR operator: 8 B values + 1 B codes per nonzero + dictionaries + row pointers when coded,
+ * 12 B per nonzero + row pointers otherwise); the roofline numerator of the fused kernels. */
+NPC_API npc_status npc_operator_matrix_bytes(npc_operator op, double *bytes);
 /* y_dev = A x_dev (one application; halo exchange included).  */
 NPC_API npc_status npc_apply_operator(npc_operator op, const double *x_dev, double *y_dev);
 

@@ -82,6 +82,7 @@ def lib():
             "npc_get_unique_id": [P],
             "npc_create_operator": [P, C.POINTER(OperatorDesc), C.POINTER(P)],
             "npc_destroy_operator": [P],
+            "npc_operator_matrix_bytes": [P, C.POINTER(D)],
             "npc_apply_operator": [P, P, P],
             "npc_estimate_spectrum": [P, I, P, C.POINTER(D), C.POINTER(D)],
             "npc_estimate_spectrum_ex": [P, I, P, P],
@@ -271,6 +272,12 @@ def npc_create_operator(ctx: Context, kind, *, n_local, n_global=0, row_begin=0,
     h = C.c_void_p()
     _check(lib().npc_create_operator(ctx.h, C.byref(desc), C.byref(h)))
     return Operator(ctx, h, int(n_local), keep if apply is not None else [])
+
+
+def npc_operator_matrix_bytes(op: Operator) -> float:
+    b = C.c_double()
+    _check(lib().npc_operator_matrix_bytes(op.h, C.byref(b)))
+    return b.value
 
 
 def npc_apply_operator(op: Operator, x, y):

@@ -187,6 +187,12 @@ npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, n
     return NPC_SUCCESS;
 }
 
+npc_status npc_operator_matrix_bytes(npc_operator op, double *bytes) {
+    NPC_GUARD(op && bytes, NPC_ERR_INVALID_ARGUMENT, "npc_operator_matrix_bytes: null argument");
+    *bytes = op->op->matrix_bytes();
+    return NPC_SUCCESS;
+}
+
 npc_status npc_destroy_operator(npc_operator op) {
     if (!op) return NPC_SUCCESS;
     {

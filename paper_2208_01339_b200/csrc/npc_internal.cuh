@@ -121,6 +121,8 @@ class Operator {
     virtual int num_partials() const = 0;
     // Algorithmic bytes of one application + recurrence, for reporting.
     virtual double bytes_per_step(bool has_s2, bool has_r) const = 0;
+    // Operator-data part of it, in the stored format (bytes_per_step minus x read + out write).
+    virtual double matrix_bytes() const { return bytes_per_step(false, false) - 16.0 * n_local; }
     // Two consecutive degrees in one pass (temporal blocking, stencils): s1 produces s_j from
     // s_{j-1} = s1.x, s_{j-2} = s1.s2, r = s1.r into s1.out; s2 produces s_{j+1} into s2.out
     // (s2.x = s1.out, s2.s2 = s1.x implied) with the optional dot of s2.  Outputs must not

@@ -11,6 +11,12 @@
 // transactions; the x gather of a 7-point row touches 3 planes that stay in L2.
 // Multi-rank: columns outside the owned block are remapped to ghost slots; tiles that touch
 // a ghost run after the halo exchange, the others overlap it.
+//
+// Coded column ids (default when every tile qualifies): the kernel is HBM-bound and the int32
+// column ids are a third of the matrix bytes, so each tile keeps a dictionary of its distinct
+// offsets (col - row), at most 256, and every entry streams a 1-byte code instead of a 4-byte
+// id: 12 -> 9 B per nonzero (config 3: 2,008.5 -> 1,657 MB per degree).  Same values, same
+// summation order: bitwise the same result as the plain form (NPC_CSR_PLAIN=1).
 #include <algorithm>
 
 #include "device_util.cuh"
@@ -21,29 +27,35 @@ namespace npc {
 static constexpr int CSR_TILE = 256;
 static constexpr int CSR_MAX_SMEM = 200 * 1024;
 
+static constexpr int CSR_DICT_MAX = 256;
+
 struct CsrDev {
     const int *rowptr;
     const int *cols;  // local ids: [0, n) owned, [n, n + n_ghost) ghost slots
     const double *vals;
     int n;
     const double *ghost;
+    const unsigned char *codes;  // coded form: entry p's column = row + dict[dict_off[tile] + codes[p]]
+    const int *dict, *dict_off;
 };
 
-template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST>
+template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST, bool CODED>
 __global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, const int *__restrict__ tiles,
                                                        int vspan_max) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t bar;
     __shared__ double red[CSR_TILE / 32];
+    __shared__ int sdict[CODED ? CSR_DICT_MAX : 1];
 
     const int tile = tiles ? tiles[blockIdx.x] : blockIdx.x;
     const int row0 = tile * CSR_TILE;
     const int nrows = min(CSR_TILE, A.n - row0);
     const int pb = A.rowptr[row0];
     const int v0 = pb & ~1;
-    const int c0 = pb & ~3;
+    const int c0 = CODED ? (pb & ~15) : (pb & ~3);  // 16 B aligned bulk-copy start
     double *sv = reinterpret_cast<double *>(smem);
     int *sc = reinterpret_cast<int *>(smem + (size_t)vspan_max * 8);
+    const unsigned char *scb = smem + (size_t)vspan_max * 8;
 
     if (STAGED) {
         if (threadIdx.x == 0) {
@@ -53,13 +65,16 @@ __global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, con
         __syncthreads();
         if (threadIdx.x == 0) {
             const int pe = A.rowptr[row0 + nrows];
-            const int v1 = (pe + 1) & ~1, c1 = (pe + 3) & ~3;
-            const uint32_t bv = (uint32_t)(v1 - v0) * 8u, bc = (uint32_t)(c1 - c0) * 4u;
+            const int v1 = (pe + 1) & ~1, c1 = CODED ? ((pe + 15) & ~15) : ((pe + 3) & ~3);
+            const uint32_t bv = (uint32_t)(v1 - v0) * 8u, bc = (uint32_t)(c1 - c0) * (CODED ? 1u : 4u);
             mbar_arrive_expect_tx(&bar, bv + bc);
             if (bv) {
                 const uint64_t pol = policy_evict_first();
                 bulk_g2s_evict_first(sv, A.vals + v0, bv, &bar, pol);
-                bulk_g2s_evict_first(sc, A.cols + c0, bc, &bar, pol);
+                if (CODED)
+                    bulk_g2s_evict_first(smem + (size_t)vspan_max * 8, A.codes + c0, bc, &bar, pol);
+                else
+                    bulk_g2s_evict_first(sc, A.cols + c0, bc, &bar, pol);
             }
         }
     }
@@ -67,6 +82,10 @@ __global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, con
     const bool active = threadIdx.x < nrows;
     int rb = 0, re = 0;
     double xs = 0.0, s2v = 0.0, rv = 0.0;
+    if (CODED) {  // the tile's offset dictionary (<= 256 entries, coalesced)
+        const int d0 = A.dict_off[tile], dn = A.dict_off[tile + 1] - d0;
+        if ((int)threadIdx.x < dn) sdict[threadIdx.x] = A.dict[d0 + threadIdx.x];
+    }
     if (active) {
         rb = A.rowptr[row];
         re = A.rowptr[row + 1];
@@ -78,7 +97,8 @@ __global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, con
     // the row loads (checked first, it delayed every CTA's start: 1.7 % of the degree time)
     const bool is_done = s.done && *s.done;
     if (STAGED) mbar_wait(&bar, 0);  // never leave with a bulk copy into shared memory in flight
-    if (is_done) return;
+    if (is_done) return;             // uniform over the CTA
+    if (CODED) __syncthreads();      // dictionary visible
     double acc = 0.0;
     if (active) {
         double y = 0.0;
@@ -86,7 +106,10 @@ __global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, con
         for (int p = rb; p < re; ++p) {
             int c;
             double v;
-            if (STAGED) {
+            if (CODED) {
+                c = row + sdict[STAGED ? scb[p - c0] : __ldcs(A.codes + p)];
+                v = STAGED ? sv[p - v0] : __ldcs(A.vals + p);
+            } else if (STAGED) {
                 c = sc[p - c0];
                 v = sv[p - v0];
             } else {
@@ -115,6 +138,9 @@ __global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, con
 class CsrOperator : public Operator {
   public:
     DevBuf rowptr, cols, vals;
+    DevBuf codes, dict, dict_off;  // coded column ids (see the file comment)
+    bool coded = false;
+    long long dict_total = 0;
     DevBuf tiles_interior, tiles_boundary;
     int ntiles = 0, n_interior = 0, n_boundary = 0;
     int vspan_max = 0, cspan_max = 0;
@@ -128,22 +154,35 @@ class CsrOperator : public Operator {
     int num_partials() const override { return std::max(ntiles, 1); }
 
     double bytes_per_step(bool has_s2, bool has_r) const override {
-        // values + column ids + row pointers once, x once (perfect gather reuse), write out,
-        // read s_{j-2} and r when present.
-        double b = (double)nnz * 12.0 + (double)(n_local + 1) * 4.0 + 2.0 * 8.0 * n_local;
+        // values + column ids (or codes + dictionaries) + row pointers once, x once (perfect
+        // gather reuse), write out, read s_{j-2} and r when present.
+        double b = matrix_bytes() + 2.0 * 8.0 * n_local;
         if (has_s2) b += 8.0 * n_local;
         if (has_r) b += 8.0 * n_local;
         return b;
     }
 
+    double matrix_bytes() const override {
+        if (coded)
+            return (double)nnz * 9.0 + (double)dict_total * 4.0 + (double)(ntiles + 1) * 4.0 +
+                   (double)(n_local + 1) * 4.0;
+        return (double)nnz * 12.0 + (double)(n_local + 1) * 4.0;
+    }
+
     template <bool ST, bool H2, bool HR, bool DT, bool GH>
     npc_status launch_t(const StepArgs &s, const int *tl, int nt, double *partials) {
+        return coded ? launch_c<ST, H2, HR, DT, GH, true>(s, tl, nt, partials)
+                     : launch_c<ST, H2, HR, DT, GH, false>(s, tl, nt, partials);
+    }
+    template <bool ST, bool H2, bool HR, bool DT, bool GH, bool CD>
+    npc_status launch_c(const StepArgs &s, const int *tl, int nt, double *partials) {
         if (nt <= 0) return NPC_SUCCESS;
         CsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local,
-                 GH ? halo.ghost_buf.as<double>() : nullptr};
+                 GH ? halo.ghost_buf.as<double>() : nullptr, codes.as<unsigned char>(), dict.as<int>(),
+                 dict_off.as<int>()};
         StepArgs a = s;
         a.partials = partials;
-        auto kern = k_csr_step<ST, H2, HR, DT, GH>;
+        auto kern = k_csr_step<ST, H2, HR, DT, GH, CD>;
         size_t sm = ST ? smem_bytes : 0;
         if (sm > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
         kern<<<nt, CSR_TILE, sm, ctx->stream>>>(A, a, tl, vspan_max);
@@ -320,7 +359,43 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
         (ghost ? tb : ti).push_back(t);
     }
     op->vspan_max = (op->vspan_max + 1) & ~1;
-    op->smem_bytes = (size_t)op->vspan_max * 8 + (size_t)op->cspan_max * 4 + 16;
+    // coded column ids: per tile, the sorted distinct offsets col - row (<= 256) and a byte per entry
+    std::vector<std::vector<int>> tdict((size_t)op->ntiles);
+    std::vector<unsigned char> hcodes;
+    bool coded = !getenv("NPC_CSR_PLAIN") && nnz > 0;
+    if (coded) {
+        hcodes.assign((size_t)nnz + 16, 0);
+        std::vector<char> ok((size_t)op->ntiles, 1);
+        host_parallel_for(op->ntiles, [&](long long t0, long long t1, int) {
+            std::vector<int> offs;
+            for (long long t = t0; t < t1; ++t) {
+                const int r0 = (int)t * CSR_TILE, r1 = std::min(n, r0 + CSR_TILE);
+                offs.clear();
+                for (int r = r0; r < r1; ++r)
+                    for (int p = d->rowptr[r]; p < d->rowptr[r + 1]; ++p) offs.push_back(lcols[p] - r);
+                std::sort(offs.begin(), offs.end());
+                offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+                if ((int)offs.size() > CSR_DICT_MAX) {
+                    ok[t] = 0;
+                    continue;
+                }
+                for (int r = r0; r < r1; ++r)
+                    for (int p = d->rowptr[r]; p < d->rowptr[r + 1]; ++p)
+                        hcodes[p] = (unsigned char)(std::lower_bound(offs.begin(), offs.end(), lcols[p] - r) -
+                                                    offs.begin());
+                tdict[t] = offs;
+            }
+        });
+        for (char c : ok) coded = coded && c;
+    }
+    op->coded = coded;
+    int cbspan_max = 0;
+    if (coded)
+        for (int t = 0; t < op->ntiles; ++t) {
+            const int pb = d->rowptr[t * CSR_TILE], pe = d->rowptr[std::min(n, (t + 1) * CSR_TILE)];
+            cbspan_max = std::max(cbspan_max, ((pe + 15) & ~15) - (pb & ~15));
+        }
+    op->smem_bytes = (size_t)op->vspan_max * 8 + (coded ? (size_t)cbspan_max : (size_t)op->cspan_max * 4) + 16;
     op->staged = op->smem_bytes <= (size_t)CSR_MAX_SMEM;
     op->n_interior = (int)ti.size();
     op->n_boundary = (int)tb.size();
@@ -334,6 +409,20 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     if (nnz) {
         NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
         NPC_CUDA_TRY(cudaMemcpy(op->vals.p, d->vals, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    }
+    if (coded) {
+        std::vector<int> doff((size_t)op->ntiles + 1, 0), dall;
+        for (int t = 0; t < op->ntiles; ++t) doff[t + 1] = doff[t] + (int)tdict[t].size();
+        dall.reserve((size_t)doff[op->ntiles]);
+        for (auto &v : tdict) dall.insert(dall.end(), v.begin(), v.end());
+        op->dict_total = (long long)dall.size();
+        NPC_TRY(op->codes.alloc(hcodes.size()));
+        NPC_TRY(op->dict.alloc(sizeof(int) * std::max<size_t>(dall.size(), 1)));
+        NPC_TRY(op->dict_off.alloc(sizeof(int) * doff.size()));
+        NPC_CUDA_TRY(cudaMemcpy(op->codes.p, hcodes.data(), hcodes.size(), cudaMemcpyHostToDevice));
+        if (!dall.empty())
+            NPC_CUDA_TRY(cudaMemcpy(op->dict.p, dall.data(), sizeof(int) * dall.size(), cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op->dict_off.p, doff.data(), sizeof(int) * doff.size(), cudaMemcpyHostToDevice));
     }
     if (!op->multi && !plan_csr_poly_cluster(n, d->rowptr, op->small)) op->small = SmallCsrPlan{};
     if (op->multi) {

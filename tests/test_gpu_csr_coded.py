@@ -1,0 +1,105 @@
+"""GPU: the CSR operator's coded column ids (op_csr.cu: per-tile dictionary of column offsets,
+one byte per nonzero) against the plain int32 form and the oracle, through the C ABI.
+
+The coded form changes only how column ids are stored: same values, same per-row summation
+order, so every result must be BITWISE equal to the plain form (NPC_CSR_PLAIN=1).  Matrices
+whose tiles have more than 256 distinct offsets (unstructured kNN in natural order) fall back
+to the plain form; npc_operator_matrix_bytes tells which form was stored.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2208_01339_b200 as npc  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = npc.npc_context_create(0)
+    yield c
+    torch.cuda.synchronize()
+
+
+def dev(a):
+    return torch.tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")
+
+
+def make(ctx, w, plain):
+    if plain:
+        os.environ["NPC_CSR_PLAIN"] = "1"
+    try:
+        return npc.create_from_workload(ctx, w, "csr")
+    finally:
+        os.environ.pop("NPC_CSR_PLAIN", None)
+
+
+WL = {"c3": lambda: W.config3(side=30), "c1": lambda: W.config1(side=64),
+      "c3_ragged": lambda: W.config3(side=23)}  # 12,167 rows: a ragged last tile
+
+
+@pytest.mark.parametrize("name", list(WL))
+def test_coded_bitwise_equals_plain(ctx, name):
+    w = WL[name]()
+    n, nnz = w["n"], int(w["rowptr"][-1])
+    opc, opp = make(ctx, w, False), make(ctx, w, True)
+    mb_c, mb_p = npc.npc_operator_matrix_bytes(opc), npc.npc_operator_matrix_bytes(opp)
+    assert mb_p == 12 * nnz + 4 * (n + 1)
+    assert mb_c < 9.5 * nnz + 4 * (n + 1), (mb_c, nnz)  # coded: 9 B/nnz + small dictionaries
+    x = np.random.default_rng(1).standard_normal(n)
+    yc = torch.empty(n, dtype=torch.float64, device="cuda")
+    yp = torch.empty_like(yc)
+    npc.npc_apply_operator(opc, dev(x), yc)
+    npc.npc_apply_operator(opp, dev(x), yp)
+    assert torch.equal(yc, yp)
+    orc = oracle.Operator(w)
+    assert np.linalg.norm(yc.cpu().numpy() - orc.apply(x)) <= 1e-13 * np.linalg.norm(orc.apply(x))
+    lo, hi = oracle.estimate_spectrum(orc, 20, W.lanczos_start(n))
+    r = np.random.default_rng(2).uniform(-1, 1, n)
+    zc, zp = torch.empty_like(yc), torch.empty_like(yc)
+    os.environ["NPC_NO_CLUSTER"] = "1"  # config 1 would otherwise take the cluster-resident kernel
+    try:
+        pc, pp = npc.npc_set_poly(opc, 17, lo, hi, 1e-3), npc.npc_set_poly(opp, 17, lo, hi, 1e-3)
+        npc.npc_apply_poly(pc, dev(r), zc)
+        npc.npc_apply_poly(pp, dev(r), zp)
+    finally:
+        os.environ.pop("NPC_NO_CLUSTER", None)
+    assert torch.equal(zc, zp)
+    ref = oracle.cheb_apply(orc, 17, lo, hi, 1e-3, r)
+    assert np.linalg.norm(zc.cpu().numpy() - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_unstructured_falls_back_to_plain(ctx):
+    w = W.config4(n=12_000)  # kNN rows: thousands of distinct offsets per 256-row tile
+    n, nnz = w["n"], int(w["rowptr"][-1])
+    op = npc.create_from_workload(ctx, w, "csr")
+    assert npc.npc_operator_matrix_bytes(op) == 12 * nnz + 4 * (n + 1)
+    x = np.random.default_rng(3).standard_normal(n)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    npc.npc_apply_operator(op, dev(x), y)
+    ref = oracle.Operator(w).apply(x)
+    assert np.linalg.norm(y.cpu().numpy() - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_coded_pcg_matches_plain(ctx):
+    """Whole PCG (graph-captured degree kernels) on the coded form: the same iterates."""
+    w = W.config3(side=20)
+    n = w["n"]
+    res = []
+    for plain in (False, True):
+        op = make(ctx, w, plain)
+        lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+        poly = npc.npc_set_poly(op, 20, lo, hi, 0.0)
+        x = torch.zeros(n, dtype=torch.float64, device="cuda")
+        st = npc.npc_pcg_solve(poly, op, dev(w["b"]), x, w["tol"], 5000)
+        res.append((st["iters"], x))
+    assert res[0][0] == res[1][0] and torch.equal(res[0][1], res[1][1])
