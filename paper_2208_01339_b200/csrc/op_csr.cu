@@ -24,7 +24,10 @@
 
 namespace npc {
 
-static constexpr int CSR_TILE = 256;
+// Rows (= threads) per CTA, A/B-tuned on config 3 (p_50): plain 256 (15.21 ms; 512: 15.54),
+// coded 512 (13.24 ms; 256: 13.60, 128: 13.69, 1024: 13.81) -- a coded tile carries 25 % fewer
+// bytes, so it takes twice the rows to keep as much of the stream in flight per SM.
+static constexpr int CSR_TILE = 256, CSR_TILE_CODED = 512;
 static constexpr int CSR_MAX_SMEM = 200 * 1024;
 
 static constexpr int CSR_DICT_MAX = 256;
@@ -39,17 +42,18 @@ struct CsrDev {
     const int *dict, *dict_off;
 };
 
-template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST, bool CODED>
-__global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, const int *__restrict__ tiles,
-                                                       int vspan_max) {
+template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST, bool CODED,
+          int TILE = CODED ? CSR_TILE_CODED : CSR_TILE>
+__global__ void __launch_bounds__(TILE) k_csr_step(CsrDev A, StepArgs s, const int *__restrict__ tiles,
+                                                   int vspan_max) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t bar;
-    __shared__ double red[CSR_TILE / 32];
+    __shared__ double red[TILE / 32];
     __shared__ int sdict[CODED ? CSR_DICT_MAX : 1];
 
     const int tile = tiles ? tiles[blockIdx.x] : blockIdx.x;
-    const int row0 = tile * CSR_TILE;
-    const int nrows = min(CSR_TILE, A.n - row0);
+    const int row0 = tile * TILE;
+    const int nrows = min(TILE, A.n - row0);
     const int pb = A.rowptr[row0];
     const int v0 = pb & ~1;
     const int c0 = CODED ? (pb & ~15) : (pb & ~3);  // 16 B aligned bulk-copy start
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(CSR_TILE) k_csr_step(CsrDev A, StepArgs s, con
         if (DOT) acc = o * s.dotv[row];
     }
     if (DOT) {
-        acc = block_sum<CSR_TILE>(acc, red);
+        acc = block_sum<TILE>(acc, red);
         if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
     }
 }
@@ -185,7 +189,7 @@ class CsrOperator : public Operator {
         auto kern = k_csr_step<ST, H2, HR, DT, GH, CD>;
         size_t sm = ST ? smem_bytes : 0;
         if (sm > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
-        kern<<<nt, CSR_TILE, sm, ctx->stream>>>(A, a, tl, vspan_max);
+        kern<<<nt, CD ? CSR_TILE_CODED : CSR_TILE, sm, ctx->stream>>>(A, a, tl, vspan_max);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
@@ -345,31 +349,19 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     std::vector<int> lcols;
     NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
     op->multi = ctx->distributed();
-    // tiles, spans, interior/boundary split
-    op->ntiles = ceil_div(n, CSR_TILE);
-    std::vector<int> ti, tb;
-    for (int t = 0; t < op->ntiles; ++t) {
-        int r0 = t * CSR_TILE, r1 = std::min(n, r0 + CSR_TILE);
-        int pb = d->rowptr[r0], pe = d->rowptr[r1];
-        op->vspan_max = std::max(op->vspan_max, ((pe + 1) & ~1) - (pb & ~1));
-        op->cspan_max = std::max(op->cspan_max, ((pe + 3) & ~3) - (pb & ~3));
-        bool ghost = false;
-        if (op->multi)
-            for (int p = pb; p < pe && !ghost; ++p) ghost = lcols[p] >= n;
-        (ghost ? tb : ti).push_back(t);
-    }
-    op->vspan_max = (op->vspan_max + 1) & ~1;
-    // coded column ids: per tile, the sorted distinct offsets col - row (<= 256) and a byte per entry
-    std::vector<std::vector<int>> tdict((size_t)op->ntiles);
+    // coded column ids: per tile of CSR_TILE_CODED rows, the sorted distinct offsets col - row
+    // (<= 256) and a byte per entry; any tile with more -> the plain form on CSR_TILE rows
+    const int ntc = ceil_div(n, CSR_TILE_CODED);
+    std::vector<std::vector<int>> tdict((size_t)ntc);
     std::vector<unsigned char> hcodes;
     bool coded = !getenv("NPC_CSR_PLAIN") && nnz > 0;
     if (coded) {
         hcodes.assign((size_t)nnz + 16, 0);
-        std::vector<char> ok((size_t)op->ntiles, 1);
-        host_parallel_for(op->ntiles, [&](long long t0, long long t1, int) {
+        std::vector<char> ok((size_t)ntc, 1);
+        host_parallel_for(ntc, [&](long long t0, long long t1, int) {
             std::vector<int> offs;
             for (long long t = t0; t < t1; ++t) {
-                const int r0 = (int)t * CSR_TILE, r1 = std::min(n, r0 + CSR_TILE);
+                const int r0 = (int)t * CSR_TILE_CODED, r1 = std::min(n, r0 + CSR_TILE_CODED);
                 offs.clear();
                 for (int r = r0; r < r1; ++r)
                     for (int p = d->rowptr[r]; p < d->rowptr[r + 1]; ++p) offs.push_back(lcols[p] - r);
@@ -389,10 +381,25 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
         for (char c : ok) coded = coded && c;
     }
     op->coded = coded;
+    const int TILE = coded ? CSR_TILE_CODED : CSR_TILE;
+    // tiles, spans, interior/boundary split
+    op->ntiles = ceil_div(n, TILE);
+    std::vector<int> ti, tb;
+    for (int t = 0; t < op->ntiles; ++t) {
+        int r0 = t * TILE, r1 = std::min(n, r0 + TILE);
+        int pb = d->rowptr[r0], pe = d->rowptr[r1];
+        op->vspan_max = std::max(op->vspan_max, ((pe + 1) & ~1) - (pb & ~1));
+        op->cspan_max = std::max(op->cspan_max, ((pe + 3) & ~3) - (pb & ~3));
+        bool ghost = false;
+        if (op->multi)
+            for (int p = pb; p < pe && !ghost; ++p) ghost = lcols[p] >= n;
+        (ghost ? tb : ti).push_back(t);
+    }
+    op->vspan_max = (op->vspan_max + 1) & ~1;
     int cbspan_max = 0;
     if (coded)
         for (int t = 0; t < op->ntiles; ++t) {
-            const int pb = d->rowptr[t * CSR_TILE], pe = d->rowptr[std::min(n, (t + 1) * CSR_TILE)];
+            const int pb = d->rowptr[t * TILE], pe = d->rowptr[std::min(n, (t + 1) * TILE)];
             cbspan_max = std::max(cbspan_max, ((pe + 15) & ~15) - (pb & ~15));
         }
     op->smem_bytes = (size_t)op->vspan_max * 8 + (coded ? (size_t)cbspan_max : (size_t)op->cspan_max * 4) + 16;
