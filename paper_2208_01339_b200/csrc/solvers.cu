@@ -899,10 +899,17 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     if (cache.exec && cache.timed != ctx->timing) cache.invalidate();
     GraphRun gr(ctx, cache);
     const bool graph_ok = op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH");
-    // Distributed: capturing the NCCL calls costs milliseconds per new graph (measured 16 ms
-    // for a DFN block of 4 iterations), so a solve without a cached graph runs its first chunk
-    // eagerly and captures only if it needs a second one.
-    bool deferred = graph_ok && h.multi && !cache.exec;
+    // A new graph costs capture + instantiation: milliseconds with NCCL calls in it (16 ms for a
+    // DFN block of 4 iterations on a 1-rank communicator) and ~0.1 ms per degree launch for high
+    // degrees (config 5, k = 200: ~140 ms for a 1-iteration solve).  So a distributed or k >= 32
+    // solve without a cached graph runs its first chunk eagerly -- its kernels are long enough
+    // to hide the launches -- and captures only if it needs a second chunk.  (Low degrees
+    // capture at once: eager 4-iteration chunks measured slower on configs 2 and 6, k = 30.)
+    bool deferred = graph_ok && !cache.exec && (h.multi || k >= 32);
+    // ... and that eager chunk is ONE iteration: a solve that converges at once (config 5) then
+    // stops there -- in a 4-iteration block the no-op iterations still launch every kernel, and
+    // the bulk-copy kernels issue their tile loads before they read the done flag
+    if (deferred) chunk = 1;
     if (graph_ok && !deferred) {
         iter_calls = 0;
         NPC_TRY(gr.capture(iteration));

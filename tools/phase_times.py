@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--distributed", action="store_true", help="1-rank NCCL context (multi-rank path)")
     ap.add_argument("--reuse-poly", action="store_true", help="one poly for all reps (PCG graph cached)")
+    ap.add_argument("--k", type=int, default=None)
     a = ap.parse_args()
     w = bench.make_workload(a.config, a.side)
     kind = bench.op_kind(w, a.config)
@@ -38,7 +39,7 @@ def main():
         lo, hi = npc.npc_estimate_spectrum(op, 20, None)
         t1 = time.perf_counter()
         if poly is None or not a.reuse_poly:
-            poly = npc.npc_set_poly(op, w["k"], lo, hi, 0.0)
+            poly = npc.npc_set_poly(op, a.k or w["k"], lo, hi, 0.0)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         x.zero_()
