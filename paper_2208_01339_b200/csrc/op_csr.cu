@@ -40,6 +40,8 @@ struct CsrDev {
     const double *ghost;
     const unsigned char *codes;  // coded form: entry p's column = row + dict[dict_off[tile] + codes[p]]
     const int *dict, *dict_off;
+    const int *tptr;              // coded form: first entry of each tile (ntiles + 1)
+    const unsigned short *roff;   // coded form: row start relative to its tile's first entry
 };
 
 template <bool STAGED, bool HAS_S2, bool HAS_R, bool DOT, bool GHOST, bool CODED,
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(TILE) k_csr_step(CsrDev A, StepArgs s, const i
     const int tile = tiles ? tiles[blockIdx.x] : blockIdx.x;
     const int row0 = tile * TILE;
     const int nrows = min(TILE, A.n - row0);
-    const int pb = A.rowptr[row0];
+    const int pb = CODED ? A.tptr[tile] : A.rowptr[row0];
     const int v0 = pb & ~1;
     const int c0 = CODED ? (pb & ~15) : (pb & ~3);  // 16 B aligned bulk-copy start
     double *sv = reinterpret_cast<double *>(smem);
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(TILE) k_csr_step(CsrDev A, StepArgs s, const i
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            const int pe = A.rowptr[row0 + nrows];
+            const int pe = CODED ? A.tptr[tile + 1] : A.rowptr[row0 + nrows];
             const int v1 = (pe + 1) & ~1, c1 = CODED ? ((pe + 15) & ~15) : ((pe + 3) & ~3);
             const uint32_t bv = (uint32_t)(v1 - v0) * 8u, bc = (uint32_t)(c1 - c0) * (CODED ? 1u : 4u);
             mbar_arrive_expect_tx(&bar, bv + bc);
@@ -91,8 +93,13 @@ __global__ void __launch_bounds__(TILE) k_csr_step(CsrDev A, StepArgs s, const i
         if ((int)threadIdx.x < dn) sdict[threadIdx.x] = A.dict[d0 + threadIdx.x];
     }
     if (active) {
-        rb = A.rowptr[row];
-        re = A.rowptr[row + 1];
+        if (CODED) {  // 2 B per row instead of 4
+            rb = pb + A.roff[row];
+            re = (int)threadIdx.x + 1 < nrows ? pb + A.roff[row + 1] : A.tptr[tile + 1];
+        } else {
+            rb = A.rowptr[row];
+            re = A.rowptr[row + 1];
+        }
         xs = s.x[row];
         if (HAS_S2) s2v = s.s2[row];
         if (HAS_R) rv = s.r[row];
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(TILE) k_csr_step(CsrDev A, StepArgs s, const i
 class CsrOperator : public Operator {
   public:
     DevBuf rowptr, cols, vals;
-    DevBuf codes, dict, dict_off;  // coded column ids (see the file comment)
+    DevBuf codes, dict, dict_off, tptr, roff;  // coded form (see the file comment)
     bool coded = false;
     long long dict_total = 0;
     DevBuf tiles_interior, tiles_boundary;
@@ -167,9 +174,9 @@ class CsrOperator : public Operator {
     }
 
     double matrix_bytes() const override {
-        if (coded)
-            return (double)nnz * 9.0 + (double)dict_total * 4.0 + (double)(ntiles + 1) * 4.0 +
-                   (double)(n_local + 1) * 4.0;
+        if (coded)  // values + codes, dictionaries + their offsets, tile pointers, 16-bit row offsets
+            return (double)nnz * 9.0 + (double)dict_total * 4.0 + (double)(ntiles + 1) * 8.0 +
+                   (double)n_local * 2.0;
         return (double)nnz * 12.0 + (double)(n_local + 1) * 4.0;
     }
 
@@ -183,7 +190,7 @@ class CsrOperator : public Operator {
         if (nt <= 0) return NPC_SUCCESS;
         CsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local,
                  GH ? halo.ghost_buf.as<double>() : nullptr, codes.as<unsigned char>(), dict.as<int>(),
-                 dict_off.as<int>()};
+                 dict_off.as<int>(), tptr.as<int>(), roff.as<unsigned short>()};
         StepArgs a = s;
         a.partials = partials;
         auto kern = k_csr_step<ST, H2, HR, DT, GH, CD>;
@@ -362,6 +369,10 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
             std::vector<int> offs;
             for (long long t = t0; t < t1; ++t) {
                 const int r0 = (int)t * CSR_TILE_CODED, r1 = std::min(n, r0 + CSR_TILE_CODED);
+                if (d->rowptr[r1] - d->rowptr[r0] > 65535) {  // 16-bit row offsets
+                    ok[t] = 0;
+                    continue;
+                }
                 offs.clear();
                 for (int r = r0; r < r1; ++r)
                     for (int p = d->rowptr[r]; p < d->rowptr[r + 1]; ++p) offs.push_back(lcols[p] - r);
@@ -430,6 +441,14 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
         if (!dall.empty())
             NPC_CUDA_TRY(cudaMemcpy(op->dict.p, dall.data(), sizeof(int) * dall.size(), cudaMemcpyHostToDevice));
         NPC_CUDA_TRY(cudaMemcpy(op->dict_off.p, doff.data(), sizeof(int) * doff.size(), cudaMemcpyHostToDevice));
+        std::vector<int> tp((size_t)op->ntiles + 1);
+        std::vector<unsigned short> ro((size_t)std::max(n, 1));
+        for (int t = 0; t <= op->ntiles; ++t) tp[t] = d->rowptr[std::min(n, t * CSR_TILE_CODED)];
+        for (int r = 0; r < n; ++r) ro[r] = (unsigned short)(d->rowptr[r] - tp[r / CSR_TILE_CODED]);
+        NPC_TRY(op->tptr.alloc(sizeof(int) * tp.size()));
+        NPC_TRY(op->roff.alloc(sizeof(unsigned short) * ro.size()));
+        NPC_CUDA_TRY(cudaMemcpy(op->tptr.p, tp.data(), sizeof(int) * tp.size(), cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op->roff.p, ro.data(), sizeof(unsigned short) * ro.size(), cudaMemcpyHostToDevice));
     }
     if (!op->multi && !plan_csr_poly_cluster(n, d->rowptr, op->small)) op->small = SmallCsrPlan{};
     if (op->multi) {
