@@ -366,27 +366,40 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
         hcodes.assign((size_t)nnz + 16, 0);
         std::vector<char> ok((size_t)ntc, 1);
         host_parallel_for(ntc, [&](long long t0, long long t1, int) {
-            std::vector<int> offs;
+            // offset -> code by a small open-addressing table (codes in first-seen order; the
+            // kernel only indexes the dictionary, so it needs no particular order)
+            constexpr int HB = 10, HS = 1 << HB;  // 1,024 slots >= 4 x CSR_DICT_MAX
+            std::vector<int> key(HS), val(HS);
+            std::vector<long long> stamp(HS, -1);
             for (long long t = t0; t < t1; ++t) {
                 const int r0 = (int)t * CSR_TILE_CODED, r1 = std::min(n, r0 + CSR_TILE_CODED);
                 if (d->rowptr[r1] - d->rowptr[r0] > 65535) {  // 16-bit row offsets
                     ok[t] = 0;
                     continue;
                 }
-                offs.clear();
-                for (int r = r0; r < r1; ++r)
-                    for (int p = d->rowptr[r]; p < d->rowptr[r + 1]; ++p) offs.push_back(lcols[p] - r);
-                std::sort(offs.begin(), offs.end());
-                offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
-                if ((int)offs.size() > CSR_DICT_MAX) {
+                std::vector<int> &offs = tdict[t];
+                bool fits = true;
+                for (int r = r0; r < r1 && fits; ++r)
+                    for (int p = d->rowptr[r]; p < d->rowptr[r + 1]; ++p) {
+                        const int o = lcols[p] - r;
+                        unsigned h = ((unsigned)o * 2654435761u) >> (32 - HB);
+                        while (stamp[h] == t && key[h] != o) h = (h + 1) & (HS - 1);
+                        if (stamp[h] != t) {
+                            if ((int)offs.size() == CSR_DICT_MAX) {
+                                fits = false;
+                                break;
+                            }
+                            stamp[h] = t;
+                            key[h] = o;
+                            val[h] = (int)offs.size();
+                            offs.push_back(o);
+                        }
+                        hcodes[p] = (unsigned char)val[h];
+                    }
+                if (!fits) {
                     ok[t] = 0;
-                    continue;
+                    offs.clear();
                 }
-                for (int r = r0; r < r1; ++r)
-                    for (int p = d->rowptr[r]; p < d->rowptr[r + 1]; ++p)
-                        hcodes[p] = (unsigned char)(std::lower_bound(offs.begin(), offs.end(), lcols[p] - r) -
-                                                    offs.begin());
-                tdict[t] = offs;
             }
         });
         for (char c : ok) coded = coded && c;
@@ -417,17 +430,19 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     op->staged = op->smem_bytes <= (size_t)CSR_MAX_SMEM;
     op->n_interior = (int)ti.size();
     op->n_boundary = (int)tb.size();
-    // upload (arrays padded so the aligned bulk copies never read past the allocation)
+    if (!op->multi && !plan_csr_poly_cluster(n, d->rowptr, op->small)) op->small = SmallCsrPlan{};
+    // upload (arrays padded so the aligned bulk copies never read past the allocation); the
+    // int32 column ids only where a kernel reads them (plain form, cluster-resident kernels)
+    const bool need_cols = !coded || op->small.cl_size > 0;
+    const long long ncols = need_cols ? nnz : 0;
     NPC_TRY(op->rowptr.alloc(sizeof(int) * (n + 1)));
-    NPC_TRY(op->cols.alloc(sizeof(int) * (nnz + 8)));
+    NPC_TRY(op->cols.alloc(sizeof(int) * (ncols + 8)));
     NPC_TRY(op->vals.alloc(sizeof(double) * (nnz + 8)));
     NPC_CUDA_TRY(cudaMemcpy(op->rowptr.p, d->rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-    NPC_CUDA_TRY(cudaMemset(op->cols.p, 0, op->cols.bytes));
-    NPC_CUDA_TRY(cudaMemset(op->vals.p, 0, op->vals.bytes));
-    if (nnz) {
-        NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-        NPC_CUDA_TRY(cudaMemcpy(op->vals.p, d->vals, sizeof(double) * nnz, cudaMemcpyHostToDevice));
-    }
+    NPC_CUDA_TRY(cudaMemset(op->cols.as<int>() + ncols, 0, sizeof(int) * 8));
+    NPC_CUDA_TRY(cudaMemset(op->vals.as<double>() + nnz, 0, sizeof(double) * 8));
+    if (ncols) NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice));
+    if (nnz) NPC_CUDA_TRY(cudaMemcpy(op->vals.p, d->vals, sizeof(double) * nnz, cudaMemcpyHostToDevice));
     if (coded) {
         std::vector<int> doff((size_t)op->ntiles + 1, 0), dall;
         for (int t = 0; t < op->ntiles; ++t) doff[t + 1] = doff[t] + (int)tdict[t].size();
@@ -450,7 +465,6 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
         NPC_CUDA_TRY(cudaMemcpy(op->tptr.p, tp.data(), sizeof(int) * tp.size(), cudaMemcpyHostToDevice));
         NPC_CUDA_TRY(cudaMemcpy(op->roff.p, ro.data(), sizeof(unsigned short) * ro.size(), cudaMemcpyHostToDevice));
     }
-    if (!op->multi && !plan_csr_poly_cluster(n, d->rowptr, op->small)) op->small = SmallCsrPlan{};
     if (op->multi) {
         NPC_TRY(op->tiles_interior.alloc(sizeof(int) * std::max<size_t>(ti.size(), 1)));
         NPC_TRY(op->tiles_boundary.alloc(sizeof(int) * std::max<size_t>(tb.size(), 1)));
