@@ -103,3 +103,59 @@ def test_coded_pcg_matches_plain(ctx):
         st = npc.npc_pcg_solve(poly, op, dev(w["b"]), x, w["tol"], 5000)
         res.append((st["iters"], x))
     assert res[0][0] == res[1][0] and torch.equal(res[0][1], res[1][1])
+
+
+def banded_spd(n, hb, seed):
+    """SPD band matrix, half-bandwidth hb (2 hb + 1 entries per interior row), diagonally
+    dominant: a coded matrix whose 512-row tiles exceed the staged kernel's shared memory."""
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    off = {}
+    for i in range(n):
+        for j in range(max(0, i - hb), min(n, i + hb + 1)):
+            if j < i:
+                v = off[(j, i)]
+            elif j > i:
+                v = off[(i, j)] = -rng.uniform(0.1, 1.0)
+            else:
+                continue
+            rows.append(i), cols.append(j), vals.append(v)
+    A = np.zeros((n, n))
+    A[rows, cols] = vals
+    A[np.arange(n), np.arange(n)] = -A.sum(axis=1) + 1.0
+    rp = np.zeros(n + 1, dtype=np.int64)
+    nz = A != 0
+    rp[1:] = np.cumsum(nz.sum(axis=1))
+    ci = np.nonzero(nz)[1].astype(np.int32)
+    return dict(kind="csr", n=n, rowptr=rp.astype(np.int32), colidx=ci, vals=A[nz].astype(np.float64))
+
+
+def test_coded_unstaged_tiles(ctx):
+    """Tiles of 512 rows x 121 entries (62K entries, ~550 KB) take the coded kernel's
+    non-staged form (codes and values read straight from HBM); bitwise equal to plain."""
+    w = banded_spd(3000, 60, seed=4)
+    n, nnz = w["n"], int(w["rowptr"][-1])
+    opc, opp = make(ctx, w, False), make(ctx, w, True)
+    assert npc.npc_operator_matrix_bytes(opc) < npc.npc_operator_matrix_bytes(opp)  # coded
+    x = np.random.default_rng(5).standard_normal(n)
+    yc = torch.empty(n, dtype=torch.float64, device="cuda")
+    yp = torch.empty_like(yc)
+    os.environ["NPC_NO_CLUSTER"] = "1"
+    try:
+        npc.npc_apply_operator(opc, dev(x), yc)
+        npc.npc_apply_operator(opp, dev(x), yp)
+        assert torch.equal(yc, yp)
+        orc = oracle.Operator(w)
+        ref = orc.apply(x)
+        assert np.linalg.norm(yc.cpu().numpy() - ref) <= 1e-13 * np.linalg.norm(ref)
+        lo, hi = oracle.estimate_spectrum(orc, 20, W.lanczos_start(n))
+        r = np.random.default_rng(6).uniform(-1, 1, n)
+        zc, zp = torch.empty_like(yc), torch.empty_like(yc)
+        npc.npc_apply_poly(npc.npc_set_poly(opc, 9, lo, hi, 0.0), dev(r), zc)
+        npc.npc_apply_poly(npc.npc_set_poly(opp, 9, lo, hi, 0.0), dev(r), zp)
+        assert torch.equal(zc, zp)
+        refz = oracle.cheb_apply(orc, 9, lo, hi, 0.0, r)
+        assert np.linalg.norm(zc.cpu().numpy() - refz) <= 1e-10 * np.linalg.norm(refz)
+    finally:
+        os.environ.pop("NPC_NO_CLUSTER", None)
+    assert nnz > 512 * 100
