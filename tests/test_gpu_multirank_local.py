@@ -138,13 +138,22 @@ def check_case(wl, name, kind, ws, runner):
         xs = torch.zeros_like(y)
         st = npc.npc_pcg_solve(p2, op, dev(w["b"]), xs, w["tol"], 5000)
         stream.synchronize()
-        return dict(r0=r0, r1=r1, y=y.cpu().numpy(), z=z.cpu().numpy(), lo=lo, hi=hi, st=st, x=xs.cpu().numpy())
+        mb = npc.npc_operator_matrix_bytes(op)
+        return dict(r0=r0, r1=r1, y=y.cpu().numpy(), z=z.cpu().numpy(), lo=lo, hi=hi, st=st, x=xs.cpu().numpy(),
+                    mb=mb)
 
     res = runner(ws, fn)
     y = np.concatenate([q["y"] for q in res])
     z = np.concatenate([q["z"] for q in res])
     xs = np.concatenate([q["x"] for q in res])
     assert [q["r0"] for q in res] == sorted(q["r0"] for q in res) and res[-1]["r1"] == n
+    if kind == "csr" and name == "c3":
+        # z-slab ghosts have one offset per neighbour plane: the coded form (9 B/nnz) holds
+        # across ranks too, boundary tiles included
+        rp = w["rowptr"]
+        for q in res:
+            nnz = int(rp[q["r1"]] - rp[q["r0"]])
+            assert q["mb"] < 9.5 * nnz + 4 * (q["r1"] - q["r0"] + 1), (q["mb"], nnz)
     # Schur: fp64 atomics + a reduce-scatter; DFN: explicit block inverses vs the oracle's
     # triangular solves -- summation order only
     assert np.linalg.norm(y - ref_apply) <= (1e-12 if kind in ("schur", "dfn") else 1e-13) * np.linalg.norm(ref_apply)
