@@ -240,6 +240,7 @@ class StencilOperator : public Operator {
     int dim = 3, nx = 0, ny = 0, nzg = 1, zb = 0, nzl = 1;
     double diag = 0, off = 0;
     bool multi = false, has_lo = false, has_hi = false;
+    int zc_main = ST_ZC;  // z-planes marched per CTA (NPC_ST_ZC for A/B)
     HaloPlan plan;
     HaloRuntime halo;
 
@@ -261,13 +262,13 @@ class StencilOperator : public Operator {
         if (nzl <= 0) return 0;
         int n = 0;
         const int lo_i = has_lo ? 1 : 0, hi_i = std::max(lo_i, has_hi ? nzl - 1 : nzl);
-        if (hi_i > lo_i) o[n++] = {lo_i, hi_i, ST_ZC, false};
+        if (hi_i > lo_i) o[n++] = {lo_i, hi_i, zc_main, false};
         if (lo_i == 1) o[n++] = {0, 1, 1, true};
         if (hi_i < nzl) o[n++] = {hi_i, nzl, 1, true};
         return n;
     }
     int num_partials() const override {
-        if (!multi) return blocks_for(nzl, ST_ZC);
+        if (!multi) return blocks_for(nzl, zc_main);
         Seg sg[3];
         const int ns = segments(sg);
         int tot = 0;
@@ -357,7 +358,7 @@ class StencilOperator : public Operator {
 
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
-        if (!multi) return launch(s, 0, nzl, ST_ZC, s.partials);
+        if (!multi) return launch(s, 0, nzl, zc_main, s.partials);
         Seg sg[3];
         const int ns = segments(sg);
         double *p = s.partials;
@@ -402,6 +403,7 @@ npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::
     op->nzl = d->stencil_dim == 3 ? d->nz_local : 1;
     op->diag = d->diag;
     op->off = d->offdiag;
+    if (const char *e = getenv("NPC_ST_ZC")) op->zc_main = std::max(1, atoi(e));
     const long long plane = (long long)op->nx * op->ny;
     if (plane * op->nzl >= (1LL << 31)) {
         set_error("stencil: more than 2^31 local rows");
