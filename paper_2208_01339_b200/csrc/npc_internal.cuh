@@ -214,6 +214,7 @@ struct Context {
     cudaStream_t comm_stream = nullptr;  // halo traffic (distributed contexts)
     bool own_stream = false;
     cudaStream_t graph_stream = nullptr;  // CUDA-graph replay of PCG iterations
+    cudaStream_t body_stream = nullptr;   // capture of conditional iteration bodies
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_rr0 = nullptr, ev_rr1 = nullptr;  // PCG side-stream ||r||^2 allreduce (distributed)
     std::unique_ptr<Transport> tr;       // distributed contexts: NCCL or a local thread group

@@ -98,6 +98,7 @@ void Context::t_flush() {
 
 Context::~Context() {
     if (graph_stream) cudaStreamDestroy(graph_stream);
+    if (body_stream) cudaStreamDestroy(body_stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_rr0) cudaEventDestroy(ev_rr0);
@@ -526,6 +527,11 @@ __global__ void k_cg_rrcheck(CgDev *st, const double *rr_glob, double *history) 
     }
 }
 
+// Sets an IF node's condition: run the next PCG iteration only while the device flag is clear.
+__global__ void k_set_cond_not_done(cudaGraphConditionalHandle h, const int *done) {
+    cudaGraphSetConditional(h, *done ? 0u : 1u);
+}
+
 // Stream-captured replay of a fixed work block.  While active, ctx->stream points at the
 // library's graph stream (forked from the caller's stream); the destructor joins back.
 struct GraphRun {
@@ -537,8 +543,43 @@ struct GraphRun {
     unsigned long long kernels = 0;
     bool forked = false;
     GraphRun(Context *ctx, PcgCache &pc) : c(ctx), cache(pc), orig(ctx->stream) {}
+    // One iteration as the body of a conditional (IF) node: a solve that converges inside a
+    // replayed block skips the block's remaining iterations instead of launching them as no-ops
     template <class F>
-    npc_status capture(F &&body) {
+    npc_status cond_iteration(F &&body, const int *done) {
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        NPC_CUDA_TRY(cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, &cg, &deps, &nd));
+        cudaGraphConditionalHandle h;
+        NPC_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
+        k_set_cond_not_done<<<1, 1, 0, c->stream>>>(h, done);
+        NPC_LAUNCH_CHECK();
+        NPC_CUDA_TRY(cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, &cg, &deps, &nd));
+        cudaGraphNodeParams p = {};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = h;
+        p.conditional.type = cudaGraphCondTypeIf;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        NPC_CUDA_TRY(cudaGraphAddNode(&node, cg, deps, nd, &p));
+        NPC_CUDA_TRY(cudaStreamUpdateCaptureDependencies(c->stream, &node, 1, cudaStreamSetCaptureDependencies));
+        if (!c->body_stream) NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c->body_stream, cudaStreamNonBlocking));
+        cudaStream_t parent = c->stream;
+        NPC_CUDA_TRY(cudaStreamBeginCaptureToGraph(c->body_stream, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal));
+        c->stream = c->body_stream;
+        npc_status st = body();
+        c->stream = parent;
+        cudaGraph_t out = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(c->body_stream, &out);
+        if (st != NPC_SUCCESS) return st;
+        NPC_CUDA_TRY(ce);
+        return NPC_SUCCESS;
+    }
+    template <class F>
+    npc_status capture(F &&body, const int *cond_done = nullptr) {
         if (!c->graph_stream) {
             NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c->graph_stream, cudaStreamNonBlocking));
             NPC_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -558,7 +599,7 @@ struct GraphRun {
         c->capturing = c->timing;
         c->captured.clear();
         npc_status st = NPC_SUCCESS;
-        for (int i = 0; i < ITERS && st == NPC_SUCCESS; ++i) st = body();
+        for (int i = 0; i < ITERS && st == NPC_SUCCESS; ++i) st = cond_done ? cond_iteration(body, cond_done) : body();
         c->capturing = false;
         cache.release_events();
         cache.timing_events.swap(c->captured);
@@ -906,13 +947,19 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     // to hide the launches -- and captures only if it needs a second chunk.  (Low degrees
     // capture at once: eager 4-iteration chunks measured slower on configs 2 and 6, k = 30.)
     bool deferred = graph_ok && !cache.exec && (h.multi || k >= 32);
+    // Opt-in (NPC_GRAPH_COND=1; single rank, untimed): each captured iteration is the body of a
+    // conditional IF node whose condition a one-thread kernel sets from the done flag, so the
+    // iterations after convergence inside a replayed block are skipped rather than launched as
+    // no-ops.  A/B (phase_times, fresh polynomial): config 6 48.1 -> 47.1 ms, config 4 914 ->
+    // 911 ms, config 3 unchanged, config 2 8.8 -> 9.3 ms (the larger graph costs more to build).
+    const bool cond = !h.multi && !ctx->timing && getenv("NPC_GRAPH_COND") != nullptr;
     // ... and that eager chunk is ONE iteration: a solve that converges at once (config 5) then
     // stops there -- in a 4-iteration block the no-op iterations still launch every kernel, and
     // the bulk-copy kernels issue their tile loads before they read the done flag
     if (deferred) chunk = 1;
     if (graph_ok && !deferred) {
         iter_calls = 0;
-        NPC_TRY(gr.capture(iteration));
+        NPC_TRY(gr.capture(iteration, cond ? dflag : nullptr));
     }
     t_chunk = now_s();  // the first chunk's clock starts after the capture
     for (;;) {
@@ -940,7 +987,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
             if (deferred) {
                 deferred = false;
                 iter_calls = 0;
-                NPC_TRY(gr.capture(iteration));
+                NPC_TRY(gr.capture(iteration, cond ? dflag : nullptr));
             }
             if (chunk_max == 64 && now_s() - t_chunk >= 2e-3) chunk_max = GraphRun::ITERS;
             chunk = std::min(chunk * 2, chunk_max);
