@@ -18,6 +18,7 @@
 // id: 12 -> 9 B per nonzero (config 3: 2,008.5 -> 1,657 MB per degree).  Same values, same
 // summation order: bitwise the same result as the plain form (NPC_CSR_PLAIN=1).
 #include <algorithm>
+#include <thread>
 
 #include "device_util.cuh"
 #include "npc_internal.cuh"
@@ -353,11 +354,30 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     const int n = d->n_local;
     const long long nnz = d->rowptr[n];
     op->nnz = nnz;
+    // the values upload (the largest array) runs on a helper thread while the host builds the
+    // column form; joined before any return
+    NPC_TRY(op->vals.alloc(sizeof(double) * (nnz + 8)));
+    NPC_CUDA_TRY(cudaMemset(op->vals.as<double>() + nnz, 0, sizeof(double) * 8));
+    cudaError_t up_err = cudaSuccess;
+    struct Joiner {
+        std::thread t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } up;
+    if (nnz) {
+        const int dev = ctx->device;
+        up.t = std::thread([&up_err, &op, d, nnz, dev]() {
+            up_err = cudaSetDevice(dev);
+            if (up_err == cudaSuccess)
+                up_err = cudaMemcpy(op->vals.p, d->vals, sizeof(double) * nnz, cudaMemcpyHostToDevice);
+        });
+    }
     std::vector<int> lcols;
     NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
     op->multi = ctx->distributed();
-    // coded column ids: per tile of CSR_TILE_CODED rows, the sorted distinct offsets col - row
-    // (<= 256) and a byte per entry; any tile with more -> the plain form on CSR_TILE rows
+    // coded column ids: per tile of CSR_TILE_CODED rows, the distinct offsets col - row (<= 256,
+    // first-seen order) and a byte per entry; any tile with more -> the plain form on CSR_TILE rows
     const int ntc = ceil_div(n, CSR_TILE_CODED);
     std::vector<std::vector<int>> tdict((size_t)ntc);
     std::vector<unsigned char> hcodes;
@@ -437,12 +457,9 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     const long long ncols = need_cols ? nnz : 0;
     NPC_TRY(op->rowptr.alloc(sizeof(int) * (n + 1)));
     NPC_TRY(op->cols.alloc(sizeof(int) * (ncols + 8)));
-    NPC_TRY(op->vals.alloc(sizeof(double) * (nnz + 8)));
     NPC_CUDA_TRY(cudaMemcpy(op->rowptr.p, d->rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
     NPC_CUDA_TRY(cudaMemset(op->cols.as<int>() + ncols, 0, sizeof(int) * 8));
-    NPC_CUDA_TRY(cudaMemset(op->vals.as<double>() + nnz, 0, sizeof(double) * 8));
     if (ncols) NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice));
-    if (nnz) NPC_CUDA_TRY(cudaMemcpy(op->vals.p, d->vals, sizeof(double) * nnz, cudaMemcpyHostToDevice));
     if (coded) {
         std::vector<int> doff((size_t)op->ntiles + 1, 0), dall;
         for (int t = 0; t < op->ntiles; ++t) doff[t + 1] = doff[t] + (int)tdict[t].size();
@@ -474,6 +491,8 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
             NPC_CUDA_TRY(cudaMemcpy(op->tiles_boundary.p, tb.data(), sizeof(int) * tb.size(), cudaMemcpyHostToDevice));
         NPC_TRY(halo_setup(ctx, op->plan, op->halo));
     }
+    if (up.t.joinable()) up.t.join();
+    NPC_CUDA_TRY(up_err);
     out = std::move(op);
     return NPC_SUCCESS;
 }
