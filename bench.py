@@ -374,7 +374,8 @@ def run_ours(args):
     t_apply = e0.elapsed_time(e1) / R  # ms per p_k(A) r (k launches)
     # roofline numerator: the bytes the kernels stream in the library's stored format (a coded
     # CSR streams 9 B per nonzero, not 12), this rank's share
-    Mf = npc.npc_operator_matrix_bytes(op)
+    # (CSR only: the other operators are reported against their §8(d) floor, like tools/bench_all.py)
+    Mf = npc.npc_operator_matrix_bytes(op) if kind == "csr" else M / ws
     Vf = 8 * nl
     apply_bytes = poly_bytes(Mf, Vf, k)
     per_launch_ms = t_apply / max(k, 1)
@@ -459,9 +460,12 @@ def run_ours(args):
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / peak, 4),
                          "frac_vs_8TBs_nominal": round(ach / 8000.0, 4), "traffic": traffic,
                          "bytes_per_launch": apply_bytes / max(k, 1), "launch_ms": round(per_launch_ms, 5),
-                         "bytes_basis": "operator data in the stored format (npc_operator_matrix_bytes: "
-                         f"{Mf / 1e6:.1f} MB per application) + the recurrence's vector streams; `value` uses the "
-                         f"format-independent SURVEY §8(d) bytes ({M / ws / 1e6:.1f} MB), the reference arm's basis",
+                         "bytes_basis": ("operator data in the stored format (npc_operator_matrix_bytes: "
+                                         f"{Mf / 1e6:.1f} MB per application) + the recurrence's vector streams; "
+                                         "`value` uses the format-independent SURVEY §8(d) bytes "
+                                         f"({M / ws / 1e6:.1f} MB), the reference arm's basis") if kind == "csr"
+                         else f"SURVEY §8(d) bytes ({M / ws / 1e6:.1f} MB of operator data per application) + the "
+                              "recurrence's vector streams, the same basis as `value`",
                          "timed": "library CUDA events on the launching stream inside the timed region: one event "
                          "pair around each p_k(A) r application (its k fused degree launches, replayed in the PCG "
                          "CUDA graph as event-record nodes); achieved = algorithmic bytes of the degree steps / their "
