@@ -455,9 +455,10 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     // int32 column ids only where a kernel reads them (plain form, cluster-resident kernels)
     const bool need_cols = !coded || op->small.cl_size > 0;
     const long long ncols = need_cols ? nnz : 0;
-    NPC_TRY(op->rowptr.alloc(sizeof(int) * (n + 1)));
+    const int nrp = need_cols ? n + 1 : 1;  // the coded kernel reads tile pointers + 16-bit offsets
+    NPC_TRY(op->rowptr.alloc(sizeof(int) * nrp));
     NPC_TRY(op->cols.alloc(sizeof(int) * (ncols + 8)));
-    NPC_CUDA_TRY(cudaMemcpy(op->rowptr.p, d->rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemcpy(op->rowptr.p, d->rowptr, sizeof(int) * nrp, cudaMemcpyHostToDevice));
     NPC_CUDA_TRY(cudaMemset(op->cols.as<int>() + ncols, 0, sizeof(int) * 8));
     if (ncols) NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice));
     if (coded) {
