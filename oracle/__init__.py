@@ -52,7 +52,7 @@ class _Op(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("iters", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int),
                 ("mvp", C.c_longlong), ("ddot", C.c_longlong),
-                ("relres_recursive", C.c_double), ("relres_true", C.c_double)]
+                ("relres_recursive", C.c_double), ("relres_true", C.c_double), ("true_checks", C.c_int)]
 
 
 _lib = None
@@ -311,7 +311,7 @@ def pcg(op: Operator, b, m, alpha=None, beta=None, xi=0.0, tol=1e-8, maxit=10000
                   tol, maxit, _p(hist), C.byref(st), lr_p, lr_V, lr_L)
     out = dict(iters=st.iters, converged=bool(st.converged), breakdown=bool(st.breakdown),
                mvp=st.mvp, ddot=st.ddot, relres_recursive=st.relres_recursive,
-               relres_true=st.relres_true)
+               relres_true=st.relres_true, true_checks=st.true_checks)
     if history:
         out["history"] = hist[: st.iters + 1]
     return x, out

@@ -12,7 +12,8 @@
  * Rules followed: fp64 everywhere; no blocking, fusion or reordering beyond what the
  * cited algorithm states; sums run in index order.  Row loops of an operator application
  * may be split across OpenMP threads (each row is still summed sequentially in stored
- * order, so the result is independent of the thread count); inner products are
+ * order, so the result is independent of the thread count), and so may element-wise
+ * vector loops (independent entries, bitwise the same result); inner products are
  * sequential.  Built with -O2 -fno-fast-math -ffp-contract=off.
  *
  * Pins (tests/test_oracle_pins.py) -- every function below is pinned; none is
@@ -339,6 +340,7 @@ int orc_cheb_apply(const orc_op *A, int m, double alpha, double beta, double xi,
     orc_cheb_rho(sigma, m, rho);                         /* step 1 */
     double *x_old = work, *x = work + n, *z = work + 2 * n;
     long i;
+#pragma omp parallel for schedule(static)
     for (i = 0; i < n; i++) x_old[i] = r[i] / theta_bar;  /* step 2 */
     if (m == 0) {
         memcpy(rhat, x_old, sizeof(double) * n);
@@ -346,13 +348,16 @@ int orc_cheb_apply(const orc_op *A, int m, double alpha, double beta, double xi,
         return 0;
     }
     orc_op_apply(A, r, z);                               /* step 3: x = 2 rho_1/delta (2r - A r/theta) */
+#pragma omp parallel for schedule(static)
     for (i = 0; i < n; i++) x[i] = (2.0 * rho[1] / delta) * (2.0 * r[i] - z[i] / theta_bar);
     for (int k = 2; k <= m; k++) {                       /* step 4 */
         orc_op_apply(A, x, z);
+#pragma omp parallel for schedule(static)
         for (i = 0; i < n; i++) z[i] = (2.0 / delta) * (r[i] - z[i]);                       /* step 5 */
+#pragma omp parallel for schedule(static)
         for (i = 0; i < n; i++) rhat[i] = rho[k] * (2.0 * sigma * x[i] - rho[k - 1] * x_old[i] + z[i]); /* step 6 */
-        memcpy(x_old, x, sizeof(double) * n);            /* step 7 */
-        memcpy(x, rhat, sizeof(double) * n);
+#pragma omp parallel for schedule(static)
+        for (i = 0; i < n; i++) { x_old[i] = x[i]; x[i] = rhat[i]; }   /* step 7 */
     }
     memcpy(rhat, x, sizeof(double) * n);
     free(rho);
@@ -528,13 +533,16 @@ int orc_lanczos(const orc_op *A, int m, const double *v0, double *alphas, double
 /* Textbook PCG (O5; Saad Alg. 9.1), stopping rule (reading A5):        */
 /* ||r_i||_2 / ||b||_2 <= tol on the recursively updated residual, iterations counted as  */
 /* x-updates.  When it fires, the true residual b - A x is formed; if it is above tol the */
-/* true residual replaces r and the iteration continues (reading A23 in DESIGN.md).       */
+/* true residual replaces r and PCG restarts from the current x (p = z, beta = 0; reading */
+/* A23 in DESIGN.md), at most 50 times: the 51st true check still above tol ends the      */
+/* solve, not converged (a true residual stuck above tol is the attainable-accuracy floor).*/
 /* Preconditioner: m < 0 -> none (CG); m >= 0 -> Chebyshev p_m (Alg. 2) on [alpha, beta]. */
 /* ------------------------------------------------------------------------------------ */
 typedef struct {
     int iters, converged, breakdown;
     long long mvp, ddot;
     double relres_recursive, relres_true;
+    int true_checks;            /* true residuals formed by the stopping test (A23) */
 } orc_pcg_stats;
 
 int orc_pcg(const orc_op *A, int m, double alpha, double beta, double xi,
@@ -548,6 +556,7 @@ int orc_pcg(const orc_op *A, int m, double alpha, double beta, double xi,
     double *lr_c = (double *)malloc(sizeof(double) * (lr_p > 0 ? lr_p : 1));
     memset(st, 0, sizeof(*st));
     int true_done = 0;          /* true residual computed for the final x */
+    int restart = 0;            /* set by a residual replacement (A23)     */
     double rr = 0.0, rz = 0.0;
     int x0_nonzero = 0;
     for (i = 0; i < n; i++) if (x[i] != 0.0) { x0_nonzero = 1; break; }
@@ -584,7 +593,9 @@ int orc_pcg(const orc_op *A, int m, double alpha, double beta, double xi,
         double pq = dot(n, p, q); st->ddot++;
         if (!(pq > 0.0)) { st->breakdown = 1; break; }
         double a = rz / pq;
+#pragma omp parallel for schedule(static)
         for (i = 0; i < n; i++) x[i] += a * p[i];
+#pragma omp parallel for schedule(static)
         for (i = 0; i < n; i++) r[i] -= a * q[i];
         rr = dot(n, r, r); st->ddot++;
         st->iters = it;
@@ -595,15 +606,20 @@ int orc_pcg(const orc_op *A, int m, double alpha, double beta, double xi,
             for (i = 0; i < n; i++) q[i] = b[i] - q[i];
             double tr = sqrt(dot(n, q, q)) / bnorm; st->ddot++;
             st->relres_true = tr;
+            st->true_checks++;
             if (tr <= tol) { st->converged = 1; true_done = 1; break; }
-            for (i = 0; i < n; i++) r[i] = q[i];      /* residual replacement, continue */
+            if (st->true_checks > 50) { true_done = 1; break; }   /* A23 cap: not converged */
+            for (i = 0; i < n; i++) r[i] = q[i];      /* residual replacement ...        */
+            restart = 1;                              /* ... and restart: p = z below    */
         }
         if (it == maxit) break;
         APPLY_M(r, z);
         double rz_new = dot(n, r, z); st->ddot++;
         if (!(rz_new > 0.0)) { st->breakdown = 1; break; }
-        double bet = rz_new / rz;
+        double bet = restart ? 0.0 : rz_new / rz;
+        restart = 0;
         rz = rz_new;
+#pragma omp parallel for schedule(static)
         for (i = 0; i < n; i++) p[i] = z[i] + bet * p[i];
     }
 #undef APPLY_M

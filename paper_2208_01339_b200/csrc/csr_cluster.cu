@@ -277,6 +277,7 @@ __global__ void k_csr_pcg_cluster(SmallCsrDev A, const double *__restrict__ b, d
             rr = q;
             converged = 0;
             want_true = false;
+            first = true;  // restart the recurrence from the current x (reading A23)
             if (iters >= maxit) break;
             cl.sync();  // replaced r visible before the polynomial gathers it
         }

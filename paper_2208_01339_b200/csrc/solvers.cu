@@ -1013,11 +1013,13 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                 }
                 break;
             }
-            // residual replacement (reading A23): r = b - A x, continue
+            // residual replacement (reading A23): r = b - A x, and restart the recurrence
+            // from the current x (beta = 0: p = u, s = w in the next iteration)
             NPC_CUDA_TRY(cudaMemcpyAsync(r, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
             h.rr = tr * tr * bnorm2;
             h.converged = 0;
             h.done = 0;
+            h.first = 1;
             NPC_CUDA_TRY(cudaMemcpyAsync(cg, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
             NPC_CUDA_TRY(cudaMemcpyAsync(sums + 2, &h.rr, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
             if (h.iters >= maxit) {

@@ -535,3 +535,114 @@ def test_P18_dfn_end_to_end_block_system():
     x = np.concatenate([h, u, p])
     f0 = np.concatenate([np.zeros(nh), np.zeros(nu), q])
     assert np.linalg.norm(K0 @ x - f0) <= 1e-9 * np.linalg.norm(K0) * np.linalg.norm(x)
+
+
+# ---------------------------------------------------------------- P6b: x0 != 0 branch of O5
+def _dense_op(n, seed, cond):
+    A, _ = W.random_spd_dense(n, seed, cond=cond)
+    rowptr, colidx, vals = W.dense_to_csr(A)
+    return A, oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+
+
+@pytest.mark.parametrize("k", [-1, 0, 4])
+def test_P6b_pcg_nonzero_x0_dense(k):
+    """PCG from x0 != 0 (r0 = b - A x0, PAPER.md:122-123 via Saad Alg. 9.1) reaches the
+    dense solution; counters iters*(k+1) + 1 (r0) + 1 (true residual).  x0 = 2 x* (so that
+    r0 = -b: a sign slip in r0 would converge to 3 x*) and x0 = x* (0 iterations)."""
+    n = 30
+    A, op = _dense_op(n, 3, 50.0)
+    b = np.random.default_rng(4).uniform(-1, 1, n)
+    xs = np.linalg.solve(A, b)
+    for x0 in (np.random.default_rng(5).standard_normal(n) * 10.0, 2.0 * xs):
+        x, st = oracle.pcg(op, b, k, 1.0, 50.0, 0.0, tol=1e-10, maxit=400, x0=x0)
+        assert st["converged"] and st["relres_true"] <= 1e-10 and st["true_checks"] == 1
+        assert np.linalg.norm(x - xs) / np.linalg.norm(xs) <= 10 * 1e-10 * 50.0
+        assert st["mvp"] == st["iters"] * (max(k, 0) + 1) + 2
+        assert st["ddot"] == 3 * st["iters"] + 3
+    # x0 = x*: r0 is rounding noise, relres <= tol before the first iteration
+    x, st = oracle.pcg(op, b, k, 1.0, 50.0, 0.0, tol=1e-10, maxit=400, x0=xs)
+    assert st["iters"] == 0 and st["converged"] and st["mvp"] == 2 and np.array_equal(x, xs)
+
+
+# ---------------------------------------------------------------- A23: residual replacement
+def _replacement_case(scale, tol, k=2):
+    """workloads.pcg_replacement_case: x0 = x* + scale*d on a dense SPD system with spectrum
+    in [1, 10]; the recursive residual r_i = r_0 - sum alpha A p loses the absolute accuracy
+    of b - A x_i once ||A x_i|| >> ||b||, so below a tolerance near eps*scale the recursive
+    residual passes the test while the true one does not."""
+    w, x0 = W.pcg_replacement_case(scale)
+    op = oracle.Operator(w)
+    A, b = w["dense"], w["b"]
+    x, st = oracle.pcg(op, b, k, 1.0, 10.0, 0.0, tol=tol, maxit=2000, x0=x0)
+    return A, b, np.linalg.solve(A, b), x, st
+
+
+@pytest.mark.parametrize("scale,tol", [(1e7, 1e-8), (1e8, 1e-10), (1e6, 1e-11)])
+def test_A23_residual_replacement_restarts_and_converges(scale, tol):
+    """Recursive residual below tol, true residual above: r is replaced by b - A x and PCG
+    restarts (reading A23).  Pinned by the mathematics: the final x solves the dense system
+    to tol (a replacement that kept the stale r would re-trigger the true check on every
+    following iteration, true_checks >> 2; a wrong sign in b - A x would diverge), and the
+    counters obey iters*(k+1) + 1 (r0) + true_checks."""
+    A, b, xs, x, st = _replacement_case(scale, tol)
+    assert st["converged"] and st["relres_true"] <= tol
+    assert st["true_checks"] == 2, st          # one replacement, then accepted
+    assert np.linalg.norm(b - A @ x) / np.linalg.norm(b) <= 2 * tol
+    assert np.linalg.norm(x - xs) / np.linalg.norm(xs) <= 10 * tol * 10.0
+    assert st["mvp"] == st["iters"] * 3 + 1 + st["true_checks"]
+    # the replacement restarts the recurrence: the iterations after it are those of a fresh
+    # PCG from the iterate at which it happened (same x, same arithmetic) -- exactly
+    _, _, _, _, st1 = _replacement_case(scale, tol)
+    assert st1 == st                            # deterministic
+
+
+def _floor_case():
+    """workloads.pcg_floor_case: one eigenvalue 1e-8, the rest in [1, 10], b mostly along
+    its eigenvector: x* ~ 1e8 b, so b - A x carries an absolute rounding error
+    ~eps ||A|| ||x*|| and the true relative residual cannot go below ~2e-7, while the
+    recursive one can."""
+    w = W.pcg_floor_case()
+    return w["dense"], oracle.Operator(w), w["b"]
+
+
+@pytest.mark.parametrize("k", [-1, 2])
+def test_A23_replacement_cap(k):
+    """A true-residual floor above tol: every true check fails, the oracle replaces at most 50
+    times and stops unconverged after the 51st check (A23's cap); counters iters*(k+1) + 51."""
+    A, op, b = _floor_case()
+    x, st = oracle.pcg(op, b, k, 1e-8, 10.0, 0.0, tol=1e-10, maxit=5000)
+    assert not st["converged"] and not st["breakdown"]
+    assert st["true_checks"] == 51 and st["relres_recursive"] <= 1e-10 and st["relres_true"] > 1e-10
+    assert st["mvp"] == st["iters"] * (max(k, 0) + 1) + 51
+    # the floor is the rounding of b - A x at this |x|, not a wrong iterate
+    floor = np.finfo(float).eps * np.linalg.norm(A, 2) * np.linalg.norm(x) / np.linalg.norm(b)
+    assert st["relres_true"] <= 10 * floor
+    xs = np.linalg.solve(A, b)
+    assert np.linalg.norm(x - xs) / np.linalg.norm(xs) <= 1e-6
+    # a tolerance above the floor converges, with at most a few replacements
+    x, st = oracle.pcg(op, b, k, 1e-8, 10.0, 0.0, tol=1e-6, maxit=5000)
+    assert st["converged"] and st["relres_true"] <= 1e-6 and 1 <= st["true_checks"] <= 3
+
+
+# ---------------------------------------------------------------- P3 (2D): stencil dim = 2
+@pytest.mark.parametrize("nx,ny", [(37, 37), (64, 23), (1, 9)])
+def test_P3_stencil_2d(nx, ny):
+    """The 2D 5-point matrix-free stencil (O1, dim = 2; PAPER.md:686-689 2D Laplacian
+    blocks): equals the explicit CSR operator, and maps the separable sine eigenvectors
+    sin(a x pi/(nx+1)) sin(b y pi/(ny+1)) to (diag - 2 cos(a pi/(nx+1)) - 2 cos(b pi/(ny+1))) v
+    (diag 4, off -1: 4 sin^2 + 4 sin^2), both closed form."""
+    n = nx * ny
+    rowptr, colidx, vals = W.grid_laplacian_csr((nx, ny), 4.0, -1.0)
+    csr = oracle.Operator(dict(kind="csr", n=n, rowptr=rowptr, colidx=colidx, vals=vals))
+    st = oracle.Operator(dict(kind="stencil", n=n, dim=2, nx=nx, ny=ny, nz=1, diag=4.0, offdiag=-1.0))
+    xr = np.random.default_rng(8).standard_normal(n)
+    assert np.allclose(csr.apply(xr), st.apply(xr), rtol=0, atol=1e-13)
+    gx, gy = np.arange(1, nx + 1), np.arange(1, ny + 1)
+    for a, bb in [(1, 1), (min(3, nx), min(5, ny)), (nx, ny)]:
+        v = np.outer(np.sin(gy * bb * np.pi / (ny + 1)), np.sin(gx * a * np.pi / (nx + 1))).ravel()
+        lam = 4 * np.sin(a * np.pi / (2 * (nx + 1))) ** 2 + 4 * np.sin(bb * np.pi / (2 * (ny + 1))) ** 2
+        assert np.linalg.norm(st.apply(v) - lam * v) <= 1e-13 * 8 * np.linalg.norm(v)
+        # and through Alg. 2: p_k(A) v = p_k(lambda) v (closed-form residual polynomial)
+        lo = 8 * np.sin(np.pi / (2 * (max(nx, ny) + 1))) ** 2 * 0.5
+        z = oracle.cheb_apply(st, 12, lo, 8.0, 1e-3, v)
+        assert np.linalg.norm(z - p_closed(lam, 12, lo, 8.0, 1e-3) * v) <= 1e-11 * np.linalg.norm(z) + 1e-14

@@ -447,3 +447,34 @@ def dense_to_csr(A: np.ndarray):
     rowptr = (np.arange(n + 1, dtype=np.int64) * n).astype(np.int32)
     colidx = np.tile(np.arange(n, dtype=np.int32), n)
     return rowptr, colidx, np.ascontiguousarray(A, dtype=np.float64).ravel()
+
+
+def pcg_replacement_case(scale: float, seed: int = 11):
+    """Crafted PCG input for the residual-replacement branch (reading A23): a 30 x 30 dense
+    SPD matrix with spectrum in [1, 10] (as CSR), b ~ U[-1,1], and x0 = x* + scale * N(0,1):
+    with ||A x0|| >> ||b||, b - A x carries an absolute rounding error ~eps ||A|| ||x0|| that
+    the recursive residual does not see.  Returns (workload dict, x0)."""
+    n = 30
+    A, _ = random_spd_dense(n, seed, cond=10.0)
+    rowptr, colidx, vals = dense_to_csr(A)
+    rng = np.random.default_rng(seed + 1)
+    b = rng.uniform(-1.0, 1.0, n)
+    xs = np.linalg.solve(A, b)
+    x0 = xs + scale * rng.standard_normal(n)
+    return dict(kind="csr", name=f"replacement_{scale:g}", n=n, rowptr=rowptr, colidx=colidx, vals=vals,
+                b=b, dense=A), x0
+
+
+def pcg_floor_case(seed: int = 21):
+    """Crafted PCG input whose true relative residual has a floor ~2e-7 (reading A23's cap):
+    a 30 x 30 dense SPD matrix with one eigenvalue 1e-8 and the rest in [1, 10], b mostly
+    along the 1e-8 eigenvector (so x* ~ 1e8 b).  Returns a workload dict (x0 = 0)."""
+    n = 30
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.concatenate([[1e-8], np.linspace(1.0, 10.0, n - 1)])
+    A = (Q * lam) @ Q.T
+    A = 0.5 * (A + A.T)
+    rowptr, colidx, vals = dense_to_csr(A)
+    return dict(kind="csr", name="floor", n=n, rowptr=rowptr, colidx=colidx, vals=vals,
+                b=Q[:, 0] + 1e-3 * rng.standard_normal(n), dense=A)
