@@ -177,8 +177,11 @@ __global__ void __launch_bounds__(ST_TILE) k_schur_tpass(SchurTDev T, StepArgs s
             const int pe = T.rowptr[row0 + nrows];
             const int v1 = (pe + 1) & ~1, c1 = (pe + 3) & ~3;
             const uint32_t bv = (uint32_t)(v1 - v0) * 8u, bc = (uint32_t)(c1 - c0) * 4u;
-            mbar_arrive_expect_tx(&bar, bv + bc);
-            if (bv) {
+            // an empty tile (pe == pb) may still have bv or bc != 0 from the alignment
+            // rounding: expect exactly the bytes issued, none for an empty tile
+            const bool any = pe > pb;
+            mbar_arrive_expect_tx(&bar, any ? bv + bc : 0u);
+            if (any) {
                 const uint64_t pol = policy_evict_first();
                 bulk_g2s_evict_first(sv, T.vals + v0, bv, &bar, pol);
                 bulk_g2s_evict_first(sc, T.cols + c0, bc, &bar, pol);

@@ -159,3 +159,27 @@ def test_coded_unstaged_tiles(ctx):
     finally:
         os.environ.pop("NPC_NO_CLUSTER", None)
     assert nnz > 512 * 100
+
+
+def empty_tile_csr(n=3000, first=18, empty_to=1600):
+    """Rows [0, first) and [empty_to, n) hold a diagonal entry, rows [first, empty_to) are
+    empty: whole 256-row (plain) and 512-row (coded) tiles with no entries, starting at entry
+    offset 18 (= 2 mod 4 and not a multiple of 16), where the bulk copies' aligned spans are
+    nonzero for an empty tile (the barrier used to wait for bytes never sent)."""
+    lens = np.ones(n, dtype=np.int64)
+    lens[first:empty_to] = 0
+    rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    rows = np.flatnonzero(lens)
+    return dict(kind="csr", n=n, rowptr=rowptr, colidx=rows.astype(np.int32),
+                vals=np.arange(1, len(rows) + 1, dtype=np.float64))
+
+
+@pytest.mark.parametrize("plain", [False, True])
+def test_empty_tiles_at_unaligned_offsets(ctx, plain):
+    w = empty_tile_csr()
+    op = make(ctx, w, plain)
+    x = np.random.default_rng(2).standard_normal(w["n"])
+    y = torch.empty(w["n"], dtype=torch.float64, device="cuda")
+    npc.npc_apply_operator(op, dev(x), y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), oracle.Operator(w).apply(x))
