@@ -368,9 +368,9 @@ npc_status allow_max_dynamic_smem(K kern) {
 // Host-side parallel loop over [0, n) in contiguous chunks (operator setup: validation and
 // format conversion of 10^7-10^8 entries).  fn(begin, end, thread_index).
 template <class F>
-void host_parallel_for(long long n, F &&fn) {
+void host_parallel_for(long long n, F &&fn, long long grain = 200000) {
     const int hw = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    const int nt = n < 200000 ? 1 : hw;
+    const int nt = n < grain ? 1 : (int)std::min<long long>(hw, n / std::max(grain / 8, 1LL) + 1);
     if (nt == 1) {
         fn(0LL, n, 0);
         return;

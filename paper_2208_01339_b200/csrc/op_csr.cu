@@ -18,6 +18,8 @@
 // id: 12 -> 9 B per nonzero (config 3: 2,008.5 -> 1,657 MB per degree).  Same values, same
 // summation order: bitwise the same result as the plain form (NPC_CSR_PLAIN=1).
 #include <algorithm>
+#include <climits>
+#include <cstring>
 #include <thread>
 
 #include "device_util.cuh"
@@ -74,8 +76,11 @@ __global__ void __launch_bounds__(TILE) k_csr_step(CsrDev A, StepArgs s, const i
             const int pe = CODED ? A.tptr[tile + 1] : A.rowptr[row0 + nrows];
             const int v1 = (pe + 1) & ~1, c1 = CODED ? ((pe + 15) & ~15) : ((pe + 3) & ~3);
             const uint32_t bv = (uint32_t)(v1 - v0) * 8u, bc = (uint32_t)(c1 - c0) * (CODED ? 1u : 4u);
-            mbar_arrive_expect_tx(&bar, bv + bc);
-            if (bv) {
+            // an empty tile (pe == pb) may still have bv or bc != 0 from the alignment
+            // rounding: expect exactly the bytes issued, none for an empty tile
+            const bool any = pe > pb;
+            mbar_arrive_expect_tx(&bar, any ? bv + bc : 0u);
+            if (any) {
                 const uint64_t pol = policy_evict_first();
                 bulk_g2s_evict_first(sv, A.vals + v0, bv, &bar, pol);
                 if (CODED)
@@ -147,11 +152,270 @@ __global__ void __launch_bounds__(TILE) k_csr_step(CsrDev A, StepArgs s, const i
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Pattern form (default when it fits): per-row pattern ids + symmetric value mirroring.
+//
+// Each row stores ONE byte, the id of its pattern in the tile's pattern table, instead of a
+// byte per nonzero: a pattern is the row's entry list in stored (ascending column) order,
+// one 32-bit word per entry.  An "own" entry (bit 0 = 0) carries its offset o = col - row
+// and takes the row's next own value.  A "mirror" entry (bit 0 = 1) is a lower-triangle
+// entry a_ij (j < i, same rank) whose transpose a_ji is stored in row j with the bitwise-
+// identical value: it carries o = j - i and pos, the index of a_ji among row j's own values,
+// and its value is read from there.  A symmetric matrix therefore streams only its upper
+// triangle: config 3 moves ~4 values per row instead of ~7.  Entries without an equal
+// transpose are own entries, so any CSR matrix qualifies as long as every tile has <= 256
+// distinct patterns, a table of <= PAT_TBL_MAX words and little padding (below).
+//
+// Own values are stored per tile of PAT_TILE rows in ELL order (position-major: the k-th own
+// value of every row of the tile, then the (k+1)-th, ...; W_t = the tile's longest own list,
+// shorter rows padded with zeros).  Every read is then coalesced and sector-exact: a thread's
+// own values are sv[k * nrows + tid] in shared memory, a mirror inside the tile is
+// sv[pos * nrows + (j - row0)], and a mirror in an earlier tile (the -N^2 and half of the -N
+// neighbours of a 3D grid) is one 8-byte L2 read whose 32 neighbouring lanes read the 256
+// contiguous bytes of the same position column -- no 32-byte sector per 8-byte value.  Same
+// values in the same order: bitwise the same result as the plain and coded forms.
+#ifndef NPC_PAT_TILE
+#define NPC_PAT_TILE 1024
+#endif
+static constexpr int PAT_TILE = NPC_PAT_TILE;  // rows per tile (A/B: NPC_PAT_TILE)
+static constexpr int PAT_TBL_MAX = 2048;  // words of one tile's pattern table (8 KB of smem)
+static constexpr int PAT_MIRROR_MAX_OFF = 1 << 22;
+
+struct PatDev {
+    const double *vals;           // own values: tile blocks of W_t x nrows (position-major)
+    const int *tptr;              // first value of each tile's block (ntiles + 1)
+    const unsigned char *pat;     // pattern id per row
+    const int *tbl, *tbl_off;     // concatenated per-tile tables: [npat + 1 starts][entry words]
+    int n;
+    const double *ghost;
+    const int *tbl2, *tbl2_off;   // staged kernel: per-tile x windows + decoded entries
+};
+
+template <bool HAS_S2, bool HAS_R, bool DOT, bool GHOST>
+__global__ void __launch_bounds__(PAT_TILE) k_csr_pat_step(PatDev A, StepArgs s, const int *__restrict__ tiles,
+                                                           int vspan_max, int tbl_max) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t bar;
+    __shared__ double red[PAT_TILE / 32];
+
+    const int tile = tiles ? tiles[blockIdx.x] : blockIdx.x;
+    const int row0 = tile * PAT_TILE;
+    const int nrows = min(PAT_TILE, A.n - row0);
+    const int pb = A.tptr[tile];  // even: every block holds an even number of values
+    double *sv = reinterpret_cast<double *>(smem);
+    int *stbl = reinterpret_cast<int *>(smem + (size_t)vspan_max * 8);
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bv = (uint32_t)(A.tptr[tile + 1] - pb) * 8u;
+        mbar_arrive_expect_tx(&bar, bv);  // an empty block expects (and issues) nothing
+        if (bv) bulk_g2s(sv, A.vals + pb, bv, &bar);  // default L2 policy: mirrors re-read it
+    }
+    {
+        const int t0 = A.tbl_off[tile], tn = A.tbl_off[tile + 1] - t0;
+        for (int k = threadIdx.x; k < tn; k += PAT_TILE) stbl[k] = A.tbl[t0 + k];
+    }
+    const int row = row0 + threadIdx.x;
+    const bool active = threadIdx.x < nrows;
+    int pid = 0;
+    double xs = 0.0, s2v = 0.0, rv = 0.0;
+    if (active) {
+        pid = A.pat[row];
+        xs = s.x[row];
+        if (HAS_S2) s2v = s.s2[row];
+        if (HAS_R) rv = s.r[row];
+    }
+    const bool is_done = s.done && *s.done;
+    mbar_wait(&bar, 0);  // never leave with a bulk copy into shared memory in flight
+    if (is_done) return;  // uniform over the CTA
+    __syncthreads();      // table visible
+    double acc = 0.0;
+    if (active) {
+        const double *__restrict__ x = s.x;
+        const int e1 = stbl[pid + 1];
+        const double *own = sv + threadIdx.x;
+        double y = 0.0;
+        for (int e = stbl[pid]; e < e1; ++e) {
+            const int w = stbl[e];
+            int c;
+            double v;
+            if (w & 1) {  // mirror: value of a_ji, position pos of row j = c
+                const int pos = (w >> 1) & 255;
+                c = row + (w >> 9);
+                if (c >= row0) {
+                    v = sv[pos * nrows + (c - row0)];
+                } else {  // an earlier (full) tile's block, through L2
+                    const int tj = c / PAT_TILE;
+                    v = __ldg(A.vals + __ldg(A.tptr + tj) + pos * PAT_TILE + (c - tj * PAT_TILE));
+                }
+            } else {
+                c = row + (w >> 1);
+                v = *own;
+                own += nrows;
+            }
+            double xv;
+            if (GHOST && c >= A.n)
+                xv = A.ghost[c - A.n];
+            else
+                xv = __ldg(x + c);
+            y += v * xv;
+        }
+        double o = s.a * y + s.b * xs;
+        if (HAS_S2) o += s.c * s2v;
+        if (HAS_R) o += s.d * rv;
+        s.out[row] = o;
+        if (DOT) acc = o * s.dotv[row];
+    }
+    if (DOT) {
+        acc = block_sum<PAT_TILE>(acc, red);
+        if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
+    }
+}
+
+// Staged pattern kernel (the default for tiles whose x windows fit in shared memory): the
+// tile's input-vector windows -- x[row0 + o, row0 + o + nrows) for every distinct offset o of
+// its patterns, merged when they overlap (a 3D grid: x[row0 - N^2 ..], x[row0 - N - 1 ..
+// row0 + nrows + N], x[row0 + N^2 ..]) -- are bulk-copied (TMA) into shared memory next to the
+// tile's own values, so every entry reads x and its value from shared memory: one table read,
+// two shared loads and an FMA per entry, no per-entry L2 round trip, and each x element
+// crosses L2 ~3.5 times per degree instead of once per (row, offset).  Mirrors of earlier tiles
+// stay one coalesced L2 read.  Entries are pre-decoded per tile as {x base, value base, o,
+// pos}: x = sx[xb + lr], value = sv[vb + lr] when lr + o >= 0 (own entries carry o = 0).
+// Two rows per thread (lr = tid, tid + PAT_TILE / 2).
+static constexpr int PAT_THREADS = PAT_TILE / 2;
+static constexpr int PAT_STAGE_SMEM = 110 * 1024;  // own block + x windows + table, per tile
+
+template <bool HAS_S2, bool HAS_R>
+__device__ __forceinline__ double pat_row(const PatDev &A, const StepArgs &s, const double *sv, const double *sx,
+                                          const int *st, const int4 *ent, int sidx, int row0, int lr, int pid,
+                                          double xs, double s2v, double rv) {
+    const int row = row0 + lr;
+    const int e1 = st[sidx + pid + 1];
+    double y = 0.0;
+    for (int e = st[sidx + pid]; e < e1; ++e) {
+        const int4 t = ent[e];
+        const double xv = sx[t.x + lr];
+        double v;
+        if (lr + t.z >= 0) {
+            v = sv[t.y + lr];
+        } else {  // mirror in an earlier (full) tile's block, through L2
+            const int c = row + t.z, tj = c / PAT_TILE;
+            v = __ldg(A.vals + __ldg(A.tptr + tj) + t.w * PAT_TILE + (c - tj * PAT_TILE));
+        }
+        y += v * xv;
+    }
+    double o = s.a * y + s.b * xs;
+    if (HAS_S2) o += s.c * s2v;
+    if (HAS_R) o += s.d * rv;
+    return o;
+}
+
+template <bool HAS_S2, bool HAS_R, bool DOT>
+__global__ void __launch_bounds__(PAT_THREADS) k_csr_pat_stage(PatDev A, StepArgs s, const int *__restrict__ tiles,
+                                                               int vspan_max, int xspan_max) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t bar;
+    __shared__ double red[PAT_THREADS / 32];
+
+    const int tile = tiles ? tiles[blockIdx.x] : blockIdx.x;
+    const int row0 = tile * PAT_TILE;
+    const int nrows = min(PAT_TILE, A.n - row0);
+    double *sv = reinterpret_cast<double *>(smem);
+    double *sx = sv + vspan_max;
+    int *st = reinterpret_cast<int *>(sx + xspan_max);
+    const int *gt = A.tbl2 + A.tbl2_off[tile];
+    const int nwin = gt[0];
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // own block + every x window on one barrier
+        const int pb = A.tptr[tile];
+        const uint32_t bv = (uint32_t)(A.tptr[tile + 1] - pb) * 8u;
+        uint32_t bx = 0;
+        for (int w = 0; w < nwin; ++w) bx += (uint32_t)gt[4 + 4 * w + 1] * 8u;
+        mbar_arrive_expect_tx(&bar, bv + bx);
+        if (bv) bulk_g2s(sv, A.vals + pb, bv, &bar);
+        for (int w = 0; w < nwin; ++w) {
+            const int ga = gt[4 + 4 * w], len = gt[4 + 4 * w + 1], sb = gt[4 + 4 * w + 2];
+            if (len) bulk_g2s(sx + sb, s.x + ga, (uint32_t)len * 8u, &bar);
+        }
+    }
+    {  // the table (header, windows, pattern starts, entries) and odd window tails
+        const int tn = A.tbl2_off[tile + 1] - A.tbl2_off[tile];
+        for (int k = threadIdx.x; k < tn; k += PAT_THREADS) st[k] = gt[k];
+        if ((int)threadIdx.x < nwin && gt[4 + 4 * threadIdx.x + 3]) {
+            const int ga = gt[4 + 4 * threadIdx.x], len = gt[4 + 4 * threadIdx.x + 1];
+            sx[gt[4 + 4 * threadIdx.x + 2] + len] = s.x[ga + len];
+        }
+    }
+    const int l0 = threadIdx.x, l1 = threadIdx.x + PAT_THREADS;
+    const bool a0 = l0 < nrows, a1 = l1 < nrows;
+    int p0 = 0, p1 = 0;
+    double x0 = 0.0, x1 = 0.0, s20 = 0.0, s21 = 0.0, r0 = 0.0, r1 = 0.0;
+    if (a0) {
+        p0 = A.pat[row0 + l0];
+        if (HAS_S2) s20 = s.s2[row0 + l0];
+        if (HAS_R) r0 = s.r[row0 + l0];
+    }
+    if (a1) {
+        p1 = A.pat[row0 + l1];
+        if (HAS_S2) s21 = s.s2[row0 + l1];
+        if (HAS_R) r1 = s.r[row0 + l1];
+    }
+    const bool is_done = s.done && *s.done;
+    mbar_wait(&bar, 0);  // never leave with a bulk copy into shared memory in flight
+    if (is_done) return;  // uniform over the CTA
+    __syncthreads();      // table and window tails visible
+    if (a0) x0 = sx[st[3] + l0];  // x[row] from the offset-0 window
+    if (a1) x1 = sx[st[3] + l1];
+    const int sidx = 4 + 4 * nwin;
+    const int4 *ent = reinterpret_cast<const int4 *>(st + st[1]);
+    double acc = 0.0;
+    if (a0) {
+        const double o = pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l0, p0, x0, s20, r0);
+        s.out[row0 + l0] = o;
+        if (DOT) acc = o * s.dotv[row0 + l0];
+    }
+    if (a1) {
+        const double o = pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l1, p1, x1, s21, r1);
+        s.out[row0 + l1] = o;
+        if (DOT) acc += o * s.dotv[row0 + l1];
+    }
+    if (DOT) {
+        acc = block_sum<PAT_THREADS>(acc, red);
+        if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
+    }
+}
+
 class CsrOperator : public Operator {
   public:
     DevBuf rowptr, cols, vals;
     DevBuf codes, dict, dict_off, tptr, roff;  // coded form (see the file comment)
     bool coded = false;
+    // pattern form (k_csr_pat_step): own values in `vals` (tile-ELL blocks), block pointers in
+    // `tptr`, and per-row pattern ids + per-tile pattern tables here
+    bool pattern = false;
+    DevBuf pat, tbl, tbl_off;
+    DevBuf tbl2, tbl2_off;  // staged kernel tables (k_csr_pat_stage)
+    int xspan_max = 0, tbl2_max = 0;
+    size_t smem_stage = 0;
+    struct PatTiles {  // a tile list split by kernel: staged / unstaged
+        DevBuf staged, unstaged;
+        int ns = 0, nu = 0;
+        bool identity = false;  // staged == [0, ns): launch without a tile list
+    } pt_all, pt_interior;
+    DevBuf cvals;  // full CSR values for the cluster-resident kernels (pattern form only)
+    const double *csr_vals() const { return pattern ? cvals.as<double>() : vals.as<double>(); }
+    long long own_nnz = 0, tbl_total = 0;
+    int tbl_max = 0;
     long long dict_total = 0;
     DevBuf tiles_interior, tiles_boundary;
     int ntiles = 0, n_interior = 0, n_boundary = 0;
@@ -175,6 +439,8 @@ class CsrOperator : public Operator {
     }
 
     double matrix_bytes() const override {
+        if (pattern)  // own values (incl. ELL padding), pattern ids, tables, tile pointers
+            return (double)own_nnz * 8.0 + (double)n_local + (double)tbl_total * 4.0 + (double)(ntiles + 1) * 8.0;
         if (coded)  // values + codes, dictionaries + their offsets, tile pointers, 16-bit row offsets
             return (double)nnz * 9.0 + (double)dict_total * 4.0 + (double)(ntiles + 1) * 8.0 +
                    (double)n_local * 2.0;
@@ -183,6 +449,7 @@ class CsrOperator : public Operator {
 
     template <bool ST, bool H2, bool HR, bool DT, bool GH>
     npc_status launch_t(const StepArgs &s, const int *tl, int nt, double *partials) {
+        if (pattern) return launch_p<H2, HR, DT, GH>(s, tl, nt, partials);
         return coded ? launch_c<ST, H2, HR, DT, GH, true>(s, tl, nt, partials)
                      : launch_c<ST, H2, HR, DT, GH, false>(s, tl, nt, partials);
     }
@@ -200,6 +467,57 @@ class CsrOperator : public Operator {
         kern<<<nt, CD ? CSR_TILE_CODED : CSR_TILE, sm, ctx->stream>>>(A, a, tl, vspan_max);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
+    }
+
+    template <bool H2, bool HR, bool DT, bool GH>
+    npc_status launch_p(const StepArgs &s, const int *tl, int nt, double *partials) {
+        if (nt <= 0) return NPC_SUCCESS;
+        PatDev A{vals.as<double>(), tptr.as<int>(), pat.as<unsigned char>(), tbl.as<int>(), tbl_off.as<int>(),
+                 n_local, GH ? halo.ghost_buf.as<double>() : nullptr, nullptr, nullptr};
+        StepArgs a = s;
+        a.partials = partials;
+        auto kern = k_csr_pat_step<H2, HR, DT, GH>;
+        if (smem_bytes > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
+        kern<<<nt, PAT_TILE, smem_bytes, ctx->stream>>>(A, a, tl, vspan_max, tbl_max);
+        NPC_LAUNCH_CHECK();
+        return NPC_SUCCESS;
+    }
+
+    template <bool H2, bool HR, bool DT>
+    npc_status launch_stage(const StepArgs &s, const int *tl, int nt, double *partials) {
+        if (nt <= 0) return NPC_SUCCESS;
+        PatDev A{vals.as<double>(), tptr.as<int>(), pat.as<unsigned char>(), tbl.as<int>(), tbl_off.as<int>(),
+                 n_local, nullptr, tbl2.as<int>(), tbl2_off.as<int>()};
+        StepArgs a = s;
+        a.partials = partials;
+        auto kern = k_csr_pat_stage<H2, HR, DT>;
+        if (smem_stage > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
+        kern<<<nt, PAT_THREADS, smem_stage, ctx->stream>>>(A, a, tl, vspan_max, xspan_max);
+        NPC_LAUNCH_CHECK();
+        return NPC_SUCCESS;
+    }
+    npc_status launch_stage_any(const StepArgs &s, const int *tl, int nt, double *partials) {
+        const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
+        if (h2 && hr && dt) return launch_stage<true, true, true>(s, tl, nt, partials);
+        if (h2 && hr) return launch_stage<true, true, false>(s, tl, nt, partials);
+        if (h2 && dt) return launch_stage<true, false, true>(s, tl, nt, partials);
+        if (h2) return launch_stage<true, false, false>(s, tl, nt, partials);
+        if (hr && dt) return launch_stage<false, true, true>(s, tl, nt, partials);
+        if (hr) return launch_stage<false, true, false>(s, tl, nt, partials);
+        if (dt) return launch_stage<false, false, true>(s, tl, nt, partials);
+        return launch_stage<false, false, false>(s, tl, nt, partials);
+    }
+    // A tile set of the pattern form: staged tiles first (their partial slots first), then the
+    // rest through k_csr_pat_step.  x must be 16-byte aligned for the window copies; otherwise
+    // every tile takes k_csr_pat_step.
+    npc_status launch_pattern_set(const StepArgs &s, const PatTiles &t, double *partials) {
+        const bool aligned = ((uintptr_t)s.x & 15) == 0;
+        const int *sl = t.identity ? nullptr : t.staged.as<int>();
+        if (aligned)
+            NPC_TRY(launch_stage_any(s, sl, t.ns, partials));
+        else if (t.ns > 0)
+            NPC_TRY(launch(s, t.staged.as<int>(), t.ns, partials, false));
+        return launch(s, t.unstaged.as<int>(), t.nu, partials ? partials + t.ns : nullptr, false);
     }
 
     template <bool H2, bool HR, bool DT>
@@ -230,7 +548,7 @@ class CsrOperator : public Operator {
     }
     npc_status apply_poly_fused(const double *r, double *z, const double *coef_dev, int k, double tb,
                                 const double *dotv, double *partials, int *nparts, const int *done) override {
-        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local, small.R, small.nnz_cta};
+        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), csr_vals(), n_local, small.R, small.nnz_cta};
         if (dotv && nparts) *nparts = small.cl_size;
         return launch_csr_poly_cluster(ctx, A, small.cl_size, small.threads, small.smem, r, z, coef_dev, k, tb, dotv,
                                        partials, done);
@@ -238,7 +556,7 @@ class CsrOperator : public Operator {
 
     bool supports_fused_lanczos() const override { return supports_fused_pcg(); }
     npc_status lanczos_fused(const double *v0, int m, double *alphas, double *betas, int *steps) override {
-        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local, small.R, small.nnz_cta};
+        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), csr_vals(), n_local, small.R, small.nnz_cta};
         return launch_csr_lanczos_cluster(ctx, A, small, v0, m, alphas, betas, steps);
     }
     bool supports_fused_pcg() const override {
@@ -246,12 +564,20 @@ class CsrOperator : public Operator {
     }
     npc_status pcg_fused(const double *b, double *x, const double *coef_dev, int k, double tb, int use_poly,
                          double tol2b, int maxit, ClusterPcgOut *out, double *history) override {
-        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), vals.as<double>(), n_local, small.R, small.nnz_cta};
+        SmallCsrDev A{rowptr.as<int>(), cols.as<int>(), csr_vals(), n_local, small.R, small.nnz_cta};
         return launch_csr_pcg_cluster(ctx, A, small, b, x, coef_dev, k, tb, use_poly, tol2b, maxit, out, history);
     }
 
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
+        if (pattern) {
+            if (!multi || ctx->nranks == 1) return launch_pattern_set(s, pt_all, s.partials);
+            NPC_TRY(halo_start(ctx, plan, halo, s.x));
+            NPC_TRY(launch_pattern_set(s, pt_interior, s.partials));
+            NPC_TRY(halo_wait(ctx, halo));
+            return launch(s, tiles_boundary.as<int>(), n_boundary, s.partials ? s.partials + n_interior : nullptr,
+                          true);
+        }
         // single rank, or a 1-rank distributed context (no halo; with more ranks the exchange
         // is collective for the local transport even when this rank's plan is empty)
         if (!multi || ctx->nranks == 1) return launch(s, nullptr, ntiles, s.partials, false);
@@ -343,6 +669,321 @@ npc_status localize_columns(Context *ctx, const npc_operator_desc *d, HaloPlan &
     return NPC_SUCCESS;
 }
 
+
+// Host side of the pattern form.  Returns false (caller falls back to the coded/plain form)
+// when a tile has more than 256 distinct patterns, a table longer than PAT_TBL_MAX words, a row
+// with more than 256 own values, ELL padding above 1/8 of the own values, or a block larger
+// than the shared-memory budget.
+struct PatHost {
+    std::vector<double> vals;
+    std::vector<int> tptr, tbl, tbl_off;
+    std::vector<unsigned char> pat;
+    int vspan_max = 0, tbl_max = 0;
+    long long own_nnz = 0;  // stored values, padding included
+    // staged kernel: per-tile table [nwin, entry offset, npat, 0 | nwin x {ga, len, sbase, tail}
+    // | npat + 1 entry starts | (pad to 4) | entries {xb, vb, o, pos}], and which tiles stage
+    std::vector<int> tbl2, tbl2_off;
+    std::vector<char> stage;
+    int xspan_max = 0, tbl2_max = 0;
+};
+
+// x windows + decoded entries of one tile for k_csr_pat_stage (see there).  pstart/pent: the
+// tile's patterns as built by build_pattern.  Returns the table, or an empty vector when the
+// tile's windows do not fit the shared-memory budget (it then runs k_csr_pat_step).
+static std::vector<int> pattern_stage_table(int n, int row0, int nrows, int own_block, const std::vector<int> &pstart,
+                                            const std::vector<int> &pent, int *xspan) {
+    const int np = (int)pstart.size() - 1;
+    std::vector<int> offs(1, 0);  // offset 0 always: the epilogue's x[row] comes from its window
+    for (int w : pent) offs.push_back((w & 1) ? (w >> 9) : (w >> 1));
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    struct Win { long long a, b; };
+    std::vector<Win> win;
+    for (int o : offs) {  // [row0 + o, row0 + o + nrows) clipped to the owned x, merged
+        const long long a = std::max<long long>(0, (long long)row0 + o),
+                        b = std::min<long long>(n, (long long)row0 + o + nrows);
+        if (a >= b) continue;
+        if (!win.empty() && a <= win.back().b + 64)
+            win.back().b = std::max(win.back().b, b);
+        else
+            win.push_back({a, b});
+    }
+    std::vector<int> t(4, 0), wdesc;
+    int sb = 0;
+    for (auto &w : win) {  // TMA part [ga, ga + len) even-aligned; an odd last element as a tail
+        const long long ga = w.a & ~1LL;
+        long long bt = (w.b + 1) & ~1LL;
+        int tail = 0;
+        if (bt > n) {
+            bt = w.b - 1;
+            tail = 1;
+        }
+        const int len = (int)(bt - ga);
+        wdesc.insert(wdesc.end(), {(int)ga, len, sb, tail});
+        sb += (len + tail + 1) & ~1;
+    }
+    *xspan = sb;
+    t[0] = (int)win.size();
+    t.insert(t.end(), wdesc.begin(), wdesc.end());
+    const int sidx = (int)t.size();
+    t.resize(sidx + np + 1);
+    while (t.size() % 4) t.push_back(0);
+    t[1] = (int)t.size();
+    t[2] = np;
+    {  // header slot 3: x base of offset 0 (x[row0 + lr] = sx[t[3] + lr])
+        int wi = 0;
+        while (wi + 1 < (int)win.size() && win[wi + 1].a <= row0) ++wi;
+        t[3] = wdesc[4 * wi + 2] + (row0 - wdesc[4 * wi]);
+    }
+    for (int q = 0; q < np; ++q) {
+        t[sidx + q] = (int)(t.size() - t[1]) / 4;
+        int k = 0;
+        for (int e = pstart[q]; e < pstart[q + 1]; ++e) {
+            const int w = pent[e];
+            const int o = (w & 1) ? (w >> 9) : (w >> 1);
+            const long long c0 = (long long)row0 + o;  // column of the tile's first row
+            int wi = 0;
+            while (wi + 1 < (int)win.size() && win[wi + 1].a <= std::max<long long>(c0, 0)) ++wi;
+            const int xb = wdesc[4 * wi + 2] + (int)(c0 - wdesc[4 * wi]);
+            if (w & 1) {
+                const int pos = (w >> 1) & 255;
+                t.insert(t.end(), {xb, pos * nrows + o, o, pos});
+            } else {
+                t.insert(t.end(), {xb, k * nrows, 0, 0});
+                ++k;
+            }
+        }
+    }
+    t[sidx + np] = (int)(t.size() - t[1]) / 4;
+    if ((size_t)own_block * 8 + (size_t)sb * 8 + t.size() * 4 > (size_t)PAT_STAGE_SMEM) return {};
+    return t;
+}
+
+static bool build_pattern(int n, long long row_begin, const int *rowptr, const int *gcol, const std::vector<int> &lcols,
+                          const double *vals, bool mirror, bool stage, PatHost &ph) {
+    const long long nnz = rowptr[n];
+    // 1. mirror partners: a_ij (j < i, owned) whose transpose a_ji exists with the
+    //    bitwise-identical value (then a_ji is an upper entry of row j, hence always own)
+    std::vector<int> partner((size_t)nnz, -1);
+    if (mirror)
+        host_parallel_for(n, [&](long long b, long long e, int) {
+            for (long long i = b; i < e; ++i)
+                for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+                    const int c = lcols[p];
+                    if (c >= i || c < 0 || i - c >= PAT_MIRROR_MAX_OFF) continue;  // ghosts: c >= n > i
+                    const int *lo = gcol + rowptr[c], *hi = gcol + rowptr[c + 1];
+                    const int *q = std::lower_bound(lo, hi, (int)(row_begin + i));
+                    if (q != hi && *q == row_begin + i &&
+                        std::memcmp(&vals[q - gcol], &vals[p], sizeof(double)) == 0)
+                        partner[p] = (int)(q - gcol);
+                }
+        });
+    // 2. index of every own entry within its row's own list (mirror positions refer to it)
+    std::vector<unsigned char> opos((size_t)nnz, 0);
+    std::vector<int> rown((size_t)std::max(n, 1), 0);
+    std::vector<char> bad(64, 0);
+    host_parallel_for(n, [&](long long b, long long e, int t) {
+        for (long long i = b; i < e; ++i) {
+            int k = 0;
+            for (int p = rowptr[i]; p < rowptr[i + 1]; ++p)
+                if (partner[p] < 0) {
+                    if (k > 255) bad[t] = 1;
+                    opos[p] = (unsigned char)k++;
+                }
+            rown[i] = k;
+        }
+    });
+    for (char c : bad)
+        if (c) return false;
+    // 3. per tile: patterns (deduplicated by hash, then by words), ELL width, tables
+    const int ntiles = ceil_div(n, PAT_TILE);
+    std::vector<std::vector<int>> ttbl((size_t)ntiles);
+    std::vector<int> twidth((size_t)ntiles, 0), txs((size_t)ntiles, 0);
+    std::vector<std::vector<int>> ttbl2((size_t)ntiles);
+    ph.pat.assign((size_t)std::max(n, 1), 0);
+    std::vector<char> ok((size_t)ntiles, 1);
+    host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
+        std::vector<int> words, pstart, pent;
+        std::vector<unsigned long long> phash;
+        for (long long t = t0; t < t1; ++t) {
+            const int r0 = (int)t * PAT_TILE, r1 = std::min(n, r0 + PAT_TILE);
+            phash.clear();
+            pstart.assign(1, 0);
+            pent.clear();
+            int wmax = 0;
+            for (int i = r0; i < r1 && ok[t]; ++i) {
+                words.clear();
+                unsigned long long h = 1469598103934665603ull;
+                for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+                    const int o = lcols[p] - i;
+                    int w;
+                    if (partner[p] >= 0)
+                        w = (int)((unsigned)o << 9) | ((int)opos[partner[p]] << 1) | 1;
+                    else
+                        w = (int)((unsigned)o << 1);
+                    words.push_back(w);
+                    h = (h ^ (unsigned)w) * 1099511628211ull;
+                }
+                h ^= words.size();
+                int id = -1;
+                for (int q = 0; q < (int)phash.size() && id < 0; ++q)
+                    if (phash[q] == h && pstart[q + 1] - pstart[q] == (int)words.size() &&
+                        std::equal(words.begin(), words.end(), pent.begin() + pstart[q]))
+                        id = q;
+                if (id < 0) {
+                    if (phash.size() == 256) {
+                        ok[t] = 0;
+                        break;
+                    }
+                    id = (int)phash.size();
+                    phash.push_back(h);
+                    pent.insert(pent.end(), words.begin(), words.end());
+                    pstart.push_back((int)pent.size());
+                }
+                ph.pat[i] = (unsigned char)id;
+                wmax = std::max(wmax, rown[i]);
+            }
+            if (!ok[t]) continue;
+            const int np = (int)phash.size();
+            std::vector<int> &tb = ttbl[t];  // [np + 1 absolute starts][entries]
+            tb.resize((size_t)np + 1 + pent.size());
+            for (int q = 0; q <= np; ++q) tb[q] = np + 1 + pstart[q];
+            std::copy(pent.begin(), pent.end(), tb.begin() + np + 1);
+            if ((int)tb.size() > PAT_TBL_MAX) ok[t] = 0;
+            twidth[t] = wmax;
+            bool ghost = false;  // tiles with ghost columns run k_csr_pat_step (x not windowed)
+            for (int p = rowptr[r0]; p < rowptr[r1] && !ghost; ++p) ghost = lcols[p] >= n;
+            if (!ghost && stage) {
+                const int nr = r1 - r0;
+                ttbl2[t] = pattern_stage_table(n, r0, nr, (wmax * nr + 1) & ~1, pstart, pent, &txs[t]);
+            }
+        }
+    }, 64);
+    for (char c : ok)
+        if (!c) return false;
+    ph.tptr.assign((size_t)ntiles + 1, 0);
+    ph.tbl_off.assign((size_t)ntiles + 1, 0);
+    long long real = 0;
+    for (int i = 0; i < n; ++i) real += rown[i];
+    for (int t = 0; t < ntiles; ++t) {
+        const int nr = std::min(PAT_TILE, n - t * PAT_TILE);
+        const long long blk = ((long long)twidth[t] * nr + 1) & ~1LL;  // even: 16-byte aligned blocks
+        if (ph.tptr[t] + blk > INT_MAX) return false;
+        ph.tptr[t + 1] = ph.tptr[t] + (int)blk;
+        ph.tbl_off[t + 1] = ph.tbl_off[t] + (int)ttbl[t].size();
+        ph.vspan_max = std::max(ph.vspan_max, (int)blk);
+        ph.tbl_max = std::max(ph.tbl_max, (int)ttbl[t].size());
+    }
+    ph.own_nnz = ph.tptr[ntiles];
+    if (8 * (ph.own_nnz - real) > real + 8LL * ntiles) return false;  // ELL padding above 1/8
+    ph.tbl_max = (ph.tbl_max + 3) & ~3;
+    if ((size_t)ph.vspan_max * 8 + (size_t)ph.tbl_max * 4 > (size_t)CSR_MAX_SMEM) return false;
+    ph.tbl.resize((size_t)ph.tbl_off[ntiles]);
+    ph.stage.assign((size_t)ntiles, 0);
+    ph.tbl2_off.assign((size_t)ntiles + 1, 0);
+    for (int t = 0; t < ntiles; ++t) {
+        if (ttbl2[t].empty()) ttbl2[t] = {0, 4, 0, 0};  // unstaged tile: an empty header
+        else ph.stage[t] = 1, ph.xspan_max = std::max(ph.xspan_max, txs[t]);
+        ph.tbl2_off[t + 1] = ph.tbl2_off[t] + (int)ttbl2[t].size();
+        ph.tbl2_max = std::max(ph.tbl2_max, (int)ttbl2[t].size());
+    }
+    ph.tbl2.resize((size_t)ph.tbl2_off[ntiles]);
+    for (int t = 0; t < ntiles; ++t) std::copy(ttbl2[t].begin(), ttbl2[t].end(), ph.tbl2.begin() + ph.tbl2_off[t]);
+    ph.vals.assign((size_t)ph.own_nnz + 8, 0.0);
+    host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
+        for (long long t = t0; t < t1; ++t) {
+            std::copy(ttbl[t].begin(), ttbl[t].end(), ph.tbl.begin() + ph.tbl_off[t]);
+            const int r0 = (int)t * PAT_TILE, r1 = std::min(n, r0 + PAT_TILE), nr = r1 - r0;
+            double *blk = ph.vals.data() + ph.tptr[t];
+            for (int i = r0; i < r1; ++i)
+                for (int p = rowptr[i]; p < rowptr[i + 1]; ++p)
+                    if (partner[p] < 0) blk[(size_t)opos[p] * nr + (i - r0)] = vals[p];
+        }
+    }, 64);
+    return true;
+}
+
+// Upload a pattern-form operator (PatHost from build_pattern) and build its tile lists.
+static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc *d, CsrOperator &op, PatHost &ph,
+                                          const std::vector<int> &lcols) {
+    const int n = d->n_local;
+    op.ntiles = ceil_div(n, PAT_TILE);
+    op.own_nnz = ph.own_nnz;
+    op.tbl_total = (long long)ph.tbl.size();
+    op.vspan_max = ph.vspan_max;
+    op.tbl_max = ph.tbl_max;
+    op.smem_bytes = (size_t)ph.vspan_max * 8 + (size_t)ph.tbl_max * 4;
+    op.staged = true;
+    std::vector<int> ti, tb;
+    for (int t = 0; t < op.ntiles; ++t) {
+        const int r0 = t * PAT_TILE, r1 = std::min(n, r0 + PAT_TILE);
+        bool ghost = false;
+        if (op.multi)
+            for (int p = d->rowptr[r0]; p < d->rowptr[r1] && !ghost; ++p) ghost = lcols[p] >= n;
+        (ghost ? tb : ti).push_back(t);
+    }
+    op.n_interior = (int)ti.size();
+    op.n_boundary = (int)tb.size();
+    op.xspan_max = ph.xspan_max;
+    op.tbl2_max = (ph.tbl2_max + 3) & ~3;
+    op.smem_stage = ((size_t)ph.vspan_max + (size_t)ph.xspan_max) * 8 + (size_t)op.tbl2_max * 4;
+    auto split = [&](const std::vector<int> &list, CsrOperator::PatTiles &pt) -> npc_status {
+        std::vector<int> st, un;
+        for (int t : list) (ph.stage[t] ? st : un).push_back(t);
+        pt.ns = (int)st.size();
+        pt.nu = (int)un.size();
+        pt.identity = true;
+        for (int q = 0; q < pt.ns && pt.identity; ++q) pt.identity = st[q] == q;
+        NPC_TRY(pt.staged.alloc(sizeof(int) * std::max<size_t>(st.size(), 1)));
+        NPC_TRY(pt.unstaged.alloc(sizeof(int) * std::max<size_t>(un.size(), 1)));
+        if (!st.empty()) NPC_CUDA_TRY(cudaMemcpy(pt.staged.p, st.data(), sizeof(int) * st.size(), cudaMemcpyHostToDevice));
+        if (!un.empty()) NPC_CUDA_TRY(cudaMemcpy(pt.unstaged.p, un.data(), sizeof(int) * un.size(), cudaMemcpyHostToDevice));
+        return NPC_SUCCESS;
+    };
+    {
+        std::vector<int> all((size_t)op.ntiles);
+        for (int t = 0; t < op.ntiles; ++t) all[t] = t;
+        NPC_TRY(split(all, op.pt_all));
+        if (op.multi) NPC_TRY(split(ti, op.pt_interior));
+    }
+    NPC_TRY(op.tbl2.alloc(sizeof(int) * std::max<size_t>(ph.tbl2.size(), 1)));
+    NPC_TRY(op.tbl2_off.alloc(sizeof(int) * ph.tbl2_off.size()));
+    if (!ph.tbl2.empty())
+        NPC_CUDA_TRY(cudaMemcpy(op.tbl2.p, ph.tbl2.data(), sizeof(int) * ph.tbl2.size(), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemcpy(op.tbl2_off.p, ph.tbl2_off.data(), sizeof(int) * ph.tbl2_off.size(), cudaMemcpyHostToDevice));
+    if (!op.multi && !plan_csr_poly_cluster(n, d->rowptr, op.small)) op.small = SmallCsrPlan{};
+    // the cluster-resident small-operator kernels read the plain arrays
+    if (op.small.cl_size > 0) {
+        NPC_TRY(op.rowptr.alloc(sizeof(int) * (n + 1)));
+        NPC_TRY(op.cols.alloc(sizeof(int) * (op.nnz + 8)));
+        NPC_TRY(op.cvals.alloc(sizeof(double) * (op.nnz + 8)));
+        NPC_CUDA_TRY(cudaMemcpy(op.rowptr.p, d->rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op.cols.p, lcols.data(), sizeof(int) * op.nnz, cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op.cvals.p, d->vals, sizeof(double) * op.nnz, cudaMemcpyHostToDevice));
+    }
+    NPC_TRY(op.vals.alloc(sizeof(double) * ph.vals.size()));
+    NPC_TRY(op.tptr.alloc(sizeof(int) * ph.tptr.size()));
+    NPC_TRY(op.pat.alloc(ph.pat.size()));
+    NPC_TRY(op.tbl.alloc(sizeof(int) * std::max<size_t>(ph.tbl.size(), 1)));
+    NPC_TRY(op.tbl_off.alloc(sizeof(int) * ph.tbl_off.size()));
+    NPC_CUDA_TRY(cudaMemcpy(op.vals.p, ph.vals.data(), sizeof(double) * ph.vals.size(), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemcpy(op.tptr.p, ph.tptr.data(), sizeof(int) * ph.tptr.size(), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemcpy(op.pat.p, ph.pat.data(), ph.pat.size(), cudaMemcpyHostToDevice));
+    if (!ph.tbl.empty())
+        NPC_CUDA_TRY(cudaMemcpy(op.tbl.p, ph.tbl.data(), sizeof(int) * ph.tbl.size(), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemcpy(op.tbl_off.p, ph.tbl_off.data(), sizeof(int) * ph.tbl_off.size(), cudaMemcpyHostToDevice));
+    if (op.multi) {
+        NPC_TRY(op.tiles_interior.alloc(sizeof(int) * std::max<size_t>(ti.size(), 1)));
+        NPC_TRY(op.tiles_boundary.alloc(sizeof(int) * std::max<size_t>(tb.size(), 1)));
+        if (!ti.empty())
+            NPC_CUDA_TRY(cudaMemcpy(op.tiles_interior.p, ti.data(), sizeof(int) * ti.size(), cudaMemcpyHostToDevice));
+        if (!tb.empty())
+            NPC_CUDA_TRY(cudaMemcpy(op.tiles_boundary.p, tb.data(), sizeof(int) * tb.size(), cudaMemcpyHostToDevice));
+        NPC_TRY(halo_setup(ctx, op.plan, op.halo));
+    }
+    return NPC_SUCCESS;
+}
+
 npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out) {
     NPC_TRY(validate_csr_desc(ctx, d));
     auto op = std::make_unique<CsrOperator>();
@@ -354,6 +995,19 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     const int n = d->n_local;
     const long long nnz = d->rowptr[n];
     op->nnz = nnz;
+    std::vector<int> lcols;
+    NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
+    op->multi = ctx->distributed();
+    if (!getenv("NPC_CSR_PLAIN") && !getenv("NPC_CSR_CODED") && nnz > 0) {
+        PatHost ph;
+        if (build_pattern(n, d->row_begin, d->rowptr, d->colidx, lcols, d->vals, !getenv("NPC_CSR_NOMIRROR"),
+                          !getenv("NPC_CSR_NOSTAGE"), ph)) {
+            op->pattern = true;
+            NPC_TRY(finish_pattern_operator(ctx, d, *op, ph, lcols));
+            out = std::move(op);
+            return NPC_SUCCESS;
+        }
+    }
     // the values upload (the largest array) runs on a helper thread while the host builds the
     // column form; joined before any return
     NPC_TRY(op->vals.alloc(sizeof(double) * (nnz + 8)));
@@ -373,9 +1027,6 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
                 up_err = cudaMemcpy(op->vals.p, d->vals, sizeof(double) * nnz, cudaMemcpyHostToDevice);
         });
     }
-    std::vector<int> lcols;
-    NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
-    op->multi = ctx->distributed();
     // coded column ids: per tile of CSR_TILE_CODED rows, the distinct offsets col - row (<= 256,
     // first-seen order) and a byte per entry; any tile with more -> the plain form on CSR_TILE rows
     const int ntc = ceil_div(n, CSR_TILE_CODED);

@@ -34,13 +34,23 @@ def dev(a):
     return torch.tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")
 
 
+FORM_ENV = {"plain": "NPC_CSR_PLAIN", "coded": "NPC_CSR_CODED", "nomirror": "NPC_CSR_NOMIRROR",
+            "nostage": "NPC_CSR_NOSTAGE"}
+
+
 def make(ctx, w, plain):
-    if plain:
-        os.environ["NPC_CSR_PLAIN"] = "1"
+    """plain: True -> int32 column ids, False -> the coded form; or a form name: 'pattern'
+    (the default form), 'nomirror' (pattern ids without symmetric mirroring), 'nostage' (pattern
+    form without the x-window staging kernel), 'coded', 'plain'."""
+    form = ("plain" if plain else "coded") if isinstance(plain, bool) else plain
+    env = FORM_ENV.get(form)
+    if env:
+        os.environ[env] = "1"
     try:
         return npc.create_from_workload(ctx, w, "csr")
     finally:
-        os.environ.pop("NPC_CSR_PLAIN", None)
+        if env:
+            os.environ.pop(env, None)
 
 
 WL = {"c3": lambda: W.config3(side=30), "c1": lambda: W.config1(side=64),
@@ -174,7 +184,7 @@ def empty_tile_csr(n=3000, first=18, empty_to=1600):
                 vals=np.arange(1, len(rows) + 1, dtype=np.float64))
 
 
-@pytest.mark.parametrize("plain", [False, True])
+@pytest.mark.parametrize("plain", ["pattern", "coded", "plain"])
 def test_empty_tiles_at_unaligned_offsets(ctx, plain):
     w = empty_tile_csr()
     op = make(ctx, w, plain)
