@@ -9,8 +9,10 @@
  * paper's counter laws (Table tab11).
  *
  * Conventions (all entry points):
- *  - Every call returns npc_status and never aborts or exits; npc_last_error() returns a
- *    thread-local message describing the last failing call on this thread.
+ *  - Every call returns npc_status and never aborts or exits; npc_last_error(ctx) returns
+ *    the message of the last failing call made on ctx (through ctx or a handle created
+ *    from it), npc_last_error(NULL) that of the last failing call on this thread (including
+ *    calls that failed before a context was known, e.g. on a NULL handle).
  *  - Pointers named *_dev are CUDA device pointers owned by the CALLER, on the context's
  *    device, holding fp64 values of the rank's n_local owned rows (contiguous, 8-byte
  *    aligned; 16-byte alignment is faster).  Everything else (operator storage, work
@@ -75,7 +77,10 @@ NPC_API npc_status npc_context_create_local(int device, int nranks, int rank, co
                                     void *cuda_stream, npc_context *out);
 NPC_API npc_status npc_context_destroy(npc_context ctx);
 NPC_API npc_status npc_get_unique_id(void *out128);
-NPC_API const char *npc_last_error(void);
+/* Message of the last failing call on ctx (ctx != NULL) or on the calling thread (NULL);
+ * "" if none.  The pointer stays valid until the next failing call on the same context /
+ * thread (or until npc_context_destroy).                                                   */
+NPC_API const char *npc_last_error(npc_context ctx);
 /* Version string, e.g. "npc 0.1 sm_100a". */
 NPC_API const char *npc_version(void);
 /* Number of CUDA kernels this library has launched in the process so far (all contexts). */
@@ -189,18 +194,22 @@ NPC_API npc_status npc_apply_operator(npc_operator op, const double *x_dev, doub
 
 /* ---- spectrum estimate (replaces the paper's DACG) ---------------------
  * nsteps-step Lanczos (no reorthogonalisation) from v0_dev, or, when v0_dev is NULL, from the
- * counter-hash vector uniform[-1,1) (splitmix64 of seed 0x5EED and the GLOBAL row index + 1,
- * so every partition draws the same vector; workloads.lanczos_start is the same generator).
+ * counter-hash vector uniform[-1,1) (splitmix64 of `seed` and the GLOBAL row index + 1, so
+ * every partition draws the same vector; workloads.lanczos_start(n, seed=...) is the same
+ * generator; NPC_DEFAULT_SEED = 0x5EED is the library's and the tests' default).  seed is
+ * ignored when v0_dev != NULL.  The wall time of the call is kept on the operator and
+ * reported as part of npc_pcg_stats.setup_seconds by solves with a poly set after it.
  * *lmin = smallest Ritz value of T_s (an over-estimate of lambda_min: harmless for the
  * polynomial); *lmax = theta_max + rho, the largest Ritz value plus its residual norm
  * rho = beta_s |e_s^T s| -- an upper estimate of lambda_max, because an interval that misses
  * the top of the spectrum makes p_k(A) grow like T_{k+1} there (reading A11).
  * Stops early (and succeeds, rho = 0) on an exact invariant subspace.  COLLECTIVE.
  * The _ex variant writes {theta_min, theta_max, rho, steps taken} to out4 (host).          */
+#define NPC_DEFAULT_SEED 0x5EEDull
 NPC_API npc_status npc_estimate_spectrum(npc_operator op, int nsteps, const double *v0_dev,
-                                 double *lmin, double *lmax);
+                                 unsigned long long seed, double *lmin, double *lmax);
 NPC_API npc_status npc_estimate_spectrum_ex(npc_operator op, int nsteps, const double *v0_dev,
-                                    double *out4);
+                                    unsigned long long seed, double *out4);
 
 /* ---- polynomial preconditioner (Alg. 2) --------------------------------
  * degree k >= 0 (k applications of A per npc_apply_poly), interval [lmin, lmax] with
@@ -227,7 +236,7 @@ NPC_API npc_status npc_set_poly_newton(npc_operator op, int nlev, double lmin, d
 NPC_API npc_status npc_poly_set_lowrank(npc_poly poly, int p, const double *V_dev);
 /* Approximate leftmost eigenvectors: nsteps-step Lanczos with FULL reorthogonalisation
  * (stores nsteps+1 basis vectors on the device) from v0_dev or, when NULL, the counter-hash
- * start of npc_estimate_spectrum; the Ritz pairs of the p smallest Ritz values of T_nsteps
+ * start of npc_estimate_spectrum with NPC_DEFAULT_SEED; the Ritz pairs of the p smallest Ritz values of T_nsteps
  * are written to theta_out[p] (host, ascending) and V_dev (p vectors of n_local rows, vector
  * j at V_dev + j*n_local, caller-owned, unit 2-norm).  1 <= p <= 16, p <= nsteps <= 4096.
  * NPC_ERR_BREAKDOWN if the Krylov space is exhausted before p steps.  COLLECTIVE.          */
@@ -242,8 +251,8 @@ NPC_API npc_status npc_apply_poly(npc_poly poly, const double *r_dev, double *z_
  * Solve A x = b with PCG preconditioned by poly (NULL -> plain CG), single-reduction
  * (Chronopoulos-Gear) form with the dot products fused into the producing kernels.
  * x_dev: in = x0, out = solution.  Stops when ||r_i|| / ||b|| <= tol on the recursive
- * residual; then the true residual is formed and, if above tol, replaces r and the
- * iteration continues (readings A5, A23).  tol in (0,1), maxit >= 1.
+ * residual; then the true residual is formed and, if above tol, replaces r and PCG
+ * restarts from the current x (at most 50 times; readings A5, A23).  tol in (0,1), maxit >= 1.
  * b == 0 -> x = 0, iters = 0, NPC_SUCCESS.  COLLECTIVE.                                     */
 typedef struct {
     int iters;                   /* x updates                                               */
@@ -258,6 +267,11 @@ typedef struct {
                                     correction, +1 each for ||b||, ||r_0||, true residual   */
     double relres_recursive;     /* ||r_iters|| / ||b|| (recursive residual)                */
     double relres_true;          /* ||b - A x|| / ||b|| of the returned x                   */
+    double setup_seconds;        /* the preconditioner's setup, reported separately as the
+                                    paper does for its eigenvalue estimate:
+                                    wall time of the last npc_estimate_spectrum on the
+                                    operator before npc_set_poly + that npc_set_poly (0 for
+                                    plain CG); not part of solve_seconds                    */
     double solve_seconds;        /* wall time of the call                                   */
     double *history;             /* optional caller HOST buffer of length maxit + 1, or NULL:
                                     history[i] = ||r_i|| / ||b||, i = 0..iters               */

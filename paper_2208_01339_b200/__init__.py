@@ -61,7 +61,7 @@ class OperatorDesc(C.Structure):
 class PcgStats(C.Structure):
     _fields_ = [("iters", C.c_int), ("converged", C.c_int), ("op_applications", C.c_longlong),
                 ("reductions", C.c_longlong), ("relres_recursive", C.c_double),
-                ("relres_true", C.c_double), ("solve_seconds", C.c_double),
+                ("relres_true", C.c_double), ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
                 ("history", C.POINTER(C.c_double))]
 
 
@@ -84,8 +84,8 @@ def lib():
             "npc_destroy_operator": [P],
             "npc_operator_matrix_bytes": [P, C.POINTER(D)],
             "npc_apply_operator": [P, P, P],
-            "npc_estimate_spectrum": [P, I, P, C.POINTER(D), C.POINTER(D)],
-            "npc_estimate_spectrum_ex": [P, I, P, P],
+            "npc_estimate_spectrum": [P, I, P, C.c_ulonglong, C.POINTER(D), C.POINTER(D)],
+            "npc_estimate_spectrum_ex": [P, I, P, C.c_ulonglong, P],
             "npc_set_poly": [P, I, D, D, D, C.POINTER(P)],
             "npc_set_poly_newton": [P, I, D, D, D, C.POINTER(P)],
             "npc_destroy_poly": [P],
@@ -104,15 +104,21 @@ def lib():
             f.argtypes = args
             f.restype = C.c_int
         L.npc_last_error.restype = C.c_char_p
+        L.npc_last_error.argtypes = [P]
         L.npc_version.restype = C.c_char_p
         L.npc_launch_count.restype = C.c_ulonglong
         _lib = L
     return _lib
 
 
+def npc_last_error(ctx=None) -> str:
+    """Message of the last failing call on ctx (a Context), or on this thread (None)."""
+    return lib().npc_last_error(ctx.h if ctx is not None else None).decode(errors="replace")
+
+
 def _check(code):
     if code != 0:
-        raise NpcError(code, lib().npc_last_error().decode(errors="replace"))
+        raise NpcError(code, lib().npc_last_error(None).decode(errors="replace"))
 
 
 def _ptr(t):
@@ -284,16 +290,19 @@ def npc_apply_operator(op: Operator, x, y):
     _check(lib().npc_apply_operator(op.h, _ptr(x), _ptr(y)))
 
 
-def npc_estimate_spectrum(op: Operator, nsteps: int = 20, v0=None):
+NPC_DEFAULT_SEED = 0x5EED
+
+
+def npc_estimate_spectrum(op: Operator, nsteps: int = 20, v0=None, seed: int = NPC_DEFAULT_SEED):
     lo, hi = C.c_double(), C.c_double()
-    _check(lib().npc_estimate_spectrum(op.h, int(nsteps), _ptr(v0), C.byref(lo), C.byref(hi)))
+    _check(lib().npc_estimate_spectrum(op.h, int(nsteps), _ptr(v0), int(seed), C.byref(lo), C.byref(hi)))
     return lo.value, hi.value
 
 
-def npc_estimate_spectrum_ex(op: Operator, nsteps: int = 20, v0=None):
+def npc_estimate_spectrum_ex(op: Operator, nsteps: int = 20, v0=None, seed: int = NPC_DEFAULT_SEED):
     """-> dict(theta_min, theta_max, rho, steps)."""
     out = np.zeros(4)
-    _check(lib().npc_estimate_spectrum_ex(op.h, int(nsteps), _ptr(v0), out.ctypes.data_as(C.c_void_p)))
+    _check(lib().npc_estimate_spectrum_ex(op.h, int(nsteps), _ptr(v0), int(seed), out.ctypes.data_as(C.c_void_p)))
     return dict(theta_min=out[0], theta_max=out[1], rho=out[2], steps=int(out[3]))
 
 
@@ -363,11 +372,12 @@ def npc_pcg_solve(poly: Poly | None, op: Operator, b, x, tol: float, maxit: int,
     out = dict(status=STATUS.get(code, code), iters=st.iters, converged=bool(st.converged),
                op_applications=st.op_applications, reductions=st.reductions,
                relres_recursive=st.relres_recursive, relres_true=st.relres_true,
-               solve_seconds=st.solve_seconds)
+               setup_seconds=st.setup_seconds, solve_seconds=st.solve_seconds)
     if history:
         out["history"] = hist[: st.iters + 1]
     if raise_on_error and code not in (0,):
-        raise NpcError(code, lib().npc_last_error().decode(errors="replace") + f" (stats {out})")
+        raise NpcError(code, lib().npc_last_error(op.ctx.h if hasattr(op, "ctx") else None).decode(errors="replace")
+                       + f" (stats {out})")
     return out
 
 

@@ -3,6 +3,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 
 #include "npc_internal.cuh"
@@ -10,18 +11,31 @@
 namespace npc {
 std::atomic<unsigned long long> g_launches{0};
 static thread_local char g_err[1024] = "";
+// The context of the API call in progress on this thread (ErrScope): set_error also records
+// the message there, for npc_last_error(ctx).
+static thread_local npc_context g_cur = nullptr;
 void set_error(const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
+    if (g_cur) memcpy(g_cur->err, g_err, sizeof(g_err));
+}
+struct ErrScope {
+    npc_context prev;
+    explicit ErrScope(npc_context c) : prev(g_cur) { g_cur = c; }
+    ~ErrScope() { g_cur = prev; }
+};
+static double wall_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 npc_status poly_coefficients(int k, double lmin, double lmax, double xi, double *theta_bar, double *delta,
                              double *sigma, double *coef);
 npc_status apply_poly(npc_poly P, const double *r, double *z);
 npc_status apply_operator(Operator *op, const double *x, double *y, DevBuf &scratch);
 npc_status pcg(npc_poly P, npc_operator H, const double *b, double *x, double tol, int maxit, npc_pcg_stats *stats);
-npc_status lanczos(Operator *op, int m, const double *v0, double *lmin, double *lmax, double *out_ex);
+npc_status lanczos(Operator *op, int m, const double *v0, unsigned long long seed, double *lmin, double *lmax,
+                   double *out_ex);
 npc_status newton_zetas(int nlev, double lmin, double lmax, double xi, std::vector<double> &zeta);
 }  // namespace npc
 
@@ -49,7 +63,7 @@ struct DeviceScope {
 
 extern "C" {
 
-const char *npc_last_error(void) { return g_err; }
+const char *npc_last_error(npc_context ctx) { return ctx ? ctx->err : g_err; }
 unsigned long long npc_launch_count(void) { return g_launches.load(); }
 const char *npc_version(void) { return "npc 0.2 sm_100a (fp64, CSR/SELL/stencil/Schur/DFN/callback)"; }
 
@@ -120,12 +134,14 @@ npc_status npc_context_create_local(int device, int nranks, int rank, const char
 
 npc_status npc_context_set_timing(npc_context ctx, int enable) {
     NPC_GUARD(ctx, NPC_ERR_INVALID_ARGUMENT, "npc_context_set_timing: null context");
+    ErrScope es(ctx);
     ctx->ctx.timing = enable != 0;
     return NPC_SUCCESS;
 }
 
 npc_status npc_context_get_timing(npc_context ctx, double *ms_out, long long *launches_out) {
     NPC_GUARD(ctx, NPC_ERR_INVALID_ARGUMENT, "npc_context_get_timing: null context");
+    ErrScope es(ctx);
     DeviceScope ds(ctx->ctx.device);
     NPC_CUDA_TRY(cudaStreamSynchronize(ctx->ctx.stream));
     ctx->ctx.t_flush();
@@ -156,6 +172,7 @@ npc_status npc_context_destroy(npc_context ctx) {
 
 npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, npc_operator *out) {
     NPC_GUARD(ctx && desc && out, NPC_ERR_INVALID_ARGUMENT, "npc_create_operator: null argument");
+    ErrScope es(ctx);
     *out = nullptr;
     NPC_GUARD(desc->n_local >= 0 && desc->row_begin >= 0, NPC_ERR_DIMENSION, "npc_create_operator: negative size");
     if (!ctx->ctx.distributed())
@@ -189,6 +206,7 @@ npc_status npc_create_operator(npc_context ctx, const npc_operator_desc *desc, n
 
 npc_status npc_operator_matrix_bytes(npc_operator op, double *bytes) {
     NPC_GUARD(op && bytes, NPC_ERR_INVALID_ARGUMENT, "npc_operator_matrix_bytes: null argument");
+    ErrScope es(op->owner);
     *bytes = op->op->matrix_bytes();
     return NPC_SUCCESS;
 }
@@ -205,6 +223,7 @@ npc_status npc_destroy_operator(npc_operator op) {
 }
 
 npc_status npc_apply_operator(npc_operator op, const double *x_dev, double *y_dev) {
+    ErrScope es(op ? op->owner : nullptr);
     NPC_GUARD(op && (x_dev || op->op->n_local == 0) && (y_dev || op->op->n_local == 0), NPC_ERR_INVALID_ARGUMENT,
               "npc_apply_operator: null argument");
     NPC_GUARD(x_dev != y_dev || op->op->n_local == 0, NPC_ERR_INVALID_ARGUMENT, "npc_apply_operator: x aliases y");
@@ -213,21 +232,31 @@ npc_status npc_apply_operator(npc_operator op, const double *x_dev, double *y_de
     return apply_operator(op->op.get(), x_dev, y_dev, scratch);
 }
 
-npc_status npc_estimate_spectrum(npc_operator op, int nsteps, const double *v0_dev, double *lmin, double *lmax) {
+npc_status npc_estimate_spectrum(npc_operator op, int nsteps, const double *v0_dev, unsigned long long seed,
+                                 double *lmin, double *lmax) {
+    ErrScope es(op ? op->owner : nullptr);
     NPC_GUARD(op && lmin && lmax, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum: null argument");
     NPC_GUARD(nsteps >= 1 && nsteps <= 100000, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum: nsteps %d", nsteps);
     NPC_GUARD(op->op->n_global >= 1, NPC_ERR_DIMENSION, "npc_estimate_spectrum: empty operator");
     DeviceScope ds(op->owner->ctx.device);
-    return lanczos(op->op.get(), nsteps, v0_dev, lmin, lmax, nullptr);
+    const double t0 = wall_s();
+    const npc_status st = lanczos(op->op.get(), nsteps, v0_dev, seed, lmin, lmax, nullptr);
+    op->estimate_seconds = wall_s() - t0;
+    return st;
 }
 
-npc_status npc_estimate_spectrum_ex(npc_operator op, int nsteps, const double *v0_dev, double *out4) {
+npc_status npc_estimate_spectrum_ex(npc_operator op, int nsteps, const double *v0_dev, unsigned long long seed,
+                                    double *out4) {
+    ErrScope es(op ? op->owner : nullptr);
     NPC_GUARD(op && out4, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum_ex: null argument");
     NPC_GUARD(nsteps >= 1 && nsteps <= 100000, NPC_ERR_INVALID_ARGUMENT, "npc_estimate_spectrum_ex: nsteps %d", nsteps);
     NPC_GUARD(op->op->n_global >= 1, NPC_ERR_DIMENSION, "npc_estimate_spectrum_ex: empty operator");
     DeviceScope ds(op->owner->ctx.device);
     double lo, hi;
-    return lanczos(op->op.get(), nsteps, v0_dev, &lo, &hi, out4);
+    const double t0 = wall_s();
+    const npc_status st = lanczos(op->op.get(), nsteps, v0_dev, seed, &lo, &hi, out4);
+    op->estimate_seconds = wall_s() - t0;
+    return st;
 }
 
 npc_status npc_poly_coefficients(int degree, double lmin, double lmax, double xi, double *theta_bar, double *delta,
@@ -237,7 +266,9 @@ npc_status npc_poly_coefficients(int degree, double lmin, double lmax, double xi
 }
 
 npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, double xi, npc_poly *out) {
+    ErrScope es(op ? op->owner : nullptr);
     NPC_GUARD(op && out, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly: null argument");
+    const double t0 = wall_s();
     *out = nullptr;
     NPC_GUARD(degree <= 100000, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly: degree %d too large", degree);
     auto P = std::make_unique<npc_poly_s>();
@@ -262,12 +293,15 @@ npc_status npc_set_poly(npc_operator op, int degree, double lmin, double lmax, d
         NPC_TRY(P->rin.alloc(sizeof(double) * n));
         NPC_TRY(P->zout.alloc(sizeof(double) * n));
     }
+    P->setup_seconds = op->estimate_seconds + (wall_s() - t0);
     *out = P.release();
     return NPC_SUCCESS;
 }
 
 npc_status npc_set_poly_newton(npc_operator op, int nlev, double lmin, double lmax, double xi, npc_poly *out) {
+    ErrScope es(op ? op->owner : nullptr);
     NPC_GUARD(op && out, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly_newton: null argument");
+    const double t0 = wall_s();
     *out = nullptr;
     NPC_GUARD(nlev >= 0 && nlev <= 16, NPC_ERR_INVALID_ARGUMENT, "npc_set_poly_newton: nlev %d not in [0, 16]", nlev);
     auto P = std::make_unique<npc_poly_s>();
@@ -289,12 +323,14 @@ npc_status npc_set_poly_newton(npc_operator op, int nlev, double lmin, double lm
         NPC_TRY(P->rin.alloc(sizeof(double) * n));
         NPC_TRY(P->zout.alloc(sizeof(double) * n));
     }
+    P->setup_seconds = op->estimate_seconds + (wall_s() - t0);
     *out = P.release();
     return NPC_SUCCESS;
 }
 
 npc_status npc_poly_set_lowrank(npc_poly poly, int p, const double *V_dev) {
     NPC_GUARD(poly, NPC_ERR_INVALID_ARGUMENT, "npc_poly_set_lowrank: null poly");
+    ErrScope es(poly->op->owner);
     NPC_GUARD(p >= 0 && p <= NPC_LOWRANK_MAX, NPC_ERR_INVALID_ARGUMENT, "npc_poly_set_lowrank: p %d not in [0, %d]", p,
               NPC_LOWRANK_MAX);
     NPC_GUARD(p == 0 || poly->op->op->n_local == 0 || V_dev, NPC_ERR_INVALID_ARGUMENT, "npc_poly_set_lowrank: null V");
@@ -306,6 +342,7 @@ npc_status npc_poly_set_lowrank(npc_poly poly, int p, const double *V_dev) {
 npc_status npc_ritz_vectors(npc_operator op, int nsteps, int p, const double *v0_dev, double *V_dev,
                             double *theta_out) {
     NPC_GUARD(op && theta_out, NPC_ERR_INVALID_ARGUMENT, "npc_ritz_vectors: null argument");
+    ErrScope es(op->owner);
     NPC_GUARD(p >= 1 && p <= NPC_LOWRANK_MAX, NPC_ERR_INVALID_ARGUMENT, "npc_ritz_vectors: p %d not in [1, %d]", p,
               NPC_LOWRANK_MAX);
     NPC_GUARD(nsteps >= p && nsteps <= 4096, NPC_ERR_INVALID_ARGUMENT, "npc_ritz_vectors: nsteps %d not in [p, 4096]",
@@ -336,6 +373,7 @@ npc_status npc_destroy_poly(npc_poly poly) {
 
 npc_status npc_apply_poly(npc_poly poly, const double *r_dev, double *z_dev) {
     NPC_GUARD(poly, NPC_ERR_INVALID_ARGUMENT, "npc_apply_poly: null poly");
+    ErrScope es(poly->op->owner);
     const int n = poly->op->op->n_local;
     NPC_GUARD(n == 0 || (r_dev && z_dev), NPC_ERR_INVALID_ARGUMENT, "npc_apply_poly: null vector");
     NPC_GUARD(n == 0 || r_dev != z_dev, NPC_ERR_INVALID_ARGUMENT, "npc_apply_poly: z must not alias r");
@@ -346,6 +384,7 @@ npc_status npc_apply_poly(npc_poly poly, const double *r_dev, double *z_dev) {
 npc_status npc_pcg_solve(npc_poly poly, npc_operator op, const double *b_dev, double *x_dev, double tol, int maxit,
                          npc_pcg_stats *stats) {
     NPC_GUARD(op, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: null operator");
+    ErrScope es(op->owner);
     NPC_GUARD(!poly || poly->op == op, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: poly built for another operator");
     NPC_GUARD(tol > 0.0 && tol < 1.0, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: tol %g not in (0,1)", tol);
     NPC_GUARD(maxit >= 1, NPC_ERR_INVALID_ARGUMENT, "npc_pcg_solve: maxit %d < 1", maxit);

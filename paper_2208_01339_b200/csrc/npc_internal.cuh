@@ -419,6 +419,7 @@ struct PcgCache {
 // Opaque handle structs of the C ABI.
 struct npc_context_s {
     npc::Context ctx;
+    char err[1024] = "";  // last failing call on this context (npc_last_error(ctx))
 };
 // Handles record their device so that destroy never dereferences another handle: Python's
 // cyclic GC may destroy a context before its operators, or an operator before its polys.
@@ -427,6 +428,7 @@ struct npc_operator_s {
     int device = 0;
     std::unique_ptr<npc::Operator> op;
     npc::PcgCache pcg;  // plain CG (poly == NULL)
+    double estimate_seconds = 0.0;  // wall time of the last npc_estimate_spectrum on it
 };
 struct npc_poly_s {
     npc_operator op = nullptr;
@@ -438,6 +440,7 @@ struct npc_poly_s {
     int degree = 0;
     double lmin = 0, lmax = 0, xi = 0;
     double theta_bar = 0, delta = 0, sigma = 0;
+    double setup_seconds = 0;  // the operator's last spectrum estimate + this set_poly
     std::vector<double> coef;  // 4 * degree: a_j, b_j, c_j, d_j (j = 1..k)
     npc::DevBuf coef_dev;      // the same table on the device (cluster-resident polynomial)
     npc::DevBuf tmp;           // second recurrence buffer (internal order)

@@ -654,6 +654,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     const int n = op->n_local;
     const int k = P ? P->degree : 0;
     npc_pcg_stats st{};
+    st.setup_seconds = P ? P->setup_seconds : 0.0;
     double *host_hist = stats ? stats->history : nullptr;
     // work vectors (internal order): b, x, r, u, w, p, s
     PcgCache &cache = P ? P->pcg : H->pcg;
@@ -1194,7 +1195,8 @@ void tridiag_inverse_iteration(const std::vector<double> &a, const std::vector<d
     tridiag_shift_solve(a, b, mu, x);
 }
 
-npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, double *lmax, double *out_ex) {
+npc_status lanczos(Operator *op, int m, const double *v0_ext, unsigned long long seed, double *lmin, double *lmax,
+                   double *out_ex) {
     Context *ctx = op->ctx;
     const int n = op->n_local;
     const size_t nn = std::max(n, 1);
@@ -1207,7 +1209,7 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, double *lmin, doub
         else
             NPC_CUDA_TRY(cudaMemcpyAsync(v0, v0_ext, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
     } else {
-        NPC_TRY(launch_hash_vector(ctx, w, n, op->row_begin, 0x5EEDull));
+        NPC_TRY(launch_hash_vector(ctx, w, n, op->row_begin, seed));
         if (op->permuted())
             NPC_TRY(op->to_internal(w, v0));
         else

@@ -431,3 +431,32 @@ def test_in_library_timing_with_graphs(ctx, wl):
     # up to 3 no-op iterations after convergence)
     assert s1["iters"] * k <= n <= (s1["iters"] + 3) * k and ms > 0.0
     assert tm["operator"][1] >= s1["iters"] and tm["update"][1] >= s1["iters"]
+
+
+def test_boundary_seed_setup_seconds_last_error(ctx):
+    """SURVEY §8(b) boundary details: npc_estimate_spectrum's seed selects the counter-hash
+    start vector (the same generator as workloads.lanczos_start), the PCG stats carry the
+    preconditioner setup (estimate + set_poly) apart from the solve, and npc_last_error(ctx)
+    holds the last failing call made through that context only."""
+    w = W.config3(side=20)
+    n = w["n"]
+    op = npc.create_from_workload(ctx, w, "csr")
+    for seed in (npc.NPC_DEFAULT_SEED, 12345):
+        a = npc.npc_estimate_spectrum(op, 20, None, seed=seed)
+        b = npc.npc_estimate_spectrum(op, 20, dev(W.lanczos_start(n, seed=seed)))
+        assert a == b, (seed, a, b)
+    assert npc.npc_estimate_spectrum(op, 20, None, seed=12345) != npc.npc_estimate_spectrum(op, 20, None)
+    lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+    poly = npc.npc_set_poly(op, 20, lo, hi, 0.0)
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    st = npc.npc_pcg_solve(poly, op, dev(w["b"]), x, w["tol"], 5000)
+    assert 0.0 < st["setup_seconds"] < 10.0 and st["solve_seconds"] > 0.0
+    st0 = npc.npc_pcg_solve(None, op, dev(w["b"]), torch.zeros_like(x), w["tol"], 5000, raise_on_error=False)
+    assert st0["setup_seconds"] == 0.0
+    # context-scoped error messages
+    other = npc.npc_context_create(0)
+    assert npc.npc_last_error(other) == ""
+    st = npc.npc_pcg_solve(poly, op, dev(w["b"]), torch.zeros_like(x), 1e-12, 2, raise_on_error=False)
+    assert st["status"] == "NPC_ERR_NOT_CONVERGED"
+    assert "did not converge" in npc.npc_last_error(ctx)
+    assert npc.npc_last_error(other) == ""

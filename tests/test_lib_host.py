@@ -127,3 +127,37 @@ def test_halo_plan_rejects_bad_input(npc):
     with pytest.raises(npc.NpcError):
         npc.npc_halo_plan(np.array([0, 1], dtype=np.int32), np.array([5], dtype=np.int32),
                           np.array([0, 1, 2], dtype=np.int64), 0)  # column out of range
+
+
+def test_pcg_stats_layout_matches_header(npc):
+    """The binding's npc_pcg_stats mirrors include/npc.h field by field (ABI drift guard)."""
+    hdr = open(os.path.join(ROOT, "include", "npc.h")).read()
+    end = hdr.index("} npc_pcg_stats;")
+    body = hdr[hdr.rindex("typedef struct {", 0, end) + len("typedef struct {"):end]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = re.findall(r"\b(\w+)\s*;", body)
+    assert names == [f[0] for f in npc.PcgStats._fields_], (names, npc.PcgStats._fields_)
+    assert "setup_seconds" in names and "solve_seconds" in names
+
+
+def test_last_error_thread_and_null_context(npc):
+    """A failing host-only call records its message for npc_last_error(NULL) (the calling
+    thread); a context-less failure never touches a context's message."""
+    with pytest.raises(npc.NpcError) as e:
+        npc.npc_poly_coefficients(5, 2.0, 2.0, 0.0)
+    assert e.value.name == "NPC_ERR_DEGENERATE_INTERVAL"
+    msg = npc.npc_last_error(None)
+    assert msg and msg in str(e.value)
+    import threading
+    other = []
+    t = threading.Thread(target=lambda: other.append(npc.npc_last_error(None)))
+    t.start()
+    t.join()
+    assert other == [""]  # thread-local
+
+
+def test_estimate_spectrum_signature_has_seed(npc):
+    hdr = open(os.path.join(ROOT, "include", "npc.h")).read()
+    decl = re.search(r"npc_estimate_spectrum\((.*?)\);", hdr, re.S).group(1)
+    assert "unsigned long long seed" in decl
+    assert "NPC_DEFAULT_SEED 0x5EED" in hdr and npc.NPC_DEFAULT_SEED == 0x5EED == W.LANCZOS_SEED
