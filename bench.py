@@ -524,9 +524,31 @@ def cpu_baseline(w, k, lo, hi, xi, M, V, max_seconds=30.0):
     oracle.cheb_apply(orc, kk, lo, hi, xi, r)
     dt = time.perf_counter() - t0
     byts = poly_bytes(M, V, kk)
-    return {"value": round(byts / dt / 1e9, 3), "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"one p_k(A) v application (k={kk}) of {w['name']} by Alg. 2 verbatim (oracle/npc_oracle.c)",
-            "seconds": round(dt, 3), **host_info()}
+    out = {"value": round(byts / dt / 1e9, 3), "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"one p_k(A) v application (k={kk}) of {w['name']} by Alg. 2 verbatim (oracle/npc_oracle.c)",
+           "seconds": round(dt, 3), **host_info()}
+    g = oracle_golden(w, kk, xi)
+    if g:
+        out["time_to_tol"] = g
+    return out
+
+
+def oracle_golden(w, k, xi):
+    """The oracle's full PCG-to-tolerance on this workload, run once by tools/oracle_golden.py
+    ("run once per benchmark session and cached"): iterations, counters and the
+    wall time on the host that wrote it (not this run's host), if a golden exists."""
+    import glob
+    side = round(w["n"] ** (1 / 3))
+    cands = glob.glob(os.path.join(ROOT, "tests", "golden", f"config*_{side}_pcg_k{k}.json")) + \
+        glob.glob(os.path.join(ROOT, "tests", "golden", f"config*_{w['n']}_pcg_k{k}.json"))
+    for path in cands:
+        g = json.load(open(path))
+        if g.get("workload") == w.get("name") and g.get("xi", 0.0) == xi:
+            return {"seconds": round(g["seconds_time_to_tol"], 1), "iters": g["iters"], "mvp": g["mvp"],
+                    "relres_true": g["relres_true"], "threads": g["threads"], "nproc": g["nproc"], "cpu": g["cpu"],
+                    "source": os.path.relpath(path, ROOT) + " (tools/oracle_golden.py; written on the build host, "
+                                                            "not this run's host)"}
+    return None
 
 
 # ------------------------------------------------------------------ reference arm (the oracle)
