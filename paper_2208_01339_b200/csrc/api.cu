@@ -107,6 +107,7 @@ static npc_status context_create(int device, int nranks, int rank, const void *n
     }
     if (nranks > 1 || local_group || nccl_unique_id) {
         NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking));
+        NPC_CUDA_TRY(cudaStreamCreateWithFlags(&c.aux_stream, cudaStreamNonBlocking));
         if (local_group)
             NPC_TRY(make_local_transport(&c, local_group, c.tr));
         else
@@ -162,6 +163,7 @@ npc_status npc_context_destroy(npc_context ctx) {
         if (c.stream) cudaStreamSynchronize(c.stream);
         c.tr.reset();
         if (c.comm_stream) cudaStreamDestroy(c.comm_stream);
+        if (c.aux_stream) cudaStreamDestroy(c.aux_stream);
         c.partials.release();
         c.scalars.release();
         if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);

@@ -130,12 +130,12 @@ npc_status halo_setup(Context *ctx, const HaloPlan &plan, HaloRuntime &rt) {
 
 // Pack x[send_idx] on the compute stream, then send/recv on the comm stream (overlapping the
 // interior kernels the caller enqueues next); halo_wait joins before the boundary kernels.
-// The local (testing) transport exchanges synchronously on the compute stream instead.
+// Both transports (NCCL, and the local thread group used for testing) run this same
+// choreography.
 npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const double *x) {
+    NvtxRange nv("npc:halo");
+    NPC_TRY(ctx->tr->before_pack(ctx, ctx->stream));
     NPC_TRY(launch_gather(ctx, x, rt.send_idx.as<int>(), rt.send_buf.as<double>(), (int)plan.send_idx.size()));
-    if (!ctx->tr->capturable())
-        return ctx->tr->exchange(ctx, rt.send_buf.as<double>(), plan.send_count, plan.send_off,
-                                 rt.ghost_buf.as<double>(), plan.recv_count, plan.recv_off, ctx->stream);
     NPC_CUDA_TRY(cudaEventRecord(rt.packed, ctx->stream));
     NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, rt.packed, 0));
     NPC_TRY(ctx->tr->exchange(ctx, rt.send_buf.as<double>(), plan.send_count, plan.send_off, rt.ghost_buf.as<double>(),
@@ -145,7 +145,6 @@ npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const
 }
 
 npc_status halo_wait(Context *ctx, HaloRuntime &rt) {
-    if (!ctx->tr->capturable()) return NPC_SUCCESS;
     NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, rt.ready, 0));
     return NPC_SUCCESS;
 }

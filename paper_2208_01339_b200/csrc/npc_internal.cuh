@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <nccl.h>
 #include <stdint.h>
 
@@ -202,7 +203,19 @@ class Transport {
                                        cudaStream_t s) = 0;
     virtual npc_status reduce_scatter_slots(Context *c, const double *full, double *mine, int m,
                                             cudaStream_t s) = 0;
+    // Host wait for stream s.  NCCL: polls the communicators' asynchronous error state while
+    // waiting and aborts them (NPC_ERR_NCCL) on an error or after NPC_NCCL_TIMEOUT_S seconds
+    // (default 600) -- a dead or wedged peer ends the call instead of hanging it.
+    virtual npc_status sync(Context *c, cudaStream_t s);
+    // Called on the compute stream before a halo pack overwrites the send buffer that peers
+    // may still be reading (local transport: waits for their copies; NCCL: nothing).
+    virtual npc_status before_pack(Context *c, cudaStream_t s) {
+        (void)c, (void)s;
+        return NPC_SUCCESS;
+    }
 };
+// Host wait for stream s of context c (through the transport when distributed).
+npc_status stream_sync(Context *c, cudaStream_t s);
 npc_status make_nccl_transport(Context *c, const void *uid, std::unique_ptr<Transport> &out);
 npc_status make_local_transport(Context *c, const char *group, std::unique_ptr<Transport> &out);
 
@@ -212,6 +225,8 @@ struct Context {
     int nranks = 1, rank = 0;
     cudaStream_t stream = nullptr;       // compute stream
     cudaStream_t comm_stream = nullptr;  // halo traffic (distributed contexts)
+    cudaStream_t aux_stream = nullptr;   // PCG side ||r||^2 allreduce (distributed): never queues
+                                         // behind (or holds up) the halo traffic on comm_stream
     bool own_stream = false;
     cudaStream_t graph_stream = nullptr;  // CUDA-graph replay of PCG iterations
     cudaStream_t body_stream = nullptr;   // capture of conditional iteration bodies
@@ -258,11 +273,26 @@ struct Context {
 // RAII bracket of a launch (or a multi-kernel step) for the timing classes above.
 // A scope nested inside a group scope (timing_suppress > 0) records nothing; a group scope
 // (count > 1) brackets several launches with one event pair and credits them all.
+// NVTX range (host side, header-only NVTX3: free unless a profiler is attached) for nsys /
+// ncu range filtering: npc:degree, npc:operator, npc:update, npc:reduce, npc:vector (every
+// TimedScope), npc:halo, npc:allreduce(_rr), npc:pcg, npc:lanczos.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+inline const char *timing_class_name(int cls) {
+    static const char *names[] = {"npc:degree", "npc:operator", "npc:update", "npc:reduce", "npc:vector"};
+    return cls >= 0 && cls < 5 ? names[cls] : "npc:other";
+}
 struct TimedScope {
     Context *c;
     int idx;
+    NvtxRange nv;
     TimedScope(Context *ctx, int cls, int count = 1)
-        : c(ctx), idx(ctx->timing && ctx->timing_suppress == 0 ? ctx->t_begin(cls, count) : -1) {}
+        : c(ctx), idx(ctx->timing && ctx->timing_suppress == 0 ? ctx->t_begin(cls, count) : -1),
+          nv(timing_class_name(cls)) {}
     ~TimedScope() {
         if (idx >= 0) c->t_end(idx);
     }

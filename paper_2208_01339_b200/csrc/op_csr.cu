@@ -570,13 +570,27 @@ class CsrOperator : public Operator {
 
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
+        // a rank without rows still joins the halo exchange and writes zero dot partials
+        // (num_partials() >= 1 of them are read)
+        const bool zero_parts = multi && ntiles == 0 && s.dotv;
         if (pattern) {
-            if (!multi || ctx->nranks == 1) return launch_pattern_set(s, pt_all, s.partials);
+            if (!multi || ctx->nranks == 1) {
+                if (zero_parts) return launch_fill(ctx, s.partials, 0.0, num_partials());
+                return launch_pattern_set(s, pt_all, s.partials);
+            }
             NPC_TRY(halo_start(ctx, plan, halo, s.x));
             NPC_TRY(launch_pattern_set(s, pt_interior, s.partials));
             NPC_TRY(halo_wait(ctx, halo));
+            if (zero_parts) return launch_fill(ctx, s.partials, 0.0, num_partials());
             return launch(s, tiles_boundary.as<int>(), n_boundary, s.partials ? s.partials + n_interior : nullptr,
                           true);
+        }
+        if (zero_parts) {
+            if (ctx->nranks > 1) {
+                NPC_TRY(halo_start(ctx, plan, halo, s.x));
+                NPC_TRY(halo_wait(ctx, halo));
+            }
+            return launch_fill(ctx, s.partials, 0.0, num_partials());
         }
         // single rank, or a 1-rank distributed context (no halo; with more ranks the exchange
         // is collective for the local transport even when this rank's plan is empty)

@@ -469,7 +469,8 @@ class DfnOperator : public Operator {
         if (halo) {
             NPC_TRY(halo_into(hplan, trt, t.as<double>(), t.as<double>(), nh));
             NPC_TRY(halo_into(hplan, u2rt, u2.as<double>(), u2.as<double>(), nh));
-            if (n_local == 0) return NPC_SUCCESS;
+            // a rank without rows writes zero dot partials (num_partials() >= 1 of them are read)
+            if (n_local == 0) return s.dotv ? launch_fill(ctx, s.partials, 0.0, num_partials()) : NPC_SUCCESS;
         }
         const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
         if (h2 && hr && dt) return launch_out<true, true, true>(s);

@@ -681,7 +681,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         if (host_hist && h.iters >= 0)
             NPC_CUDA_TRY(cudaMemcpyAsync(host_hist, dhist, sizeof(double) * ((size_t)maxit + 1),
                                          cudaMemcpyDeviceToHost, ctx->stream));
-        NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        NPC_TRY(stream_sync(ctx, ctx->stream));
         if (ctx->timing) ctx->t_flush();
         st.iters = h.iters;
         st.converged = h.converged;
@@ -749,7 +749,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     NPC_TRY(ctx->allreduce_sum(sums, 2));
     double h2[2];
     NPC_CUDA_TRY(cudaMemcpyAsync(h2, sums, sizeof(h2), cudaMemcpyDeviceToHost, ctx->stream));
-    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    NPC_TRY(stream_sync(ctx, ctx->stream));
     st.reductions += 1;
     const double bnorm2 = h2[0];
     const bool x0_nonzero = h2[1] != 0.0;
@@ -773,7 +773,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         st.reductions += 1;
         double tr;
         NPC_CUDA_TRY(cudaMemcpyAsync(&tr, sums + 3, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        NPC_TRY(stream_sync(ctx, ctx->stream));
         *relres = sqrt(tr / bnorm2);
         return NPC_SUCCESS;
     };
@@ -785,7 +785,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     npc_status result = NPC_SUCCESS;
     if (bnorm2 == 0.0) {  // b = 0 -> x = 0
         NPC_CUDA_TRY(cudaMemsetAsync(x_ext, 0, sizeof(double) * n, ctx->stream));
-        NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        NPC_TRY(stream_sync(ctx, ctx->stream));
         st.converged = 1;
         st.solve_seconds = now_s() - t0;
         if (stats) {
@@ -821,7 +821,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     }
     double rr0;
     NPC_CUDA_TRY(cudaMemcpyAsync(&rr0, sums + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    NPC_TRY(stream_sync(ctx, ctx->stream));
     std::vector<double> hist_host;
     if (host_hist) host_hist[0] = sqrt(rr0 / bnorm2);
     CgDev h{};
@@ -840,7 +840,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
             st.converged = 1;
             st.relres_true = tr;
             NPC_TRY(export_x());
-            NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            NPC_TRY(stream_sync(ctx, ctx->stream));
             st.solve_seconds = now_s() - t0;
             if (stats) {
                 double *hh = stats->history;
@@ -920,12 +920,13 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                 NPC_LAUNCH_CHECK();
             }
             if (h.multi) {  // ||r_{i+1}||^2: allreduce + check on the side stream
+                NvtxRange nv("npc:allreduce_rr");
                 NPC_CUDA_TRY(cudaEventRecord(ctx->ev_rr0, ctx->stream));
-                NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_rr0, 0));
-                NPC_TRY(ctx->tr->allreduce_sum_aux(ctx, sums + 4, 1, ctx->comm_stream));
-                k_cg_rrcheck<<<1, 1, 0, ctx->comm_stream>>>(cg, sums + 4, dhist);
+                NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_rr0, 0));
+                NPC_TRY(ctx->tr->allreduce_sum_aux(ctx, sums + 4, 1, ctx->aux_stream));
+                k_cg_rrcheck<<<1, 1, 0, ctx->aux_stream>>>(cg, sums + 4, dhist);
                 NPC_LAUNCH_CHECK();
-                NPC_CUDA_TRY(cudaEventRecord(ctx->ev_rr1, ctx->comm_stream));
+                NPC_CUDA_TRY(cudaEventRecord(ctx->ev_rr1, ctx->aux_stream));
                 rr_pending = true;
                 // a captured block of GraphRun::ITERS iterations ends joined
                 if (++iter_calls % GraphRun::ITERS == 0) NPC_TRY(join_rr());
@@ -970,7 +971,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                     NPC_TRY(gr.launch());
                     int dflag_h = 0;
                     NPC_CUDA_TRY(cudaMemcpyAsync(&dflag_h, dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-                    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+                    NPC_TRY(stream_sync(ctx, ctx->stream));
                     ctx->t_flush_graph(cache.timing_events);
                     if (dflag_h) break;
                 }
@@ -982,7 +983,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
             NPC_TRY(join_rr());
         }
         NPC_CUDA_TRY(cudaMemcpyAsync(&h, cg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-        NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        NPC_TRY(stream_sync(ctx, ctx->stream));
         if (ctx->timing) ctx->t_flush();
         if (!h.done) {
             if (deferred) {
@@ -1049,7 +1050,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         NPC_CUDA_TRY(cudaMemcpyAsync(host_hist + 1, dhist + 1, sizeof(double) * h.iters, cudaMemcpyDeviceToHost,
                                      ctx->stream));
     NPC_TRY(export_x());
-    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    NPC_TRY(stream_sync(ctx, ctx->stream));
     st.solve_seconds = now_s() - t0;
     if (stats) {
         double *hh = stats->history;
@@ -1228,7 +1229,7 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, unsigned long long
     NPC_TRY(ctx->allreduce_sum(&lz->vn2, 1));
     double vn2;
     NPC_CUDA_TRY(cudaMemcpyAsync(&vn2, &lz->vn2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    NPC_TRY(stream_sync(ctx, ctx->stream));
     if (!(vn2 > 0.0)) {
         set_error("estimate_spectrum: start vector is zero");
         return NPC_ERR_INVALID_ARGUMENT;
@@ -1286,7 +1287,7 @@ npc_status lanczos(Operator *op, int m, const double *v0_ext, unsigned long long
     NPC_CUDA_TRY(cudaMemcpyAsync(&hl, lz, sizeof(hl), cudaMemcpyDeviceToHost, ctx->stream));
     NPC_CUDA_TRY(cudaMemcpyAsync(ha.data(), alphas, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
     NPC_CUDA_TRY(cudaMemcpyAsync(hb.data(), betas, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    NPC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    NPC_TRY(stream_sync(ctx, ctx->stream));
     if (ctx->timing) ctx->t_flush();
     const int sN = std::max(1, hl.steps);
     const double beta_last = hb[sN - 1];
