@@ -392,11 +392,28 @@ def run_ours(args):
         per_launch_ms = ktime["degree"][0] / n_deg
         in_step = {c: {"ms": round(v[0], 3), "launches": v[1], "share": round(v[0] / (ms_step * args.steps), 4)}
                    for c, v in ktime.items()}
+    # -------- per-rank timing (N > 1): each rank's own step time and its in-library kernel
+    # classes; what the kernels do not cover is halo / allreduce waiting and host work
+    per_rank = None
+    if ws > 1:
+        mine = {"rank": rank, "n_local": nl, "step_ms": round(ms / args.steps, 3)}
+        if ktime is not None:
+            kms = {c: v[0] / args.steps for c, v in ktime.items()}
+            mine.update({f"{c}_ms": round(v, 3) for c, v in kms.items()})
+            mine["outside_kernels_ms"] = round(ms / args.steps - sum(kms.values()), 3)
+        per_rank = [None] * ws
+        dist.all_gather_object(per_rank, mine)
+    # DRAM traffic of one degree launch from the committed ncu --set full capture of this
+    # workload's kernel (profiles/traffic_config<C>.json, tools/traffic_from_ncu.py); used only
+    # if it was captured on the operator format this run stores (same matrix bytes), else null
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_config{cfg}.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and ws == 1:
         try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+            tj = json.load(open(tf))
+            mb = npc.npc_operator_matrix_bytes(op)
+            if tj.get("matrix_bytes") and abs(tj["matrix_bytes"] - mb) <= 1e-6 * mb and tj.get("k", k) == k:
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -478,6 +495,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h,
                     "includes": "npc_create_operator from host CSR + b H2D (pinned) + estimate + set_poly + solve + x D2H"},
             "gpu_launches": int(launches),
+            **({"per_rank": per_rank} if per_rank else {}),
             "clocks": clk,
             "cpu_baseline": cpu,
         }
