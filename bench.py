@@ -42,6 +42,16 @@ METRIC = "p_k(A)v GB/s (algorithmic bytes of the timed step / step time)"
 FALLBACK_HBM = 6650.0
 
 
+def l2_peaks():
+    """The L2 roofline denominators measured by tools/microbench/l2_peak.cu on this pool's B200
+    (profiles/r02_l2_peak.json): L2-resident copy GB/s and random 8-byte gathers (sectors/s)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_l2_peak.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def hbm_peak():
     try:
         with open(PEAKS_FILE) as f:
@@ -417,6 +427,26 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # -------- L2 rooflines where HBM is not the bound: an L2-resident stencil (config 2: the
+    # four vector streams fit in L2) against the measured L2 copy rate, and the Schur operator
+    # (config 5) against the measured random-sector rate: its two passes gather v and t at
+    # random, one 32-byte L2 sector per 8-byte value, 2 nnz(B) sectors per application
+    l2_roof = None
+    l2p = l2_peaks()
+    if l2p and ws == 1:
+        if kind == "stencil" and 4 * V <= 0.75 * 126e6:
+            l2_roof = {"bound": "l2", "achieved": round(ach, 1), "peak": l2p["l2_copy_rw_gbs"], "unit": "GB/s",
+                       "frac": round(ach / l2p["l2_copy_rw_gbs"], 4),
+                       "peak_source": "measured L2-resident copy (profiles/r02_l2_peak.json)"}
+        if kind == "schur":
+            sectors = 2.0 * int(w["browptr"][-1])  # random gathers per application (v, then t)
+            t_deg = per_launch_ms * 1e-3
+            l2_roof = {"bound": "l2_random_sectors", "achieved": round(sectors / t_deg, 1),
+                       "peak": l2p["l2_random8B_sectors_per_s"], "unit": "sectors/s",
+                       "frac": round(sectors / t_deg / l2p["l2_random8B_sectors_per_s"], 4),
+                       "floor_ms_per_degree": round(sectors / l2p["l2_random8B_sectors_per_s"] * 1e3, 4),
+                       "peak_source": "measured random 8-byte gathers (profiles/r02_l2_peak.json)"}
+
     # -------- e2e: the public API from host buffers: operator upload (npc_create_operator
     # copies the host CSR), b H2D from pinned memory, estimate + set_poly + solve, x D2H
     e2e_val = None
@@ -491,6 +521,7 @@ def run_ours(args):
                          "isolated_achieved": round(ach_isolated, 1),
                          "isolated": f"{R} x npc_apply_poly back to back after the timed region",
                          "step_breakdown": in_step},
+            **({"roofline_l2": l2_roof} if l2_roof else {}),
             "e2e": {"value": round(e2e_val, 2) if e2e_val else None, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "includes": "npc_create_operator from host CSR + b H2D (pinned) + estimate + set_poly + solve + x D2H"},

@@ -67,9 +67,18 @@ def run(cfg, reps, ctx, kinds=None):
                     p2.close()
             tt = sorted(tts)[len(tts) // 2]
             sb = bench.solve_bytes(M, V, k, st["iters"], 20)
+            # the roofline that bounds this operator: HBM, except an L2-resident stencil (L2
+            # copy rate) and the Schur operator (random L2 sectors: 2 nnz(B) per application)
+            l2p = bench.l2_peaks() or {}
+            bound, frac_bound = "hbm", round(gbs_f / bench.hbm_peak()[0], 3)
+            if kind == "stencil" and 4 * V <= 0.75 * 126e6 and l2p:
+                bound, frac_bound = "l2 copy", round(gbs_f / l2p["l2_copy_rw_gbs"], 3)
+            elif kind == "schur" and l2p:
+                sec = 2.0 * int(w["browptr"][-1]) * k / (ms * 1e-3)
+                bound, frac_bound = "l2 random sectors", round(sec / l2p["l2_random8B_sectors_per_s"], 3)
             row = dict(config=cfg, name=w["name"], operator=kind, n=w["n"], k=k, apply_ms=round(ms, 4),
                        apply_gbs=round(gbs, 1), apply_gbs_format=round(gbs_f, 1),
-                       frac_measured=round(gbs_f / bench.hbm_peak()[0], 3),
+                       frac_measured=round(gbs_f / bench.hbm_peak()[0], 3), bound=bound, frac_bound=frac_bound,
                        applications_per_s=round(k / (ms * 1e-3), 1), pcg_status=st["status"], iters=st["iters"],
                        relres_true=st["relres_true"], time_to_tol_s=round(tt, 4),
                        solve_gbs=round(sb / tt / 1e9, 1), lmin=lo2, lmax=hi2, gen_s=round(gen_s, 1))
@@ -96,12 +105,14 @@ def main():
     if a.md:
         with open(a.md, "w") as f:
             f.write("| config | operator | n | k | p_k(A)v ms | GB/s (alg., §8(d) bytes) | GB/s (stored format) | "
-                    "frac of measured HBM (format) | applications/s | "
-                    "PCG iters | time-to-tol s | solve GB/s | true relres |\n|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+                    "frac of measured HBM (format) | bound | frac of that bound | applications/s | "
+                    "PCG iters | time-to-tol s | solve GB/s | true relres |\n"
+                    "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
             for r in rows:
                 f.write(f"| {r['name']} | {r['operator']} | {r['n']} | {r['k']} | {r['apply_ms']} | {r['apply_gbs']} | "
                         f"{r['apply_gbs_format']} | "
-                        f"{r['frac_measured']} | {r['applications_per_s']} | {r['iters']} | {r['time_to_tol_s']} | "
+                        f"{r['frac_measured']} | {r['bound']} | {r['frac_bound']} | {r['applications_per_s']} | "
+                        f"{r['iters']} | {r['time_to_tol_s']} | "
                         f"{r['solve_gbs']} | {r['relres_true']:.2e} |\n")
 
 
