@@ -290,19 +290,47 @@ __global__ void __launch_bounds__(PAT_TILE) k_csr_pat_step(PatDev A, StepArgs s,
 static constexpr int PAT_THREADS = PAT_TILE / 2;
 static constexpr int PAT_STAGE_SMEM = 110 * 1024;  // own block + x windows + table, per tile
 
+// Values of a row's first two mirrors in EARLIER tiles (coalesced L2 reads; a 3D grid: -N^2,
+// and -N for the first rows of a tile), loaded ahead of the row's sum (k_csr_pat_pipe issues
+// them one tile early).  Entries are in column order, so those mirrors come first.
+struct PatMirrors {
+    double v0 = 0.0, v1 = 0.0;
+    int n = 0;  // how many were loaded (0: pat_row loads them itself)
+};
+__device__ __forceinline__ PatMirrors pat_mirrors(const PatDev &A, const int *st, const int4 *ent, int sidx,
+                                                  int row0, int lr, int pid) {
+    // predicated loads into fixed registers: nothing depends on a loaded value here, so the
+    // loads stay in flight until pat_row uses them
+    PatMirrors m;
+    const int eb = st[sidx + pid], e1 = st[sidx + pid + 1];
+    const int4 z4 = make_int4(0, 0, 0, 0);
+    const int4 t0 = eb < e1 ? ent[eb] : z4, t1 = eb + 1 < e1 ? ent[eb + 1] : z4;
+    const bool g0 = eb < e1 && lr + t0.z < 0, g1 = g0 && eb + 1 < e1 && lr + t1.z < 0;
+    const int c0 = row0 + lr + t0.z, c1 = row0 + lr + t1.z;
+    const int j0 = g0 ? c0 / PAT_TILE : 0, j1 = g1 ? c1 / PAT_TILE : 0;
+    m.v0 = g0 ? __ldg(A.vals + __ldg(A.tptr + j0) + t0.w * PAT_TILE + (c0 - j0 * PAT_TILE)) : 0.0;
+    m.v1 = g1 ? __ldg(A.vals + __ldg(A.tptr + j1) + t1.w * PAT_TILE + (c1 - j1 * PAT_TILE)) : 0.0;
+    m.n = 2;
+    return m;
+}
+
 template <bool HAS_S2, bool HAS_R>
 __device__ __forceinline__ double pat_row(const PatDev &A, const StepArgs &s, const double *sv, const double *sx,
                                           const int *st, const int4 *ent, int sidx, int row0, int lr, int pid,
-                                          double xs, double s2v, double rv) {
+                                          double xs, double s2v, double rv, const PatMirrors *pm = nullptr) {
     const int row = row0 + lr;
     const int e1 = st[sidx + pid + 1];
     double y = 0.0;
+    int km = 0;
     for (int e = st[sidx + pid]; e < e1; ++e) {
         const int4 t = ent[e];
         const double xv = sx[t.x + lr];
         double v;
         if (lr + t.z >= 0) {
             v = sv[t.y + lr];
+        } else if (pm && km < 2) {  // loaded ahead
+            v = km == 0 ? pm->v0 : pm->v1;
+            ++km;
         } else {  // mirror in an earlier (full) tile's block, through L2
             const int c = row + t.z, tj = c / PAT_TILE;
             v = __ldg(A.vals + __ldg(A.tptr + tj) + t.w * PAT_TILE + (c - tj * PAT_TILE));
@@ -395,6 +423,160 @@ __global__ void __launch_bounds__(PAT_THREADS) k_csr_pat_stage(PatDev A, StepArg
     }
 }
 
+// Pipelined persistent form of k_csr_pat_stage (opt-in, NPC_CSR_PIPE=1; see the A/B where it is
+// enabled in finish_pattern_operator): one CTA per SM walks its tiles (blockIdx.x, + gridDim.x, ...) through a
+// ring of stages, each holding a tile's own-value block, x windows and table.  Warp-
+// specialised: a producer warp (warp PAT_THREADS / 32) waits for a stage to be released
+// (`empty` mbarrier, one arrival per consumer warp), reads the tile's copy descriptors and
+// issues its bulk copies on the stage's `full` mbarrier, running up to PAT_PIPE_NS tiles ahead;
+// the PAT_THREADS consumer threads (two rows each) wait on `full`, compute, release the stage.
+// The per-row streams of the next tile (pattern ids, s_{j-2}, r) are loaded into registers one
+// tile ahead.  Load and compute phases of consecutive tiles thus overlap instead of each CTA
+// waiting for its single tile (config 3: the copies alone run at 0.96 of HBM, 172 us per degree;
+// with the row sums in the same CTA lifetime, k_csr_pat_stage, 231 us).  Dot partial: one per
+// CTA; CTA 0 zeroes the slots of the other launches' layout up to npart_total.
+static constexpr int PAT_PIPE_NS = 3;
+static constexpr int PAT_PIPE_THREADS = PAT_THREADS + 32;
+
+template <bool HAS_S2, bool HAS_R, bool DOT>
+__global__ void __launch_bounds__(PAT_PIPE_THREADS, 1)
+    k_csr_pat_pipe(PatDev A, StepArgs s, const int *__restrict__ tiles, int ntl, int vspan_max, int xspan_max,
+                   int tbl2_max, int stage_dbl, int npart_total) {
+    extern __shared__ __align__(128) unsigned char pp_raw[];
+    double *base = reinterpret_cast<double *>(pp_raw + ((128u - (smem_u32(pp_raw) & 127u)) & 127u));
+    __shared__ uint64_t full[PAT_PIPE_NS], empty[PAT_PIPE_NS];
+    __shared__ double red[PAT_PIPE_THREADS / 32];
+    if (s.done && *s.done) return;  // uniform: before any copy is issued
+    constexpr int NCW = PAT_THREADS / 32;  // consumer warps
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < PAT_PIPE_NS; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto tile_of = [&](int i) { const int q = blockIdx.x + i * gridDim.x; return tiles ? tiles[q] : q; };
+    const int nmine = ntl > (int)blockIdx.x ? (ntl - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    double acc = 0.0;
+    if (warp == NCW) {
+        // ---------------- producer (one elected lane)
+        if (lane == 0) {
+            uint32_t ephase = 0;
+            for (int i = 0; i < nmine; ++i) {
+                const int b = i % PAT_PIPE_NS, tile = tile_of(i);
+                if (i >= PAT_PIPE_NS) {  // the consumers released tile i - NS's stage
+                    mbar_wait(&empty[b], (ephase >> b) & 1u);
+                    ephase ^= 1u << b;
+                }
+                double *sv = base + (size_t)b * stage_dbl, *sx = sv + vspan_max;
+                int *st = reinterpret_cast<int *>(sx + xspan_max);
+                const int *gt = A.tbl2 + A.tbl2_off[tile];
+                const int nwin = gt[0], tn = A.tbl2_off[tile + 1] - A.tbl2_off[tile];
+                const int pb = A.tptr[tile];
+                const uint32_t bv = (uint32_t)(A.tptr[tile + 1] - pb) * 8u;
+                uint32_t bytes = bv + (uint32_t)tn * 4u;
+                for (int w = 0; w < nwin; ++w) {
+                    const int ga = gt[4 + 4 * w], len = gt[4 + 4 * w + 1];
+                    bytes += (uint32_t)len * 8u;
+                    if (gt[4 + 4 * w + 3]) sx[gt[4 + 4 * w + 2] + len] = s.x[ga + len];  // odd tail
+                }
+                const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
+                const uint32_t bp = (uint32_t)((nrows + 15) & ~15);  // pattern ids (array padded)
+                bytes += bp;
+                mbar_arrive_expect_tx(&full[b], bytes);  // releases the tail stores with it
+                if (bv) bulk_g2s(sv, A.vals + pb, bv, &full[b]);
+                bulk_g2s(st, gt, (uint32_t)tn * 4u, &full[b]);
+                bulk_g2s(st + tbl2_max, A.pat + row0, bp, &full[b]);
+                for (int w = 0; w < nwin; ++w) {
+                    const int ga = gt[4 + 4 * w], len = gt[4 + 4 * w + 1], sb = gt[4 + 4 * w + 2];
+                    if (len) bulk_g2s(sx + sb, s.x + ga, (uint32_t)len * 8u, &full[b]);
+                }
+            }
+        }
+    } else {
+        // ---------------- consumers: rows l0 and l1 of every tile
+        const int l0 = threadIdx.x, l1 = threadIdx.x + PAT_THREADS;
+        int np0 = 0, np1 = 0;
+        double ns20 = 0.0, ns21 = 0.0, nr0 = 0.0, nr1 = 0.0;
+        auto load_rows = [&](int i) {  // s_{j-2} and r of tile i, one tile ahead
+            const int tile = tile_of(i), row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
+            if (l0 < nrows) {
+                if (HAS_S2) ns20 = s.s2[row0 + l0];
+                if (HAS_R) nr0 = s.r[row0 + l0];
+            }
+            if (l1 < nrows) {
+                if (HAS_S2) ns21 = s.s2[row0 + l1];
+                if (HAS_R) nr1 = s.r[row0 + l1];
+            }
+        };
+        uint32_t fphase = 0;
+        // stage i landed -> the earlier-tile mirror values of its rows, loaded into registers
+        auto wait_and_mirrors = [&](int i, PatMirrors &m0, PatMirrors &m1) {
+            const int b = i % PAT_PIPE_NS, tile = tile_of(i);
+            const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
+            const double *sx = base + (size_t)b * stage_dbl + vspan_max;
+            const int *st = reinterpret_cast<const int *>(sx + xspan_max);
+            mbar_wait(&full[b], (fphase >> b) & 1u);
+            fphase ^= 1u << b;
+            const int sidx = 4 + 4 * st[0];
+            const int4 *ent = reinterpret_cast<const int4 *>(st + st[1]);
+            const unsigned char *sp = reinterpret_cast<const unsigned char *>(st + tbl2_max);
+            if (l0 < nrows) {
+                np0 = sp[l0];
+                m0 = pat_mirrors(A, st, ent, sidx, row0, l0, np0);
+            }
+            if (l1 < nrows) {
+                np1 = sp[l1];
+                m1 = pat_mirrors(A, st, ent, sidx, row0, l1, np1);
+            }
+        };
+        PatMirrors m0, m1, q0, q1;
+        if (nmine > 0) {
+            load_rows(0);
+            wait_and_mirrors(0, m0, m1);
+        }
+        for (int i = 0; i < nmine; ++i) {
+            const int b = i % PAT_PIPE_NS, tile = tile_of(i);
+            const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
+            const int p0 = np0, p1 = np1;
+            const double s20 = ns20, s21 = ns21, r0 = nr0, r1 = nr1;
+            if (i + 1 < nmine) {  // next tile: row streams, then (its stage landed) its mirrors
+                load_rows(i + 1);
+                wait_and_mirrors(i + 1, q0, q1);
+            }
+            const double *sv = base + (size_t)b * stage_dbl;
+            const double *sx = sv + vspan_max;
+            const int *st = reinterpret_cast<const int *>(sx + xspan_max);
+            const int sidx = 4 + 4 * st[0];
+            const int4 *ent = reinterpret_cast<const int4 *>(st + st[1]);
+            if (l0 < nrows) {
+                const double o =
+                    pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l0, p0, sx[st[3] + l0], s20, r0, &m0);
+                s.out[row0 + l0] = o;
+                if (DOT) acc += o * s.dotv[row0 + l0];
+            }
+            if (l1 < nrows) {
+                const double o =
+                    pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l1, p1, sx[st[3] + l1], s21, r1, &m1);
+                s.out[row0 + l1] = o;
+                if (DOT) acc += o * s.dotv[row0 + l1];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[b]);  // this warp is done with stage b
+            m0 = q0;
+            m1 = q1;
+        }
+    }
+    if (DOT) {
+        acc = block_sum<PAT_PIPE_THREADS>(acc, red);
+        if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
+        if (blockIdx.x == 0)
+            for (int k = gridDim.x + threadIdx.x; k < npart_total; k += PAT_PIPE_THREADS) s.partials[k] = 0.0;
+    }
+}
+
 class CsrOperator : public Operator {
   public:
     DevBuf rowptr, cols, vals;
@@ -407,6 +589,9 @@ class CsrOperator : public Operator {
     DevBuf tbl2, tbl2_off;  // staged kernel tables (k_csr_pat_stage)
     int xspan_max = 0, tbl2_max = 0;
     size_t smem_stage = 0;
+    bool pipe = false;       // k_csr_pat_pipe (three stages fit in shared memory)
+    int pipe_ctas = 0;       // its resident CTAs per SM (queried at the first launch)
+    int pipe_stage_dbl = 0;  // doubles per pipeline stage
     struct PatTiles {  // a tile list split by kernel: staged / unstaged
         DevBuf staged, unstaged;
         int ns = 0, nu = 0;
@@ -496,8 +681,39 @@ class CsrOperator : public Operator {
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
+    template <bool H2, bool HR, bool DT>
+    npc_status launch_pipe(const StepArgs &s, const int *tl, int nt, double *partials) {
+        if (nt <= 0) return NPC_SUCCESS;
+        PatDev A{vals.as<double>(), tptr.as<int>(), pat.as<unsigned char>(), tbl.as<int>(), tbl_off.as<int>(),
+                 n_local, nullptr, tbl2.as<int>(), tbl2_off.as<int>()};
+        StepArgs a = s;
+        a.partials = partials;
+        auto kern = k_csr_pat_pipe<H2, HR, DT>;
+        const size_t sm = (size_t)PAT_PIPE_NS * pipe_stage_dbl * 8 + 128;
+        NPC_TRY(allow_max_dynamic_smem(kern));
+        if (pipe_ctas == 0) {  // resident CTAs per SM at this stage size (1 at 1,024-row tiles)
+            int occ = 0;
+            NPC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PAT_PIPE_THREADS, sm));
+            pipe_ctas = std::max(1, occ);
+        }
+        const int grid = std::min(nt, ctx->num_sms * pipe_ctas);
+        kern<<<grid, PAT_PIPE_THREADS, sm, ctx->stream>>>(A, a, tl, nt, vspan_max, xspan_max, tbl2_max, pipe_stage_dbl,
+                                                           nt);
+        NPC_LAUNCH_CHECK();
+        return NPC_SUCCESS;
+    }
     npc_status launch_stage_any(const StepArgs &s, const int *tl, int nt, double *partials) {
         const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
+        if (pipe) {
+            if (h2 && hr && dt) return launch_pipe<true, true, true>(s, tl, nt, partials);
+            if (h2 && hr) return launch_pipe<true, true, false>(s, tl, nt, partials);
+            if (h2 && dt) return launch_pipe<true, false, true>(s, tl, nt, partials);
+            if (h2) return launch_pipe<true, false, false>(s, tl, nt, partials);
+            if (hr && dt) return launch_pipe<false, true, true>(s, tl, nt, partials);
+            if (hr) return launch_pipe<false, true, false>(s, tl, nt, partials);
+            if (dt) return launch_pipe<false, false, true>(s, tl, nt, partials);
+            return launch_pipe<false, false, false>(s, tl, nt, partials);
+        }
         if (h2 && hr && dt) return launch_stage<true, true, true>(s, tl, nt, partials);
         if (h2 && hr) return launch_stage<true, true, false>(s, tl, nt, partials);
         if (h2 && dt) return launch_stage<true, false, true>(s, tl, nt, partials);
@@ -941,6 +1157,12 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
     op.xspan_max = ph.xspan_max;
     op.tbl2_max = (ph.tbl2_max + 3) & ~3;
     op.smem_stage = ((size_t)ph.vspan_max + (size_t)ph.xspan_max) * 8 + (size_t)op.tbl2_max * 4;
+    // pipeline stage: own block + x windows + table, rounded to 128 bytes (bulk-copy targets)
+    op.pipe_stage_dbl = (int)(((op.smem_stage + PAT_TILE + 127) / 128) * 16);  // + the tile's pattern ids
+    // opt-in (NPC_CSR_PIPE=1): measured slower than k_csr_pat_stage on config 3 (p_50 14.2 vs 11.4 ms,
+    // 512-row tiles 13.9 vs 11.6): one or two CTAs per SM leave too few warps to hide the row sums'
+    // shared-memory and FMA chains, while three independent CTAs of k_csr_pat_stage overlap them
+    op.pipe = (size_t)PAT_PIPE_NS * op.pipe_stage_dbl * 8 + 128 + 2048 <= 227 * 1024 && getenv("NPC_CSR_PIPE");
     auto split = [&](const std::vector<int> &list, CsrOperator::PatTiles &pt) -> npc_status {
         std::vector<int> st, un;
         for (int t : list) (ph.stage[t] ? st : un).push_back(t);
@@ -977,7 +1199,7 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
     }
     NPC_TRY(op.vals.alloc(sizeof(double) * ph.vals.size()));
     NPC_TRY(op.tptr.alloc(sizeof(int) * ph.tptr.size()));
-    NPC_TRY(op.pat.alloc(ph.pat.size()));
+    NPC_TRY(op.pat.alloc(ph.pat.size() + 16));  // bulk copies of a tile's ids round up to 16 bytes
     NPC_TRY(op.tbl.alloc(sizeof(int) * std::max<size_t>(ph.tbl.size(), 1)));
     NPC_TRY(op.tbl_off.alloc(sizeof(int) * ph.tbl_off.size()));
     NPC_CUDA_TRY(cudaMemcpy(op.vals.p, ph.vals.data(), sizeof(double) * ph.vals.size(), cudaMemcpyHostToDevice));

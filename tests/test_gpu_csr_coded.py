@@ -35,7 +35,7 @@ def dev(a):
 
 
 FORM_ENV = {"plain": "NPC_CSR_PLAIN", "coded": "NPC_CSR_CODED", "nomirror": "NPC_CSR_NOMIRROR",
-            "nostage": "NPC_CSR_NOSTAGE"}
+            "nostage": "NPC_CSR_NOSTAGE", "pipe": "NPC_CSR_PIPE"}
 
 
 def make(ctx, w, plain):

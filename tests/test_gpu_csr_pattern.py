@@ -64,7 +64,7 @@ WL = {"c3": lambda: W.config3(side=30), "c3_ragged": lambda: W.config3(side=23),
 
 def _all_forms_bitwise(ctx, w, k=17, xi=1e-3):
     n = w["n"]
-    ops = {f: make(ctx, w, f) for f in ("pattern", "nomirror", "nostage", "coded", "plain")}
+    ops = {f: make(ctx, w, f) for f in ("pattern", "nomirror", "nostage", "pipe", "coded", "plain")}
     x = np.random.default_rng(1).standard_normal(n)
     ys = {}
     os.environ["NPC_NO_CLUSTER"] = "1"

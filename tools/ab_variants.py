@@ -31,7 +31,10 @@ else:
 kind = KIND or bench.op_kind(w, CFG)
 ctx = npc.npc_context_create(0)
 op = npc.create_from_workload(ctx, w, kind)
-lo, hi = npc.npc_estimate_spectrum(op, 20, None)
+if os.environ.get("AB_INTERVAL"):  # fixed interval (variants whose operator is wrong on purpose)
+    lo, hi = (float(v) for v in os.environ["AB_INTERVAL"].split(":"))
+else:
+    lo, hi = npc.npc_estimate_spectrum(op, 20, None)
 poly = npc.npc_set_poly(op, K, lo, hi, 0.0)
 b = torch.tensor(w["b"], device="cuda"); z = torch.empty_like(b)
 for _ in range(3): npc.npc_apply_poly(poly, b, z)
