@@ -343,6 +343,37 @@ __device__ __forceinline__ double pat_row(const PatDev &A, const StepArgs &s, co
     return o;
 }
 
+// Two rows with the same pattern (lr0 < lr1, the common case: rows tid and tid + PAT_TILE/2 of
+// an interior tile): one table read per entry and two independent FMA chains (each row's sum in
+// its own stored order, so bitwise the same as two pat_row calls).
+__device__ __forceinline__ void pat_row_pair(const PatDev &A, const double *sv, const double *sx, const int *st,
+                                             const int4 *ent, int sidx, int row0, int lr0, int lr1, int pid,
+                                             double &y0, double &y1) {
+    const int e1 = st[sidx + pid + 1];
+    double a0 = 0.0, a1 = 0.0;
+    for (int e = st[sidx + pid]; e < e1; ++e) {
+        const int4 t = ent[e];
+        const double x0 = sx[t.x + lr0], x1 = sx[t.x + lr1];
+        double v0, v1;
+        if (lr1 + t.z >= 0) {
+            v1 = sv[t.y + lr1];
+        } else {
+            const int c = row0 + lr1 + t.z, tj = c / PAT_TILE;
+            v1 = __ldg(A.vals + __ldg(A.tptr + tj) + t.w * PAT_TILE + (c - tj * PAT_TILE));
+        }
+        if (lr0 + t.z >= 0) {
+            v0 = sv[t.y + lr0];
+        } else {
+            const int c = row0 + lr0 + t.z, tj = c / PAT_TILE;
+            v0 = __ldg(A.vals + __ldg(A.tptr + tj) + t.w * PAT_TILE + (c - tj * PAT_TILE));
+        }
+        a0 += v0 * x0;
+        a1 += v1 * x1;
+    }
+    y0 = a0;
+    y1 = a1;
+}
+
 template <bool HAS_S2, bool HAS_R, bool DOT>
 __global__ void __launch_bounds__(PAT_THREADS) k_csr_pat_stage(PatDev A, StepArgs s, const int *__restrict__ tiles,
                                                                int vspan_max, int xspan_max) {
@@ -407,15 +438,29 @@ __global__ void __launch_bounds__(PAT_THREADS) k_csr_pat_stage(PatDev A, StepArg
     const int sidx = 4 + 4 * nwin;
     const int4 *ent = reinterpret_cast<const int4 *>(st + st[1]);
     double acc = 0.0;
-    if (a0) {
-        const double o = pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l0, p0, x0, s20, r0);
-        s.out[row0 + l0] = o;
-        if (DOT) acc = o * s.dotv[row0 + l0];
-    }
-    if (a1) {
-        const double o = pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l1, p1, x1, s21, r1);
-        s.out[row0 + l1] = o;
-        if (DOT) acc += o * s.dotv[row0 + l1];
+#ifndef NPC_PAT_NOPAIR
+    if (a1 && p0 == p1) {  // both rows, one pattern: interleaved sums
+        double y0, y1;
+        pat_row_pair(A, sv, sx, st, ent, sidx, row0, l0, l1, p0, y0, y1);
+        double o0 = s.a * y0 + s.b * x0, o1 = s.a * y1 + s.b * x1;
+        if (HAS_S2) o0 += s.c * s20, o1 += s.c * s21;
+        if (HAS_R) o0 += s.d * r0, o1 += s.d * r1;
+        s.out[row0 + l0] = o0;
+        s.out[row0 + l1] = o1;
+        if (DOT) acc = o0 * s.dotv[row0 + l0] + o1 * s.dotv[row0 + l1];
+    } else
+#endif
+    {
+        if (a0) {
+            const double o = pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l0, p0, x0, s20, r0);
+            s.out[row0 + l0] = o;
+            if (DOT) acc = o * s.dotv[row0 + l0];
+        }
+        if (a1) {
+            const double o = pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l1, p1, x1, s21, r1);
+            s.out[row0 + l1] = o;
+            if (DOT) acc += o * s.dotv[row0 + l1];
+        }
     }
     if (DOT) {
         acc = block_sum<PAT_THREADS>(acc, red);
