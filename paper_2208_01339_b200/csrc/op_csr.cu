@@ -713,6 +713,25 @@ class CsrOperator : public Operator {
         return NPC_SUCCESS;
     }
 
+    // opt every pattern-form kernel variant into large dynamic shared memory up front
+    template <bool H2, bool HR, bool DT>
+    npc_status prepare3() {
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_stage<H2, HR, DT>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_pipe<H2, HR, DT>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_step<H2, HR, DT, false>));
+        return allow_max_dynamic_smem(k_csr_pat_step<H2, HR, DT, true>);
+    }
+    npc_status prepare_kernels() {
+        NPC_TRY((prepare3<true, true, true>()));
+        NPC_TRY((prepare3<true, true, false>()));
+        NPC_TRY((prepare3<true, false, true>()));
+        NPC_TRY((prepare3<true, false, false>()));
+        NPC_TRY((prepare3<false, true, true>()));
+        NPC_TRY((prepare3<false, true, false>()));
+        NPC_TRY((prepare3<false, false, true>()));
+        return prepare3<false, false, false>();
+    }
+
     template <bool H2, bool HR, bool DT>
     npc_status launch_stage(const StepArgs &s, const int *tl, int nt, double *partials) {
         if (nt <= 0) return NPC_SUCCESS;
@@ -1233,6 +1252,7 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
         NPC_CUDA_TRY(cudaMemcpy(op.tbl2.p, ph.tbl2.data(), sizeof(int) * ph.tbl2.size(), cudaMemcpyHostToDevice));
     NPC_CUDA_TRY(cudaMemcpy(op.tbl2_off.p, ph.tbl2_off.data(), sizeof(int) * ph.tbl2_off.size(), cudaMemcpyHostToDevice));
     if (!op.multi && !plan_csr_poly_cluster(n, d->rowptr, op.small)) op.small = SmallCsrPlan{};
+    NPC_TRY(op.prepare_kernels());  // before any launch can happen inside a PCG graph capture
     // the cluster-resident small-operator kernels read the plain arrays
     if (op.small.cl_size > 0) {
         NPC_TRY(op.rowptr.alloc(sizeof(int) * (n + 1)));

@@ -20,6 +20,18 @@ namespace npc {
 
 static constexpr int ST_BX = 32, ST_BY = 8, ST_ZC = 8;
 
+// The fused epilogue's arithmetic, spelled out as explicit FMAs so that every stencil kernel
+// (register, TMA, one- and two-degree) rounds identically whatever the compiler would contract:
+//   A x = diag x_i + off (sum of neighbours);  out = a (A x) + b x  [+ c s_{j-2}] [+ d r]
+__device__ __forceinline__ double st_ax(double diag, double x, double off, double nb) {
+    return __fma_rn(diag, x, off * nb);
+}
+__device__ __forceinline__ double st_lin(double a, double ax, double b, double x) {
+    return __fma_rn(a, ax, b * x);
+}
+
+
+
 struct StencilDev {
     int nx, ny, nzl;
     double diag, off;
@@ -62,10 +74,10 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
             if (x < S.nx - 1) nb += X[i + 1];
             if (y < S.ny - 1) nb += X[i + S.nx];
             nb += above;
-            const double ax = S.diag * cur + S.off * nb;
-            double o = s.a * ax + s.b * cur;
-            if (HAS_S2) o += s.c * s.s2[i];
-            if (HAS_R) o += s.d * s.r[i];
+            const double ax = st_ax(S.diag, cur, S.off, nb);
+            double o = st_lin(s.a, ax, s.b, cur);
+            if (HAS_S2) o = __fma_rn(s.c, s.s2[i], o);
+            if (HAS_R) o = __fma_rn(s.d, s.r[i], o);
             s.out[i] = o;
             if (DOT) acc += o * s.dotv[i];
             below = cur;
@@ -186,10 +198,10 @@ __global__ void __launch_bounds__(TS_THREADS) k_stencil_tma(const __grid_constan
                 nb += cur[c + 1];
                 nb += cur[c + TS_PX];
                 if (DIM == 3) nb += abv[c];
-                const double ax = T.diag * xc + T.off * nb;
-                double o = s.a * ax + s.b * xc;
-                if (HAS_S2) o += s.c * cur[TS_XSLOT + ly * TS_X + tx];
-                if (HAS_R) o += s.d * cur[TS_XSLOT + TS_VBOX + ly * TS_X + tx];
+                const double ax = st_ax(T.diag, xc, T.off, nb);
+                double o = st_lin(s.a, ax, s.b, xc);
+                if (HAS_S2) o = __fma_rn(s.c, cur[TS_XSLOT + ly * TS_X + tx], o);
+                if (HAS_R) o = __fma_rn(s.d, cur[TS_XSLOT + TS_VBOX + ly * TS_X + tx], o);
                 if (x < T.nx && y < T.ny) {
                     const long long i = x + (long long)T.nx * y + plane * z;
                     s.out[i] = o;
@@ -325,10 +337,10 @@ __global__ void __launch_bounds__(TBT) k_stencil_step2(int nx, int ny, int nz, i
                     nb += P0[pe + 1];
                     nb += P0[pe + TPX];
                     nb += Pp[pe];
-                    const double ax = diag * cur + off * nb;
-                    v = S.a1 * ax + S.b1 * cur;
-                    if (S.x2) v += S.c1 * s2c[u];
-                    v += S.d1 * rc[u];
+                    const double ax = st_ax(diag, cur, off, nb);
+                    v = st_lin(S.a1, ax, S.b1, cur);
+                    if (S.x2) v = __fma_rn(S.c1, s2c[u], v);
+                    v = __fma_rn(S.d1, rc[u], v);
                 }
                 Qz[e] = v;
                 Rz[e] = rc[u];
@@ -349,9 +361,11 @@ __global__ void __launch_bounds__(TBT) k_stencil_step2(int nx, int ny, int nz, i
                 nb += Q0[qe + 1];
                 nb += Q0[qe + TQX];
                 nb += Qp[qe];
-                const double ax = diag * cur + off * nb;
+                const double ax = st_ax(diag, cur, off, nb);
                 const double sjm1 = P[(zo + 4) & 3][(threadIdx.y + 2) * TPX + threadIdx.x + 2];
-                const double o = S.a2 * ax + S.b2 * cur + S.c2 * sjm1 + S.d2 * Rr[(zo + 3) % 3][qe];
+                double o = st_lin(S.a2, ax, S.b2, cur);
+                o = __fma_rn(S.c2, sjm1, o);
+                o = __fma_rn(S.d2, Rr[(zo + 3) % 3][qe], o);
                 const long long i = gx + (long long)nx * gy + plane * zo;
                 S.o1[i] = cur;
                 S.o2[i] = o;
@@ -367,6 +381,155 @@ __global__ void __launch_bounds__(TBT) k_stencil_step2(int nx, int ny, int nz, i
     if (DOT) {
         acc = block_sum<TBT>(acc, red);
         if (tid == 0) S.partials[linear_bid()] = acc;
+    }
+}
+
+// ---------------------------------------------------------------- TMA-staged two-degree kernel
+// Temporal blocking (as k_stencil_step2) on the TMA pipeline of k_stencil_tma: a 32 x 16 tile
+// marches z; stage q holds three tensor boxes of plane q -- s_{j-1} with a halo of 2
+// ((32 + 4) x (16 + 4) from (x0 - 2, y0 - 2)), s_{j-2} and r with a halo of 1 rounded to the
+// aligned box (32 + 4) x (16 + 2) from (x0 - 2, y0 - 1) -- in a ring of T2_NS stages; s_j is
+// computed on the tile + halo 1 into a shared ring of 3 planes (zero outside the grid), and
+// s_{j+1} of plane z - 1 from s_j planes z - 2 .. z.  Both outputs are written (s_j is the next
+// pair's s_{j-2}).  Per point and two degrees HBM sees s_{j-1}, s_{j-2}, r read and s_j, s_{j+1}
+// written: 5 streams instead of 8; the halo re-reads come from L2.  Same arithmetic and order
+// as the one-degree kernels: bitwise equal to two k_stencil_tma / k_stencil_step launches.
+static constexpr int T2_X = 32, T2_Y = 16, T2_THREADS = 256, T2_NS = 5;
+static constexpr int T2_PX = T2_X + 4, T2_PY = T2_Y + 4;  // s_{j-1} box
+static constexpr int T2_VX = T2_X + 4, T2_VY = T2_Y + 2;  // s_{j-2} / r box
+static constexpr int T2_QX = T2_X + 2, T2_QY = T2_Y + 2;  // s_j region (halo 1)
+static constexpr int T2_PSLOT = ((T2_PX * T2_PY * 8 + 127) / 128) * 16;  // doubles, 128-byte multiple
+static constexpr int T2_VSLOT = ((T2_VX * T2_VY * 8 + 127) / 128) * 16;
+static constexpr int T2_STAGE = T2_PSLOT + 2 * T2_VSLOT;
+static constexpr int T2_QN = T2_QX * T2_QY;
+static constexpr size_t T2_SMEM = ((size_t)T2_NS * T2_STAGE + 3 * T2_QN) * 8 + 128;
+
+struct StencilTma2 {
+    int nx, ny, nz, zc, tiles_x, tiles_y, items, npart_total;
+    double diag, off;
+    double a1, b1, c1, d1, a2, b2, c2, d2;
+    double *o1, *o2;
+    const double *dotv;
+    double *partials;
+    const int *done;
+    bool has_s2;
+};
+
+template <bool DOT>
+__global__ void __launch_bounds__(T2_THREADS) k_stencil_tma2(const __grid_constant__ CUtensorMap mp,
+                                                             const __grid_constant__ CUtensorMap m2,
+                                                             const __grid_constant__ CUtensorMap mr, StencilTma2 T) {
+    extern __shared__ __align__(128) unsigned char t2_raw[];
+    double *sm = reinterpret_cast<double *>(t2_raw + ((128u - (smem_u32(t2_raw) & 127u)) & 127u));
+    double *Q = sm + (size_t)T2_NS * T2_STAGE;  // s_j ring, 3 planes
+    __shared__ uint64_t bar[T2_NS];
+    __shared__ double red[T2_THREADS / 32];
+    if (T.done && *T.done) return;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < T2_NS; ++b) mbar_init(&bar[b], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    const long long plane = (long long)T.nx * T.ny;
+    const int ntiles = T.tiles_x * T.tiles_y;
+    double acc = 0.0;
+    for (int item = blockIdx.x; item < T.items; item += gridDim.x) {
+        const int tile = item % ntiles, chunk = item / ntiles;
+        const int x0 = (tile % T.tiles_x) * T2_X, y0 = (tile / T.tiles_x) * T2_Y;
+        const int z0 = chunk * T.zc, z1 = min(z0 + T.zc, T.nz);
+        const int qlo = z0 - 2, qhi = z1 + 1;  // planes staged: s_j is needed on z0-1 .. z1
+        auto slot = [&](int q) { return (q - qlo) % T2_NS; };
+        auto issue = [&](int q) {
+            const int b = slot(q);
+            double *st = sm + (size_t)b * T2_STAGE;
+            const bool need_v = q >= z0 - 1 && q <= z1;  // s_{j-2}, r: where s_j is computed
+            const uint32_t bytes = T2_PX * T2_PY * 8u + (need_v ? ((T.has_s2 ? 1u : 0u) + 1u) * T2_VX * T2_VY * 8u : 0u);
+            mbar_arrive_expect_tx(&bar[b], bytes);
+            tma_load_3d(st, &mp, x0 - 2, y0 - 2, q, &bar[b]);
+            if (need_v) {
+                if (T.has_s2) tma_load_3d(st + T2_PSLOT, &m2, x0 - 2, y0 - 1, q, &bar[b]);
+                tma_load_3d(st + T2_PSLOT + T2_VSLOT, &mr, x0 - 2, y0 - 1, q, &bar[b]);
+            }
+        };
+        if (threadIdx.x == 0)
+            for (int q = qlo; q <= min(qhi, qlo + T2_NS - 1); ++q) issue(q);
+        int waited = qlo - 1;
+        for (int zz = z0 - 1; zz <= z1; ++zz) {
+            // s_j at plane zz needs s_{j-1} planes zz-1 .. zz+1 (and s_{j-2}, r of plane zz)
+            for (int q = waited + 1; q <= zz + 1; ++q) {
+                const int b = slot(q);
+                mbar_wait(&bar[b], (phase >> b) & 1u);
+                phase ^= 1u << b;
+            }
+            waited = zz + 1;
+            const double *Pm = sm + (size_t)slot(zz - 1) * T2_STAGE, *P0 = sm + (size_t)slot(zz) * T2_STAGE,
+                         *Pp = sm + (size_t)slot(zz + 1) * T2_STAGE;
+            double *Qz = Q + (size_t)((zz + 3) % 3) * T2_QN;
+            for (int e = threadIdx.x; e < T2_QN; e += T2_THREADS) {
+                const int qx = e % T2_QX, qy = e / T2_QX;
+                const int gx = x0 + qx - 1, gy = y0 + qy - 1;
+                double v = 0.0;
+                if (gx >= 0 && gx < T.nx && gy >= 0 && gy < T.ny && zz >= 0 && zz < T.nz) {
+                    const int pe = (qy + 1) * T2_PX + qx + 1;  // s_{j-1} box position
+                    const int ve = qy * T2_VX + qx + 1;        // s_{j-2} / r box position
+                    const double cur = P0[pe];
+                    double nb = Pm[pe];
+                    nb += P0[pe - T2_PX];
+                    nb += P0[pe - 1];
+                    nb += P0[pe + 1];
+                    nb += P0[pe + T2_PX];
+                    nb += Pp[pe];
+                    const double ax = st_ax(T.diag, cur, T.off, nb);
+                    v = st_lin(T.a1, ax, T.b1, cur);
+                    if (T.has_s2) v = __fma_rn(T.c1, P0[T2_PSLOT + ve], v);
+                    v = __fma_rn(T.d1, P0[T2_PSLOT + T2_VSLOT + ve], v);
+                }
+                Qz[e] = v;
+            }
+            __syncthreads();  // s_j plane zz complete
+            // s_{j+1} at plane zo = zz - 1 on the tile
+            const int zo = zz - 1;
+            if (zo >= z0 && zo < z1) {
+                const double *Qm = Q + (size_t)((zo + 2) % 3) * T2_QN, *Q0 = Q + (size_t)((zo + 3) % 3) * T2_QN,
+                             *Qp = Q + (size_t)((zo + 4) % 3) * T2_QN;
+                const double *Po = sm + (size_t)slot(zo) * T2_STAGE;
+                for (int e = threadIdx.x; e < T2_X * T2_Y; e += T2_THREADS) {
+                    const int lx = e % T2_X, ly = e / T2_X;
+                    const int gx = x0 + lx, gy = y0 + ly;
+                    if (gx < T.nx && gy < T.ny) {
+                        const int qe = (ly + 1) * T2_QX + lx + 1;
+                        const double cur = Q0[qe];
+                        double nb = Qm[qe];
+                        nb += Q0[qe - T2_QX];
+                        nb += Q0[qe - 1];
+                        nb += Q0[qe + 1];
+                        nb += Q0[qe + T2_QX];
+                        nb += Qp[qe];
+                        const double ax = st_ax(T.diag, cur, T.off, nb);
+                        const double sjm1 = Po[(ly + 2) * T2_PX + lx + 2];
+                        const double rr = Po[T2_PSLOT + T2_VSLOT + (ly + 1) * T2_VX + lx + 2];
+                        double o = st_lin(T.a2, ax, T.b2, cur);
+                        o = __fma_rn(T.c2, sjm1, o);
+                        o = __fma_rn(T.d2, rr, o);
+                        const long long i = gx + (long long)T.nx * gy + plane * zo;
+                        T.o1[i] = cur;
+                        T.o2[i] = o;
+                        if (DOT) acc += o * T.dotv[i];
+                    }
+                }
+            }
+            __syncthreads();  // stage of plane zz - 1 and s_j plane zz - 2 are free
+            // plane zz - 1's stage is free once s_{j+1} of plane zz - 1 is done: refill it with
+            // plane zz - 1 + T2_NS
+            if (threadIdx.x == 0 && zz - 1 + T2_NS <= qhi && zz - 1 >= qlo) issue(zz - 1 + T2_NS);
+        }
+    }
+    if (DOT) {
+        acc = block_sum<T2_THREADS>(acc, red);
+        if (threadIdx.x == 0) T.partials[blockIdx.x] = acc;
+        if (blockIdx.x == 0)
+            for (int k = gridDim.x + threadIdx.x; k < T.npart_total; k += T2_THREADS) T.partials[k] = 0.0;
     }
 }
 
@@ -395,10 +558,15 @@ class StencilOperator : public Operator {
     // aligned vectors; tensor maps cached per (pointer, box kind)
     bool tma = false;
     int tma_blocks = 0, tma_zc = 0, tma_items = 0;
+    bool tma2 = false;  // k_stencil_tma2 for the paired degrees (step2)
+    int tma2_blocks = 0, tma2_zc = 0, tma2_items = 0;
     std::map<std::pair<const void *, int>, CUtensorMap> tmaps;
 
-    const CUtensorMap *tensor_map(const double *p, bool halo_box) {
-        auto key = std::make_pair((const void *)p, halo_box ? 1 : 0);
+    // box kinds: 0 = TS_X x TS_Y (k_stencil_tma s_{j-2}, r), 1 = its s_{j-1} box with halo,
+    // 2 = T2_PX x T2_PY (k_stencil_tma2 s_{j-1}), 3 = T2_VX x T2_VY (its s_{j-2}, r)
+    const CUtensorMap *tensor_map(const double *p, int box_kind) {
+        static const cuuint32_t BX[4] = {TS_X, TS_PX, T2_PX, T2_VX}, BY[4] = {TS_Y, TS_PY, T2_PY, T2_VY};
+        auto key = std::make_pair((const void *)p, box_kind);
         auto it = tmaps.find(key);
         if (it != tmaps.end()) return &it->second;
         auto enc = tensor_map_encoder();
@@ -406,7 +574,7 @@ class StencilOperator : public Operator {
         CUtensorMap m;
         const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)std::max(nzl, 1)};
         const cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
-        const cuuint32_t box[3] = {(cuuint32_t)(halo_box ? TS_PX : TS_X), (cuuint32_t)(halo_box ? TS_PY : TS_Y), 1};
+        const cuuint32_t box[3] = {BX[box_kind], BY[box_kind], 1};
         const cuuint32_t es[3] = {1, 1, 1};
         const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, dim == 3 ? 3 : 2, const_cast<double *>(p), dims,
                                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -442,9 +610,9 @@ class StencilOperator : public Operator {
     npc_status try_launch_tma(const StepArgs &s, bool *done) {
         *done = false;
         if (!tma || !al16(s.x) || !al16(s.s2) || !al16(s.r)) return NPC_SUCCESS;
-        const CUtensorMap *mx = tensor_map(s.x, true);
-        const CUtensorMap *m2 = s.s2 ? tensor_map(s.s2, false) : nullptr;
-        const CUtensorMap *mr = s.r ? tensor_map(s.r, false) : nullptr;
+        const CUtensorMap *mx = tensor_map(s.x, 1);
+        const CUtensorMap *m2 = s.s2 ? tensor_map(s.s2, 0) : nullptr;
+        const CUtensorMap *mr = s.r ? tensor_map(s.r, 0) : nullptr;
         if (!mx || (s.s2 && !m2) || (s.r && !mr)) return NPC_SUCCESS;
         *done = true;
         return dim == 3 ? launch_tma_d<3>(s, mx, m2, mr) : launch_tma_d<2>(s, mx, m2, mr);
@@ -536,7 +704,7 @@ class StencilOperator : public Operator {
         // needed two degrees deep
         if (dim != 3 || (multi && ctx->nranks > 1) || n_local == 0 || getenv("NPC_NO_STEP2")) return false;
         if (getenv("NPC_STEP2")) return true;
-        if (tma) return false;  // the TMA one-degree kernel is faster (r02: 256^3 p_30 2.55 vs 2.64 ms)
+        if (tma) return tma2;  // k_stencil_tma2 only when opted in (NPC_ST_TMA2=1)
         int l2 = 0;
         if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device) != cudaSuccess || l2 <= 0)
             l2 = 126 << 20;
@@ -544,7 +712,7 @@ class StencilOperator : public Operator {
     }
     int num_partials2() const override {
         dim3 g = grid2();
-        return (int)(g.x * g.y * g.z);
+        return std::max((int)(g.x * g.y * g.z), tma2 ? tma2_blocks : 0);
     }
     double bytes_per_step2() const override { return 5.0 * 8.0 * n_local; }
     npc_status step2(const StepArgs &s1, const StepArgs &s2) override {
@@ -553,6 +721,29 @@ class StencilOperator : public Operator {
         if (!S.r) {
             set_error("stencil step2: r is required");
             return NPC_ERR_INVALID_ARGUMENT;
+        }
+        if (tma2 && al16(s1.x) && al16(s1.s2) && al16(s1.r)) {
+            const CUtensorMap *mp = tensor_map(s1.x, 2);
+            const CUtensorMap *m2 = s1.s2 ? tensor_map(s1.s2, 3) : nullptr;
+            const CUtensorMap *mr = tensor_map(s1.r, 3);
+            if (mp && mr && (!s1.s2 || m2)) {
+                StencilTma2 T{nx, ny, nzl, tma2_zc, ceil_div(nx, T2_X), ceil_div(ny, T2_Y), tma2_items,
+                              num_partials2(), diag, off, s1.a, s1.b, s1.c, s1.d, s2.a, s2.b, s2.c, s2.d,
+                              s1.out, s2.out, s2.dotv, s2.partials, s1.done, s1.s2 != nullptr};
+                if (s2.dotv) {
+                    NPC_TRY(allow_max_dynamic_smem(k_stencil_tma2<true>));
+                    k_stencil_tma2<true><<<tma2_blocks, T2_THREADS, T2_SMEM, ctx->stream>>>(*mp, m2 ? *m2 : *mr, *mr, T);
+                } else {
+                    NPC_TRY(allow_max_dynamic_smem(k_stencil_tma2<false>));
+                    k_stencil_tma2<false><<<tma2_blocks, T2_THREADS, T2_SMEM, ctx->stream>>>(*mp, m2 ? *m2 : *mr, *mr, T);
+                }
+                NPC_LAUNCH_CHECK();
+                return NPC_SUCCESS;
+            }
+        }
+        if (S.dotv && num_partials2() > (int)(grid2().x * grid2().y * grid2().z)) {
+            const int nb = (int)(grid2().x * grid2().y * grid2().z);
+            NPC_TRY(launch_fill(ctx, S.partials + nb, 0.0, num_partials2() - nb));
         }
         const int zc = zc2();
         if (s2.dotv)
@@ -649,6 +840,20 @@ npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::
         op->tma_zc = std::min(zc, std::max(op->nzl, 1));
         op->tma_items = tiles * (op->dim == 3 ? ceil_div(op->nzl, op->tma_zc) : 1);
         op->tma_blocks = std::min(op->tma_items, blocks_max);
+        // paired degrees (opt-in, NPC_ST_TMA2=1): measured slower than the one-degree TMA kernel
+        // (256^3 p_30 2.65 vs 2.55 ms, 200^3 1.51 vs 1.39 ms: two barriers and two compute phases per
+        // plane at 16 warps per SM do not keep enough copies in flight), so k_stencil_tma serves
+        // every degree by default
+        if (op->dim == 3 && getenv("NPC_ST_TMA2")) {  // 2 CTAs of T2_SMEM per SM
+            op->tma2 = true;
+            const int tiles2 = ceil_div(op->nx, T2_X) * ceil_div(op->ny, T2_Y);
+            const int bmax2 = std::max(1, (int)((227 * 1024) / (T2_SMEM + 1024))) * ctx->num_sms;
+            int zc2v = std::max(8, (int)((long long)op->nzl * tiles2 / (4LL * bmax2)));
+            if (const char *e = getenv("NPC_ST_T2ZC")) zc2v = std::max(2, atoi(e));
+            op->tma2_zc = std::min(zc2v, std::max(op->nzl, 1));
+            op->tma2_items = tiles2 * ceil_div(op->nzl, op->tma2_zc);
+            op->tma2_blocks = std::min(op->tma2_items, bmax2);
+        }
     }
     if (ctx->distributed()) {
         if (op->dim != 3) {

@@ -17,10 +17,17 @@ npc_status allow_max_dynamic_smem_ptr(const void *kern) {
         if (k == kern) return NPC_SUCCESS;
     int dev = 0, optin = 0;
     cudaFuncAttributes fa{};
-    NPC_CUDA_TRY(cudaGetDevice(&dev));
-    NPC_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    NPC_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
-    NPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+    // may run while a PCG iteration is being stream-captured (a kernel variant's first launch):
+    // these are not stream operations, so let this thread make them in relaxed capture mode
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kern);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    NPC_CUDA_TRY(e);
     done.push_back(kern);
     return NPC_SUCCESS;
 }
