@@ -191,7 +191,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         inside = [ln for t, ln in self.lines if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
         for ln in inside or [ln for _, ln in self.lines[-3:]]:
@@ -203,11 +203,16 @@ class ClockSampler:
                 mx = float(p[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(p[2]))
+            except ValueError:
+                pass
             for nm, v in zip(names, p[3:7]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": float(np.median(pw)) if pw else None,
+                "power_w_max": float(np.max(pw)) if pw else None}
 
 
 # ------------------------------------------------------------------ distributed helpers
@@ -493,6 +498,9 @@ def run_ours(args):
         line = {
             "metric": METRIC,
             "value": round(gbs, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "value_basis": "effective bandwidth: format-independent SURVEY §8(d) bytes of the step (CSR: 12 B per "
+                           "nonzero) / time-to-tol, so it can exceed the copy rate when the stored format moves less "
+                           "(the pattern form streams ~4.7 B per nonzero); roofline.* uses the bytes actually streamed",
             "ms_per_step": round(ms_step, 3), "step_ms": step_ms, "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads/, BASELINE.json config recipe)",
