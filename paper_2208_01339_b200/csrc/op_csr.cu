@@ -936,7 +936,9 @@ npc_status localize_columns(Context *ctx, const npc_operator_desc *d, HaloPlan &
     const long long nnz = d->rowptr[n];
     local_cols.resize((size_t)nnz);
     if (!ctx->distributed()) {
-        for (long long p = 0; p < nnz; ++p) local_cols[p] = d->colidx[p];
+        host_parallel_for(nnz, [&](long long b, long long e, int) {
+            std::memcpy(local_cols.data() + b, d->colidx + b, sizeof(int) * (size_t)(e - b));
+        });
         return NPC_SUCCESS;
     }
     // partition: gather every rank's row_begin (collective)
@@ -969,7 +971,7 @@ npc_status localize_columns(Context *ctx, const npc_operator_desc *d, HaloPlan &
 // with more than 256 own values, ELL padding above 1/8 of the own values, or a block larger
 // than the shared-memory budget.
 struct PatHost {
-    std::vector<double> vals;
+    std::unique_ptr<double[]> vals;  // own values, tile-ELL blocks (own_nnz + 8 padding)
     std::vector<int> tptr, tbl, tbl_off;
     std::vector<unsigned char> pat;
     int vspan_max = 0, tbl_max = 0;
@@ -1058,11 +1060,13 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
     const long long nnz = rowptr[n];
     // 1. mirror partners: a_ij (j < i, owned) whose transpose a_ji exists with the
     //    bitwise-identical value (then a_ji is an upper entry of row j, hence always own)
-    std::vector<int> partner((size_t)nnz, -1);
-    if (mirror)
-        host_parallel_for(n, [&](long long b, long long e, int) {
+    std::unique_ptr<int[]> partner_buf(new int[(size_t)std::max<long long>(nnz, 1)]);
+    int *partner = partner_buf.get();
+    host_parallel_for(n, [&](long long b, long long e, int) {
             for (long long i = b; i < e; ++i)
                 for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+                    partner[p] = -1;
+                    if (!mirror) continue;
                     const int c = lcols[p];
                     if (c >= i || c < 0 || i - c >= PAT_MIRROR_MAX_OFF) continue;  // ghosts: c >= n > i
                     const int *lo = gcol + rowptr[c], *hi = gcol + rowptr[c + 1];
@@ -1073,17 +1077,20 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
                 }
         });
     // 2. index of every own entry within its row's own list (mirror positions refer to it)
-    std::vector<unsigned char> opos((size_t)nnz, 0);
+    std::unique_ptr<unsigned char[]> opos_buf(new unsigned char[(size_t)std::max<long long>(nnz, 1)]);
+    unsigned char *opos = opos_buf.get();
     std::vector<int> rown((size_t)std::max(n, 1), 0);
     std::vector<char> bad(64, 0);
     host_parallel_for(n, [&](long long b, long long e, int t) {
         for (long long i = b; i < e; ++i) {
             int k = 0;
-            for (int p = rowptr[i]; p < rowptr[i + 1]; ++p)
+            for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+                opos[p] = 0;
                 if (partner[p] < 0) {
                     if (k > 255) bad[t] = 1;
                     opos[p] = (unsigned char)k++;
                 }
+            }
             rown[i] = k;
         }
     });
@@ -1183,12 +1190,14 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
     }
     ph.tbl2.resize((size_t)ph.tbl2_off[ntiles]);
     for (int t = 0; t < ntiles; ++t) std::copy(ttbl2[t].begin(), ttbl2[t].end(), ph.tbl2.begin() + ph.tbl2_off[t]);
-    ph.vals.assign((size_t)ph.own_nnz + 8, 0.0);
+    ph.vals.reset(new double[(size_t)ph.own_nnz + 8]);
+    std::fill(ph.vals.get() + ph.own_nnz, ph.vals.get() + ph.own_nnz + 8, 0.0);
     host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
         for (long long t = t0; t < t1; ++t) {
             std::copy(ttbl[t].begin(), ttbl[t].end(), ph.tbl.begin() + ph.tbl_off[t]);
             const int r0 = (int)t * PAT_TILE, r1 = std::min(n, r0 + PAT_TILE), nr = r1 - r0;
-            double *blk = ph.vals.data() + ph.tptr[t];
+            double *blk = ph.vals.get() + ph.tptr[t];
+            std::fill(blk, ph.vals.get() + ph.tptr[t + 1], 0.0);  // ELL padding
             for (int i = r0; i < r1; ++i)
                 for (int p = rowptr[i]; p < rowptr[i + 1]; ++p)
                     if (partner[p] < 0) blk[(size_t)opos[p] * nr + (i - r0)] = vals[p];
@@ -1262,12 +1271,13 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
         NPC_CUDA_TRY(cudaMemcpy(op.cols.p, lcols.data(), sizeof(int) * op.nnz, cudaMemcpyHostToDevice));
         NPC_CUDA_TRY(cudaMemcpy(op.cvals.p, d->vals, sizeof(double) * op.nnz, cudaMemcpyHostToDevice));
     }
-    NPC_TRY(op.vals.alloc(sizeof(double) * ph.vals.size()));
+    const size_t nvals = (size_t)ph.own_nnz + 8;
+    NPC_TRY(op.vals.alloc(sizeof(double) * nvals));
     NPC_TRY(op.tptr.alloc(sizeof(int) * ph.tptr.size()));
     NPC_TRY(op.pat.alloc(ph.pat.size() + 16));  // bulk copies of a tile's ids round up to 16 bytes
     NPC_TRY(op.tbl.alloc(sizeof(int) * std::max<size_t>(ph.tbl.size(), 1)));
     NPC_TRY(op.tbl_off.alloc(sizeof(int) * ph.tbl_off.size()));
-    NPC_CUDA_TRY(cudaMemcpy(op.vals.p, ph.vals.data(), sizeof(double) * ph.vals.size(), cudaMemcpyHostToDevice));
+    NPC_CUDA_TRY(cudaMemcpy(op.vals.p, ph.vals.get(), sizeof(double) * nvals, cudaMemcpyHostToDevice));
     NPC_CUDA_TRY(cudaMemcpy(op.tptr.p, ph.tptr.data(), sizeof(int) * ph.tptr.size(), cudaMemcpyHostToDevice));
     NPC_CUDA_TRY(cudaMemcpy(op.pat.p, ph.pat.data(), ph.pat.size(), cudaMemcpyHostToDevice));
     if (!ph.tbl.empty())
