@@ -197,7 +197,9 @@ __global__ void NPC_DFN_LB(32 * DFN_WARPS) k_dfn_dense(DfnDev D, const int4 *__r
             for (size_t o = (size_t)lane * 128; o < bytes; o += 32 * 128)
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
         };
+#ifndef NPC_DFN_NOPF_AI
         pf(Ai, (size_t)m * m * 8);
+#endif
         pf(D.cv + br.x, (size_t)(br.y - br.x) * 8);
         pf(D.cci + br.x, (size_t)(br.y - br.x) * 4);
         pf(D.bv + br.z, (size_t)(br.w - br.z) * 8);
@@ -232,7 +234,17 @@ __global__ void NPC_DFN_LB(32 * DFN_WARPS) k_dfn_dense(DfnDev D, const int4 *__r
 #pragma unroll
         for (int r = 0; r < RPL; ++r) {
             const int i = lane + 32 * r;
+#ifdef NPC_DFN_EVL  // A/B: the first pass marks A_f^-1 evict-last so that the second pass hits L2
+            double aij = 0.0;
+            if (i < m) {
+                const double *pa = Ai + (size_t)j * m + i;
+                uint64_t pol;
+                asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(aij) : "l"(pa), "l"(pol));
+            }
+#else
             const double aij = (i < m) ? __ldg(Ai + (size_t)j * m + i) : 0.0;
+#endif
             ai[r] += aij * vj;
             wi[r] += aij * zj;
         }
