@@ -179,3 +179,10 @@ def test_config4_full_8m_pcg_vs_oracle_golden(ctx):
     g = _golden("config4_8000000_pcg_k60.json")
     w = W.config4()
     _pcg_vs_golden(ctx, w, "sell", g)
+
+
+def test_config3_full_pcg_xi_vs_oracle_golden(ctx):
+    """The headline solve with the paper's xi (Eq. thetamod, reading A12: xi = 1e-3) at full
+    size against the oracle's golden."""
+    g = _golden("config3_256_pcg_k50_xi0.001.json")
+    _pcg_vs_golden(ctx, W.config3(256), "csr", g, check_x1=True)
