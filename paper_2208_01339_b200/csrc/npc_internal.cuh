@@ -110,6 +110,18 @@ struct StepArgs {
     double a = 1.0, b = 0.0, c = 0.0, d = 0.0;
 };
 
+// Fused degree-step epilogue o = a*y + b*x (+ c*s_{j-2}) (+ d*r) in ONE rounding order --
+// a*y rounded, then one FMA per term in this order -- for every kernel of an operator family,
+// whose storage forms are compared bitwise (the compiler's own contraction choice differs
+// between kernels).
+template <bool HAS_S2, bool HAS_R>
+__device__ __forceinline__ double degree_epilogue(const StepArgs &s, double y, double x, double s2v, double rv) {
+    double o = fma(s.b, x, __dmul_rn(s.a, y));
+    if (HAS_S2) o = fma(s.c, s2v, o);
+    if (HAS_R) o = fma(s.d, rv, o);
+    return o;
+}
+
 struct Context;
 struct ClusterPcgOut;
 

@@ -140,9 +140,7 @@ __global__ void __launch_bounds__(TILE) k_csr_step(CsrDev A, StepArgs s, const i
                 xv = __ldg(x + c);
             y += v * xv;
         }
-        double o = s.a * y + s.b * xs;
-        if (HAS_S2) o += s.c * s2v;
-        if (HAS_R) o += s.d * rv;
+        const double o = degree_epilogue<HAS_S2, HAS_R>(s, y, xs, s2v, rv);
         s.out[row] = o;
         if (DOT) acc = o * s.dotv[row];
     }
@@ -248,7 +246,7 @@ __global__ void __launch_bounds__(PAT_TILE) k_csr_pat_step(PatDev A, StepArgs s,
                 const int pos = (w >> 1) & 255;
                 c = row + (w >> 9);
                 if (c >= row0) {
-                    v = sv[pos * nrows + (c - row0)];
+                    v = sv[pos * ((nrows + 1) & ~1) + (c - row0)];  // even column stride
                 } else {  // an earlier (full) tile's block, through L2
                     const int tj = c / PAT_TILE;
                     v = __ldg(A.vals + __ldg(A.tptr + tj) + pos * PAT_TILE + (c - tj * PAT_TILE));
@@ -256,7 +254,7 @@ __global__ void __launch_bounds__(PAT_TILE) k_csr_pat_step(PatDev A, StepArgs s,
             } else {
                 c = row + (w >> 1);
                 v = *own;
-                own += nrows;
+                own += (nrows + 1) & ~1;
             }
             double xv;
             if (GHOST && c >= A.n)
@@ -265,9 +263,7 @@ __global__ void __launch_bounds__(PAT_TILE) k_csr_pat_step(PatDev A, StepArgs s,
                 xv = __ldg(x + c);
             y += v * xv;
         }
-        double o = s.a * y + s.b * xs;
-        if (HAS_S2) o += s.c * s2v;
-        if (HAS_R) o += s.d * rv;
+        const double o = degree_epilogue<HAS_S2, HAS_R>(s, y, xs, s2v, rv);
         s.out[row] = o;
         if (DOT) acc = o * s.dotv[row];
     }
@@ -290,57 +286,26 @@ __global__ void __launch_bounds__(PAT_TILE) k_csr_pat_step(PatDev A, StepArgs s,
 static constexpr int PAT_THREADS = PAT_TILE / 2;
 static constexpr int PAT_STAGE_SMEM = 110 * 1024;  // own block + x windows + table, per tile
 
-// Values of a row's first two mirrors in EARLIER tiles (coalesced L2 reads; a 3D grid: -N^2,
-// and -N for the first rows of a tile), loaded ahead of the row's sum (k_csr_pat_pipe issues
-// them one tile early).  Entries are in column order, so those mirrors come first.
-struct PatMirrors {
-    double v0 = 0.0, v1 = 0.0;
-    int n = 0;  // how many were loaded (0: pat_row loads them itself)
-};
-__device__ __forceinline__ PatMirrors pat_mirrors(const PatDev &A, const int *st, const int4 *ent, int sidx,
-                                                  int row0, int lr, int pid) {
-    // predicated loads into fixed registers: nothing depends on a loaded value here, so the
-    // loads stay in flight until pat_row uses them
-    PatMirrors m;
-    const int eb = st[sidx + pid], e1 = st[sidx + pid + 1];
-    const int4 z4 = make_int4(0, 0, 0, 0);
-    const int4 t0 = eb < e1 ? ent[eb] : z4, t1 = eb + 1 < e1 ? ent[eb + 1] : z4;
-    const bool g0 = eb < e1 && lr + t0.z < 0, g1 = g0 && eb + 1 < e1 && lr + t1.z < 0;
-    const int c0 = row0 + lr + t0.z, c1 = row0 + lr + t1.z;
-    const int j0 = g0 ? c0 / PAT_TILE : 0, j1 = g1 ? c1 / PAT_TILE : 0;
-    m.v0 = g0 ? __ldg(A.vals + __ldg(A.tptr + j0) + t0.w * PAT_TILE + (c0 - j0 * PAT_TILE)) : 0.0;
-    m.v1 = g1 ? __ldg(A.vals + __ldg(A.tptr + j1) + t1.w * PAT_TILE + (c1 - j1 * PAT_TILE)) : 0.0;
-    m.n = 2;
-    return m;
-}
-
 template <bool HAS_S2, bool HAS_R>
 __device__ __forceinline__ double pat_row(const PatDev &A, const StepArgs &s, const double *sv, const double *sx,
                                           const int *st, const int4 *ent, int sidx, int row0, int lr, int pid,
-                                          double xs, double s2v, double rv, const PatMirrors *pm = nullptr) {
+                                          double xs, double s2v, double rv) {
     const int row = row0 + lr;
     const int e1 = st[sidx + pid + 1];
     double y = 0.0;
-    int km = 0;
     for (int e = st[sidx + pid]; e < e1; ++e) {
         const int4 t = ent[e];
         const double xv = sx[t.x + lr];
         double v;
         if (lr + t.z >= 0) {
             v = sv[t.y + lr];
-        } else if (pm && km < 2) {  // loaded ahead
-            v = km == 0 ? pm->v0 : pm->v1;
-            ++km;
         } else {  // mirror in an earlier (full) tile's block, through L2
             const int c = row + t.z, tj = c / PAT_TILE;
             v = __ldg(A.vals + __ldg(A.tptr + tj) + t.w * PAT_TILE + (c - tj * PAT_TILE));
         }
         y += v * xv;
     }
-    double o = s.a * y + s.b * xs;
-    if (HAS_S2) o += s.c * s2v;
-    if (HAS_R) o += s.d * rv;
-    return o;
+    return degree_epilogue<HAS_S2, HAS_R>(s, y, xs, s2v, rv);
 }
 
 // Two rows with the same pattern (lr0 < lr1, the common case: rows tid and tid + PAT_TILE/2 of
@@ -358,14 +323,22 @@ __device__ __forceinline__ void pat_row_pair(const PatDev &A, const double *sv, 
         if (lr1 + t.z >= 0) {
             v1 = sv[t.y + lr1];
         } else {
+#ifdef NPC_AB_NOL2M  // A/B only (results wrong): no earlier-tile mirror reads
+            v1 = 0.0;
+#else
             const int c = row0 + lr1 + t.z, tj = c / PAT_TILE;
             v1 = __ldg(A.vals + __ldg(A.tptr + tj) + t.w * PAT_TILE + (c - tj * PAT_TILE));
+#endif
         }
         if (lr0 + t.z >= 0) {
             v0 = sv[t.y + lr0];
         } else {
+#ifdef NPC_AB_NOL2M
+            v0 = 0.0;
+#else
             const int c = row0 + lr0 + t.z, tj = c / PAT_TILE;
             v0 = __ldg(A.vals + __ldg(A.tptr + tj) + t.w * PAT_TILE + (c - tj * PAT_TILE));
+#endif
         }
         a0 += v0 * x0;
         a1 += v1 * x1;
@@ -438,16 +411,20 @@ __global__ void __launch_bounds__(PAT_THREADS) k_csr_pat_stage(PatDev A, StepArg
     const int sidx = 4 + 4 * nwin;
     const int4 *ent = reinterpret_cast<const int4 *>(st + st[1]);
     double acc = 0.0;
+#ifdef NPC_AB_NOSUM  // A/B only (results wrong): the copies and the epilogue, no row sums
+    if (a0) s.out[row0 + l0] = s.b * x0 + s.c * s20 + s.d * r0 + sv[l0] + (double)p0;
+    if (a1) s.out[row0 + l1] = s.b * x1 + s.c * s21 + s.d * r1 + sv[l1] + (double)p1;
+    if (false)
+#endif
 #ifndef NPC_PAT_NOPAIR
     if (a1 && p0 == p1) {  // both rows, one pattern: interleaved sums
         double y0, y1;
         pat_row_pair(A, sv, sx, st, ent, sidx, row0, l0, l1, p0, y0, y1);
-        double o0 = s.a * y0 + s.b * x0, o1 = s.a * y1 + s.b * x1;
-        if (HAS_S2) o0 += s.c * s20, o1 += s.c * s21;
-        if (HAS_R) o0 += s.d * r0, o1 += s.d * r1;
+        const double o0 = degree_epilogue<HAS_S2, HAS_R>(s, y0, x0, s20, r0),
+                     o1 = degree_epilogue<HAS_S2, HAS_R>(s, y1, x1, s21, r1);
         s.out[row0 + l0] = o0;
         s.out[row0 + l1] = o1;
-        if (DOT) acc = o0 * s.dotv[row0 + l0] + o1 * s.dotv[row0 + l1];
+        if (DOT) acc = fma(o1, s.dotv[row0 + l1], __dmul_rn(o0, s.dotv[row0 + l0]));  // as two acc += steps
     } else
 #endif
     {
@@ -468,157 +445,150 @@ __global__ void __launch_bounds__(PAT_THREADS) k_csr_pat_stage(PatDev A, StepArg
     }
 }
 
-// Pipelined persistent form of k_csr_pat_stage (opt-in, NPC_CSR_PIPE=1; see the A/B where it is
-// enabled in finish_pattern_operator): one CTA per SM walks its tiles (blockIdx.x, + gridDim.x, ...) through a
-// ring of stages, each holding a tile's own-value block, x windows and table.  Warp-
-// specialised: a producer warp (warp PAT_THREADS / 32) waits for a stage to be released
-// (`empty` mbarrier, one arrival per consumer warp), reads the tile's copy descriptors and
-// issues its bulk copies on the stage's `full` mbarrier, running up to PAT_PIPE_NS tiles ahead;
-// the PAT_THREADS consumer threads (two rows each) wait on `full`, compute, release the stage.
-// The per-row streams of the next tile (pattern ids, s_{j-2}, r) are loaded into registers one
-// tile ahead.  Load and compute phases of consecutive tiles thus overlap instead of each CTA
-// waiting for its single tile (config 3: the copies alone run at 0.96 of HBM, 172 us per degree;
-// with the row sums in the same CTA lifetime, k_csr_pat_stage, 231 us).  Dot partial: one per
-// CTA; CTA 0 zeroes the slots of the other launches' layout up to npart_total.
-static constexpr int PAT_PIPE_NS = 3;
-static constexpr int PAT_PIPE_THREADS = PAT_THREADS + 32;
+// Ring kernel (the default for staged tiles; NPC_CSR_RING=0 -> k_csr_pat_stage): every operand
+// of a tile's row sums is in shared memory before the sums start, so the compute phase has no
+// global-memory round trip.  Per tile the host precomputes (pattern_ring_table):
+//   * a copy list of <= RING_MAXD - 1 bulk copies (cp.async.bulk, one mbarrier): the tile's table,
+//     its pattern ids, its own-value columns, the values of mirrors in EARLIER tiles -- near ones
+//     (a 3D grid's -N for the first rows of a tile) as a "gap" directly in front of the column
+//     they come from, so D[col_p + o + lr] addresses both halves, far ones (-N^2) as a window of
+//     the earlier tile's column -- and the x windows; lanes of warp 0 issue one copy each, so the
+//     first byte is requested one global load after the CTA starts;
+//   * a table of entries {xb, vb}: x = D[xb + lr], value = D[vb + lr] for row lr of the tile --
+//     one branch-free form for own values, in-tile, near and far mirrors.
+// Two rows per thread (lr = tid, tid + PAT_THREADS) summed in one loop when their patterns have
+// the same length.  Same values in the same order as the plain form: bitwise the same results.
+// NS = 1: one tile per CTA (grid = tiles), 3 CTAs per SM, each CTA's copies in flight while the
+// other CTAs compute.  NS > 1 (A/B, NPC_RING_NS): persistent CTAs walking tiles blockIdx.x +
+// i * gridDim.x through NS stages, the copies of tile i + NS issued as tile i's sums finish.
+static constexpr int RING_MAXD = 16;              // int4 copy descriptors per tile (header + copies)
+static constexpr int RING_GAP_MAX = PAT_TILE;  // near earlier-tile mirrors held as a column gap
+static constexpr int RING_STAGE_MAX = 110 * 1024;  // bytes of one stage
 
-template <bool HAS_S2, bool HAS_R, bool DOT>
-__global__ void __launch_bounds__(PAT_PIPE_THREADS, 1)
-    k_csr_pat_pipe(PatDev A, StepArgs s, const int *__restrict__ tiles, int ntl, int vspan_max, int xspan_max,
-                   int tbl2_max, int stage_dbl, int npart_total) {
-    extern __shared__ __align__(128) unsigned char pp_raw[];
-    double *base = reinterpret_cast<double *>(pp_raw + ((128u - (smem_u32(pp_raw) & 127u)) & 127u));
-    __shared__ uint64_t full[PAT_PIPE_NS], empty[PAT_PIPE_NS];
-    __shared__ double red[PAT_PIPE_THREADS / 32];
-    if (s.done && *s.done) return;  // uniform: before any copy is issued
-    constexpr int NCW = PAT_THREADS / 32;  // consumer warps
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+struct RingDev {
+    const double *vals;          // own values (tile-ELL blocks, as PatDev::vals)
+    const int *tbl;              // concatenated per-tile ring tables (16-byte aligned each)
+    const unsigned char *pat;    // pattern id per row
+    const int4 *desc;            // RING_MAXD descriptors per tile: {ncopies, bytes} + {kind, dst, src, bytes}
+    int n;
+};
+
+template <bool HAS_S2, bool HAS_R, bool DOT, int NS>
+__global__ void __launch_bounds__(PAT_THREADS, NS == 1 ? 1536 / PAT_THREADS : 1)
+    k_csr_pat_ring(RingDev A, StepArgs s, const int *__restrict__ tiles, int ntl, int stage_bytes, int tbl_bytes) {
+    extern __shared__ __align__(16) unsigned char rg_smem[];
+    __shared__ uint64_t full[NS];
+    __shared__ double red[PAT_THREADS / 32];
+    if (s.done && *s.done) return;  // uniform, before any copy is issued
+    const int lane = threadIdx.x & 31;
+    const bool issuer = threadIdx.x < 32;
     if (threadIdx.x == 0) {
-        for (int b = 0; b < PAT_PIPE_NS; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&empty[b], NCW);
-        }
+        for (int b = 0; b < NS; ++b) mbar_init(&full[b], 1);
         fence_mbar_init();
     }
     __syncthreads();
-    auto tile_of = [&](int i) { const int q = blockIdx.x + i * gridDim.x; return tiles ? tiles[q] : q; };
     const int nmine = ntl > (int)blockIdx.x ? (ntl - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto tile_of = [&](int i) {
+        const int q = (int)blockIdx.x + i * (int)gridDim.x;
+        return tiles ? tiles[q] : q;
+    };
+    // warp 0: the copies of tile i into stage i % NS
+    auto issue = [&](int i) {
+        const int tile = tile_of(i);
+        unsigned char *st = rg_smem + (size_t)(i % NS) * stage_bytes;
+        uint64_t *bar = &full[i % NS];
+        int4 d = make_int4(0, 0, 0, 0);
+        if (lane < RING_MAXD) d = A.desc[(size_t)tile * RING_MAXD + lane];
+        if (lane > 0 && d.x == 4) *reinterpret_cast<double *>(st + d.y) = s.x[d.z];  // odd x tail
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)d.y);  // header {ncopies, bytes}
+        __syncwarp();
+        if (lane > 0 && d.w > 0) {
+            const void *src = d.x == 0   ? (const void *)(A.vals + d.z)
+                              : d.x == 1 ? (const void *)(s.x + d.z)
+                              : d.x == 2 ? (const void *)(A.tbl + d.z)
+                                         : (const void *)(A.pat + d.z);
+            bulk_g2s(st + d.y, src, (uint32_t)d.w, bar);
+        }
+    };
+    if (issuer)
+        for (int i = 0; i < NS && i < nmine; ++i) issue(i);
+    const int l0 = threadIdx.x, l1 = threadIdx.x + PAT_THREADS;
+    // per-row streams of a tile (s_{j-2}, r), loaded one tile ahead into registers
+    double c20 = 0.0, c21 = 0.0, cr0 = 0.0, cr1 = 0.0;
+    auto load_rows = [&](int i, double &s20, double &s21, double &r0v, double &r1v) {
+        const int row0 = tile_of(i) * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
+        if (l0 < nrows) {
+            if (HAS_S2) s20 = s.s2[row0 + l0];
+            if (HAS_R) r0v = s.r[row0 + l0];
+        }
+        if (l1 < nrows) {
+            if (HAS_S2) s21 = s.s2[row0 + l1];
+            if (HAS_R) r1v = s.r[row0 + l1];
+        }
+    };
+    if (nmine > 0) load_rows(0, c20, c21, cr0, cr1);
     double acc = 0.0;
-    if (warp == NCW) {
-        // ---------------- producer (one elected lane)
-        if (lane == 0) {
-            uint32_t ephase = 0;
-            for (int i = 0; i < nmine; ++i) {
-                const int b = i % PAT_PIPE_NS, tile = tile_of(i);
-                if (i >= PAT_PIPE_NS) {  // the consumers released tile i - NS's stage
-                    mbar_wait(&empty[b], (ephase >> b) & 1u);
-                    ephase ^= 1u << b;
-                }
-                double *sv = base + (size_t)b * stage_dbl, *sx = sv + vspan_max;
-                int *st = reinterpret_cast<int *>(sx + xspan_max);
-                const int *gt = A.tbl2 + A.tbl2_off[tile];
-                const int nwin = gt[0], tn = A.tbl2_off[tile + 1] - A.tbl2_off[tile];
-                const int pb = A.tptr[tile];
-                const uint32_t bv = (uint32_t)(A.tptr[tile + 1] - pb) * 8u;
-                uint32_t bytes = bv + (uint32_t)tn * 4u;
-                for (int w = 0; w < nwin; ++w) {
-                    const int ga = gt[4 + 4 * w], len = gt[4 + 4 * w + 1];
-                    bytes += (uint32_t)len * 8u;
-                    if (gt[4 + 4 * w + 3]) sx[gt[4 + 4 * w + 2] + len] = s.x[ga + len];  // odd tail
-                }
-                const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
-                const uint32_t bp = (uint32_t)((nrows + 15) & ~15);  // pattern ids (array padded)
-                bytes += bp;
-                mbar_arrive_expect_tx(&full[b], bytes);  // releases the tail stores with it
-                if (bv) bulk_g2s(sv, A.vals + pb, bv, &full[b]);
-                bulk_g2s(st, gt, (uint32_t)tn * 4u, &full[b]);
-                bulk_g2s(st + tbl2_max, A.pat + row0, bp, &full[b]);
-                for (int w = 0; w < nwin; ++w) {
-                    const int ga = gt[4 + 4 * w], len = gt[4 + 4 * w + 1], sb = gt[4 + 4 * w + 2];
-                    if (len) bulk_g2s(sx + sb, s.x + ga, (uint32_t)len * 8u, &full[b]);
-                }
+    for (int i = 0; i < nmine; ++i) {
+        double n20 = 0.0, n21 = 0.0, nr0 = 0.0, nr1 = 0.0;
+        if (NS > 1 && i + 1 < nmine) load_rows(i + 1, n20, n21, nr0, nr1);
+        const int b = i % NS;
+        const int row0 = tile_of(i) * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
+        mbar_wait(&full[b], (uint32_t)((i / NS) & 1));
+        const unsigned char *st8 = rg_smem + (size_t)b * stage_bytes;
+        const int *st = reinterpret_cast<const int *>(st8);
+        const unsigned char *sp = st8 + tbl_bytes;
+        const double *D = reinterpret_cast<const double *>(sp + PAT_TILE);
+        const int2 *E = reinterpret_cast<const int2 *>(st + st[1]);
+        const int *ps = st + 4;
+        const int x0b = st[2];
+        const bool a0 = l0 < nrows, a1 = l1 < nrows;
+        const int p0 = a0 ? sp[l0] : 0, p1 = a1 ? sp[l1] : 0;
+        const int b0 = ps[p0], n0 = ps[p0 + 1] - b0, b1 = ps[p1], n1 = ps[p1 + 1] - b1;
+        const double *D0 = D + l0, *D1 = D + l1;
+        double y0 = 0.0, y1 = 0.0;
+        if (a1 && n0 == n1) {  // both rows in one loop (the common case: one pattern)
+#pragma unroll 4
+            for (int k = 0; k < n0; ++k) {
+                const int2 u = E[b0 + k], w = E[b1 + k];
+                y0 = fma(D0[u.y], D0[u.x], y0);
+                y1 = fma(D1[w.y], D1[w.x], y1);
             }
+        } else {
+            if (a0)
+                for (int k = 0; k < n0; ++k) {
+                    const int2 u = E[b0 + k];
+                    y0 = fma(D0[u.y], D0[u.x], y0);
+                }
+            if (a1)
+                for (int k = 0; k < n1; ++k) {
+                    const int2 w = E[b1 + k];
+                    y1 = fma(D1[w.y], D1[w.x], y1);
+                }
         }
-    } else {
-        // ---------------- consumers: rows l0 and l1 of every tile
-        const int l0 = threadIdx.x, l1 = threadIdx.x + PAT_THREADS;
-        int np0 = 0, np1 = 0;
-        double ns20 = 0.0, ns21 = 0.0, nr0 = 0.0, nr1 = 0.0;
-        auto load_rows = [&](int i) {  // s_{j-2} and r of tile i, one tile ahead
-            const int tile = tile_of(i), row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
-            if (l0 < nrows) {
-                if (HAS_S2) ns20 = s.s2[row0 + l0];
-                if (HAS_R) nr0 = s.r[row0 + l0];
-            }
-            if (l1 < nrows) {
-                if (HAS_S2) ns21 = s.s2[row0 + l1];
-                if (HAS_R) nr1 = s.r[row0 + l1];
-            }
-        };
-        uint32_t fphase = 0;
-        // stage i landed -> the earlier-tile mirror values of its rows, loaded into registers
-        auto wait_and_mirrors = [&](int i, PatMirrors &m0, PatMirrors &m1) {
-            const int b = i % PAT_PIPE_NS, tile = tile_of(i);
-            const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
-            const double *sx = base + (size_t)b * stage_dbl + vspan_max;
-            const int *st = reinterpret_cast<const int *>(sx + xspan_max);
-            mbar_wait(&full[b], (fphase >> b) & 1u);
-            fphase ^= 1u << b;
-            const int sidx = 4 + 4 * st[0];
-            const int4 *ent = reinterpret_cast<const int4 *>(st + st[1]);
-            const unsigned char *sp = reinterpret_cast<const unsigned char *>(st + tbl2_max);
-            if (l0 < nrows) {
-                np0 = sp[l0];
-                m0 = pat_mirrors(A, st, ent, sidx, row0, l0, np0);
-            }
-            if (l1 < nrows) {
-                np1 = sp[l1];
-                m1 = pat_mirrors(A, st, ent, sidx, row0, l1, np1);
-            }
-        };
-        PatMirrors m0, m1, q0, q1;
-        if (nmine > 0) {
-            load_rows(0);
-            wait_and_mirrors(0, m0, m1);
+        if (a0) {
+            const double o = degree_epilogue<HAS_S2, HAS_R>(s, y0, D0[x0b], c20, cr0);
+            s.out[row0 + l0] = o;
+            if (DOT) acc += o * s.dotv[row0 + l0];
         }
-        for (int i = 0; i < nmine; ++i) {
-            const int b = i % PAT_PIPE_NS, tile = tile_of(i);
-            const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
-            const int p0 = np0, p1 = np1;
-            const double s20 = ns20, s21 = ns21, r0 = nr0, r1 = nr1;
-            if (i + 1 < nmine) {  // next tile: row streams, then (its stage landed) its mirrors
-                load_rows(i + 1);
-                wait_and_mirrors(i + 1, q0, q1);
+        if (a1) {
+            const double o = degree_epilogue<HAS_S2, HAS_R>(s, y1, D1[x0b], c21, cr1);
+            s.out[row0 + l1] = o;
+            if (DOT) acc += o * s.dotv[row0 + l1];
+        }
+        if (NS > 1) {
+            c20 = n20, c21 = n21, cr0 = nr0, cr1 = nr1;
+            if (i + NS < nmine) {
+                __syncthreads();  // every row of stage b summed: it can be refilled
+                if (issuer) issue(i + NS);
             }
-            const double *sv = base + (size_t)b * stage_dbl;
-            const double *sx = sv + vspan_max;
-            const int *st = reinterpret_cast<const int *>(sx + xspan_max);
-            const int sidx = 4 + 4 * st[0];
-            const int4 *ent = reinterpret_cast<const int4 *>(st + st[1]);
-            if (l0 < nrows) {
-                const double o =
-                    pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l0, p0, sx[st[3] + l0], s20, r0, &m0);
-                s.out[row0 + l0] = o;
-                if (DOT) acc += o * s.dotv[row0 + l0];
-            }
-            if (l1 < nrows) {
-                const double o =
-                    pat_row<HAS_S2, HAS_R>(A, s, sv, sx, st, ent, sidx, row0, l1, p1, sx[st[3] + l1], s21, r1, &m1);
-                s.out[row0 + l1] = o;
-                if (DOT) acc += o * s.dotv[row0 + l1];
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[b]);  // this warp is done with stage b
-            m0 = q0;
-            m1 = q1;
         }
     }
     if (DOT) {
-        acc = block_sum<PAT_PIPE_THREADS>(acc, red);
+        acc = block_sum<PAT_THREADS>(acc, red);
         if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
-        if (blockIdx.x == 0)
-            for (int k = gridDim.x + threadIdx.x; k < npart_total; k += PAT_PIPE_THREADS) s.partials[k] = 0.0;
+        if (blockIdx.x == 0)  // persistent grid: the slots of the tiles beyond the grid read as 0
+            for (int k = gridDim.x + threadIdx.x; k < ntl; k += PAT_THREADS) s.partials[k] = 0.0;
     }
 }
 
@@ -634,9 +604,11 @@ class CsrOperator : public Operator {
     DevBuf tbl2, tbl2_off;  // staged kernel tables (k_csr_pat_stage)
     int xspan_max = 0, tbl2_max = 0;
     size_t smem_stage = 0;
-    bool pipe = false;       // k_csr_pat_pipe (three stages fit in shared memory)
-    int pipe_ctas = 0;       // its resident CTAs per SM (queried at the first launch)
-    int pipe_stage_dbl = 0;  // doubles per pipeline stage
+    DevBuf rtbl, rdesc;      // ring kernel: per-tile tables and copy descriptors (k_csr_pat_ring)
+    bool ring = false;
+    int ring_ns = 1;         // stages per CTA (1: one tile per CTA)
+    int ring_ctas = 0;       // resident CTAs per SM of the persistent form (queried at the first launch)
+    int ring_stage = 0, ring_tbl_bytes = 0;
     struct PatTiles {  // a tile list split by kernel: staged / unstaged
         DevBuf staged, unstaged;
         int ns = 0, nu = 0;
@@ -717,7 +689,9 @@ class CsrOperator : public Operator {
     template <bool H2, bool HR, bool DT>
     npc_status prepare3() {
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_stage<H2, HR, DT>));
-        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_pipe<H2, HR, DT>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 1>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 2>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 3>));
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_step<H2, HR, DT, false>));
         return allow_max_dynamic_smem(k_csr_pat_step<H2, HR, DT, true>);
     }
@@ -745,38 +719,44 @@ class CsrOperator : public Operator {
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
-    template <bool H2, bool HR, bool DT>
-    npc_status launch_pipe(const StepArgs &s, const int *tl, int nt, double *partials) {
-        if (nt <= 0) return NPC_SUCCESS;
-        PatDev A{vals.as<double>(), tptr.as<int>(), pat.as<unsigned char>(), tbl.as<int>(), tbl_off.as<int>(),
-                 n_local, nullptr, tbl2.as<int>(), tbl2_off.as<int>()};
+    template <bool H2, bool HR, bool DT, int NS>
+    npc_status launch_ring_ns(const StepArgs &s, const int *tl, int nt, double *partials) {
+        RingDev A{vals.as<double>(), rtbl.as<int>(), pat.as<unsigned char>(), rdesc.as<int4>(), n_local};
         StepArgs a = s;
         a.partials = partials;
-        auto kern = k_csr_pat_pipe<H2, HR, DT>;
-        const size_t sm = (size_t)PAT_PIPE_NS * pipe_stage_dbl * 8 + 128;
-        NPC_TRY(allow_max_dynamic_smem(kern));
-        if (pipe_ctas == 0) {  // resident CTAs per SM at this stage size (1 at 1,024-row tiles)
-            int occ = 0;
-            NPC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PAT_PIPE_THREADS, sm));
-            pipe_ctas = std::max(1, occ);
+        auto kern = k_csr_pat_ring<H2, HR, DT, NS>;
+        const size_t sm = (size_t)NS * ring_stage;
+        int grid = nt;
+        if (NS > 1) {
+            if (ring_ctas == 0) {  // resident CTAs per SM at this stage size
+                int occ = 0;
+                NPC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PAT_THREADS, sm));
+                ring_ctas = std::max(1, occ);
+            }
+            grid = std::min(nt, ctx->num_sms * ring_ctas);
         }
-        const int grid = std::min(nt, ctx->num_sms * pipe_ctas);
-        kern<<<grid, PAT_PIPE_THREADS, sm, ctx->stream>>>(A, a, tl, nt, vspan_max, xspan_max, tbl2_max, pipe_stage_dbl,
-                                                           nt);
+        kern<<<grid, PAT_THREADS, sm, ctx->stream>>>(A, a, tl, nt, ring_stage, ring_tbl_bytes);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
+    template <bool H2, bool HR, bool DT>
+    npc_status launch_ring(const StepArgs &s, const int *tl, int nt, double *partials) {
+        if (nt <= 0) return NPC_SUCCESS;
+        if (ring_ns == 3) return launch_ring_ns<H2, HR, DT, 3>(s, tl, nt, partials);
+        if (ring_ns == 2) return launch_ring_ns<H2, HR, DT, 2>(s, tl, nt, partials);
+        return launch_ring_ns<H2, HR, DT, 1>(s, tl, nt, partials);
+    }
     npc_status launch_stage_any(const StepArgs &s, const int *tl, int nt, double *partials) {
         const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
-        if (pipe) {
-            if (h2 && hr && dt) return launch_pipe<true, true, true>(s, tl, nt, partials);
-            if (h2 && hr) return launch_pipe<true, true, false>(s, tl, nt, partials);
-            if (h2 && dt) return launch_pipe<true, false, true>(s, tl, nt, partials);
-            if (h2) return launch_pipe<true, false, false>(s, tl, nt, partials);
-            if (hr && dt) return launch_pipe<false, true, true>(s, tl, nt, partials);
-            if (hr) return launch_pipe<false, true, false>(s, tl, nt, partials);
-            if (dt) return launch_pipe<false, false, true>(s, tl, nt, partials);
-            return launch_pipe<false, false, false>(s, tl, nt, partials);
+        if (ring) {
+            if (h2 && hr && dt) return launch_ring<true, true, true>(s, tl, nt, partials);
+            if (h2 && hr) return launch_ring<true, true, false>(s, tl, nt, partials);
+            if (h2 && dt) return launch_ring<true, false, true>(s, tl, nt, partials);
+            if (h2) return launch_ring<true, false, false>(s, tl, nt, partials);
+            if (hr && dt) return launch_ring<false, true, true>(s, tl, nt, partials);
+            if (hr) return launch_ring<false, true, false>(s, tl, nt, partials);
+            if (dt) return launch_ring<false, false, true>(s, tl, nt, partials);
+            return launch_ring<false, false, false>(s, tl, nt, partials);
         }
         if (h2 && hr && dt) return launch_stage<true, true, true>(s, tl, nt, partials);
         if (h2 && hr) return launch_stage<true, true, false>(s, tl, nt, partials);
@@ -981,6 +961,11 @@ struct PatHost {
     std::vector<int> tbl2, tbl2_off;
     std::vector<char> stage;
     int xspan_max = 0, tbl2_max = 0;
+    // ring kernel (k_csr_pat_ring): per-tile tables (16-byte aligned), RING_MAXD int4 copy
+    // descriptors per tile, the stage size and its table region; ring = every staged tile has one
+    std::vector<int> rtbl, rdesc;
+    int ring_stage = 0, ring_tbl_bytes = 0;
+    bool ring = false;
 };
 
 // x windows + decoded entries of one tile for k_csr_pat_stage (see there).  pstart/pent: the
@@ -988,6 +973,7 @@ struct PatHost {
 // tile's windows do not fit the shared-memory budget (it then runs k_csr_pat_step).
 static std::vector<int> pattern_stage_table(int n, int row0, int nrows, int own_block, const std::vector<int> &pstart,
                                             const std::vector<int> &pent, int *xspan) {
+    const int nrs = (nrows + 1) & ~1;  // column stride of the tile's own block (even)
     const int np = (int)pstart.size() - 1;
     std::vector<int> offs(1, 0);  // offset 0 always: the epilogue's x[row] comes from its window
     for (int w : pent) offs.push_back((w & 1) ? (w >> 9) : (w >> 1));
@@ -1043,9 +1029,9 @@ static std::vector<int> pattern_stage_table(int n, int row0, int nrows, int own_
             const int xb = wdesc[4 * wi + 2] + (int)(c0 - wdesc[4 * wi]);
             if (w & 1) {
                 const int pos = (w >> 1) & 255;
-                t.insert(t.end(), {xb, pos * nrows + o, o, pos});
+                t.insert(t.end(), {xb, pos * nrs + o, o, pos});
             } else {
-                t.insert(t.end(), {xb, k * nrows, 0, 0});
+                t.insert(t.end(), {xb, k * nrs, 0, 0});
                 ++k;
             }
         }
@@ -1053,6 +1039,177 @@ static std::vector<int> pattern_stage_table(int n, int row0, int nrows, int own_
     t[sidx + np] = (int)(t.size() - t[1]) / 4;
     if ((size_t)own_block * 8 + (size_t)sb * 8 + t.size() * 4 > (size_t)PAT_STAGE_SMEM) return {};
     return t;
+}
+
+// Ring-kernel table of one staged tile (see k_csr_pat_ring).  tb: the tile's pattern table as
+// built by build_pattern ([np + 1 starts][entry words]); prow: the pattern id of each row.
+// Shared-memory stage: [table][pattern ids][D], D = own-value columns (column p preceded by its
+// gap G_p: values of column p of the previous tile's last G_p rows), far mirror windows, x
+// windows.  Copies carry a region (0 table, 1 pattern ids, 2 D in doubles) fixed up once the
+// table region's size is known.  Returns false when the tile needs more copies than a
+// descriptor holds or a mirror the layout cannot address (the operator then keeps
+// k_csr_pat_stage).
+struct RingCopy {
+    int kind, region, dst, src, bytes;  // kind: 0 vals, 1 x, 2 table, 3 pattern ids, 4 x tail
+};
+struct RingTile {
+    std::vector<int> tbl;
+    std::vector<RingCopy> cp;
+    int dbl = 0;
+};
+
+static bool pattern_ring_table(int n, int t, const std::vector<int> &tptr, const std::vector<int> &twidth,
+                               const std::vector<int> &tb, const unsigned char *prow, RingTile &rt) {
+    const int T = PAT_TILE, r0 = t * T, nr = std::min(T, n - r0), nrs = (nr + 1) & ~1, W = twidth[t];
+    const int np = tb[0] - 1;
+    std::vector<int> lmin((size_t)np, INT_MAX), lmax((size_t)np, -1);
+    for (int lr = 0; lr < nr; ++lr) {
+        const int q = prow[lr];
+        lmin[q] = std::min(lmin[q], lr);
+        lmax[q] = std::max(lmax[q], lr);
+    }
+    // x windows: [r0 + o, r0 + o + nr) for every distinct offset, clipped and merged
+    std::vector<int> offs(1, 0);
+    for (int e = np + 1; e < (int)tb.size(); ++e) offs.push_back((tb[e] & 1) ? (tb[e] >> 9) : (tb[e] >> 1));
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    struct Win { long long a, b; };
+    std::vector<Win> win;
+    for (int o : offs) {
+        const long long a = std::max<long long>(0, (long long)r0 + o), b = std::min<long long>(n, (long long)r0 + o + nr);
+        if (a >= b) continue;
+        if (!win.empty() && a <= win.back().b + 64)
+            win.back().b = std::max(win.back().b, b);
+        else
+            win.push_back({a, b});
+    }
+    struct XW { int ga, len, sb, tail; };
+    std::vector<XW> xw;
+    int xs = 0;
+    for (auto &w : win) {
+        const long long ga = w.a & ~1LL;
+        long long bt = (w.b + 1) & ~1LL;
+        int tail = 0;
+        if (bt > n) bt = w.b - 1, tail = 1;
+        xw.push_back({(int)ga, (int)(bt - ga), xs, tail});
+        xs += ((int)(bt - ga) + tail + 1) & ~1;
+    }
+    auto xwin_of = [&](long long c) {
+        int wi = 0;
+        while (wi + 1 < (int)win.size() && win[wi + 1].a <= std::max<long long>(c, 0)) ++wi;
+        return wi;
+    };
+    // mirror classes: 0 in tile / near (column gap), 1 far (window)
+    std::vector<int> G((size_t)W, 0);
+    struct Far { long long lo, hi; int pos; };
+    std::vector<Far> far;
+    std::vector<char> cls(tb.size(), 0);
+    for (int q = 0; q < np; ++q)
+        for (int e = tb[q]; e < tb[q + 1]; ++e) {
+            const int w = tb[e];
+            if (!(w & 1)) continue;
+            const int o = w >> 9, pos = (w >> 1) & 255;
+            const long long cmin = (long long)r0 + lmin[q] + o, cmax = (long long)r0 + lmax[q] + o;
+            if (cmin >= r0) {
+                if (pos >= W) return false;
+            } else if (r0 - cmin <= RING_GAP_MAX && pos < W && t > 0 && pos < twidth[t - 1]) {
+                G[pos] = std::max(G[pos], (int)(r0 - cmin));
+            } else if (cmax < r0) {
+                cls[e] = 1;
+                far.push_back({cmin, cmax, pos});
+            } else {
+                return false;
+            }
+        }
+    for (int &g : G) g = (g + 1) & ~1;
+    std::sort(far.begin(), far.end(), [](const Far &a, const Far &b) { return a.pos != b.pos ? a.pos < b.pos : a.lo < b.lo; });
+    std::vector<Far> fw;  // merged far windows, [lo, hi) even-aligned
+    for (auto &f : far) {
+        if (!fw.empty() && fw.back().pos == f.pos && f.lo <= fw.back().hi + 64)
+            fw.back().hi = std::max(fw.back().hi, (f.hi + 2) & ~1LL);
+        else
+            fw.push_back({f.lo & ~1LL, (f.hi + 2) & ~1LL, f.pos});
+    }
+    // D layout
+    std::vector<int> col((size_t)W);
+    int off = 0;
+    for (int p = 0; p < W; ++p) {
+        off += G[p];
+        col[p] = off;
+        off += nrs;
+    }
+    std::vector<int> fwb(fw.size());
+    for (size_t k = 0; k < fw.size(); ++k) fwb[k] = off, off += (int)(fw[k].hi - fw[k].lo);
+    const int xbase = off;
+    rt.dbl = off + xs;
+    // copies
+    rt.cp.clear();
+    rt.cp.push_back({2, 0, 0, -1, 0});                     // table (source and size filled below)
+    rt.cp.push_back({3, 1, 0, r0, (nr + 15) & ~15});       // pattern ids
+    for (int p = 0; p < W;) {                              // own columns, in runs without gaps
+        int p1 = p;
+        while (p1 + 1 < W && G[p1 + 1] == 0) ++p1;
+        rt.cp.push_back({0, 2, col[p], tptr[t] + p * nrs, (p1 - p + 1) * nrs * 8});
+        p = p1 + 1;
+    }
+    for (int p = 0; p < W; ++p)  // gaps: column p of the previous (full) tile's last G_p rows
+        if (G[p]) rt.cp.push_back({0, 2, col[p] - G[p], tptr[t - 1] + p * T + (T - G[p]), G[p] * 8});
+    for (size_t k = 0; k < fw.size(); ++k)  // far windows, one copy per source tile
+        for (long long c = fw[k].lo; c < fw[k].hi;) {
+            const int tj = (int)(c / T);
+            const long long ce = std::min<long long>(fw[k].hi, (long long)(tj + 1) * T);
+            if (fw[k].pos < twidth[tj])
+                rt.cp.push_back({0, 2, fwb[k] + (int)(c - fw[k].lo), tptr[tj] + fw[k].pos * T + (int)(c - (long long)tj * T),
+                                 (int)(ce - c) * 8});
+            c = ce;
+        }
+    for (auto &w : xw) {
+        if (w.len) rt.cp.push_back({1, 2, xbase + w.sb, w.ga, w.len * 8});
+        if (w.tail) rt.cp.push_back({4, 2, xbase + w.sb + w.len, w.ga + w.len, 0});
+    }
+    if ((int)rt.cp.size() > RING_MAXD - 1) return false;
+    // table: [np, entry start, x0 base, nrs][np + 1 starts (entries)][pad][entries {xb, vb}]
+    std::vector<int> &o = rt.tbl;
+    o.assign(4, 0);
+    o[0] = np;
+    o[3] = nrs;
+    {
+        const int wi = xwin_of(r0);
+        o[2] = xbase + xw[wi].sb + (r0 - xw[wi].ga);
+    }
+    const int sidx = 4;
+    o.resize(sidx + np + 1);
+    if (o.size() & 1) o.push_back(0);
+    o[1] = (int)o.size();
+    for (int q = 0; q < np; ++q) {
+        o[sidx + q] = (int)(o.size() - o[1]) / 2;
+        int k = 0;
+        for (int e = tb[q]; e < tb[q + 1]; ++e) {
+            const int w = tb[e];
+            const int of = (w & 1) ? (w >> 9) : (w >> 1);
+            const long long c0 = (long long)r0 + of;
+            const int wi = xwin_of(c0);
+            const int xb = xbase + xw[wi].sb + (int)(c0 - xw[wi].ga);
+            int vb;
+            if (!(w & 1)) {
+                vb = col[k++];
+            } else if (!cls[e]) {
+                vb = col[(w >> 1) & 255] + of;
+            } else {
+                const int pos = (w >> 1) & 255;
+                const long long cmin = (long long)r0 + lmin[q] + of;
+                size_t f = 0;
+                while (!(fw[f].pos == pos && fw[f].lo <= cmin && cmin < fw[f].hi)) ++f;
+                vb = fwb[f] + (int)((long long)r0 + of - fw[f].lo);
+            }
+            o.push_back(xb);
+            o.push_back(vb);
+        }
+    }
+    o[sidx + np] = (int)(o.size() - o[1]) / 2;
+    while (o.size() % 4) o.push_back(0);
+    rt.cp[0].bytes = (int)o.size() * 4;
+    return true;
 }
 
 static bool build_pattern(int n, long long row_begin, const int *rowptr, const int *gcol, const std::vector<int> &lcols,
@@ -1096,6 +1253,25 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
     });
     for (char c : bad)
         if (c) return false;
+    // 2b. a row with fewer own values than its tile's widest row streams ELL padding anyway: its
+    //     mirrors of EARLIER tiles (farthest first) become own values in those slots -- the same
+    //     bytes, one L2 read (or ring-kernel copy) less; bitwise the same values and order
+    if (mirror && !getenv("NPC_CSR_NOFILL")) {
+        host_parallel_for(ceil_div(n, PAT_TILE), [&](long long t0, long long t1, int) {
+            for (long long t = t0; t < t1; ++t) {
+                const int r0 = (int)t * PAT_TILE, r1 = std::min(n, r0 + PAT_TILE);
+                int w = 0;
+                for (int i = r0; i < r1; ++i) w = std::max(w, rown[i]);
+                for (int i = r0; i < r1; ++i) {
+                    if (rown[i] >= w) continue;
+                    for (int p = rowptr[i]; p < rowptr[i + 1] && rown[i] < w; ++p)
+                        if (partner[p] >= 0 && lcols[p] < r0) partner[p] = -1, ++rown[i];
+                    int k = 0;
+                    for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) opos[p] = partner[p] < 0 ? (unsigned char)k++ : 0;
+                }
+            }
+        }, 64);
+    }
     // 3. per tile: patterns (deduplicated by hash, then by words), ELL width, tables
     const int ntiles = ceil_div(n, PAT_TILE);
     std::vector<std::vector<int>> ttbl((size_t)ntiles);
@@ -1156,7 +1332,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
             for (int p = rowptr[r0]; p < rowptr[r1] && !ghost; ++p) ghost = lcols[p] >= n;
             if (!ghost && stage) {
                 const int nr = r1 - r0;
-                ttbl2[t] = pattern_stage_table(n, r0, nr, (wmax * nr + 1) & ~1, pstart, pent, &txs[t]);
+                ttbl2[t] = pattern_stage_table(n, r0, nr, wmax * ((nr + 1) & ~1), pstart, pent, &txs[t]);
             }
         }
     }, 64);
@@ -1168,7 +1344,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
     for (int i = 0; i < n; ++i) real += rown[i];
     for (int t = 0; t < ntiles; ++t) {
         const int nr = std::min(PAT_TILE, n - t * PAT_TILE);
-        const long long blk = ((long long)twidth[t] * nr + 1) & ~1LL;  // even: 16-byte aligned blocks
+        const long long blk = (long long)twidth[t] * ((nr + 1) & ~1);  // even column stride: 16-byte aligned
         if (ph.tptr[t] + blk > INT_MAX) return false;
         ph.tptr[t + 1] = ph.tptr[t] + (int)blk;
         ph.tbl_off[t + 1] = ph.tbl_off[t] + (int)ttbl[t].size();
@@ -1190,17 +1366,64 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
     }
     ph.tbl2.resize((size_t)ph.tbl2_off[ntiles]);
     for (int t = 0; t < ntiles; ++t) std::copy(ttbl2[t].begin(), ttbl2[t].end(), ph.tbl2.begin() + ph.tbl2_off[t]);
+    // 4. ring-kernel tables: every staged tile gets one, or the operator keeps k_csr_pat_stage
+    if (stage && !getenv("NPC_CSR_NORING")) {
+        std::vector<RingTile> rts((size_t)ntiles);
+        std::vector<char> rok((size_t)ntiles, 1);
+        host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
+            for (long long t = t0; t < t1; ++t)
+                if (ph.stage[t])
+                    rok[t] = pattern_ring_table(n, (int)t, ph.tptr, twidth, ttbl[t], ph.pat.data() + t * PAT_TILE, rts[t]);
+        }, 64);
+        ph.ring = std::all_of(rok.begin(), rok.end(), [](char c) { return c != 0; });
+        if (ph.ring) {
+            size_t tmax = 0, dmax = 0;
+            std::vector<long long> toff((size_t)ntiles + 1, 0);
+            for (int t = 0; t < ntiles; ++t) {
+                tmax = std::max(tmax, rts[t].tbl.size());
+                dmax = std::max(dmax, (size_t)rts[t].dbl);
+                toff[t + 1] = toff[t] + (long long)rts[t].tbl.size();
+            }
+            ph.ring_tbl_bytes = (int)(((tmax * 4) + 15) & ~(size_t)15);
+            const size_t stage = ((size_t)ph.ring_tbl_bytes + PAT_TILE + dmax * 8 + 127) & ~(size_t)127;
+            ph.ring = stage <= (size_t)RING_STAGE_MAX && toff[ntiles] < INT_MAX;
+            ph.ring_stage = (int)stage;
+            if (ph.ring) {
+                ph.rtbl.assign((size_t)toff[ntiles] + 4, 0);
+                ph.rdesc.assign((size_t)ntiles * RING_MAXD * 4, 0);
+                host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
+                    for (long long t = t0; t < t1; ++t) {
+                        if (!ph.stage[t]) continue;
+                        std::copy(rts[t].tbl.begin(), rts[t].tbl.end(), ph.rtbl.begin() + toff[t]);
+                        int *dd = ph.rdesc.data() + (size_t)t * RING_MAXD * 4;
+                        long long total = 0;
+                        for (size_t k = 0; k < rts[t].cp.size(); ++k) {
+                            const RingCopy &c = rts[t].cp[k];
+                            const int dst = c.region == 0 ? c.dst
+                                            : c.region == 1 ? ph.ring_tbl_bytes + c.dst
+                                                            : ph.ring_tbl_bytes + PAT_TILE + c.dst * 8;
+                            int *q = dd + 4 * (k + 1);
+                            q[0] = c.kind, q[1] = dst, q[2] = c.kind == 2 ? (int)toff[t] : c.src, q[3] = c.bytes;
+                            total += c.bytes;
+                        }
+                        dd[0] = (int)rts[t].cp.size();
+                        dd[1] = (int)total;
+                    }
+                }, 256);
+            }
+        }
+    }
     ph.vals.reset(new double[(size_t)ph.own_nnz + 8]);
     std::fill(ph.vals.get() + ph.own_nnz, ph.vals.get() + ph.own_nnz + 8, 0.0);
     host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
         for (long long t = t0; t < t1; ++t) {
             std::copy(ttbl[t].begin(), ttbl[t].end(), ph.tbl.begin() + ph.tbl_off[t]);
-            const int r0 = (int)t * PAT_TILE, r1 = std::min(n, r0 + PAT_TILE), nr = r1 - r0;
+            const int r0 = (int)t * PAT_TILE, r1 = std::min(n, r0 + PAT_TILE), nrs = (r1 - r0 + 1) & ~1;
             double *blk = ph.vals.get() + ph.tptr[t];
             std::fill(blk, ph.vals.get() + ph.tptr[t + 1], 0.0);  // ELL padding
             for (int i = r0; i < r1; ++i)
                 for (int p = rowptr[i]; p < rowptr[i + 1]; ++p)
-                    if (partner[p] < 0) blk[(size_t)opos[p] * nr + (i - r0)] = vals[p];
+                    if (partner[p] < 0) blk[(size_t)opos[p] * nrs + (i - r0)] = vals[p];
         }
     }, 64);
     return true;
@@ -1230,12 +1453,17 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
     op.xspan_max = ph.xspan_max;
     op.tbl2_max = (ph.tbl2_max + 3) & ~3;
     op.smem_stage = ((size_t)ph.vspan_max + (size_t)ph.xspan_max) * 8 + (size_t)op.tbl2_max * 4;
-    // pipeline stage: own block + x windows + table, rounded to 128 bytes (bulk-copy targets)
-    op.pipe_stage_dbl = (int)(((op.smem_stage + PAT_TILE + 127) / 128) * 16);  // + the tile's pattern ids
-    // opt-in (NPC_CSR_PIPE=1): measured slower than k_csr_pat_stage on config 3 (p_50 14.2 vs 11.4 ms,
-    // 512-row tiles 13.9 vs 11.6): one or two CTAs per SM leave too few warps to hide the row sums'
-    // shared-memory and FMA chains, while three independent CTAs of k_csr_pat_stage overlap them
-    op.pipe = (size_t)PAT_PIPE_NS * op.pipe_stage_dbl * 8 + 128 + 2048 <= 227 * 1024 && getenv("NPC_CSR_PIPE");
+    op.ring = ph.ring;
+    if (op.ring) {
+        op.ring_stage = ph.ring_stage;
+        op.ring_tbl_bytes = ph.ring_tbl_bytes;
+        if (const char *e = getenv("NPC_RING_NS")) op.ring_ns = std::min(3, std::max(1, atoi(e)));
+        if ((size_t)op.ring_ns * op.ring_stage > 227 * 1024) op.ring_ns = 1;
+        NPC_TRY(op.rtbl.alloc(sizeof(int) * ph.rtbl.size()));
+        NPC_TRY(op.rdesc.alloc(sizeof(int) * ph.rdesc.size()));
+        NPC_CUDA_TRY(cudaMemcpy(op.rtbl.p, ph.rtbl.data(), sizeof(int) * ph.rtbl.size(), cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op.rdesc.p, ph.rdesc.data(), sizeof(int) * ph.rdesc.size(), cudaMemcpyHostToDevice));
+    }
     auto split = [&](const std::vector<int> &list, CsrOperator::PatTiles &pt) -> npc_status {
         std::vector<int> st, un;
         for (int t : list) (ph.stage[t] ? st : un).push_back(t);

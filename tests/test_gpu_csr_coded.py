@@ -35,22 +35,26 @@ def dev(a):
 
 
 FORM_ENV = {"plain": "NPC_CSR_PLAIN", "coded": "NPC_CSR_CODED", "nomirror": "NPC_CSR_NOMIRROR",
-            "nostage": "NPC_CSR_NOSTAGE", "pipe": "NPC_CSR_PIPE"}
+            "nostage": "NPC_CSR_NOSTAGE", "stage": "NPC_CSR_NORING", "nofill": "NPC_CSR_NOFILL",
+            "ring2": "NPC_RING_NS=2", "ring3": "NPC_RING_NS=3"}
 
 
 def make(ctx, w, plain):
     """plain: True -> int32 column ids, False -> the coded form; or a form name: 'pattern'
-    (the default form), 'nomirror' (pattern ids without symmetric mirroring), 'nostage' (pattern
-    form without the x-window staging kernel), 'coded', 'plain'."""
+    (the default form: ring kernel), 'nomirror' (pattern ids without symmetric mirroring), 'nostage'
+    (pattern form without the x-window staging kernels), 'stage' (k_csr_pat_stage instead of the
+    ring kernel), 'ring2' / 'ring3' (persistent ring kernel with 2 / 3 stages), 'nofill' (no
+    earlier-tile mirrors moved into ELL padding), 'coded', 'plain'."""
     form = ("plain" if plain else "coded") if isinstance(plain, bool) else plain
     env = FORM_ENV.get(form)
-    if env:
-        os.environ[env] = "1"
+    key, val = (env.split("=", 1) if "=" in env else (env, "1")) if env else (None, None)
+    if key:
+        os.environ[key] = val
     try:
         return npc.create_from_workload(ctx, w, "csr")
     finally:
-        if env:
-            os.environ.pop(env, None)
+        if key:
+            os.environ.pop(key, None)
 
 
 WL = {"c3": lambda: W.config3(side=30), "c1": lambda: W.config1(side=64),
