@@ -17,6 +17,7 @@
 // offsets (col - row), at most 256, and every entry streams a 1-byte code instead of a 4-byte
 // id: 12 -> 9 B per nonzero (config 3: 2,008.5 -> 1,657 MB per degree).  Same values, same
 // summation order: bitwise the same result as the plain form (NPC_CSR_PLAIN=1).
+#include <unordered_map>
 #include <algorithm>
 #include <climits>
 #include <cstring>
@@ -609,6 +610,7 @@ class CsrOperator : public Operator {
     int ring_ns = 1;         // stages per CTA (1: one tile per CTA)
     int ring_ctas = 0;       // resident CTAs per SM of the persistent form (queried at the first launch)
     int ring_stage = 0, ring_tbl_bytes = 0;
+    long long ring_tbl_ints = 0;  // stored (deduplicated) ring-table words
     struct PatTiles {  // a tile list split by kernel: staged / unstaged
         DevBuf staged, unstaged;
         int ns = 0, nu = 0;
@@ -641,6 +643,9 @@ class CsrOperator : public Operator {
     }
 
     double matrix_bytes() const override {
+        if (pattern && ring)  // own values (incl. ELL padding), pattern ids, shared tables, copy descriptors
+            return (double)own_nnz * 8.0 + (double)n_local + (double)ring_tbl_ints * 4.0 +
+                   (double)pt_all.ns * RING_MAXD * 16.0;
         if (pattern)  // own values (incl. ELL padding), pattern ids, tables, tile pointers
             return (double)own_nnz * 8.0 + (double)n_local + (double)tbl_total * 4.0 + (double)(ntiles + 1) * 8.0;
         if (coded)  // values + codes, dictionaries + their offsets, tile pointers, 16-bit row offsets
@@ -1377,24 +1382,42 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
         }, 64);
         ph.ring = std::all_of(rok.begin(), rok.end(), [](char c) { return c != 0; });
         if (ph.ring) {
+            // tables are tile-relative: tiles with the same row patterns share one (a 3D grid's
+            // interior tiles all do), so the stored tables stay L2-resident
             size_t tmax = 0, dmax = 0;
-            std::vector<long long> toff((size_t)ntiles + 1, 0);
+            std::vector<long long> toff((size_t)ntiles, 0);
+            std::unordered_map<unsigned long long, std::vector<int>> seen;  // hash -> tiles stored
+            long long total_ints = 0;
             for (int t = 0; t < ntiles; ++t) {
                 tmax = std::max(tmax, rts[t].tbl.size());
                 dmax = std::max(dmax, (size_t)rts[t].dbl);
-                toff[t + 1] = toff[t] + (long long)rts[t].tbl.size();
+                if (!ph.stage[t]) continue;
+                unsigned long long h = 1469598103934665603ull;
+                for (int v : rts[t].tbl) h = (h ^ (unsigned)v) * 1099511628211ull;
+                auto &cand = seen[h];
+                int same = -1;
+                for (int u : cand)
+                    if (rts[u].tbl == rts[t].tbl) same = u;
+                if (same >= 0) {
+                    toff[t] = toff[same];
+                } else {
+                    toff[t] = total_ints;
+                    total_ints += (long long)rts[t].tbl.size();
+                    cand.push_back(t);
+                }
             }
             ph.ring_tbl_bytes = (int)(((tmax * 4) + 15) & ~(size_t)15);
             const size_t stage = ((size_t)ph.ring_tbl_bytes + PAT_TILE + dmax * 8 + 127) & ~(size_t)127;
-            ph.ring = stage <= (size_t)RING_STAGE_MAX && toff[ntiles] < INT_MAX;
+            ph.ring = stage <= (size_t)RING_STAGE_MAX && total_ints < INT_MAX;
             ph.ring_stage = (int)stage;
             if (ph.ring) {
-                ph.rtbl.assign((size_t)toff[ntiles] + 4, 0);
+                ph.rtbl.assign((size_t)total_ints + 4, 0);
+                for (auto &kv : seen)
+                    for (int u : kv.second) std::copy(rts[u].tbl.begin(), rts[u].tbl.end(), ph.rtbl.begin() + toff[u]);
                 ph.rdesc.assign((size_t)ntiles * RING_MAXD * 4, 0);
                 host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
                     for (long long t = t0; t < t1; ++t) {
                         if (!ph.stage[t]) continue;
-                        std::copy(rts[t].tbl.begin(), rts[t].tbl.end(), ph.rtbl.begin() + toff[t]);
                         int *dd = ph.rdesc.data() + (size_t)t * RING_MAXD * 4;
                         long long total = 0;
                         for (size_t k = 0; k < rts[t].cp.size(); ++k) {
@@ -1457,6 +1480,7 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
     if (op.ring) {
         op.ring_stage = ph.ring_stage;
         op.ring_tbl_bytes = ph.ring_tbl_bytes;
+        op.ring_tbl_ints = (long long)ph.rtbl.size();
         if (const char *e = getenv("NPC_RING_NS")) op.ring_ns = std::min(3, std::max(1, atoi(e)));
         if ((size_t)op.ring_ns * op.ring_stage > 227 * 1024) op.ring_ns = 1;
         NPC_TRY(op.rtbl.alloc(sizeof(int) * ph.rtbl.size()));
