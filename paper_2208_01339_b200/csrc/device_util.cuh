@@ -91,6 +91,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         : "memory");
 }
 
+// Same, with a suspend-time hint (ns): a waiting warp sleeps in the barrier instead of
+// re-issuing try_wait (fewer issue slots and less power while the copies are in flight).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t phase, uint32_t hint_ns) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "NPC_WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra NPC_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase), "r"(hint_ns)
+        : "memory");
+}
+
 // ------------------------------------------------------------------ tensor TMA (tiled)
 // Global -> shared copy of one box of a tensor map (cp.async.bulk.tensor, tile mode):
 // out-of-bounds elements of the box are zero-filled by the hardware.  `map` is the generic

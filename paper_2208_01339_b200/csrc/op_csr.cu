@@ -474,12 +474,18 @@ struct RingDev {
     int n;
 };
 
-template <bool HAS_S2, bool HAS_R, bool DOT, int NS>
-__global__ void __launch_bounds__(PAT_THREADS, NS == 1 ? 1536 / PAT_THREADS : 1)
+#ifndef NPC_RING_WAIT_NS
+#define NPC_RING_WAIT_NS 1000
+#endif
+// R rows per thread (lr = tid + q * PAT_TILE / R), summed in one interleaved loop when their
+// patterns have the same length.
+template <bool HAS_S2, bool HAS_R, bool DOT, int NS, int R>
+__global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 1)
     k_csr_pat_ring(RingDev A, StepArgs s, const int *__restrict__ tiles, int ntl, int stage_bytes, int tbl_bytes) {
+    constexpr int NT = PAT_TILE / R;  // threads
     extern __shared__ __align__(16) unsigned char rg_smem[];
     __shared__ uint64_t full[NS];
-    __shared__ double red[PAT_THREADS / 32];
+    __shared__ double red[NT / 32];
     if (s.done && *s.done) return;  // uniform, before any copy is issued
     const int lane = threadIdx.x & 31;
     const bool issuer = threadIdx.x < 32;
@@ -488,7 +494,8 @@ __global__ void __launch_bounds__(PAT_THREADS, NS == 1 ? 1536 / PAT_THREADS : 1)
         fence_mbar_init();
     }
     __syncthreads();
-    const int nmine = ntl > (int)blockIdx.x ? (ntl - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    // NS = 1: grid = tiles, one each
+    const int nmine = NS == 1 ? 1 : ntl > (int)blockIdx.x ? (ntl - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     auto tile_of = [&](int i) {
         const int q = (int)blockIdx.x + i * (int)gridDim.x;
         return tiles ? tiles[q] : q;
@@ -514,71 +521,82 @@ __global__ void __launch_bounds__(PAT_THREADS, NS == 1 ? 1536 / PAT_THREADS : 1)
     };
     if (issuer)
         for (int i = 0; i < NS && i < nmine; ++i) issue(i);
-    const int l0 = threadIdx.x, l1 = threadIdx.x + PAT_THREADS;
-    // per-row streams of a tile (s_{j-2}, r), loaded one tile ahead into registers
-    double c20 = 0.0, c21 = 0.0, cr0 = 0.0, cr1 = 0.0;
-    auto load_rows = [&](int i, double &s20, double &s21, double &r0v, double &r1v) {
+    // per-row streams of a tile (s_{j-2}, r, the dot operand), loaded a tile ahead into registers
+    struct Rows {
+        double s2[R], r[R], v[R];
+    };
+    auto load_rows = [&](int i, Rows &q) {
         const int row0 = tile_of(i) * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
-        if (l0 < nrows) {
-            if (HAS_S2) s20 = s.s2[row0 + l0];
-            if (HAS_R) r0v = s.r[row0 + l0];
-        }
-        if (l1 < nrows) {
-            if (HAS_S2) s21 = s.s2[row0 + l1];
-            if (HAS_R) r1v = s.r[row0 + l1];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int l = threadIdx.x + k * NT;
+            q.s2[k] = q.r[k] = q.v[k] = 0.0;
+            if (l < nrows) {
+                if (HAS_S2) q.s2[k] = s.s2[row0 + l];
+                if (HAS_R) q.r[k] = s.r[row0 + l];
+                if (DOT) q.v[k] = s.dotv[row0 + l];
+            }
         }
     };
-    if (nmine > 0) load_rows(0, c20, c21, cr0, cr1);
+    Rows cur;
+    if (nmine > 0) load_rows(0, cur);
     double acc = 0.0;
     for (int i = 0; i < nmine; ++i) {
-        double n20 = 0.0, n21 = 0.0, nr0 = 0.0, nr1 = 0.0;
-        if (NS > 1 && i + 1 < nmine) load_rows(i + 1, n20, n21, nr0, nr1);
+        Rows nxt;
+        if (NS > 1 && i + 1 < nmine) load_rows(i + 1, nxt);
         const int b = i % NS;
         const int row0 = tile_of(i) * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
-        mbar_wait(&full[b], (uint32_t)((i / NS) & 1));
+        mbar_wait_sleep(&full[b], (uint32_t)((i / NS) & 1), NPC_RING_WAIT_NS);
         const unsigned char *st8 = rg_smem + (size_t)b * stage_bytes;
         const int *st = reinterpret_cast<const int *>(st8);
         const unsigned char *sp = st8 + tbl_bytes;
-        const double *D = reinterpret_cast<const double *>(sp + PAT_TILE);
+        const char *Db = reinterpret_cast<const char *>(sp + PAT_TILE);  // D; entries are byte offsets
         const int2 *E = reinterpret_cast<const int2 *>(st + st[1]);
         const int *ps = st + 4;
         const int x0b = st[2];
-        const bool a0 = l0 < nrows, a1 = l1 < nrows;
-        const int p0 = a0 ? sp[l0] : 0, p1 = a1 ? sp[l1] : 0;
-        const int b0 = ps[p0], n0 = ps[p0 + 1] - b0, b1 = ps[p1], n1 = ps[p1 + 1] - b1;
-        const double *D0 = D + l0, *D1 = D + l1;
-        double y0 = 0.0, y1 = 0.0;
-        if (a1 && n0 == n1) {  // both rows in one loop (the common case: one pattern)
-#pragma unroll 4
-            for (int k = 0; k < n0; ++k) {
-                const int2 u = E[b0 + k], w = E[b1 + k];
-                y0 = fma(D0[u.y], D0[u.x], y0);
-                y1 = fma(D1[w.y], D1[w.x], y1);
+        auto ld = [](const char *p, int off) { return *reinterpret_cast<const double *>(p + off); };
+        int eb[R], ne[R];
+        const char *Dr[R];
+        double y[R];
+        bool same = true;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int l = threadIdx.x + k * NT;
+            const int p = l < nrows ? sp[l] : 0;
+            eb[k] = ps[p];
+            ne[k] = l < nrows ? ps[p + 1] - eb[k] : 0;
+            Dr[k] = Db + 8 * l;
+            y[k] = 0.0;
+            same = same && ne[k] == ne[0];
+        }
+        if (same) {  // every row in one loop (the common case: one pattern length)
+#pragma unroll 2
+            for (int e = 0; e < ne[0]; ++e) {
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const int2 u = E[eb[k] + e];
+                    y[k] = fma(ld(Dr[k], u.y), ld(Dr[k], u.x), y[k]);
+                }
             }
         } else {
-            if (a0)
-                for (int k = 0; k < n0; ++k) {
-                    const int2 u = E[b0 + k];
-                    y0 = fma(D0[u.y], D0[u.x], y0);
-                }
-            if (a1)
-                for (int k = 0; k < n1; ++k) {
-                    const int2 w = E[b1 + k];
-                    y1 = fma(D1[w.y], D1[w.x], y1);
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+                for (int e = 0; e < ne[k]; ++e) {
+                    const int2 u = E[eb[k] + e];
+                    y[k] = fma(ld(Dr[k], u.y), ld(Dr[k], u.x), y[k]);
                 }
         }
-        if (a0) {
-            const double o = degree_epilogue<HAS_S2, HAS_R>(s, y0, D0[x0b], c20, cr0);
-            s.out[row0 + l0] = o;
-            if (DOT) acc += o * s.dotv[row0 + l0];
-        }
-        if (a1) {
-            const double o = degree_epilogue<HAS_S2, HAS_R>(s, y1, D1[x0b], c21, cr1);
-            s.out[row0 + l1] = o;
-            if (DOT) acc += o * s.dotv[row0 + l1];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int l = threadIdx.x + k * NT;
+            if (l < nrows) {
+                const double o = degree_epilogue<HAS_S2, HAS_R>(s, y[k], ld(Dr[k], x0b), cur.s2[k], cur.r[k]);
+                s.out[row0 + l] = o;
+                if (DOT) acc = fma(o, cur.v[k], acc);
+            }
         }
         if (NS > 1) {
-            c20 = n20, c21 = n21, cr0 = nr0, cr1 = nr1;
+            cur = nxt;
             if (i + NS < nmine) {
                 __syncthreads();  // every row of stage b summed: it can be refilled
                 if (issuer) issue(i + NS);
@@ -586,10 +604,10 @@ __global__ void __launch_bounds__(PAT_THREADS, NS == 1 ? 1536 / PAT_THREADS : 1)
         }
     }
     if (DOT) {
-        acc = block_sum<PAT_THREADS>(acc, red);
+        acc = block_sum<NT>(acc, red);
         if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
-        if (blockIdx.x == 0)  // persistent grid: the slots of the tiles beyond the grid read as 0
-            for (int k = gridDim.x + threadIdx.x; k < ntl; k += PAT_THREADS) s.partials[k] = 0.0;
+        if (NS > 1 && blockIdx.x == 0)  // persistent grid: the slots of the tiles beyond the grid read as 0
+            for (int k = gridDim.x + threadIdx.x; k < ntl; k += NT) s.partials[k] = 0.0;
     }
 }
 
@@ -607,7 +625,8 @@ class CsrOperator : public Operator {
     size_t smem_stage = 0;
     DevBuf rtbl, rdesc;      // ring kernel: per-tile tables and copy descriptors (k_csr_pat_ring)
     bool ring = false;
-    int ring_ns = 1;         // stages per CTA (1: one tile per CTA)
+    int ring_ns = 1;         // stages per CTA (1: one tile per CTA; A/B NPC_RING_NS=2)
+    int ring_rpt = 2;        // rows per thread (A/B NPC_RING_RPT=4)
     int ring_ctas = 0;       // resident CTAs per SM of the persistent form (queried at the first launch)
     int ring_stage = 0, ring_tbl_bytes = 0;
     long long ring_tbl_ints = 0;  // stored (deduplicated) ring-table words
@@ -694,9 +713,10 @@ class CsrOperator : public Operator {
     template <bool H2, bool HR, bool DT>
     npc_status prepare3() {
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_stage<H2, HR, DT>));
-        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 1>));
-        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 2>));
-        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 3>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 1, 2>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 2, 2>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 1, 4>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 2, 4>));
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_step<H2, HR, DT, false>));
         return allow_max_dynamic_smem(k_csr_pat_step<H2, HR, DT, true>);
     }
@@ -724,32 +744,34 @@ class CsrOperator : public Operator {
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
-    template <bool H2, bool HR, bool DT, int NS>
+    template <bool H2, bool HR, bool DT, int NS, int R>
     npc_status launch_ring_ns(const StepArgs &s, const int *tl, int nt, double *partials) {
         RingDev A{vals.as<double>(), rtbl.as<int>(), pat.as<unsigned char>(), rdesc.as<int4>(), n_local};
         StepArgs a = s;
         a.partials = partials;
-        auto kern = k_csr_pat_ring<H2, HR, DT, NS>;
+        auto kern = k_csr_pat_ring<H2, HR, DT, NS, R>;
         const size_t sm = (size_t)NS * ring_stage;
         int grid = nt;
         if (NS > 1) {
             if (ring_ctas == 0) {  // resident CTAs per SM at this stage size
                 int occ = 0;
-                NPC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PAT_THREADS, sm));
+                NPC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PAT_TILE / R, sm));
                 ring_ctas = std::max(1, occ);
             }
             grid = std::min(nt, ctx->num_sms * ring_ctas);
         }
-        kern<<<grid, PAT_THREADS, sm, ctx->stream>>>(A, a, tl, nt, ring_stage, ring_tbl_bytes);
+        kern<<<grid, PAT_TILE / R, sm, ctx->stream>>>(A, a, tl, nt, ring_stage, ring_tbl_bytes);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
     template <bool H2, bool HR, bool DT>
     npc_status launch_ring(const StepArgs &s, const int *tl, int nt, double *partials) {
         if (nt <= 0) return NPC_SUCCESS;
-        if (ring_ns == 3) return launch_ring_ns<H2, HR, DT, 3>(s, tl, nt, partials);
-        if (ring_ns == 2) return launch_ring_ns<H2, HR, DT, 2>(s, tl, nt, partials);
-        return launch_ring_ns<H2, HR, DT, 1>(s, tl, nt, partials);
+        if (ring_rpt == 4)
+            return ring_ns == 2 ? launch_ring_ns<H2, HR, DT, 2, 4>(s, tl, nt, partials)
+                                : launch_ring_ns<H2, HR, DT, 1, 4>(s, tl, nt, partials);
+        return ring_ns == 2 ? launch_ring_ns<H2, HR, DT, 2, 2>(s, tl, nt, partials)
+                            : launch_ring_ns<H2, HR, DT, 1, 2>(s, tl, nt, partials);
     }
     npc_status launch_stage_any(const StepArgs &s, const int *tl, int nt, double *partials) {
         const bool h2 = s.s2 != nullptr, hr = s.r != nullptr, dt = s.dotv != nullptr;
@@ -1180,7 +1202,7 @@ static bool pattern_ring_table(int n, int t, const std::vector<int> &tptr, const
     o[3] = nrs;
     {
         const int wi = xwin_of(r0);
-        o[2] = xbase + xw[wi].sb + (r0 - xw[wi].ga);
+        o[2] = 8 * (xbase + xw[wi].sb + (r0 - xw[wi].ga));
     }
     const int sidx = 4;
     o.resize(sidx + np + 1);
@@ -1207,8 +1229,8 @@ static bool pattern_ring_table(int n, int t, const std::vector<int> &tptr, const
                 while (!(fw[f].pos == pos && fw[f].lo <= cmin && cmin < fw[f].hi)) ++f;
                 vb = fwb[f] + (int)((long long)r0 + of - fw[f].lo);
             }
-            o.push_back(xb);
-            o.push_back(vb);
+            o.push_back(8 * xb);  // byte offsets into D
+            o.push_back(8 * vb);
         }
     }
     o[sidx + np] = (int)(o.size() - o[1]) / 2;
@@ -1481,7 +1503,8 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
         op.ring_stage = ph.ring_stage;
         op.ring_tbl_bytes = ph.ring_tbl_bytes;
         op.ring_tbl_ints = (long long)ph.rtbl.size();
-        if (const char *e = getenv("NPC_RING_NS")) op.ring_ns = std::min(3, std::max(1, atoi(e)));
+        if (const char *e = getenv("NPC_RING_NS")) op.ring_ns = std::min(2, std::max(1, atoi(e)));
+        if (const char *e = getenv("NPC_RING_RPT")) op.ring_rpt = atoi(e) == 4 ? 4 : 2;
         if ((size_t)op.ring_ns * op.ring_stage > 227 * 1024) op.ring_ns = 1;
         NPC_TRY(op.rtbl.alloc(sizeof(int) * ph.rtbl.size()));
         NPC_TRY(op.rdesc.alloc(sizeof(int) * ph.rdesc.size()));

@@ -36,14 +36,14 @@ def dev(a):
 
 FORM_ENV = {"plain": "NPC_CSR_PLAIN", "coded": "NPC_CSR_CODED", "nomirror": "NPC_CSR_NOMIRROR",
             "nostage": "NPC_CSR_NOSTAGE", "stage": "NPC_CSR_NORING", "nofill": "NPC_CSR_NOFILL",
-            "ring2": "NPC_RING_NS=2", "ring3": "NPC_RING_NS=3"}
+            "ring2": "NPC_RING_NS=2", "rpt4": "NPC_RING_RPT=4"}
 
 
 def make(ctx, w, plain):
     """plain: True -> int32 column ids, False -> the coded form; or a form name: 'pattern'
     (the default form: ring kernel), 'nomirror' (pattern ids without symmetric mirroring), 'nostage'
     (pattern form without the x-window staging kernels), 'stage' (k_csr_pat_stage instead of the
-    ring kernel), 'ring2' / 'ring3' (persistent ring kernel with 2 / 3 stages), 'nofill' (no
+    ring kernel), 'ring2' (persistent ring kernel, 2 stages), 'rpt4' (4 rows per thread), 'nofill' (no
     earlier-tile mirrors moved into ELL padding), 'coded', 'plain'."""
     form = ("plain" if plain else "coded") if isinstance(plain, bool) else plain
     env = FORM_ENV.get(form)
