@@ -477,6 +477,103 @@ struct RingDev {
 #ifndef NPC_RING_WAIT_NS
 #define NPC_RING_WAIT_NS 1000
 #endif
+// Warp 0: the bulk copies of one tile into a stage (x = the input vector of this step).
+__device__ __forceinline__ void ring_issue(const RingDev &A, const double *x, int tile, unsigned char *st, uint64_t *bar,
+                                           int lane, uint64_t vals_policy, bool hint) {
+    int4 d = make_int4(0, 0, 0, 0);
+    if (lane < RING_MAXD) d = A.desc[(size_t)tile * RING_MAXD + lane];
+    if (lane > 0 && d.x == 4) *reinterpret_cast<double *>(st + d.y) = x[d.z];  // odd x tail
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)d.y);  // header {ncopies, bytes}
+    __syncwarp();
+    if (lane > 0 && d.w > 0) {
+        if (d.x == 0 && hint) {
+            bulk_g2s_evict_first(st + d.y, A.vals + d.z, (uint32_t)d.w, bar, vals_policy);  // any L2 policy
+        } else {
+            const void *src = d.x == 0   ? (const void *)(A.vals + d.z)
+                              : d.x == 1 ? (const void *)(x + d.z)
+                              : d.x == 2 ? (const void *)(A.tbl + d.z)
+                                         : (const void *)(A.pat + d.z);
+            bulk_g2s(st + d.y, src, (uint32_t)d.w, bar);
+        }
+    }
+}
+
+// Per-row streams of a tile (s_{j-2}, r, the dot operand), loaded ahead into registers.
+template <int R>
+struct RingRows {
+    double s2[R], r[R], v[R];
+};
+template <bool HAS_S2, bool HAS_R, bool DOT, int R>
+__device__ __forceinline__ void ring_load_rows(const double *s2, const double *r, const double *dotv, int row0,
+                                               int nrows, RingRows<R> &q) {
+    constexpr int NT = PAT_TILE / R;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int l = threadIdx.x + k * NT;
+        q.s2[k] = q.r[k] = q.v[k] = 0.0;
+        if (l < nrows) {
+            if (HAS_S2) q.s2[k] = s2[row0 + l];
+            if (HAS_R) q.r[k] = r[row0 + l];
+            if (DOT) q.v[k] = dotv[row0 + l];
+        }
+    }
+}
+
+// The row sums and epilogue of one staged tile (every operand in shared memory).
+template <bool HAS_S2, bool HAS_R, bool DOT, int R>
+__device__ __forceinline__ void ring_tile(const StepArgs &s, const unsigned char *st8, int tbl_bytes, int row0,
+                                          int nrows, const RingRows<R> &cur, double &acc) {
+    constexpr int NT = PAT_TILE / R;
+    const int *st = reinterpret_cast<const int *>(st8);
+    const unsigned char *sp = st8 + tbl_bytes;
+    const char *Db = reinterpret_cast<const char *>(sp + PAT_TILE);  // D; entries are byte offsets
+    const int2 *E = reinterpret_cast<const int2 *>(st + st[1]);
+    const int *ps = st + 4;
+    const int x0b = st[2];
+    auto ld = [](const char *p, int off) { return *reinterpret_cast<const double *>(p + off); };
+    int eb[R], ne[R];
+    const char *Dr[R];
+    double y[R];
+    bool same = true;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int l = threadIdx.x + k * NT;
+        const int p = l < nrows ? sp[l] : 0;
+        eb[k] = ps[p];
+        ne[k] = l < nrows ? ps[p + 1] - eb[k] : 0;
+        Dr[k] = Db + 8 * l;
+        y[k] = 0.0;
+        same = same && ne[k] == ne[0];
+    }
+    if (same) {  // every row in one loop (the common case: one pattern length)
+#pragma unroll 2
+        for (int e = 0; e < ne[0]; ++e) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const int2 u = E[eb[k] + e];
+                y[k] = fma(ld(Dr[k], u.y), ld(Dr[k], u.x), y[k]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+            for (int e = 0; e < ne[k]; ++e) {
+                const int2 u = E[eb[k] + e];
+                y[k] = fma(ld(Dr[k], u.y), ld(Dr[k], u.x), y[k]);
+            }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int l = threadIdx.x + k * NT;
+        if (l < nrows) {
+            const double o = degree_epilogue<HAS_S2, HAS_R>(s, y[k], ld(Dr[k], x0b), cur.s2[k], cur.r[k]);
+            s.out[row0 + l] = o;
+            if (DOT) acc = fma(o, cur.v[k], acc);
+        }
+    }
+}
+
 // R rows per thread (lr = tid + q * PAT_TILE / R), summed in one interleaved loop when their
 // patterns have the same length.
 template <bool HAS_S2, bool HAS_R, bool DOT, int NS, int R>
@@ -500,106 +597,29 @@ __global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 
         const int q = (int)blockIdx.x + i * (int)gridDim.x;
         return tiles ? tiles[q] : q;
     };
-    // warp 0: the copies of tile i into stage i % NS
-    auto issue = [&](int i) {
-        const int tile = tile_of(i);
-        unsigned char *st = rg_smem + (size_t)(i % NS) * stage_bytes;
-        uint64_t *bar = &full[i % NS];
-        int4 d = make_int4(0, 0, 0, 0);
-        if (lane < RING_MAXD) d = A.desc[(size_t)tile * RING_MAXD + lane];
-        if (lane > 0 && d.x == 4) *reinterpret_cast<double *>(st + d.y) = s.x[d.z];  // odd x tail
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)d.y);  // header {ncopies, bytes}
-        __syncwarp();
-        if (lane > 0 && d.w > 0) {
-            const void *src = d.x == 0   ? (const void *)(A.vals + d.z)
-                              : d.x == 1 ? (const void *)(s.x + d.z)
-                              : d.x == 2 ? (const void *)(A.tbl + d.z)
-                                         : (const void *)(A.pat + d.z);
-            bulk_g2s(st + d.y, src, (uint32_t)d.w, bar);
-        }
-    };
     if (issuer)
-        for (int i = 0; i < NS && i < nmine; ++i) issue(i);
-    // per-row streams of a tile (s_{j-2}, r, the dot operand), loaded a tile ahead into registers
-    struct Rows {
-        double s2[R], r[R], v[R];
+        for (int i = 0; i < NS && i < nmine; ++i)
+            ring_issue(A, s.x, tile_of(i), rg_smem + (size_t)(i % NS) * stage_bytes, &full[i % NS], lane, 0, false);
+    RingRows<R> cur;
+    auto rows_of = [&](int i, RingRows<R> &q) {
+        const int row0 = tile_of(i) * PAT_TILE;
+        ring_load_rows<HAS_S2, HAS_R, DOT, R>(s.s2, s.r, s.dotv, row0, min(PAT_TILE, A.n - row0), q);
     };
-    auto load_rows = [&](int i, Rows &q) {
-        const int row0 = tile_of(i) * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-            const int l = threadIdx.x + k * NT;
-            q.s2[k] = q.r[k] = q.v[k] = 0.0;
-            if (l < nrows) {
-                if (HAS_S2) q.s2[k] = s.s2[row0 + l];
-                if (HAS_R) q.r[k] = s.r[row0 + l];
-                if (DOT) q.v[k] = s.dotv[row0 + l];
-            }
-        }
-    };
-    Rows cur;
-    if (nmine > 0) load_rows(0, cur);
+    if (nmine > 0) rows_of(0, cur);
     double acc = 0.0;
     for (int i = 0; i < nmine; ++i) {
-        Rows nxt;
-        if (NS > 1 && i + 1 < nmine) load_rows(i + 1, nxt);
+        RingRows<R> nxt;
+        if (NS > 1 && i + 1 < nmine) rows_of(i + 1, nxt);
         const int b = i % NS;
         const int row0 = tile_of(i) * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
         mbar_wait_sleep(&full[b], (uint32_t)((i / NS) & 1), NPC_RING_WAIT_NS);
-        const unsigned char *st8 = rg_smem + (size_t)b * stage_bytes;
-        const int *st = reinterpret_cast<const int *>(st8);
-        const unsigned char *sp = st8 + tbl_bytes;
-        const char *Db = reinterpret_cast<const char *>(sp + PAT_TILE);  // D; entries are byte offsets
-        const int2 *E = reinterpret_cast<const int2 *>(st + st[1]);
-        const int *ps = st + 4;
-        const int x0b = st[2];
-        auto ld = [](const char *p, int off) { return *reinterpret_cast<const double *>(p + off); };
-        int eb[R], ne[R];
-        const char *Dr[R];
-        double y[R];
-        bool same = true;
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-            const int l = threadIdx.x + k * NT;
-            const int p = l < nrows ? sp[l] : 0;
-            eb[k] = ps[p];
-            ne[k] = l < nrows ? ps[p + 1] - eb[k] : 0;
-            Dr[k] = Db + 8 * l;
-            y[k] = 0.0;
-            same = same && ne[k] == ne[0];
-        }
-        if (same) {  // every row in one loop (the common case: one pattern length)
-#pragma unroll 2
-            for (int e = 0; e < ne[0]; ++e) {
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const int2 u = E[eb[k] + e];
-                    y[k] = fma(ld(Dr[k], u.y), ld(Dr[k], u.x), y[k]);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < R; ++k)
-                for (int e = 0; e < ne[k]; ++e) {
-                    const int2 u = E[eb[k] + e];
-                    y[k] = fma(ld(Dr[k], u.y), ld(Dr[k], u.x), y[k]);
-                }
-        }
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-            const int l = threadIdx.x + k * NT;
-            if (l < nrows) {
-                const double o = degree_epilogue<HAS_S2, HAS_R>(s, y[k], ld(Dr[k], x0b), cur.s2[k], cur.r[k]);
-                s.out[row0 + l] = o;
-                if (DOT) acc = fma(o, cur.v[k], acc);
-            }
-        }
+        ring_tile<HAS_S2, HAS_R, DOT, R>(s, rg_smem + (size_t)b * stage_bytes, tbl_bytes, row0, nrows, cur, acc);
         if (NS > 1) {
             cur = nxt;
             if (i + NS < nmine) {
                 __syncthreads();  // every row of stage b summed: it can be refilled
-                if (issuer) issue(i + NS);
+                if (issuer)
+                    ring_issue(A, s.x, tile_of(i + NS), rg_smem + (size_t)b * stage_bytes, &full[b], lane, 0, false);
             }
         }
     }
@@ -608,6 +628,119 @@ __global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 
         if (threadIdx.x == 0) s.partials[blockIdx.x] = acc;
         if (NS > 1 && blockIdx.x == 0)  // persistent grid: the slots of the tiles beyond the grid read as 0
             for (int k = gridDim.x + threadIdx.x; k < ntl; k += NT) s.partials[k] = 0.0;
+    }
+}
+
+// ---------------------------------------------------------------- two degrees per pass (L2 wavefront)
+// Temporal blocking for the pattern form without any grid geometry: one launch computes s_j
+// (step s1) and s_{j+1} (step s2) for every tile.  Work items are taken in ticket order (an
+// atomic counter, so a taken item only ever waits on items taken before it): s_j of tile u,
+// interleaved with s_{j+1} of tile u - L.  s_{j+1} of tile t reads s_j through its x windows,
+// i.e. tiles deps[t].x .. deps[t].y; the CTA's warp 0 waits until those tiles' epoch flags show
+// this launch (release/acquire), then copies them.  With the lag L larger than that reach plus
+// the items in flight, the wait is normally already satisfied, and tile t's own values, s_{j-1}
+// and r -- read by s_j of tile t only L tiles earlier -- come from L2 the second time: per two
+// degrees HBM sees the matrix once and five vectors (s_{j-1}, s_{j-2}, r read; s_j, s_{j+1}
+// written) instead of the matrix twice and eight vectors.  Same sums and epilogues as two
+// k_csr_pat_ring launches: bitwise equal.  The ticket counter is never reset: every launch
+// takes exactly 2 x tiles tickets (or none, when the PCG's done flag is set), so ticket / (2
+// tiles) numbers the launch -- the epoch the flags carry (graph-replay safe, no host state).
+struct WaveState {
+    unsigned long long ticket;  // items taken over all launches: launch = ticket / (2 ntiles)
+};
+#ifndef NPC_WAVE_HINTS
+#define NPC_WAVE_HINTS 1
+#endif
+#ifndef NPC_WAVE_NOWAIT  // A/B only (results may be wrong): no dependency wait
+#define NPC_WAVE_NOWAIT 0
+#endif
+template <bool DOT>
+__global__ void __launch_bounds__(PAT_THREADS, 1536 / PAT_THREADS)
+    k_csr_pat_wave(RingDev A, StepArgs s1, StepArgs s2, int ntl, int L, int stage_bytes, int tbl_bytes,
+                   WaveState *ws, unsigned *flags, const int2 *__restrict__ deps) {
+    constexpr int R = 2;
+    extern __shared__ __align__(16) unsigned char rg_smem[];
+    __shared__ uint64_t full;
+    __shared__ double red[PAT_THREADS / 32];
+    __shared__ int sh_item;
+    __shared__ unsigned sh_ep;
+    if (s1.done && *s1.done) return;  // uniform, before a ticket is taken
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&full, 1);
+        fence_mbar_init();
+        const unsigned long long tk = atomicAdd(&ws->ticket, 1ull), per = 2ull * (unsigned long long)ntl;
+        sh_item = (int)(tk % per);
+        sh_ep = (unsigned)(tk / per) + 1u;  // this launch's flag value
+    }
+    __syncthreads();
+    const int item = sh_item;
+    const unsigned ep = sh_ep;
+    // item -> (role, tile): s_j of tiles 0 .. L'-1, then pairs (s_j of u, s_{j+1} of u - L), then
+    // the remaining s_{j+1}
+    const int Lp = min(L, ntl), n2 = max(0, ntl - L);
+    int role, tile;
+    if (item < Lp) {
+        role = 0, tile = item;
+    } else if (item - Lp < 2 * n2) {
+        const int k = (item - Lp) >> 1;
+        role = (item - Lp) & 1;
+        tile = role == 0 ? L + k : k;
+    } else {
+        role = 1, tile = n2 + (item - Lp - 2 * n2);
+    }
+    const StepArgs &s = role == 0 ? s1 : s2;
+    const double *x = role == 0 ? s1.x : s1.out;   // s_{j-1} / s_j
+    const double *s2v = role == 0 ? s1.s2 : s1.x;  // s_{j-2} / s_{j-1}
+    const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
+    if (threadIdx.x < 32) {
+        if (role == 1 && !NPC_WAVE_NOWAIT) {  // s_j of every tile this one's x windows cover must be complete
+            const int2 dp = deps[tile];
+            bool ok;
+            do {
+                ok = true;
+                for (int t = dp.x + lane; t <= dp.y; t += 32) {
+                    unsigned f;
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flags + t) : "memory");
+                    ok = ok && (int)(f - ep) >= 0;
+                }
+                ok = __all_sync(0xffffffffu, ok);
+                if (!ok) __nanosleep(500);
+            } while (!ok);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> bulk copies
+        }
+        uint64_t pol = 0;
+        if (NPC_WAVE_HINTS) {
+            if (role == 0)
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            else
+                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        }
+        ring_issue(A, x, tile, rg_smem, &full, lane, pol, NPC_WAVE_HINTS != 0);
+    }
+    RingRows<R> cur;
+    const bool dot = DOT && role == 1;
+    if (dot)
+        ring_load_rows<true, true, true, R>(s2v, s.r, s.dotv, row0, nrows, cur);
+    else
+        ring_load_rows<true, true, false, R>(s2v, s.r, nullptr, row0, nrows, cur);
+    double acc = 0.0;
+    mbar_wait_sleep(&full, 0, NPC_RING_WAIT_NS);
+    if (dot)
+        ring_tile<true, true, true, R>(s, rg_smem, tbl_bytes, row0, nrows, cur, acc);
+    else
+        ring_tile<true, true, false, R>(s, rg_smem, tbl_bytes, row0, nrows, cur, acc);
+    if (DOT && role == 1) {
+        acc = block_sum<PAT_THREADS>(acc, red);  // uniform over the CTA (role is)
+        if (threadIdx.x == 0) s2.partials[tile] = acc;
+    }
+    __syncthreads();  // every row of this item stored
+    if (threadIdx.x == 0) {
+        if (role == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + tile), "r"(ep) : "memory");
+        }
     }
 }
 
@@ -630,6 +763,10 @@ class CsrOperator : public Operator {
     int ring_ctas = 0;       // resident CTAs per SM of the persistent form (queried at the first launch)
     int ring_stage = 0, ring_tbl_bytes = 0;
     long long ring_tbl_ints = 0;  // stored (deduplicated) ring-table words
+    // two degrees per pass (k_csr_pat_wave): per-tile x-window reach, epoch flags, ticket state
+    DevBuf wdeps, wflags, wstate;
+    int wave_lag = 0, ring_span = 0;
+    bool wave = false;
     struct PatTiles {  // a tile list split by kernel: staged / unstaged
         DevBuf staged, unstaged;
         int ns = 0, nu = 0;
@@ -721,6 +858,8 @@ class CsrOperator : public Operator {
         return allow_max_dynamic_smem(k_csr_pat_step<H2, HR, DT, true>);
     }
     npc_status prepare_kernels() {
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_wave<true>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_wave<false>));
         NPC_TRY((prepare3<true, true, true>()));
         NPC_TRY((prepare3<true, true, false>()));
         NPC_TRY((prepare3<true, false, true>()));
@@ -827,6 +966,32 @@ class CsrOperator : public Operator {
         if (hr) return launch_g<false, true, false>(s, tl, nt, partials, ghost);
         if (dt) return launch_g<false, false, true>(s, tl, nt, partials, ghost);
         return launch_g<false, false, false>(s, tl, nt, partials, ghost);
+    }
+
+    bool supports_step2() const override { return pattern && ring && wave && ring_ns == 1; }
+    int num_partials2() const override { return std::max(ntiles, 1); }
+    double bytes_per_step2() const override { return matrix_bytes() + 5.0 * 8.0 * n_local; }
+    npc_status step2(const StepArgs &s1, const StepArgs &s2) override {
+        if (!s1.x || !s1.s2 || !s1.r || !s2.r || !s1.out || !s2.out) {
+            set_error("CSR step2: x, s_{j-2}, r and both outputs are required");
+            return NPC_ERR_INVALID_ARGUMENT;
+        }
+        if (((uintptr_t)s1.x & 15) || ((uintptr_t)s1.out & 15)) {  // window copies need 16-byte aligned inputs
+            NPC_TRY(step(s1));
+            StepArgs t = s2;
+            t.x = s1.out;
+            t.s2 = s1.x;
+            return step(t);
+        }
+        RingDev A{vals.as<double>(), rtbl.as<int>(), pat.as<unsigned char>(), rdesc.as<int4>(), n_local};
+        auto go = [&](auto kern) -> npc_status {
+            kern<<<2 * ntiles, PAT_THREADS, ring_stage, ctx->stream>>>(A, s1, s2, ntiles, wave_lag, ring_stage,
+                                                                      ring_tbl_bytes, wstate.as<WaveState>(),
+                                                                      wflags.as<unsigned>(), wdeps.as<int2>());
+            NPC_LAUNCH_CHECK();
+            return NPC_SUCCESS;
+        };
+        return s2.dotv ? go(k_csr_pat_wave<true>) : go(k_csr_pat_wave<false>);
     }
 
     SmallCsrPlan small;  // cluster-resident polynomial (single rank, n <= 16384)
@@ -990,8 +1155,8 @@ struct PatHost {
     int xspan_max = 0, tbl2_max = 0;
     // ring kernel (k_csr_pat_ring): per-tile tables (16-byte aligned), RING_MAXD int4 copy
     // descriptors per tile, the stage size and its table region; ring = every staged tile has one
-    std::vector<int> rtbl, rdesc;
-    int ring_stage = 0, ring_tbl_bytes = 0;
+    std::vector<int> rtbl, rdesc, rdeps;
+    int ring_stage = 0, ring_tbl_bytes = 0, ring_span = 0;
     bool ring = false;
 };
 
@@ -1083,6 +1248,7 @@ struct RingTile {
     std::vector<int> tbl;
     std::vector<RingCopy> cp;
     int dbl = 0;
+    int dep_lo = 0, dep_hi = -1;  // tiles of x the tile's windows cover (two-degree pass)
 };
 
 static bool pattern_ring_table(int n, int t, const std::vector<int> &tptr, const std::vector<int> &twidth,
@@ -1190,9 +1356,14 @@ static bool pattern_ring_table(int n, int t, const std::vector<int> &tptr, const
                                  (int)(ce - c) * 8});
             c = ce;
         }
+    rt.dep_lo = INT_MAX, rt.dep_hi = -1;
     for (auto &w : xw) {
         if (w.len) rt.cp.push_back({1, 2, xbase + w.sb, w.ga, w.len * 8});
         if (w.tail) rt.cp.push_back({4, 2, xbase + w.sb + w.len, w.ga + w.len, 0});
+        if (w.len + w.tail > 0) {
+            rt.dep_lo = std::min(rt.dep_lo, w.ga / T);
+            rt.dep_hi = std::max(rt.dep_hi, (w.ga + w.len + w.tail - 1) / T);
+        }
     }
     if ((int)rt.cp.size() > RING_MAXD - 1) return false;
     // table: [np, entry start, x0 base, nrs][np + 1 starts (entries)][pad][entries {xb, vb}]
@@ -1437,6 +1608,12 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
                 for (auto &kv : seen)
                     for (int u : kv.second) std::copy(rts[u].tbl.begin(), rts[u].tbl.end(), ph.rtbl.begin() + toff[u]);
                 ph.rdesc.assign((size_t)ntiles * RING_MAXD * 4, 0);
+                ph.rdeps.assign((size_t)ntiles * 2, 0);
+                for (int t = 0; t < ntiles; ++t) {
+                    ph.rdeps[2 * t] = std::min(rts[t].dep_lo, t);
+                    ph.rdeps[2 * t + 1] = std::max(rts[t].dep_hi, t);
+                    ph.ring_span = std::max(ph.ring_span, ph.rdeps[2 * t + 1] - t);
+                }
                 host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
                     for (long long t = t0; t < t1; ++t) {
                         if (!ph.stage[t]) continue;
@@ -1510,6 +1687,25 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
         NPC_TRY(op.rdesc.alloc(sizeof(int) * ph.rdesc.size()));
         NPC_CUDA_TRY(cudaMemcpy(op.rtbl.p, ph.rtbl.data(), sizeof(int) * ph.rtbl.size(), cudaMemcpyHostToDevice));
         NPC_CUDA_TRY(cudaMemcpy(op.rdesc.p, ph.rdesc.data(), sizeof(int) * ph.rdesc.size(), cudaMemcpyHostToDevice));
+        // the two-degree pass (opt-in NPC_CSR_WAVE=1): single rank, every tile staged.  Measured on
+        // config 3 (profiles/r02_wave_ab.md): DRAM per pair 1.21 GB instead of 2.17 GB, but the pass
+        // is then bound by its doubled L2 / bulk-copy volume and the dependency waits (p_50 10.0 ms
+        // vs 8.7 ms one degree per pass)
+        op.ring_span = ph.ring_span;
+        op.wave = !op.multi && ph.rdeps.size() == (size_t)op.ntiles * 2 && getenv("NPC_NO_STEP2") == nullptr &&
+                  getenv("NPC_CSR_WAVE") != nullptr;
+        for (int t = 0; t < op.ntiles && op.wave; ++t) op.wave = ph.stage[t] != 0;
+        if (op.wave) {
+            NPC_TRY(op.wdeps.alloc(sizeof(int) * ph.rdeps.size()));
+            NPC_TRY(op.wflags.alloc(sizeof(unsigned) * op.ntiles));
+            NPC_TRY(op.wstate.alloc(sizeof(WaveState)));
+            NPC_CUDA_TRY(cudaMemcpy(op.wdeps.p, ph.rdeps.data(), sizeof(int) * ph.rdeps.size(), cudaMemcpyHostToDevice));
+            NPC_CUDA_TRY(cudaMemset(op.wflags.p, 0, sizeof(unsigned) * op.ntiles));
+            NPC_CUDA_TRY(cudaMemset(op.wstate.p, 0, sizeof(WaveState)));
+            // lag: the x-window reach plus the items in flight (3 CTAs per SM, half of them s_j)
+            op.wave_lag = op.ring_span + ctx->num_sms * 3 / 2 + 64;
+            if (const char *e = getenv("NPC_WAVE_LAG")) op.wave_lag = std::max(op.ring_span + 1, atoi(e));
+        }
     }
     auto split = [&](const std::vector<int> &list, CsrOperator::PatTiles &pt) -> npc_status {
         std::vector<int> st, un;

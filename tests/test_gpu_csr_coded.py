@@ -36,24 +36,26 @@ def dev(a):
 
 FORM_ENV = {"plain": "NPC_CSR_PLAIN", "coded": "NPC_CSR_CODED", "nomirror": "NPC_CSR_NOMIRROR",
             "nostage": "NPC_CSR_NOSTAGE", "stage": "NPC_CSR_NORING", "nofill": "NPC_CSR_NOFILL",
-            "ring2": "NPC_RING_NS=2", "rpt4": "NPC_RING_RPT=4"}
+            "ring2": "NPC_RING_NS=2", "rpt4": "NPC_RING_RPT=4",
+            "wave": "NPC_CSR_WAVE", "lag1": "NPC_CSR_WAVE,NPC_WAVE_LAG=1"}
 
 
 def make(ctx, w, plain):
     """plain: True -> int32 column ids, False -> the coded form; or a form name: 'pattern'
     (the default form: ring kernel), 'nomirror' (pattern ids without symmetric mirroring), 'nostage'
     (pattern form without the x-window staging kernels), 'stage' (k_csr_pat_stage instead of the
-    ring kernel), 'ring2' (persistent ring kernel, 2 stages), 'rpt4' (4 rows per thread), 'nofill' (no
+    ring kernel), 'ring2' (persistent ring kernel, 2 stages), 'rpt4' (4 rows per thread), 'wave' (two degrees per
+    pass: the wave kernel), 'lag1' (the wave kernel at its smallest lag), 'nofill' (no
     earlier-tile mirrors moved into ELL padding), 'coded', 'plain'."""
     form = ("plain" if plain else "coded") if isinstance(plain, bool) else plain
     env = FORM_ENV.get(form)
-    key, val = (env.split("=", 1) if "=" in env else (env, "1")) if env else (None, None)
-    if key:
+    kv = [(e.split("=", 1) if "=" in e else (e, "1")) for e in env.split(",")] if env else []
+    for key, val in kv:
         os.environ[key] = val
     try:
         return npc.create_from_workload(ctx, w, "csr")
     finally:
-        if key:
+        for key, _ in kv:
             os.environ.pop(key, None)
 
 
