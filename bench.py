@@ -387,8 +387,8 @@ def run_ours(args):
     e1.record(stream)
     barrier()
     t_apply = e0.elapsed_time(e1) / R  # ms per p_k(A) r (k launches)
-    # roofline numerator: the bytes the kernels stream in the library's stored format (a coded
-    # CSR streams 9 B per nonzero, not 12), this rank's share
+    # roofline numerator: the bytes the kernels stream in the library's stored format (the
+    # pattern form streams ~4.7 B per nonzero, not 12), this rank's share
     # (CSR only: the other operators are reported against their §8(d) floor, like tools/bench_all.py)
     Mf = npc.npc_operator_matrix_bytes(op) if kind == "csr" else M / ws
     Vf = 8 * nl
