@@ -477,26 +477,39 @@ struct RingDev {
 #ifndef NPC_RING_WAIT_NS
 #define NPC_RING_WAIT_NS 1000
 #endif
-// Warp 0: the bulk copies of one tile into a stage (x = the input vector of this step).
-__device__ __forceinline__ void ring_issue(const RingDev &A, const double *x, int tile, unsigned char *st, uint64_t *bar,
-                                           int lane, uint64_t vals_policy, bool hint) {
-    int4 d = make_int4(0, 0, 0, 0);
-    if (lane < RING_MAXD) d = A.desc[(size_t)tile * RING_MAXD + lane];
-    if (lane > 0 && d.x == 4) *reinterpret_cast<double *>(st + d.y) = x[d.z];  // odd x tail
-    __syncwarp();
-    if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)d.y);  // header {ncopies, bytes}
-    __syncwarp();
-    if (lane > 0 && d.w > 0) {
+// Warp 0: the bulk copies of one tile into a stage (x = the input vector of this step), from the
+// tile's descriptor block d (lane 0: header {ncopies, bytes, has an odd x tail}; lanes 1..: one
+// copy each).  part 0: everything; part 1: the barrier's arrive and the copies that do not read
+// x; part 2: the x windows (a tile with an odd x tail takes part 0 only: its tail store must
+// precede the arrive).
+__device__ __forceinline__ int4 ring_desc(const RingDev &A, int tile, int lane) {
+    return lane < RING_MAXD ? A.desc[(size_t)tile * RING_MAXD + lane] : make_int4(0, 0, 0, 0);
+}
+__device__ __forceinline__ void ring_issue_d(const int4 &d, const RingDev &A, const double *x, unsigned char *st,
+                                             uint64_t *bar, int lane, uint64_t vals_policy, bool hint, int part) {
+    if (part == 0 && lane > 0 && d.x == 4) *reinterpret_cast<double *>(st + d.y) = x[d.z];  // odd x tail
+    if (part != 2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)d.y);
+        __syncwarp();
+    }
+    if (lane == 0 || d.w <= 0) return;
+    if (d.x == 1) {
+        if (part != 1) bulk_g2s(st + d.y, x + d.z, (uint32_t)d.w, bar);
+    } else if (part != 2) {
         if (d.x == 0 && hint) {
             bulk_g2s_evict_first(st + d.y, A.vals + d.z, (uint32_t)d.w, bar, vals_policy);  // any L2 policy
         } else {
-            const void *src = d.x == 0   ? (const void *)(A.vals + d.z)
-                              : d.x == 1 ? (const void *)(x + d.z)
+            const void *src = d.x == 0 ? (const void *)(A.vals + d.z)
                               : d.x == 2 ? (const void *)(A.tbl + d.z)
                                          : (const void *)(A.pat + d.z);
             bulk_g2s(st + d.y, src, (uint32_t)d.w, bar);
         }
     }
+}
+__device__ __forceinline__ void ring_issue(const RingDev &A, const double *x, int tile, unsigned char *st, uint64_t *bar,
+                                           int lane, uint64_t vals_policy, bool hint) {
+    ring_issue_d(ring_desc(A, tile, lane), A, x, st, bar, lane, vals_policy, hint, 0);
 }
 
 // Per-row streams of a tile (s_{j-2}, r, the dot operand), loaded ahead into registers.
@@ -651,6 +664,9 @@ struct WaveState {
 #ifndef NPC_WAVE_HINTS
 #define NPC_WAVE_HINTS 1
 #endif
+#ifndef NPC_WAVE_SLEEP_NS
+#define NPC_WAVE_SLEEP_NS 500
+#endif
 #ifndef NPC_WAVE_NOWAIT  // A/B only (results may be wrong): no dependency wait
 #define NPC_WAVE_NOWAIT 0
 #endif
@@ -694,21 +710,6 @@ __global__ void __launch_bounds__(PAT_THREADS, 1536 / PAT_THREADS)
     const double *s2v = role == 0 ? s1.s2 : s1.x;  // s_{j-2} / s_{j-1}
     const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
     if (threadIdx.x < 32) {
-        if (role == 1 && !NPC_WAVE_NOWAIT) {  // s_j of every tile this one's x windows cover must be complete
-            const int2 dp = deps[tile];
-            bool ok;
-            do {
-                ok = true;
-                for (int t = dp.x + lane; t <= dp.y; t += 32) {
-                    unsigned f;
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flags + t) : "memory");
-                    ok = ok && (int)(f - ep) >= 0;
-                }
-                ok = __all_sync(0xffffffffu, ok);
-                if (!ok) __nanosleep(500);
-            } while (!ok);
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> bulk copies
-        }
         uint64_t pol = 0;
         if (NPC_WAVE_HINTS) {
             if (role == 0)
@@ -716,7 +717,35 @@ __global__ void __launch_bounds__(PAT_THREADS, 1536 / PAT_THREADS)
             else
                 asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         }
-        ring_issue(A, x, tile, rg_smem, &full, lane, pol, NPC_WAVE_HINTS != 0);
+        // the copies that do not read s_j go out before the dependency wait
+        const int4 d = ring_desc(A, tile, lane);
+        const bool tail = __shfl_sync(0xffffffffu, d.z, 0) != 0;
+        if (!tail) ring_issue_d(d, A, x, rg_smem, &full, lane, pol, NPC_WAVE_HINTS != 0, 1);
+        if (role == 1 && !NPC_WAVE_NOWAIT) {  // s_j of every tile this one's x windows cover must be complete
+            const int2 dp = deps[tile];
+            bool ok;
+            // relaxed loads, all in flight together (an acquire per load would serialise them),
+            // then one acquire fence once every flag shows this launch
+            do {
+                ok = true;
+                for (int base = dp.x; base <= dp.y; base += 256) {
+                    unsigned f[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int t = base + lane + 32 * k;
+                        f[k] = ep;
+                        if (t <= dp.y) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f[k]) : "l"(flags + t));
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) ok = ok && (int)(f[k] - ep) >= 0;
+                }
+                ok = __all_sync(0xffffffffu, ok);
+                if (!ok) __nanosleep(NPC_WAVE_SLEEP_NS);
+            } while (!ok);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> bulk copies
+        }
+        ring_issue_d(d, A, x, rg_smem, &full, lane, pol, NPC_WAVE_HINTS != 0, tail ? 0 : 2);
     }
     RingRows<R> cur;
     const bool dot = DOT && role == 1;
@@ -738,7 +767,6 @@ __global__ void __launch_bounds__(PAT_THREADS, 1536 / PAT_THREADS)
     if (threadIdx.x == 0) {
         if (role == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            __threadfence();
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + tile), "r"(ep) : "memory");
         }
     }
@@ -1630,6 +1658,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
                         }
                         dd[0] = (int)rts[t].cp.size();
                         dd[1] = (int)total;
+                        dd[2] = std::any_of(rts[t].cp.begin(), rts[t].cp.end(), [](const RingCopy &c) { return c.kind == 4; });
                     }
                 }, 256);
             }
