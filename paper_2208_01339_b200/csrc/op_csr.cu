@@ -660,6 +660,7 @@ __global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 
 // tiles) numbers the launch -- the epoch the flags carry (graph-replay safe, no host state).
 struct WaveState {
     unsigned long long ticket;  // items taken over all launches: launch = ticket / (2 ntiles)
+    unsigned pticket, pepoch;   // persistent form: items taken in this launch, launch number
 };
 #ifndef NPC_WAVE_HINTS
 #define NPC_WAVE_HINTS 1
@@ -772,6 +773,140 @@ __global__ void __launch_bounds__(PAT_THREADS, 1536 / PAT_THREADS)
     }
 }
 
+// Persistent form of the wave pass (NPC_WAVE_PERSIST=1 with NPC_CSR_WAVE=1): 3 CTAs per SM of
+// 16 consumer warps + 1 producer warp.  The producer takes the NEXT item's ticket, publishes it
+// and, for an s_{j+1} item, polls its dependency flags (and fences) while the consumers still
+// sum the current item; once they release the stage it issues the next item's copies at once.
+// So the acquire latency of the dependency check is off the critical path.  k_wave_begin resets
+// the per-launch ticket and advances the epoch (one thread, before every launch).
+__global__ void k_wave_begin(WaveState *ws) {
+    ws->pticket = 0;
+    ws->pepoch += 1;
+}
+template <bool DOT>
+__global__ void __maxnreg__(40)
+    k_csr_pat_wave_p(RingDev A, StepArgs s1, StepArgs s2, int ntl, int L, int tbl_bytes, WaveState *ws,
+                     unsigned *flags, const int2 *__restrict__ deps) {
+    constexpr int R = 2, NCW = PAT_THREADS / 32;
+    extern __shared__ __align__(16) unsigned char rg_smem[];
+    __shared__ uint64_t full, empty, info_bar[2];
+    __shared__ int info[2][2];  // {role, tile} of items i (slot i % 2); role -1: no more items
+    __shared__ double red[NCW];
+    if (s1.done && *s1.done) return;  // uniform
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&full, 1);
+        mbar_init(&empty, NCW);
+        mbar_init(&info_bar[0], 1);
+        mbar_init(&info_bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const unsigned ep = *reinterpret_cast<volatile unsigned *>(&ws->pepoch);
+    const int per = 2 * ntl;
+    auto map_item = [&](int item, int L, int &role, int &tile) {
+        const int l0 = min(L, ntl), n2 = max(0, ntl - L);
+        if (item < l0) {
+            role = 0, tile = item;
+        } else if (item - l0 < 2 * n2) {
+            const int k = (item - l0) >> 1;
+            role = (item - l0) & 1;
+            tile = role == 0 ? L + k : k;
+        } else {
+            role = 1, tile = n2 + (item - l0 - 2 * n2);
+        }
+    };
+    if (warp == NCW) {
+        // ---------------- producer
+        uint64_t pol0 = 0, pol1 = 0;
+        if (NPC_WAVE_HINTS) {
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol0));
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol1));
+        }
+        for (int i = 0;; ++i) {
+            int item = 0;
+            if (lane == 0) item = (int)atomicAdd(&ws->pticket, 1u);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            int role = -1, tile = 0;
+            if (item < per) map_item(item, L, role, tile);
+            if (lane == 0) {
+                info[i & 1][0] = role;
+                info[i & 1][1] = tile;
+                mbar_arrive(&info_bar[i & 1]);
+            }
+            if (role < 0) break;  // the consumers leave on the published role
+            const double *x = role == 0 ? s1.x : s1.out;
+            const int4 d = ring_desc(A, tile, lane);
+            if (role == 1) {  // s_j of the tiles this one's x windows cover: while the consumers sum
+                const int2 dp = deps[tile];
+                bool ok;
+                do {
+                    ok = true;
+                    for (int base = dp.x; base <= dp.y; base += 256) {
+                        unsigned f[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int t = base + lane + 32 * k;
+                            f[k] = ep;
+                            if (t <= dp.y) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f[k]) : "l"(flags + t));
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) ok = ok && (int)(f[k] - ep) >= 0;
+                    }
+                    ok = __all_sync(0xffffffffu, ok);
+                    if (!ok) __nanosleep(NPC_WAVE_SLEEP_NS);
+                } while (!ok);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            if (i > 0) mbar_wait(&empty, (uint32_t)((i - 1) & 1));  // the consumers left the stage
+            ring_issue_d(d, A, x, rg_smem, &full, lane, role == 0 ? pol0 : pol1, NPC_WAVE_HINTS != 0, 0);
+        }
+    } else {
+        // ---------------- consumers
+        for (int i = 0;; ++i) {
+            mbar_wait(&info_bar[i & 1], (uint32_t)((i >> 1) & 1));
+            const int role = info[i & 1][0], tile = info[i & 1][1];
+            if (role < 0) break;
+            const StepArgs &s = role == 0 ? s1 : s2;
+            const double *s2v = role == 0 ? s1.s2 : s1.x;
+            const int row0 = tile * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
+            RingRows<R> cur;
+            const bool dot = DOT && role == 1;
+            if (dot)
+                ring_load_rows<true, true, true, R>(s2v, s.r, s.dotv, row0, nrows, cur);
+            else
+                ring_load_rows<true, true, false, R>(s2v, s.r, nullptr, row0, nrows, cur);
+            mbar_wait_sleep(&full, (uint32_t)(i & 1), NPC_RING_WAIT_NS);
+            double a = 0.0;
+            if (dot)
+                ring_tile<true, true, true, R>(s, rg_smem, tbl_bytes, row0, nrows, cur, a);
+            else
+                ring_tile<true, true, false, R>(s, rg_smem, tbl_bytes, row0, nrows, cur, a);
+            if (dot) {  // this tile's partial, as block_sum<PAT_THREADS> (consumers only: named barrier 1)
+                a = warp_sum(a);
+                if (lane == 0) red[warp] = a;
+                asm volatile("bar.sync 1, %0;" ::"r"(PAT_THREADS));
+                if (warp == 0) {
+                    double t = lane < NCW ? red[lane] : 0.0;
+                    t = warp_sum(t);
+                    if (lane == 0) s2.partials[tile] = t;
+                }
+            }
+            if (role == 0) {  // every row stored -> the tile's flag
+                asm volatile("bar.sync 1, %0;" ::"r"(PAT_THREADS));
+                if (threadIdx.x == 0) {
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + tile), "r"(ep) : "memory");
+                }
+            }
+            if (dot) asm volatile("bar.sync 1, %0;" ::"r"(PAT_THREADS));  // red[] reused next item
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty);
+        }
+    }
+}
+
 class CsrOperator : public Operator {
   public:
     DevBuf rowptr, cols, vals;
@@ -794,7 +929,7 @@ class CsrOperator : public Operator {
     // two degrees per pass (k_csr_pat_wave): per-tile x-window reach, epoch flags, ticket state
     DevBuf wdeps, wflags, wstate;
     int wave_lag = 0, ring_span = 0;
-    bool wave = false;
+    bool wave = false, wave_persist = false;
     struct PatTiles {  // a tile list split by kernel: staged / unstaged
         DevBuf staged, unstaged;
         int ns = 0, nu = 0;
@@ -888,6 +1023,8 @@ class CsrOperator : public Operator {
     npc_status prepare_kernels() {
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_wave<true>));
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_wave<false>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_wave_p<true>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_wave_p<false>));
         NPC_TRY((prepare3<true, true, true>()));
         NPC_TRY((prepare3<true, true, false>()));
         NPC_TRY((prepare3<true, false, true>()));
@@ -1012,6 +1149,19 @@ class CsrOperator : public Operator {
             return step(t);
         }
         RingDev A{vals.as<double>(), rtbl.as<int>(), pat.as<unsigned char>(), rdesc.as<int4>(), n_local};
+        if (wave_persist) {
+            k_wave_begin<<<1, 1, 0, ctx->stream>>>(wstate.as<WaveState>());
+            NPC_LAUNCH_CHECK();
+            auto gop = [&](auto kern) -> npc_status {
+                const int grid = std::min(2 * ntiles, ctx->num_sms * (1536 / PAT_THREADS));
+                kern<<<grid, PAT_THREADS + 32, ring_stage, ctx->stream>>>(A, s1, s2, ntiles, wave_lag, ring_tbl_bytes,
+                                                                         wstate.as<WaveState>(), wflags.as<unsigned>(),
+                                                                         wdeps.as<int2>());
+                NPC_LAUNCH_CHECK();
+                return NPC_SUCCESS;
+            };
+            return s2.dotv ? gop(k_csr_pat_wave_p<true>) : gop(k_csr_pat_wave_p<false>);
+        }
         auto go = [&](auto kern) -> npc_status {
             kern<<<2 * ntiles, PAT_THREADS, ring_stage, ctx->stream>>>(A, s1, s2, ntiles, wave_lag, ring_stage,
                                                                       ring_tbl_bytes, wstate.as<WaveState>(),
@@ -1732,7 +1882,9 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
             NPC_CUDA_TRY(cudaMemset(op.wflags.p, 0, sizeof(unsigned) * op.ntiles));
             NPC_CUDA_TRY(cudaMemset(op.wstate.p, 0, sizeof(WaveState)));
             // lag: the x-window reach plus the items in flight (3 CTAs per SM, half of them s_j)
-            op.wave_lag = op.ring_span + ctx->num_sms * 3 / 2 + 64;
+            op.wave_persist = getenv("NPC_WAVE_PERSIST") != nullptr;
+            // persistent: each CTA holds its current and its next item
+            op.wave_lag = op.ring_span + ctx->num_sms * 3 / (op.wave_persist ? 1 : 2) + 64;
             if (const char *e = getenv("NPC_WAVE_LAG")) op.wave_lag = std::max(op.ring_span + 1, atoi(e));
         }
     }

@@ -37,7 +37,8 @@ def dev(a):
 FORM_ENV = {"plain": "NPC_CSR_PLAIN", "coded": "NPC_CSR_CODED", "nomirror": "NPC_CSR_NOMIRROR",
             "nostage": "NPC_CSR_NOSTAGE", "stage": "NPC_CSR_NORING", "nofill": "NPC_CSR_NOFILL",
             "ring2": "NPC_RING_NS=2", "rpt4": "NPC_RING_RPT=4",
-            "wave": "NPC_CSR_WAVE", "lag1": "NPC_CSR_WAVE,NPC_WAVE_LAG=1"}
+            "wave": "NPC_CSR_WAVE", "lag1": "NPC_CSR_WAVE,NPC_WAVE_LAG=1",
+            "wavep": "NPC_CSR_WAVE,NPC_WAVE_PERSIST", "wavep1": "NPC_CSR_WAVE,NPC_WAVE_PERSIST,NPC_WAVE_LAG=1"}
 
 
 def make(ctx, w, plain):
@@ -45,7 +46,8 @@ def make(ctx, w, plain):
     (the default form: ring kernel), 'nomirror' (pattern ids without symmetric mirroring), 'nostage'
     (pattern form without the x-window staging kernels), 'stage' (k_csr_pat_stage instead of the
     ring kernel), 'ring2' (persistent ring kernel, 2 stages), 'rpt4' (4 rows per thread), 'wave' (two degrees per
-    pass: the wave kernel), 'lag1' (the wave kernel at its smallest lag), 'nofill' (no
+    pass: the wave kernel), 'lag1' (the wave kernel at its smallest lag), 'wavep' / 'wavep1' (its persistent producer-warp
+    form, default / smallest lag), 'nofill' (no
     earlier-tile mirrors moved into ELL padding), 'coded', 'plain'."""
     form = ("plain" if plain else "coded") if isinstance(plain, bool) else plain
     env = FORM_ENV.get(form)

@@ -65,7 +65,7 @@ WL = {"c3": lambda: W.config3(side=30), "c3_ragged": lambda: W.config3(side=23),
 def _all_forms_bitwise(ctx, w, k=17, xi=1e-3):
     n = w["n"]
     ops = {f: make(ctx, w, f)
-           for f in ("pattern", "nomirror", "nostage", "stage", "ring2", "rpt4", "wave", "lag1", "nofill", "coded",
+           for f in ("pattern", "nomirror", "nostage", "stage", "ring2", "rpt4", "wave", "lag1", "wavep", "wavep1", "nofill", "coded",
                      "plain")}
     x = np.random.default_rng(1).standard_normal(n)
     ys = {}
@@ -148,7 +148,7 @@ def test_ring_pcg_forms(ctx):
     w = W.config3(side=40)
     n = w["n"]
     res = {}
-    for form in ("pattern", "stage", "ring2", "rpt4", "wave", "lag1"):
+    for form in ("pattern", "stage", "ring2", "rpt4", "wave", "lag1", "wavep", "wavep1"):
         op = make(ctx, w, form)
         lo, hi = npc.npc_estimate_spectrum(op, 20, None)
         poly = npc.npc_set_poly(op, 20, lo, hi, 0.0)
@@ -156,7 +156,7 @@ def test_ring_pcg_forms(ctx):
         st = npc.npc_pcg_solve(poly, op, dev(w["b"]), x, w["tol"], 5000)
         assert st["converged"] and st["relres_true"] <= w["tol"], (form, st)
         res[form] = (st["iters"], x)
-    for f in ("stage", "wave", "lag1"):  # two-degree wave passes: the same sums and partials
+    for f in ("stage", "wave", "lag1", "wavep", "wavep1"):  # two-degree wave passes: the same sums and partials
         assert res["pattern"][0] == res[f][0] and torch.equal(res["pattern"][1], res[f][1]), f
     for f in ("ring2", "rpt4"):
         assert abs(res[f][0] - res["pattern"][0]) <= 1, (f, res[f][0], res["pattern"][0])
