@@ -49,7 +49,8 @@ typedef enum {
     NPC_ERR_CUDA = 6,
     NPC_ERR_NCCL = 7,
     NPC_ERR_OUT_OF_MEMORY = 8,
-    NPC_ERR_UNSUPPORTED = 9
+    NPC_ERR_UNSUPPORTED = 9,
+    NPC_ERR_INTERNAL = 10           /* a host-side layout check failed (npc_pattern_check)     */
 } npc_status;
 
 typedef struct npc_context_s *npc_context;
@@ -289,6 +290,21 @@ NPC_API npc_status npc_pcg_solve(npc_poly poly, npc_operator op, const double *b
 NPC_API npc_status npc_halo_plan(int n_local, const int *rowptr, const int *colidx, int nranks,
                          const long long *row_starts, int rank, int *n_ghost,
                          long long *ghost_ids, int *recv_counts);
+/* Layout check of the CSR operator's pattern form (op_csr.cu, Alg. 2's
+ * operator application): builds the storage a single-rank
+ * npc_create_operator would build for the n x n CSR matrix (rowptr[n + 1], colidx, vals: HOST
+ * arrays, read only, column ids ascending within a row) and evaluates y = A x ON THE HOST
+ * (x, y: host arrays of n doubles) by replaying every ring-kernel tile's bulk-copy
+ * descriptors into a staging buffer pre-filled with NaN bytes and summing each row from the
+ * tile's entry table in the kernel's order (an fma chain in ascending column order); tiles
+ * without a ring layout are summed from the CSR arrays.  Every copy's 16-byte alignment,
+ * bounds and the header's byte count are checked.  info[8] (host) receives {pattern form,
+ * ring layout, tiles, ring tiles, most copies in a tile, stage bytes, stored ring-table
+ * words, stored own values}.  Returns NPC_ERR_UNSUPPORTED when the matrix does not take the
+ * pattern form, NPC_ERR_DIMENSION on invalid CSR, NPC_ERR_INTERNAL (message in
+ * npc_last_error) when the layout violates a check.  Honours the NPC_CSR_* layout knobs.    */
+NPC_API npc_status npc_pattern_check(int n, const int *rowptr, const int *colidx, const double *vals,
+                             const double *x, double *y, long long *info);
 /* Chebyshev coefficients as used by the kernels: for j = 1..k the fused degree step is
  * s_j = a_j (A s_{j-1}) + b_j s_{j-1} + c_j s_{j-2} + d_j r with s_0 = r / theta_bar,
  * s_{-1} = 0.  Writes theta_bar, delta, sigma and the 4*k table coef[4*(j-1) + {0,1,2,3}]. */

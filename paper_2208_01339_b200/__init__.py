@@ -92,6 +92,7 @@ def lib():
             "npc_apply_poly": [P, P, P],
             "npc_pcg_solve": [P, P, P, P, D, I, C.POINTER(PcgStats)],
             "npc_halo_plan": [I, P, P, I, P, I, C.POINTER(I), P, P],
+            "npc_pattern_check": [I, P, P, P, P, P, P],
             "npc_poly_coefficients": [I, D, D, D, C.POINTER(D), C.POINTER(D), C.POINTER(D), P],
             "npc_context_set_timing": [P, I],
             "npc_context_create_local": [I, I, I, C.c_char_p, P, C.POINTER(P)],
@@ -403,6 +404,25 @@ def npc_halo_plan(rowptr, colidx, row_starts, rank: int):
     _check(lib().npc_halo_plan(n_local, prp, pci, nranks, prs, rank, C.byref(cap), ids.ctypes.data_as(C.c_void_p),
                                counts.ctypes.data_as(C.c_void_p)))
     return ids[: ng.value], counts
+
+
+PATTERN_INFO = ("pattern", "ring", "tiles", "ring_tiles", "max_copies", "stage_bytes", "ring_table_words",
+                "own_values")
+
+
+def npc_pattern_check(rowptr, colidx, vals, x):
+    """Host-only layout check of the CSR pattern form (include/npc.h): returns (y = A x evaluated
+    by replaying the ring layout on the host, info dict)."""
+    rp, prp = _host(rowptr, np.int32)
+    n = len(rp) - 1
+    ci, pci = _host(colidx if len(colidx) else np.zeros(1), np.int32)
+    va, pva = _host(vals if len(vals) else np.zeros(1), np.float64)
+    xx, pxx = _host(x, np.float64)
+    y = np.zeros(max(n, 1))
+    info = np.zeros(8, dtype=np.int64)
+    _check(lib().npc_pattern_check(n, prp, pci, pva, pxx, y.ctypes.data_as(C.c_void_p),
+                                   info.ctypes.data_as(C.c_void_p)))
+    return y[:n], dict(zip(PATTERN_INFO, (int(v) for v in info)))
 
 
 # ---------------------------------------------------------------- convenience (marshalling)

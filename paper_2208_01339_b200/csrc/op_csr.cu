@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(PAT_THREADS) k_csr_pat_stage(PatDev A, StepArg
 // NS = 1: one tile per CTA (grid = tiles), 3 CTAs per SM, each CTA's copies in flight while the
 // other CTAs compute.  NS > 1 (A/B, NPC_RING_NS): persistent CTAs walking tiles blockIdx.x +
 // i * gridDim.x through NS stages, the copies of tile i + NS issued as tile i's sums finish.
-static constexpr int RING_MAXD = 16;              // int4 copy descriptors per tile (header + copies)
+static constexpr int RING_MAXD = 32;              // int4 copy descriptors per tile (header + copies)
 static constexpr int RING_GAP_MAX = PAT_TILE;  // near earlier-tile mirrors held as a column gap
 static constexpr int RING_STAGE_MAX = 110 * 1024;  // bytes of one stage
 
@@ -483,7 +483,11 @@ struct RingDev {
 // x; part 2: the x windows (a tile with an odd x tail takes part 0 only: its tail store must
 // precede the arrive).
 __device__ __forceinline__ int4 ring_desc(const RingDev &A, int tile, int lane) {
-    return lane < RING_MAXD ? A.desc[(size_t)tile * RING_MAXD + lane] : make_int4(0, 0, 0, 0);
+    // lanes 0..15 always (the common case: <= 15 copies); 16..31 only for a tile with more
+    const int4 *p = A.desc + (size_t)tile * RING_MAXD;
+    int4 d = lane < 16 ? p[lane] : make_int4(0, 0, 0, 0);
+    if (__shfl_sync(0xffffffffu, d.x, 0) > 15 && lane >= 16) d = p[lane];
+    return d;
 }
 __device__ __forceinline__ void ring_issue_d(const int4 &d, const RingDev &A, const double *x, unsigned char *st,
                                              uint64_t *bar, int lane, uint64_t vals_policy, bool hint, int part) {
@@ -926,6 +930,7 @@ class CsrOperator : public Operator {
     int ring_ctas = 0;       // resident CTAs per SM of the persistent form (queried at the first launch)
     int ring_stage = 0, ring_tbl_bytes = 0;
     long long ring_tbl_ints = 0;  // stored (deduplicated) ring-table words
+    long long ring_desc_bytes = 0;  // descriptor bytes the kernels read per application
     // two degrees per pass (k_csr_pat_wave): per-tile x-window reach, epoch flags, ticket state
     DevBuf wdeps, wflags, wstate;
     int wave_lag = 0, ring_span = 0;
@@ -963,8 +968,7 @@ class CsrOperator : public Operator {
 
     double matrix_bytes() const override {
         if (pattern && ring)  // own values (incl. ELL padding), pattern ids, shared tables, copy descriptors
-            return (double)own_nnz * 8.0 + (double)n_local + (double)ring_tbl_ints * 4.0 +
-                   (double)pt_all.ns * RING_MAXD * 16.0;
+            return (double)own_nnz * 8.0 + (double)n_local + (double)ring_tbl_ints * 4.0 + (double)ring_desc_bytes;
         if (pattern)  // own values (incl. ELL padding), pattern ids, tables, tile pointers
             return (double)own_nnz * 8.0 + (double)n_local + (double)tbl_total * 4.0 + (double)(ntiles + 1) * 8.0;
         if (coded)  // values + codes, dictionaries + their offsets, tile pointers, 16-bit row offsets
@@ -1859,6 +1863,8 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
         op.ring_stage = ph.ring_stage;
         op.ring_tbl_bytes = ph.ring_tbl_bytes;
         op.ring_tbl_ints = (long long)ph.rtbl.size();
+        for (int t = 0; t < op.ntiles; ++t)
+            if (ph.stage[t]) op.ring_desc_bytes += ph.rdesc[(size_t)t * RING_MAXD * 4] > 15 ? 512 : 256;
         if (const char *e = getenv("NPC_RING_NS")) op.ring_ns = std::min(2, std::max(1, atoi(e)));
         if (const char *e = getenv("NPC_RING_RPT")) op.ring_rpt = atoi(e) == 4 ? 4 : 2;
         if ((size_t)op.ring_ns * op.ring_stage > 227 * 1024) op.ring_ns = 1;
@@ -2113,3 +2119,115 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
 }
 
 }  // namespace npc
+
+// ---------------------------------------------------------------- host-only layout check
+// npc_pattern_check (include/npc.h): the pattern form and ring layout of a single-rank CSR
+// matrix built exactly as npc_create_operator builds them, and y = A x evaluated ON THE HOST by
+// replaying every ring tile's copy descriptors into a stage buffer (pre-filled with NaN bytes,
+// so a sum that reads a byte no copy wrote is caught) and summing its rows from the entry table
+// in the kernel's order (fma chain).  Alignment, bounds and byte counts of every copy are
+// checked as the bulk-copy engine requires.  Tiles without a ring layout are summed from the
+// CSR arrays in stored order.  A test hook for the host logic; no GPU, no context.
+namespace npc {
+static npc_status pattern_check_impl(int n, const int *rowptr, const int *colidx, const double *vals, const double *x,
+                                     double *y, long long *info) {
+    NPC_TRY(validate_csr(n, n, rowptr, colidx, vals));
+    std::vector<int> lcols(colidx, colidx + rowptr[n]);
+    PatHost ph;
+    for (int k = 0; k < 8; ++k) info[k] = 0;
+    if (!build_pattern(n, 0, rowptr, colidx, lcols, vals, !getenv("NPC_CSR_NOMIRROR"), !getenv("NPC_CSR_NOSTAGE"), ph)) {
+        set_error("npc_pattern_check: the matrix does not take the pattern form");
+        return NPC_ERR_UNSUPPORTED;
+    }
+    const int ntiles = ceil_div(n, PAT_TILE);
+    info[0] = 1;
+    info[1] = ph.ring ? 1 : 0;
+    info[2] = ntiles;
+    info[5] = ph.ring_stage;
+    info[6] = (long long)ph.rtbl.size();
+    info[7] = ph.own_nnz;
+    auto fail = [&](const char *what, int t, int k) {
+        set_error("npc_pattern_check: tile %d copy %d: %s", t, k, what);
+        return NPC_ERR_INTERNAL;
+    };
+    std::vector<unsigned char> stage(ph.ring ? (size_t)ph.ring_stage : 0);
+    for (int t = 0; t < ntiles; ++t) {
+        const int r0 = t * PAT_TILE, nr = std::min(PAT_TILE, n - r0);
+        if (!(ph.ring && ph.stage[t])) {
+            for (int i = r0; i < r0 + nr; ++i) {
+                double s = 0.0;
+                for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) s = std::fma(vals[p], x[colidx[p]], s);
+                y[i] = s;
+            }
+            continue;
+        }
+        ++info[3];
+        std::fill(stage.begin(), stage.end(), (unsigned char)0xFF);  // NaN doubles
+        const int *dd = ph.rdesc.data() + (size_t)t * RING_MAXD * 4;
+        const int nc = dd[0];
+        info[4] = std::max<long long>(info[4], nc);
+        if (nc < 0 || nc > RING_MAXD - 1) return fail("copy count", t, 0);
+        long long total = 0;
+        for (int k = 1; k <= nc; ++k) {
+            const int kind = dd[4 * k], dst = dd[4 * k + 1], src = dd[4 * k + 2], bytes = dd[4 * k + 3];
+            if (kind == 4) {  // odd x tail: one double stored by a thread
+                if (dst % 8 || dst < 0 || dst + 8 > ph.ring_stage || src < 0 || src >= n) return fail("tail", t, k);
+                std::memcpy(&stage[dst], &x[src], 8);
+                continue;
+            }
+            if (dst % 16 || bytes % 16 || bytes <= 0 || dst < 0 || dst + bytes > ph.ring_stage)
+                return fail("destination alignment / bounds", t, k);
+            const unsigned char *s8 = nullptr;
+            long long sbyte = 0, slen = 0;
+            if (kind == 0) s8 = reinterpret_cast<const unsigned char *>(ph.vals.get()), sbyte = 8LL * src, slen = 8LL * (ph.own_nnz + 8);
+            else if (kind == 1) s8 = reinterpret_cast<const unsigned char *>(x), sbyte = 8LL * src, slen = 8LL * n;
+            else if (kind == 2) s8 = reinterpret_cast<const unsigned char *>(ph.rtbl.data()), sbyte = 4LL * src, slen = 4LL * (long long)ph.rtbl.size();
+            else if (kind == 3) s8 = ph.pat.data(), sbyte = src, slen = (long long)ph.pat.size() + 16;
+            else return fail("kind", t, k);
+            if (sbyte % 16 || sbyte < 0 || sbyte + bytes > slen) return fail("source alignment / bounds", t, k);
+            const long long avail = kind == 3 ? (long long)ph.pat.size() : slen;  // the id array is padded on the GPU
+            std::memcpy(&stage[dst], s8 + sbyte, (size_t)std::max<long long>(0, std::min<long long>(bytes, avail - sbyte)));
+            total += bytes;
+        }
+        if (total != dd[1]) return fail("header byte count", t, 0);
+        const int *st = reinterpret_cast<const int *>(stage.data());
+        const int ent = st[1], x0b = st[2];
+        const unsigned char *sp = stage.data() + ph.ring_tbl_bytes;
+        const unsigned char *Db = sp + PAT_TILE;
+        const long long dlen = (long long)ph.ring_stage - ph.ring_tbl_bytes - PAT_TILE;
+        auto ld = [&](long long off, double *v) {
+            if (off < 0 || off + 8 > dlen || off % 8) return false;
+            std::memcpy(v, Db + off, 8);
+            return true;
+        };
+        for (int lr = 0; lr < nr; ++lr) {
+            const int p = sp[lr];
+            if (p >= st[0]) return fail("pattern id", t, lr);
+            double s = 0.0, xv, vv;
+            for (int e = st[4 + p]; e < st[4 + p + 1]; ++e) {
+                const int ux = st[ent + 2 * e], uy = st[ent + 2 * e + 1];
+                if (!ld(ux + 8LL * lr, &xv) || !ld(uy + 8LL * lr, &vv)) return fail("entry offset", t, lr);
+                s = std::fma(vv, xv, s);
+            }
+            if (!ld(x0b + 8LL * lr, &xv) || std::memcmp(&xv, &x[r0 + lr], 8) != 0) return fail("x[row] window", t, lr);
+            y[r0 + lr] = s;
+        }
+    }
+    return NPC_SUCCESS;
+}
+}  // namespace npc
+
+extern "C" npc_status npc_pattern_check(int n, const int *rowptr, const int *colidx, const double *vals,
+                                        const double *x, double *y, long long *info) {
+    using namespace npc;
+    if (!(n >= 0 && rowptr && x && y && info && (rowptr[n] == 0 || (colidx && vals)))) {
+        set_error("npc_pattern_check: null argument");
+        return NPC_ERR_INVALID_ARGUMENT;
+    }
+    try {
+        return pattern_check_impl(n, rowptr, colidx, vals, x, y, info);
+    } catch (const std::bad_alloc &) {
+        set_error("npc_pattern_check: host out of memory");
+        return NPC_ERR_OUT_OF_MEMORY;
+    }
+}
