@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(PAT_THREADS) k_csr_pat_stage(PatDev A, StepArg
 // NS = 1: one tile per CTA (grid = tiles), 3 CTAs per SM, each CTA's copies in flight while the
 // other CTAs compute.  NS > 1 (A/B, NPC_RING_NS): persistent CTAs walking tiles blockIdx.x +
 // i * gridDim.x through NS stages, the copies of tile i + NS issued as tile i's sums finish.
-static constexpr int RING_MAXD = 32;              // int4 copy descriptors per tile (header + copies)
+static constexpr int RING_MAXD = 32;  // int4 copy descriptors per tile at most (header + copies)
 static constexpr int RING_GAP_MAX = PAT_TILE;  // near earlier-tile mirrors held as a column gap
 static constexpr int RING_STAGE_MAX = 110 * 1024;  // bytes of one stage
 
@@ -470,8 +470,9 @@ struct RingDev {
     const double *vals;          // own values (tile-ELL blocks, as PatDev::vals)
     const int *tbl;              // concatenated per-tile ring tables (16-byte aligned each)
     const unsigned char *pat;    // pattern id per row
-    const int4 *desc;            // RING_MAXD descriptors per tile: {ncopies, bytes} + {kind, dst, src, bytes}
+    const int4 *desc;            // dstride descriptors per tile: {ncopies, bytes} + {kind, dst, src, bytes}
     int n;
+    int dstride;                 // 16, or 32 when some tile needs more than 15 copies
 };
 
 #ifndef NPC_RING_WAIT_NS
@@ -482,11 +483,14 @@ struct RingDev {
 // copy each).  part 0: everything; part 1: the barrier's arrive and the copies that do not read
 // x; part 2: the x windows (a tile with an odd x tail takes part 0 only: its tail store must
 // precede the arrive).
+// WIDE = 0: stride 16 (every tile <= 15 copies); 1: stride 32; -1: the operator's A.dstride
+template <int WIDE = -1>
 __device__ __forceinline__ int4 ring_desc(const RingDev &A, int tile, int lane) {
+    if (WIDE == 0) return lane < 16 ? A.desc[(size_t)tile * 16 + lane] : make_int4(0, 0, 0, 0);
     // lanes 0..15 always (the common case: <= 15 copies); 16..31 only for a tile with more
-    const int4 *p = A.desc + (size_t)tile * RING_MAXD;
+    const int4 *p = A.desc + (size_t)tile * (WIDE == 1 ? 32 : A.dstride);
     int4 d = lane < 16 ? p[lane] : make_int4(0, 0, 0, 0);
-    if (__shfl_sync(0xffffffffu, d.x, 0) > 15 && lane >= 16) d = p[lane];
+    if (A.dstride > 16 && __shfl_sync(0xffffffffu, d.x, 0) > 15 && lane >= 16) d = p[lane];
     return d;
 }
 __device__ __forceinline__ void ring_issue_d(const int4 &d, const RingDev &A, const double *x, unsigned char *st,
@@ -511,9 +515,10 @@ __device__ __forceinline__ void ring_issue_d(const int4 &d, const RingDev &A, co
         }
     }
 }
+template <int WIDE = -1>
 __device__ __forceinline__ void ring_issue(const RingDev &A, const double *x, int tile, unsigned char *st, uint64_t *bar,
                                            int lane, uint64_t vals_policy, bool hint) {
-    ring_issue_d(ring_desc(A, tile, lane), A, x, st, bar, lane, vals_policy, hint, 0);
+    ring_issue_d(ring_desc<WIDE>(A, tile, lane), A, x, st, bar, lane, vals_policy, hint, 0);
 }
 
 // Per-row streams of a tile (s_{j-2}, r, the dot operand), loaded ahead into registers.
@@ -593,7 +598,7 @@ __device__ __forceinline__ void ring_tile(const StepArgs &s, const unsigned char
 
 // R rows per thread (lr = tid + q * PAT_TILE / R), summed in one interleaved loop when their
 // patterns have the same length.
-template <bool HAS_S2, bool HAS_R, bool DOT, int NS, int R>
+template <bool HAS_S2, bool HAS_R, bool DOT, int NS, int R, int WIDE = 0>
 __global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 1)
     k_csr_pat_ring(RingDev A, StepArgs s, const int *__restrict__ tiles, int ntl, int stage_bytes, int tbl_bytes) {
     constexpr int NT = PAT_TILE / R;  // threads
@@ -616,7 +621,8 @@ __global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 
     };
     if (issuer)
         for (int i = 0; i < NS && i < nmine; ++i)
-            ring_issue(A, s.x, tile_of(i), rg_smem + (size_t)(i % NS) * stage_bytes, &full[i % NS], lane, 0, false);
+            ring_issue<WIDE>(A, s.x, tile_of(i), rg_smem + (size_t)(i % NS) * stage_bytes, &full[i % NS], lane, 0,
+                             false);
     RingRows<R> cur;
     auto rows_of = [&](int i, RingRows<R> &q) {
         const int row0 = tile_of(i) * PAT_TILE;
@@ -636,7 +642,8 @@ __global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 
             if (i + NS < nmine) {
                 __syncthreads();  // every row of stage b summed: it can be refilled
                 if (issuer)
-                    ring_issue(A, s.x, tile_of(i + NS), rg_smem + (size_t)b * stage_bytes, &full[b], lane, 0, false);
+                    ring_issue<WIDE>(A, s.x, tile_of(i + NS), rg_smem + (size_t)b * stage_bytes, &full[b], lane, 0,
+                                     false);
             }
         }
     }
@@ -931,6 +938,7 @@ class CsrOperator : public Operator {
     int ring_stage = 0, ring_tbl_bytes = 0;
     long long ring_tbl_ints = 0;  // stored (deduplicated) ring-table words
     long long ring_desc_bytes = 0;  // descriptor bytes the kernels read per application
+    int ring_dstride = 16;
     // two degrees per pass (k_csr_pat_wave): per-tile x-window reach, epoch flags, ticket state
     DevBuf wdeps, wflags, wstate;
     int wave_lag = 0, ring_span = 0;
@@ -1018,6 +1026,7 @@ class CsrOperator : public Operator {
     npc_status prepare3() {
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_stage<H2, HR, DT>));
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 1, 2>));
+        NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 1, 2, 1>));
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 2, 2>));
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 1, 4>));
         NPC_TRY(allow_max_dynamic_smem(k_csr_pat_ring<H2, HR, DT, 2, 4>));
@@ -1052,12 +1061,12 @@ class CsrOperator : public Operator {
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
-    template <bool H2, bool HR, bool DT, int NS, int R>
+    template <bool H2, bool HR, bool DT, int NS, int R, int WIDE = 0>
     npc_status launch_ring_ns(const StepArgs &s, const int *tl, int nt, double *partials) {
-        RingDev A{vals.as<double>(), rtbl.as<int>(), pat.as<unsigned char>(), rdesc.as<int4>(), n_local};
+        RingDev A{vals.as<double>(), rtbl.as<int>(), pat.as<unsigned char>(), rdesc.as<int4>(), n_local, ring_dstride};
         StepArgs a = s;
         a.partials = partials;
-        auto kern = k_csr_pat_ring<H2, HR, DT, NS, R>;
+        auto kern = k_csr_pat_ring<H2, HR, DT, NS, R, WIDE>;
         const size_t sm = (size_t)NS * ring_stage;
         int grid = nt;
         if (NS > 1) {
@@ -1075,6 +1084,7 @@ class CsrOperator : public Operator {
     template <bool H2, bool HR, bool DT>
     npc_status launch_ring(const StepArgs &s, const int *tl, int nt, double *partials) {
         if (nt <= 0) return NPC_SUCCESS;
+        if (ring_dstride > 16) return launch_ring_ns<H2, HR, DT, 1, 2, 1>(s, tl, nt, partials);  // > 15 copies
         if (ring_rpt == 4)
             return ring_ns == 2 ? launch_ring_ns<H2, HR, DT, 2, 4>(s, tl, nt, partials)
                                 : launch_ring_ns<H2, HR, DT, 1, 4>(s, tl, nt, partials);
@@ -1152,7 +1162,7 @@ class CsrOperator : public Operator {
             t.s2 = s1.x;
             return step(t);
         }
-        RingDev A{vals.as<double>(), rtbl.as<int>(), pat.as<unsigned char>(), rdesc.as<int4>(), n_local};
+        RingDev A{vals.as<double>(), rtbl.as<int>(), pat.as<unsigned char>(), rdesc.as<int4>(), n_local, ring_dstride};
         if (wave_persist) {
             k_wave_begin<<<1, 1, 0, ctx->stream>>>(wstate.as<WaveState>());
             NPC_LAUNCH_CHECK();
@@ -1338,7 +1348,7 @@ struct PatHost {
     // ring kernel (k_csr_pat_ring): per-tile tables (16-byte aligned), RING_MAXD int4 copy
     // descriptors per tile, the stage size and its table region; ring = every staged tile has one
     std::vector<int> rtbl, rdesc, rdeps;
-    int ring_stage = 0, ring_tbl_bytes = 0, ring_span = 0;
+    int ring_stage = 0, ring_tbl_bytes = 0, ring_span = 0, ring_dstride = 16;
     bool ring = false;
 };
 
@@ -1789,7 +1799,10 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
                 ph.rtbl.assign((size_t)total_ints + 4, 0);
                 for (auto &kv : seen)
                     for (int u : kv.second) std::copy(rts[u].tbl.begin(), rts[u].tbl.end(), ph.rtbl.begin() + toff[u]);
-                ph.rdesc.assign((size_t)ntiles * RING_MAXD * 4, 0);
+                size_t most = 0;
+                for (int t = 0; t < ntiles; ++t) most = std::max(most, rts[t].cp.size());
+                ph.ring_dstride = most > 15 ? 32 : 16;
+                ph.rdesc.assign((size_t)ntiles * ph.ring_dstride * 4, 0);
                 ph.rdeps.assign((size_t)ntiles * 2, 0);
                 for (int t = 0; t < ntiles; ++t) {
                     ph.rdeps[2 * t] = std::min(rts[t].dep_lo, t);
@@ -1799,7 +1812,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
                 host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
                     for (long long t = t0; t < t1; ++t) {
                         if (!ph.stage[t]) continue;
-                        int *dd = ph.rdesc.data() + (size_t)t * RING_MAXD * 4;
+                        int *dd = ph.rdesc.data() + (size_t)t * ph.ring_dstride * 4;
                         long long total = 0;
                         for (size_t k = 0; k < rts[t].cp.size(); ++k) {
                             const RingCopy &c = rts[t].cp[k];
@@ -1863,8 +1876,9 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
         op.ring_stage = ph.ring_stage;
         op.ring_tbl_bytes = ph.ring_tbl_bytes;
         op.ring_tbl_ints = (long long)ph.rtbl.size();
+        op.ring_dstride = ph.ring_dstride;
         for (int t = 0; t < op.ntiles; ++t)
-            if (ph.stage[t]) op.ring_desc_bytes += ph.rdesc[(size_t)t * RING_MAXD * 4] > 15 ? 512 : 256;
+            if (ph.stage[t]) op.ring_desc_bytes += ph.rdesc[(size_t)t * ph.ring_dstride * 4] > 15 ? 512 : 256;
         if (const char *e = getenv("NPC_RING_NS")) op.ring_ns = std::min(2, std::max(1, atoi(e)));
         if (const char *e = getenv("NPC_RING_RPT")) op.ring_rpt = atoi(e) == 4 ? 4 : 2;
         if ((size_t)op.ring_ns * op.ring_stage > 227 * 1024) op.ring_ns = 1;
@@ -2163,7 +2177,7 @@ static npc_status pattern_check_impl(int n, const int *rowptr, const int *colidx
         }
         ++info[3];
         std::fill(stage.begin(), stage.end(), (unsigned char)0xFF);  // NaN doubles
-        const int *dd = ph.rdesc.data() + (size_t)t * RING_MAXD * 4;
+        const int *dd = ph.rdesc.data() + (size_t)t * ph.ring_dstride * 4;
         const int nc = dd[0];
         info[4] = std::max<long long>(info[4], nc);
         if (nc < 0 || nc > RING_MAXD - 1) return fail("copy count", t, 0);
