@@ -22,7 +22,8 @@ LIB_PATH = os.environ.get("NPC_LIB_PATH") or os.path.join(_HERE, "libnpc.so")  #
 NPC_OP_CSR, NPC_OP_SELL, NPC_OP_STENCIL, NPC_OP_SCHUR, NPC_OP_CALLBACK, NPC_OP_DFN = range(6)
 STATUS = {0: "NPC_SUCCESS", 1: "NPC_ERR_INVALID_ARGUMENT", 2: "NPC_ERR_DIMENSION",
           3: "NPC_ERR_DEGENERATE_INTERVAL", 4: "NPC_ERR_NOT_CONVERGED", 5: "NPC_ERR_BREAKDOWN",
-          6: "NPC_ERR_CUDA", 7: "NPC_ERR_NCCL", 8: "NPC_ERR_OUT_OF_MEMORY", 9: "NPC_ERR_UNSUPPORTED"}
+          6: "NPC_ERR_CUDA", 7: "NPC_ERR_NCCL", 8: "NPC_ERR_OUT_OF_MEMORY", 9: "NPC_ERR_UNSUPPORTED",
+          10: "NPC_ERR_INTERNAL"}
 KIND = {"csr": NPC_OP_CSR, "sell": NPC_OP_SELL, "stencil": NPC_OP_STENCIL, "schur": NPC_OP_SCHUR,
         "callback": NPC_OP_CALLBACK, "dfn": NPC_OP_DFN}
 
