@@ -19,6 +19,8 @@
 // summation order: bitwise the same result as the plain form (NPC_CSR_PLAIN=1).
 #include <unordered_map>
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <climits>
 #include <cstring>
 #include <thread>
@@ -1602,9 +1604,22 @@ static bool pattern_ring_table(int n, int t, const std::vector<int> &tptr, const
     return true;
 }
 
+// Phase wall times of operator creation on stderr (NPC_CREATE_TIMES=1; profiling only).
+struct CreateTimer {
+    bool on = getenv("NPC_CREATE_TIMES") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char *what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "npc create: %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 static bool build_pattern(int n, long long row_begin, const int *rowptr, const int *gcol, const std::vector<int> &lcols,
                           const double *vals, bool mirror, bool stage, PatHost &ph) {
     const long long nnz = rowptr[n];
+    CreateTimer tm;
     // 1. mirror partners: a_ij (j < i, owned) whose transpose a_ji exists with the
     //    bitwise-identical value (then a_ji is an upper entry of row j, hence always own)
     std::unique_ptr<int[]> partner_buf(new int[(size_t)std::max<long long>(nnz, 1)]);
@@ -1623,6 +1638,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
                         partner[p] = (int)(q - gcol);
                 }
         });
+    tm.mark("mirror partners");
     // 2. index of every own entry within its row's own list (mirror positions refer to it)
     std::unique_ptr<unsigned char[]> opos_buf(new unsigned char[(size_t)std::max<long long>(nnz, 1)]);
     unsigned char *opos = opos_buf.get();
@@ -1643,6 +1659,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
     });
     for (char c : bad)
         if (c) return false;
+    tm.mark("own positions");
     // 2b. a row with fewer own values than its tile's widest row streams ELL padding anyway: its
     //     mirrors of EARLIER tiles (farthest first) become own values in those slots -- the same
     //     bytes, one L2 read (or ring-kernel copy) less; bitwise the same values and order
@@ -1662,6 +1679,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
             }
         }, 64);
     }
+    tm.mark("padding fill");
     // 3. per tile: patterns (deduplicated by hash, then by words), ELL width, tables
     const int ntiles = ceil_div(n, PAT_TILE);
     std::vector<std::vector<int>> ttbl((size_t)ntiles);
@@ -1756,6 +1774,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
     }
     ph.tbl2.resize((size_t)ph.tbl2_off[ntiles]);
     for (int t = 0; t < ntiles; ++t) std::copy(ttbl2[t].begin(), ttbl2[t].end(), ph.tbl2.begin() + ph.tbl2_off[t]);
+    tm.mark("patterns + stage tables");
     // 4. ring-kernel tables: every staged tile gets one, or the operator keeps k_csr_pat_stage
     if (stage && !getenv("NPC_CSR_NORING")) {
         std::vector<RingTile> rts((size_t)ntiles);
@@ -1831,6 +1850,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
             }
         }
     }
+    tm.mark("ring tables");
     ph.vals.reset(new double[(size_t)ph.own_nnz + 8]);
     std::fill(ph.vals.get() + ph.own_nnz, ph.vals.get() + ph.own_nnz + 8, 0.0);
     host_parallel_for(ntiles, [&](long long t0, long long t1, int) {
@@ -1844,6 +1864,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
                     if (partner[p] < 0) blk[(size_t)opos[p] * nrs + (i - r0)] = vals[p];
         }
     }, 64);
+    tm.mark("tile-ELL values");
     return true;
 }
 
@@ -1968,6 +1989,7 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
 }
 
 npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::unique_ptr<Operator> &out) {
+    CreateTimer tm;
     NPC_TRY(validate_csr_desc(ctx, d));
     auto op = std::make_unique<CsrOperator>();
     op->ctx = ctx;
@@ -1981,12 +2003,15 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     std::vector<int> lcols;
     NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
     op->multi = ctx->distributed();
+    tm.mark("validate + localize");
     if (!getenv("NPC_CSR_PLAIN") && !getenv("NPC_CSR_CODED") && nnz > 0) {
         PatHost ph;
         if (build_pattern(n, d->row_begin, d->rowptr, d->colidx, lcols, d->vals, !getenv("NPC_CSR_NOMIRROR"),
                           !getenv("NPC_CSR_NOSTAGE"), ph)) {
             op->pattern = true;
+            tm.mark("build_pattern");
             NPC_TRY(finish_pattern_operator(ctx, d, *op, ph, lcols));
+            tm.mark("uploads + tile lists");
             out = std::move(op);
             return NPC_SUCCESS;
         }
