@@ -1435,6 +1435,9 @@ static std::vector<int> pattern_stage_table(int n, int row0, int nrows, int own_
 // table region's size is known.  Returns false when the tile needs more copies than a
 // descriptor holds or a mirror the layout cannot address (the operator then keeps
 // k_csr_pat_stage).
+#ifndef NPC_AB_NOZWIN
+#define NPC_AB_NOZWIN 0
+#endif
 struct RingCopy {
     int kind, region, dst, src, bytes;  // kind: 0 vals, 1 x, 2 table, 3 pattern ids, 4 x tail
 };
@@ -1542,7 +1545,7 @@ static bool pattern_ring_table(int n, int t, const std::vector<int> &tptr, const
     for (int p = 0; p < W; ++p)  // gaps: column p of the previous (full) tile's last G_p rows
         if (G[p]) rt.cp.push_back({0, 2, col[p] - G[p], tptr[t - 1] + p * T + (T - G[p]), G[p] * 8});
     for (size_t k = 0; k < fw.size(); ++k)  // far windows, one copy per source tile
-        for (long long c = fw[k].lo; c < fw[k].hi;) {
+        for (long long c = fw[k].lo; c < fw[k].hi && !NPC_AB_NOZWIN;) {
             const int tj = (int)(c / T);
             const long long ce = std::min<long long>(fw[k].hi, (long long)(tj + 1) * T);
             if (fw[k].pos < twidth[tj])
@@ -1552,6 +1555,8 @@ static bool pattern_ring_table(int n, int t, const std::vector<int> &tptr, const
         }
     rt.dep_lo = INT_MAX, rt.dep_hi = -1;
     for (auto &w : xw) {
+        // A/B only (results wrong): drop the x windows that do not contain the tile's own rows
+        if (NPC_AB_NOZWIN && (w.ga + w.len <= r0 || w.ga >= r0 + nr)) continue;
         if (w.len) rt.cp.push_back({1, 2, xbase + w.sb, w.ga, w.len * 8});
         if (w.tail) rt.cp.push_back({4, 2, xbase + w.sb + w.len, w.ga + w.len, 0});
         if (w.len + w.tail > 0) {
