@@ -528,9 +528,11 @@ template <int R>
 struct RingRows {
     double s2[R], r[R], v[R];
 };
+// dot_src (DOT): 0 = load dotv, 1 = dotv is the input x (taken from its staged window),
+// 2 = dotv is r (taken from the r stream): the dot operand then costs no extra stream
 template <bool HAS_S2, bool HAS_R, bool DOT, int R>
 __device__ __forceinline__ void ring_load_rows(const double *s2, const double *r, const double *dotv, int row0,
-                                               int nrows, RingRows<R> &q) {
+                                               int nrows, RingRows<R> &q, int dot_src = 0) {
     constexpr int NT = PAT_TILE / R;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -539,7 +541,7 @@ __device__ __forceinline__ void ring_load_rows(const double *s2, const double *r
         if (l < nrows) {
             if (HAS_S2) q.s2[k] = s2[row0 + l];
             if (HAS_R) q.r[k] = r[row0 + l];
-            if (DOT) q.v[k] = dotv[row0 + l];
+            if (DOT && dot_src == 0) q.v[k] = dotv[row0 + l];
         }
     }
 }
@@ -547,7 +549,7 @@ __device__ __forceinline__ void ring_load_rows(const double *s2, const double *r
 // The row sums and epilogue of one staged tile (every operand in shared memory).
 template <bool HAS_S2, bool HAS_R, bool DOT, int R>
 __device__ __forceinline__ void ring_tile(const StepArgs &s, const unsigned char *st8, int tbl_bytes, int row0,
-                                          int nrows, const RingRows<R> &cur, double &acc) {
+                                          int nrows, const RingRows<R> &cur, double &acc, int dot_src = 0) {
     constexpr int NT = PAT_TILE / R;
     const int *st = reinterpret_cast<const int *>(st8);
     const unsigned char *sp = st8 + tbl_bytes;
@@ -591,9 +593,10 @@ __device__ __forceinline__ void ring_tile(const StepArgs &s, const unsigned char
     for (int k = 0; k < R; ++k) {
         const int l = threadIdx.x + k * NT;
         if (l < nrows) {
-            const double o = degree_epilogue<HAS_S2, HAS_R>(s, y[k], ld(Dr[k], x0b), cur.s2[k], cur.r[k]);
+            const double xv = ld(Dr[k], x0b);
+            const double o = degree_epilogue<HAS_S2, HAS_R>(s, y[k], xv, cur.s2[k], cur.r[k]);
             s.out[row0 + l] = o;
-            if (DOT) acc = fma(o, cur.v[k], acc);
+            if (DOT) acc = fma(o, dot_src == 1 ? xv : dot_src == 2 ? cur.r[k] : cur.v[k], acc);
         }
     }
 }
@@ -626,9 +629,10 @@ __global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 
             ring_issue<WIDE>(A, s.x, tile_of(i), rg_smem + (size_t)(i % NS) * stage_bytes, &full[i % NS], lane, 0,
                              false);
     RingRows<R> cur;
+    const int dot_src = !DOT ? 0 : s.dotv == s.x ? 1 : (HAS_R && s.dotv == s.r) ? 2 : 0;
     auto rows_of = [&](int i, RingRows<R> &q) {
         const int row0 = tile_of(i) * PAT_TILE;
-        ring_load_rows<HAS_S2, HAS_R, DOT, R>(s.s2, s.r, s.dotv, row0, min(PAT_TILE, A.n - row0), q);
+        ring_load_rows<HAS_S2, HAS_R, DOT, R>(s.s2, s.r, s.dotv, row0, min(PAT_TILE, A.n - row0), q, dot_src);
     };
     if (nmine > 0) rows_of(0, cur);
     double acc = 0.0;
@@ -638,7 +642,8 @@ __global__ void __launch_bounds__(PAT_TILE / R, NS == 1 ? 1536 * 2 / PAT_TILE : 
         const int b = i % NS;
         const int row0 = tile_of(i) * PAT_TILE, nrows = min(PAT_TILE, A.n - row0);
         mbar_wait_sleep(&full[b], (uint32_t)((i / NS) & 1), NPC_RING_WAIT_NS);
-        ring_tile<HAS_S2, HAS_R, DOT, R>(s, rg_smem + (size_t)b * stage_bytes, tbl_bytes, row0, nrows, cur, acc);
+        ring_tile<HAS_S2, HAS_R, DOT, R>(s, rg_smem + (size_t)b * stage_bytes, tbl_bytes, row0, nrows, cur, acc,
+                                         dot_src);
         if (NS > 1) {
             cur = nxt;
             if (i + NS < nmine) {
