@@ -1626,50 +1626,47 @@ struct CreateTimer {
     }
 };
 
-static bool build_pattern(int n, long long row_begin, const int *rowptr, const int *gcol, const std::vector<int> &lcols,
+static bool build_pattern(int n, long long row_begin, const int *rowptr, const int *gcol, const int *lcols,
                           const double *vals, bool mirror, bool stage, PatHost &ph) {
     const long long nnz = rowptr[n];
     CreateTimer tm;
     // 1. mirror partners: a_ij (j < i, owned) whose transpose a_ji exists with the
-    //    bitwise-identical value (then a_ji is an upper entry of row j, hence always own)
+    //    bitwise-identical value (then a_ji is an upper entry of row j, hence always own);
+    // 2. (same pass, the row still in cache) the index of every own entry within its row's own
+    //    list -- mirror positions refer to it
     std::unique_ptr<int[]> partner_buf(new int[(size_t)std::max<long long>(nnz, 1)]);
     int *partner = partner_buf.get();
-    host_parallel_for(n, [&](long long b, long long e, int) {
-            for (long long i = b; i < e; ++i)
-                for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
-                    partner[p] = -1;
-                    if (!mirror) continue;
-                    const int c = lcols[p];
-                    if (c >= i || c < 0 || i - c >= PAT_MIRROR_MAX_OFF) continue;  // ghosts: c >= n > i
-                    const int *lo = gcol + rowptr[c], *hi = gcol + rowptr[c + 1];
-                    const int *q = std::lower_bound(lo, hi, (int)(row_begin + i));
-                    if (q != hi && *q == row_begin + i &&
-                        std::memcmp(&vals[q - gcol], &vals[p], sizeof(double)) == 0)
-                        partner[p] = (int)(q - gcol);
-                }
-        });
-    tm.mark("mirror partners");
-    // 2. index of every own entry within its row's own list (mirror positions refer to it)
     std::unique_ptr<unsigned char[]> opos_buf(new unsigned char[(size_t)std::max<long long>(nnz, 1)]);
     unsigned char *opos = opos_buf.get();
-    std::vector<int> rown((size_t)std::max(n, 1), 0);
+    std::unique_ptr<int[]> rown_buf(new int[(size_t)std::max(n, 1)]);
+    int *rown = rown_buf.get();
     std::vector<char> bad(64, 0);
     host_parallel_for(n, [&](long long b, long long e, int t) {
-        for (long long i = b; i < e; ++i) {
-            int k = 0;
-            for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
-                opos[p] = 0;
-                if (partner[p] < 0) {
-                    if (k > 255) bad[t] = 1;
-                    opos[p] = (unsigned char)k++;
+            for (long long i = b; i < e; ++i) {
+                int k = 0;
+                for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+                    int pp = -1;
+                    const int c = lcols[p];
+                    if (mirror && c < i && c >= 0 && i - c < PAT_MIRROR_MAX_OFF) {  // ghosts: c >= n > i
+                        const int *lo = gcol + rowptr[c], *hi = gcol + rowptr[c + 1];
+                        const int *q = std::lower_bound(lo, hi, (int)(row_begin + i));
+                        if (q != hi && *q == row_begin + i &&
+                            std::memcmp(&vals[q - gcol], &vals[p], sizeof(double)) == 0)
+                            pp = (int)(q - gcol);
+                    }
+                    partner[p] = pp;
+                    opos[p] = 0;
+                    if (pp < 0) {
+                        if (k > 255) bad[t] = 1;
+                        opos[p] = (unsigned char)k++;
+                    }
                 }
+                rown[i] = k;
             }
-            rown[i] = k;
-        }
-    });
+        });
     for (char c : bad)
         if (c) return false;
-    tm.mark("own positions");
+    tm.mark("partners + own positions");
     // 2b. a row with fewer own values than its tile's widest row streams ELL padding anyway: its
     //     mirrors of EARLIER tiles (farthest first) become own values in those slots -- the same
     //     bytes, one L2 read (or ring-kernel copy) less; bitwise the same values and order
@@ -1880,7 +1877,7 @@ static bool build_pattern(int n, long long row_begin, const int *rowptr, const i
 
 // Upload a pattern-form operator (PatHost from build_pattern) and build its tile lists.
 static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc *d, CsrOperator &op, PatHost &ph,
-                                          const std::vector<int> &lcols) {
+                                          const int *lcols) {
     const int n = d->n_local;
     op.ntiles = ceil_div(n, PAT_TILE);
     op.own_nnz = ph.own_nnz;
@@ -1971,7 +1968,7 @@ static npc_status finish_pattern_operator(Context *ctx, const npc_operator_desc 
         NPC_TRY(op.cols.alloc(sizeof(int) * (op.nnz + 8)));
         NPC_TRY(op.cvals.alloc(sizeof(double) * (op.nnz + 8)));
         NPC_CUDA_TRY(cudaMemcpy(op.rowptr.p, d->rowptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-        NPC_CUDA_TRY(cudaMemcpy(op.cols.p, lcols.data(), sizeof(int) * op.nnz, cudaMemcpyHostToDevice));
+        NPC_CUDA_TRY(cudaMemcpy(op.cols.p, lcols, sizeof(int) * op.nnz, cudaMemcpyHostToDevice));
         NPC_CUDA_TRY(cudaMemcpy(op.cvals.p, d->vals, sizeof(double) * op.nnz, cudaMemcpyHostToDevice));
     }
     const size_t nvals = (size_t)ph.own_nnz + 8;
@@ -2010,8 +2007,13 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     const int n = d->n_local;
     const long long nnz = d->rowptr[n];
     op->nnz = nnz;
-    std::vector<int> lcols;
-    NPC_TRY(localize_columns(ctx, d, op->plan, lcols));
+    // single rank: the caller's column ids are already local (no 4 B/nnz copy)
+    std::vector<int> lvec;
+    const int *lcols = d->colidx;
+    if (ctx->distributed()) {
+        NPC_TRY(localize_columns(ctx, d, op->plan, lvec));
+        lcols = lvec.data();
+    }
     op->multi = ctx->distributed();
     tm.mark("validate + localize");
     if (!getenv("NPC_CSR_PLAIN") && !getenv("NPC_CSR_CODED") && nnz > 0) {
@@ -2129,7 +2131,7 @@ npc_status make_csr_operator(Context *ctx, const npc_operator_desc *d, std::uniq
     NPC_TRY(op->cols.alloc(sizeof(int) * (ncols + 8)));
     NPC_CUDA_TRY(cudaMemcpy(op->rowptr.p, d->rowptr, sizeof(int) * nrp, cudaMemcpyHostToDevice));
     NPC_CUDA_TRY(cudaMemset(op->cols.as<int>() + ncols, 0, sizeof(int) * 8));
-    if (ncols) NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice));
+    if (ncols) NPC_CUDA_TRY(cudaMemcpy(op->cols.p, lcols, sizeof(int) * ncols, cudaMemcpyHostToDevice));
     if (coded) {
         std::vector<int> doff((size_t)op->ntiles + 1, 0), dall;
         for (int t = 0; t < op->ntiles; ++t) doff[t + 1] = doff[t] + (int)tdict[t].size();
@@ -2181,7 +2183,7 @@ namespace npc {
 static npc_status pattern_check_impl(int n, const int *rowptr, const int *colidx, const double *vals, const double *x,
                                      double *y, long long *info) {
     NPC_TRY(validate_csr(n, n, rowptr, colidx, vals));
-    std::vector<int> lcols(colidx, colidx + rowptr[n]);
+    const int *lcols = colidx;
     PatHost ph;
     for (int k = 0; k < 8; ++k) info[k] = 0;
     if (!build_pattern(n, 0, rowptr, colidx, lcols, vals, !getenv("NPC_CSR_NOMIRROR"), !getenv("NPC_CSR_NOSTAGE"), ph)) {
