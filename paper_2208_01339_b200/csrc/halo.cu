@@ -132,13 +132,14 @@ npc_status halo_setup(Context *ctx, const HaloPlan &plan, HaloRuntime &rt) {
 // interior kernels the caller enqueues next); halo_wait joins before the boundary kernels.
 // Both transports (NCCL, and the local thread group used for testing) run this same
 // choreography.
-npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const double *x) {
+npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const double *x, double *recv) {
     NvtxRange nv("npc:halo");
     NPC_TRY(ctx->tr->before_pack(ctx, ctx->stream));
     NPC_TRY(launch_gather(ctx, x, rt.send_idx.as<int>(), rt.send_buf.as<double>(), (int)plan.send_idx.size()));
     NPC_CUDA_TRY(cudaEventRecord(rt.packed, ctx->stream));
     NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, rt.packed, 0));
-    NPC_TRY(ctx->tr->exchange(ctx, rt.send_buf.as<double>(), plan.send_count, plan.send_off, rt.ghost_buf.as<double>(),
+    NPC_TRY(ctx->tr->exchange(ctx, rt.send_buf.as<double>(), plan.send_count, plan.send_off,
+                              recv ? recv : rt.ghost_buf.as<double>(),
                               plan.recv_count, plan.recv_off, ctx->comm_stream));
     NPC_CUDA_TRY(cudaEventRecord(rt.ready, ctx->comm_stream));
     return NPC_SUCCESS;

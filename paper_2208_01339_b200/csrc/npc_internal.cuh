@@ -395,7 +395,9 @@ struct HaloRuntime {
     ~HaloRuntime();
 };
 npc_status halo_setup(Context *ctx, const HaloPlan &plan, HaloRuntime &rt);
-npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const double *x);
+// recv: where the ghosts land (default rt.ghost_buf), e.g. the tail of a local+ghost vector.
+npc_status halo_start(Context *ctx, const HaloPlan &plan, HaloRuntime &rt, const double *x,
+                      double *recv = nullptr);
 npc_status halo_wait(Context *ctx, HaloRuntime &rt);
 
 // Raise a kernel's dynamic shared memory limit to the device maximum once (thread-safe).

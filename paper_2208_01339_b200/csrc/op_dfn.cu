@@ -32,8 +32,11 @@
 //     fused with the Chebyshev epilogue out = a_j y + b_j x + c_j s2 + d_j r (+ PCG partial).
 // Multi-rank: the paper's DSMat partition -- whole fracture blocks per rank,
 // u rows grouped by owning fracture (C is fracture-local, so Alg. 4 stays rank-local); per
-// application a u-space halo of x (B's E part, G^u) and an h-space halo of t and u2 (rows of
-// B^T held by other ranks' fractures, gathered once at setup).
+// application a u-space halo of x (B's E part, G^u) and an h-space halo of t (rows of B^T held
+// by other ranks' fractures, gathered once at setup; u2 needs none: C is fracture-local).
+// Both halos overlap block work: the fracture blocks are ordered [t sent, no x ghost | t sent,
+// x ghosts | t not sent], the first group runs while the x halo is in flight, the last while
+// the t halo is, and the ghosts land straight in the tails of xg and t.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -380,11 +383,14 @@ class DfnOperator : public Operator {
     DevBuf ainv, dense_info, band_list, perm;
     // multi-rank (the paper's DSMat partition): whole fracture blocks per
     // rank, u rows by owning fracture; per application a u-space halo of x (columns of B's E
-    // part and of G^u) and an h-space halo of t and u2 (rows of B^T from other ranks' fractures)
+    // part and of G^u) and an h-space halo of t (rows of B^T from other ranks' fractures)
     bool multi = false;
     int ngu = 0, ngh = 0;
     HaloPlan uplan, hplan;
-    HaloRuntime urt, trt, u2rt;
+    HaloRuntime urt, trt;
+    // block groups in the dense / band lists: [0, cut[0]) t rows sent, no x ghost; [cut[0],
+    // cut[1]) t rows sent, x ghosts read; [cut[1], n) no t row sent (single rank: all group 0)
+    int dense_cut[2] = {0, 0}, band_cut[2] = {0, 0};
     DevBuf xg;  // x of the owned u rows followed by the u ghosts
     bool permuted() const override { return !multi; }
     npc_status to_internal(const double *in, double *out) override {
@@ -412,7 +418,7 @@ class DfnOperator : public Operator {
         return b;
     }
     template <int G>
-    npc_status launch_block(const double *x, const int *done) {
+    npc_status launch_block(const double *x, const int *done, int b0, int b1) {
         DfnDev D{hblk.as<int>(), bw.as<int>(), loff.as<long long>(), L.as<double>(), crp.as<int>(), cci.as<int>(),
                  cv.as<double>(), brp.as<int>(), bci.as<int>(), bv.as<double>(), ghrp.as<int>(), ghci.as<int>(),
                  ghv.as<double>(), nblk, alpha};
@@ -420,19 +426,22 @@ class DfnOperator : public Operator {
         const size_t sm = sizeof(double) * 3 * (size_t)band_max_nf * groups_per_cta;
         auto kern = k_dfn_block<G>;
         if (sm > 48 * 1024) NPC_TRY(allow_max_dynamic_smem(kern));
-        kern<<<ceil_div(n_band, groups_per_cta), threads, sm, ctx->stream>>>(D, band_list.as<int>(), n_band, x,
+        if (b1 <= b0) return NPC_SUCCESS;
+        kern<<<ceil_div(b1 - b0, groups_per_cta), threads, sm, ctx->stream>>>(D, band_list.as<int>() + b0, b1 - b0, x,
                                                                            t.as<double>(), u2.as<double>(),
                                                                            band_max_nf, done);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
     template <int NT>
-    npc_status launch_dense(const double *x, const int *done) {
+    npc_status launch_dense(const double *x, const int *done, int b0, int b1) {
         DfnDev D{hblk.as<int>(), bw.as<int>(), loff.as<long long>(), L.as<double>(), crp.as<int>(), cci.as<int>(),
                  cv.as<double>(), brp.as<int>(), bci.as<int>(), bv.as<double>(), ghrp.as<int>(), ghci.as<int>(),
                  ghv.as<double>(), nblk, alpha};
-        k_dfn_dense<NT><<<ceil_div(n_dense, DFN_WARPS), 32 * DFN_WARPS, 0, ctx->stream>>>(D, dense_info.as<int4>(),
-                                                                                        n_dense,
+        if (b1 <= b0) return NPC_SUCCESS;
+        k_dfn_dense<NT><<<ceil_div(b1 - b0, DFN_WARPS), 32 * DFN_WARPS, 0, ctx->stream>>>(D,
+                                                                                        dense_info.as<int4>() + 2 * b0,
+                                                                                        b1 - b0,
                                                                        ainv.as<double>(), x, t.as<double>(),
                                                                        u2.as<double>(), done);
         NPC_LAUNCH_CHECK();
@@ -447,40 +456,37 @@ class DfnOperator : public Operator {
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
-    // ghosts of a halo -> the tail of a local+ghost buffer
-    npc_status halo_into(const HaloPlan &plan, HaloRuntime &rt, const double *src, double *full, int nown) {
-        NPC_TRY(halo_start(ctx, plan, rt, src));
-        NPC_TRY(halo_wait(ctx, rt));
-        if (plan.n_ghost)
-            NPC_CUDA_TRY(cudaMemcpyAsync(full + nown, rt.ghost_buf.p, sizeof(double) * plan.n_ghost,
-                                         cudaMemcpyDeviceToDevice, ctx->stream));
+    // the dense blocks at list positions [g0, g1) and the band blocks at [b0, b1)
+    npc_status launch_blocks(const double *xin, const int *done, int g0, int g1, int b0, int b1) {
+        if (dense_nt == 32) NPC_TRY(launch_dense<1>(xin, done, g0, g1));
+        else if (dense_nt == 64) NPC_TRY(launch_dense<2>(xin, done, g0, g1));
+        else NPC_TRY(launch_dense<4>(xin, done, g0, g1));
+        if (lanes == 4) NPC_TRY(launch_block<4>(xin, done, b0, b1));
+        else if (lanes == 8) NPC_TRY(launch_block<8>(xin, done, b0, b1));
+        else if (lanes == 16) NPC_TRY(launch_block<16>(xin, done, b0, b1));
+        else NPC_TRY(launch_block<32>(xin, done, b0, b1));
         return NPC_SUCCESS;
     }
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
-        const double *xin = s.x;
         const bool halo = multi && ctx->nranks > 1;  // a 1-rank distributed context has no ghosts
-        if (halo) {
+        if (!halo) {
+            NPC_TRY(launch_blocks(s.x, s.done, 0, n_dense, 0, n_band));
+        } else {
+            // x | x ghosts in xg: the ghosts arrive while the blocks that read no x ghost (and
+            // send t rows) run; then the t halo overlaps the blocks whose t stays on this rank.
+            // Receive buffers are safe to overwrite: their readers precede the pack on ctx->stream.
+            double *xg_ = xg.as<double>(), *t_ = t.as<double>();
             if (n_local)
-                NPC_CUDA_TRY(cudaMemcpyAsync(xg.p, s.x, sizeof(double) * n_local, cudaMemcpyDeviceToDevice,
+                NPC_CUDA_TRY(cudaMemcpyAsync(xg_, s.x, sizeof(double) * n_local, cudaMemcpyDeviceToDevice,
                                              ctx->stream));
-            NPC_TRY(halo_into(uplan, urt, s.x, xg.as<double>(), n_local));
-            xin = xg.as<double>();
-        }
-        if (n_dense > 0) {  // rows per lane
-            if (dense_nt == 32) NPC_TRY(launch_dense<1>(xin, s.done));
-            else if (dense_nt == 64) NPC_TRY(launch_dense<2>(xin, s.done));
-            else NPC_TRY(launch_dense<4>(xin, s.done));
-        }
-        if (n_band > 0) {
-            if (lanes == 4) NPC_TRY(launch_block<4>(xin, s.done));
-            else if (lanes == 8) NPC_TRY(launch_block<8>(xin, s.done));
-            else if (lanes == 16) NPC_TRY(launch_block<16>(xin, s.done));
-            else NPC_TRY(launch_block<32>(xin, s.done));
-        }
-        if (halo) {
-            NPC_TRY(halo_into(hplan, trt, t.as<double>(), t.as<double>(), nh));
-            NPC_TRY(halo_into(hplan, u2rt, u2.as<double>(), u2.as<double>(), nh));
+            NPC_TRY(halo_start(ctx, uplan, urt, s.x, xg_ + n_local));
+            NPC_TRY(launch_blocks(xg_, s.done, 0, dense_cut[0], 0, band_cut[0]));
+            NPC_TRY(halo_wait(ctx, urt));
+            NPC_TRY(launch_blocks(xg_, s.done, dense_cut[0], dense_cut[1], band_cut[0], band_cut[1]));
+            NPC_TRY(halo_start(ctx, hplan, trt, t_, t_ + nh));
+            NPC_TRY(launch_blocks(xg_, s.done, dense_cut[1], n_dense, band_cut[1], n_band));
+            NPC_TRY(halo_wait(ctx, trt));
             // a rank without rows writes zero dot partials (num_partials() >= 1 of them are read)
             if (n_local == 0) return s.dotv ? launch_fill(ctx, s.partials, 0.0, num_partials()) : NPC_SUCCESS;
         }
@@ -863,7 +869,6 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d0, std::uni
             BsT.v.push_back(0.0);
         }
         NPC_TRY(halo_setup(ctx, op->hplan, op->trt));
-        NPC_TRY(halo_setup(ctx, op->hplan, op->u2rt));
         NPC_TRY(op->xg.alloc(sizeof(double) * std::max(nu + ngu, 1)));
     }
     op->nnz_c = d->c_rowptr[nh];
@@ -888,6 +893,33 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d0, std::uni
             op->band_max_nf = std::max(op->band_max_nf, m);
             band_max_bw = std::max(band_max_bw, bwv[f]);
         }
+    }
+    if (multi) {  // group order (see dense_cut): a stable partition of each list
+        std::vector<char> snd_h(std::max(nh, 1), 0);
+        for (int h : op->hplan.send_idx) snd_h[h] = 1;
+        auto group = [&](int f) {
+            bool snd = false, ng = false;
+            for (int h = hb[f]; h < hb[f + 1]; ++h) {
+                snd = snd || snd_h[h];
+                for (int p = brp[h]; p < brp[h + 1] && !ng; ++p) ng = bci_i[p] >= nu;
+            }
+            return snd ? (ng ? 1 : 0) : 2;
+        };
+        auto partition = [&](std::vector<int> &lst, int *cut) {
+            std::vector<int> g(lst.size()), o;
+            for (size_t q = 0; q < lst.size(); ++q) g[q] = group(lst[q]);
+            for (int k = 0; k < 3; ++k) {
+                for (size_t q = 0; q < lst.size(); ++q)
+                    if (g[q] == k) o.push_back(lst[q]);
+                if (k < 2) cut[k] = (int)o.size();
+            }
+            lst.swap(o);
+        };
+        partition(dlist, op->dense_cut);
+        partition(blist, op->band_cut);
+    } else {
+        op->dense_cut[0] = op->dense_cut[1] = (int)dlist.size();
+        op->band_cut[0] = op->band_cut[1] = (int)blist.size();
     }
     std::vector<double> ainvh((size_t)std::max(dtot, 1LL), 0.0);
     {
@@ -978,7 +1010,7 @@ npc_status make_dfn_operator(Context *ctx, const npc_operator_desc *d0, std::uni
     NPC_TRY(upload(op->dense_info, dinfo.data(), dinfo.size()));
     NPC_TRY(upload(op->band_list, blist.data(), blist.size()));
     NPC_TRY(op->t.alloc(sizeof(double) * std::max(nh + op->ngh, 1)));   // owned h rows + h ghosts
-    NPC_TRY(op->u2.alloc(sizeof(double) * std::max(nh + op->ngh, 1)));
+    NPC_TRY(op->u2.alloc(sizeof(double) * std::max(nh, 1)));  // read by C^T only: fracture-local
     out = std::move(op);
     return NPC_SUCCESS;
 }
