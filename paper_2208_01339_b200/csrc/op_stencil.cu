@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <map>
 
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -17,6 +18,8 @@
 #include "npc_internal.cuh"
 
 namespace npc {
+
+namespace cg = cooperative_groups;
 
 static constexpr int ST_BX = 32, ST_BY = 8, ST_ZC = 8;
 
@@ -87,6 +90,88 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
     if (DOT) {
         acc = block_sum<ST_BX * ST_BY>(acc, red);
         if (threadIdx.x == 0 && threadIdx.y == 0) s.partials[linear_bid()] = acc;
+    }
+}
+
+// ---------------------------------------------------------------- all k degrees in one launch
+// For grids whose vectors sit in L2 (config 2: 4 x 16.8 MB), a degree takes ~10 us and kernel
+// boundaries (launch gap, ramp-up, tail) are a large part of it.  This cooperative kernel runs
+// every degree of p_k(A) r with a grid-wide barrier between degrees instead of a kernel
+// boundary: each CTA takes (x, y, z-chunk) items of k_stencil_step's decomposition and marches
+// them with the same arithmetic (same neighbour order, same explicit FMAs), so s_k is bitwise
+// equal to k launches of k_stencil_step.  s_j is written over s_{j-2} (the same element, read
+// first by the same thread); the barrier after degree j makes s_j visible before any CTA
+// gathers it and frees s_{j-1} for s_{j+1}.  Coefficients as the per-degree path
+// (solvers.cu: j = 1 folds s_0 = r / theta_bar, j = 2 its c_2 s_0 term).  The <r_or_dotv, z>
+// partial of the last degree goes to partials[blockIdx.x] (nparts = grid).
+#ifndef NPC_GRID_MINB
+#define NPC_GRID_MINB 4  // A/B (config 2): 4 CTAs per SM (62 registers, no spill); 6 or 8 spill and run 1.8x slower
+#endif
+template <int DIM>
+__global__ void __launch_bounds__(ST_BX *ST_BY, NPC_GRID_MINB) k_stencil_poly_grid(StencilDev S, const double *__restrict__ r,
+                                                                    double *z, double *tmp,
+                                                                    const double *__restrict__ coef, int k, double tb,
+                                                                    int zc, const double *__restrict__ dotv,
+                                                                    double *partials, const int *done) {
+    if (done && *done) return;  // uniform over the grid (no kernel writes the flag meanwhile)
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[ST_BX * ST_BY / 32];
+    const int gx = (S.nx + ST_BX - 1) / ST_BX, gy = (S.ny + ST_BY - 1) / ST_BY;
+    const int gz = DIM == 3 ? (S.nzl + zc - 1) / zc : 1;
+    const int items = gx * gy * gz;
+    const long long plane = (long long)S.nx * S.ny;
+    double acc = 0.0;
+    for (int j = 1; j <= k; ++j) {
+        const double *cf = coef + 4 * (j - 1);
+        double a, b, c = 0.0, d = 0.0;
+        double *out = ((k - j) & 1) ? tmp : z;  // s_k lands in z
+        const double *X = j == 1 ? r : (((k - j + 1) & 1) ? tmp : z);
+        if (j == 1) {
+            a = cf[0] / tb;
+            b = cf[1] / tb + cf[3];
+        } else if (j == 2) {
+            a = cf[0];
+            b = cf[1];
+            d = cf[2] / tb + cf[3];
+        } else {
+            a = cf[0];
+            b = cf[1];
+            c = cf[2];
+            d = cf[3];
+        }
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            const int bx = it % gx, by = (it / gx) % gy, bz = it / (gx * gy);
+            const int x = bx * ST_BX + threadIdx.x, y = by * ST_BY + threadIdx.y;
+            const int z0 = DIM == 3 ? bz * zc : 0, z1 = DIM == 3 ? min(z0 + zc, S.nzl) : 1;
+            if (x >= S.nx || y >= S.ny) continue;
+            const int pidx = x + S.nx * y;
+            long long i = pidx + plane * z0;
+            double below = 0.0, cur = X[i];
+            if (DIM == 3 && z0 > 0) below = X[i - plane];
+            for (int zz = z0; zz < z1; ++zz, i += plane) {
+                double above = 0.0;
+                if (DIM == 3 && zz + 1 < S.nzl) above = X[i + plane];
+                double nb = below;
+                if (y > 0) nb += X[i - S.nx];
+                if (x > 0) nb += X[i - 1];
+                if (x < S.nx - 1) nb += X[i + 1];
+                if (y < S.ny - 1) nb += X[i + S.nx];
+                nb += above;
+                const double ax = st_ax(S.diag, cur, S.off, nb);
+                double o = st_lin(a, ax, b, cur);
+                if (j >= 3) o = __fma_rn(c, out[i], o);
+                if (j >= 2) o = __fma_rn(d, r[i], o);
+                out[i] = o;
+                if (j == k && dotv) acc += o * dotv[i];
+                below = cur;
+                cur = above;
+            }
+        }
+        if (j < k) grid.sync();
+    }
+    if (dotv) {
+        acc = block_sum<ST_BX * ST_BY>(acc, red);
+        if (threadIdx.x == 0 && threadIdx.y == 0) partials[blockIdx.x] = acc;
     }
 }
 
@@ -559,6 +644,9 @@ class StencilOperator : public Operator {
     bool tma = false;
     int tma_blocks = 0, tma_zc = 0, tma_items = 0;
     bool tma2 = false;  // k_stencil_tma2 for the paired degrees (step2)
+    // k_stencil_poly_grid: single rank, vectors L2-resident; co-resident grid size (0 = off)
+    int grid_blocks = 0, grid_zc = 1;
+    DevBuf poly_tmp;  // its scratch vector (s_{k-1}, s_{k-3}, ...), allocated at create
     int tma2_blocks = 0, tma2_zc = 0, tma2_items = 0;
     std::map<std::pair<const void *, int>, CUtensorMap> tmaps;
 
@@ -754,6 +842,33 @@ class StencilOperator : public Operator {
         return NPC_SUCCESS;
     }
 
+    bool supports_fused_poly() const override { return grid_blocks > 0 && !getenv("NPC_NO_GRID_POLY"); }
+    npc_status apply_poly_fused(const double *r, double *z, const double *coef_dev, int k, double tb,
+                                const double *dotv, double *partials, int *nparts, const int *done) override {
+        double *tmp = poly_tmp.as<double>();  // z holds s_k, s_{k-2}, ...
+        StencilDev S{nx, ny, nzl, diag, off, nullptr, nullptr};
+        const int zc = grid_zc;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid_blocks, 1, 1);
+        cfg.blockDim = dim3(ST_BX, ST_BY, 1);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (dim == 3)
+            NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_poly_grid<3>, S, r, z, tmp, coef_dev, k, tb, zc, dotv,
+                                            partials, done));
+        else
+            NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_poly_grid<2>, S, r, z, tmp, coef_dev, k, tb, zc, dotv,
+                                            partials, done));
+        NPC_LAUNCH_CHECK();
+        if (dotv && nparts) *nparts = grid_blocks;
+        return NPC_SUCCESS;
+    }
+
     npc_status step(const StepArgs &s) override {
         if (n_local == 0 && !multi) return NPC_SUCCESS;
         if (!multi) {
@@ -854,6 +969,28 @@ npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::
             op->tma2_items = tiles2 * ceil_div(op->nzl, op->tma2_zc);
             op->tma2_blocks = std::min(op->tma2_items, bmax2);
         }
+    }
+    // all degrees in one cooperative launch when the vectors are L2-resident (single rank):
+    // grid = min(items, co-resident CTAs)
+    if (!ctx->distributed() && !big && !op->tma && op->n_local > 0 && !getenv("NPC_NO_GRID_POLY")) {
+        int per_sm = 0, coop = 0;
+        if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device) == cudaSuccess && coop &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, op->dim == 3 ? k_stencil_poly_grid<3> : k_stencil_poly_grid<2>, ST_BX * ST_BY, 0) ==
+                cudaSuccess &&
+            per_sm > 0) {
+            // z-chunks sized so that every (x, y, z-chunk) item has its own co-resident CTA (one
+            // round per degree, no tail): chunks = co-resident CTAs / (x, y) tiles
+            const long long tiles = (long long)ceil_div(op->nx, ST_BX) * ceil_div(op->ny, ST_BY);
+            const long long cap = (long long)per_sm * ctx->num_sms;
+            const long long chunks = std::max(1LL, std::min<long long>(op->nzl, cap / std::max(tiles, 1LL)));
+            op->grid_zc = op->dim == 3 ? (int)ceil_div((long long)op->nzl, chunks) : 1;
+            if (const char *e = getenv("NPC_GRID_ZC")) op->grid_zc = std::max(1, atoi(e));
+            const long long items = tiles * (op->dim == 3 ? ceil_div(op->nzl, op->grid_zc) : 1);
+            op->grid_blocks = (int)std::min<long long>(items, cap);
+            NPC_TRY(op->poly_tmp.alloc(sizeof(double) * (size_t)op->n_local));
+        }
+        cudaGetLastError();
     }
     if (ctx->distributed()) {
         if (op->dim != 3) {
