@@ -842,7 +842,17 @@ class StencilOperator : public Operator {
         return NPC_SUCCESS;
     }
 
-    bool supports_fused_poly() const override { return grid_blocks > 0 && !getenv("NPC_NO_GRID_POLY"); }
+    // Eager calls only: while the PCG captures its CUDA graph the per-degree kernels are taken.
+    // Measured on config 2 (profiles/r02_stencil_grid_ab.md): eagerly, k launches pay ~1 us of
+    // launch gap each and the one cooperative launch is 9 % faster per p_30; inside a graph the
+    // kernel nodes follow each other as closely as the grid barriers do, and the per-degree
+    // kernel's 8 CTAs/SM beat the grid kernel's 4 (PCG solve 8.87 vs 9.12 ms).
+    bool supports_fused_poly() const override {
+        if (grid_blocks <= 0 || getenv("NPC_NO_GRID_POLY")) return false;
+        if (getenv("NPC_GRID_IN_GRAPH")) return true;  // A/B
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        return cudaStreamIsCapturing(ctx->stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+    }
     npc_status apply_poly_fused(const double *r, double *z, const double *coef_dev, int k, double tb,
                                 const double *dotv, double *partials, int *nparts, const int *done) override {
         double *tmp = poly_tmp.as<double>();  // z holds s_k, s_{k-2}, ...

@@ -89,10 +89,13 @@ def test_grid_poly_bitwise_equals_per_degree_and_oracle(ctx, name):
                 assert np.linalg.norm(zg.cpu().numpy() - refz) <= 1e-10 * np.linalg.norm(refz), (k, xi)
 
 
-@pytest.mark.parametrize("name,k", [("c2_24", 10), ("c2_64", 30), ("2d_64x23", 10), ("box_67x33x17", 7)])
+@pytest.mark.parametrize("name,k", [("c2_24", 10), ("c2_64", 30), ("2d_64x23", 10), ("box_67x33x17", 7),
+                                    ("c2_64", 40)])  # k >= 32: first iteration eager (grid kernel), then the graph
 def test_grid_poly_pcg_parity(ctx, name, k):
     """PCG with the fused-poly kernel (gamma partial from its last degree) against the oracle's
-    textbook PCG (+-2 iterations, true residual <= tol) and the per-degree path."""
+    textbook PCG (+-2 iterations, true residual <= tol) and the per-degree path.  By default
+    the PCG's captured graph takes the per-degree kernels (faster there); NPC_GRID_IN_GRAPH=1
+    puts the cooperative kernel into the graph, which must work and agree."""
     w = CASES[name]()
     n = w["n"]
     orc = oracle.Operator(w)
@@ -104,7 +107,11 @@ def test_grid_poly_pcg_parity(ctx, name, k):
         lo, hi = npc.npc_estimate_spectrum(op, 20, None)
         x = torch.zeros(n, dtype=torch.float64, device="cuda")
         if grid:
-            st = npc.npc_pcg_solve(npc.npc_set_poly(op, k, lo, hi, 0.0), op, dev(w["b"]), x, w["tol"], 5000)
+            os.environ["NPC_GRID_IN_GRAPH"] = "1"
+            try:
+                st = npc.npc_pcg_solve(npc.npc_set_poly(op, k, lo, hi, 0.0), op, dev(w["b"]), x, w["tol"], 5000)
+            finally:
+                os.environ.pop("NPC_GRID_IN_GRAPH", None)
         else:
             with per_degree():
                 st = npc.npc_pcg_solve(npc.npc_set_poly(op, k, lo, hi, 0.0), op, dev(w["b"]), x, w["tol"], 5000)
