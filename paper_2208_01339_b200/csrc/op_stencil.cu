@@ -730,7 +730,7 @@ class StencilOperator : public Operator {
         return n;
     }
     int num_partials() const override {
-        if (!multi) return std::max(blocks_for(nzl, zc_main), tma ? tma_blocks : 0);
+        if (!multi) return std::max(std::max(blocks_for(nzl, zc_main), tma ? tma_blocks : 0), grid_blocks);
         Seg sg[3];
         const int ns = segments(sg);
         int tot = 0;
