@@ -77,6 +77,18 @@ NPC_API npc_status npc_context_create(int device, int nranks, int rank, const vo
 NPC_API npc_status npc_context_create_local(int device, int nranks, int rank, const char *group,
                                     void *cuda_stream, npc_context *out);
 NPC_API npc_status npc_context_destroy(npc_context ctx);
+/* Global reductions of npc_pcg_solve on a DISTRIBUTED context (no effect otherwise), SURVEY
+ * §8(a) a5/a6; the paper's point is that the preconditioner itself needs none
+ * (PAPER.md:18-20, 1234-1237).
+ *   0 (default): one allreduce of {gamma, delta} on the critical path and a second, 1-scalar
+ *      allreduce of ||r_{i+1}||^2 on a side stream that overlaps the next p_k(A) r; the exit
+ *      is seen about one allreduce latency into that application (stats.reductions = 2/iter).
+ *   1: ONE allreduce of {gamma, delta, ||r_i||^2} per iteration (the north star's form); the
+ *      exit is seen only after u = p_k(A) r and w = A u of the next iteration exist, so each
+ *      solve computes one extra (k+1)-application block, counted in stats.op_applications
+ *      ((iters+1)(k+1)); same iterates and iteration count as form 0.
+ * NPC_PCG_FUSED_ALLREDUCE=1 in the environment sets the default of new distributed contexts. */
+NPC_API npc_status npc_context_set_fused_allreduce(npc_context ctx, int enable);
 NPC_API npc_status npc_get_unique_id(void *out128);
 /* Message of the last failing call on ctx (ctx != NULL) or on the calling thread (NULL);
  * "" if none.  The pointer stays valid until the next failing call on the same context /

@@ -96,6 +96,7 @@ def lib():
             "npc_pattern_check": [I, P, P, P, P, P, P],
             "npc_poly_coefficients": [I, D, D, D, C.POINTER(D), C.POINTER(D), C.POINTER(D), P],
             "npc_context_set_timing": [P, I],
+            "npc_context_set_fused_allreduce": [P, I],
             "npc_context_create_local": [I, I, I, C.c_char_p, P, C.POINTER(P)],
             "npc_context_get_timing": [P, P, P],
             "npc_poly_set_lowrank": [P, I, P],
@@ -207,6 +208,11 @@ TIMING_CLASSES = ("degree", "operator", "update", "reduce", "vector")
 
 def npc_context_set_timing(ctx: Context, enable: bool = True):
     _check(lib().npc_context_set_timing(ctx.h, int(bool(enable))))
+
+
+def npc_context_set_fused_allreduce(ctx: Context, enable: bool = True):
+    """PCG on a distributed context: one {gamma, delta, ||r||^2} allreduce per iteration."""
+    _check(lib().npc_context_set_fused_allreduce(ctx.h, int(bool(enable))))
 
 
 def npc_context_get_timing(ctx: Context) -> dict:

@@ -112,6 +112,8 @@ static npc_status context_create(int device, int nranks, int rank, const void *n
             NPC_TRY(make_local_transport(&c, local_group, c.tr));
         else
             NPC_TRY(make_nccl_transport(&c, nccl_unique_id, c.tr));
+        const char *e = getenv("NPC_PCG_FUSED_ALLREDUCE");
+        c.fused_allreduce = e && atoi(e) != 0;
     }
     NPC_TRY(c.ensure_partials(4096));
     *out = h.release();
@@ -137,6 +139,13 @@ npc_status npc_context_set_timing(npc_context ctx, int enable) {
     NPC_GUARD(ctx, NPC_ERR_INVALID_ARGUMENT, "npc_context_set_timing: null context");
     ErrScope es(ctx);
     ctx->ctx.timing = enable != 0;
+    return NPC_SUCCESS;
+}
+
+npc_status npc_context_set_fused_allreduce(npc_context ctx, int enable) {
+    NPC_GUARD(ctx, NPC_ERR_INVALID_ARGUMENT, "npc_context_set_fused_allreduce: null context");
+    ErrScope es(ctx);
+    ctx->ctx.fused_allreduce = enable != 0;
     return NPC_SUCCESS;
 }
 

@@ -267,6 +267,10 @@ struct Context {
         cudaEvent_t e0, e1;
         int count;  // launches (degree applications) the interval covers
     };
+    // PCG on a distributed context: false (default) = {gamma, delta} on the critical path +
+    // ||r||^2 on the side stream; true = ONE allreduce of {gamma, delta, ||r||^2} per iteration
+    // (npc_context_set_fused_allreduce / NPC_PCG_FUSED_ALLREDUCE=1; solvers.cu).
+    bool fused_allreduce = false;
     bool timing = false;
     int timing_suppress = 0;         // > 0: inside a scope that times a whole group of launches
     bool capturing = false;          // a PCG iteration is being stream-captured (timing on)
@@ -441,6 +445,7 @@ struct PcgCache {
     const void *key_partials = nullptr;
     size_t key_cap = 0;
     bool timed = false;                         // captured with timing event nodes
+    bool fused = false;                         // captured with the single fused allreduce
     std::vector<Context::Pending> timing_events;  // owned by the graph (re-recorded per replay)
     void release_events() {
         for (auto &p : timing_events) {

@@ -435,9 +435,25 @@ struct CgDev {
 
 // sums[0] = <r, u> (gamma), sums[1] = <u, A u> (delta) -- the one allreduce of the iteration.
 // (Distributed contexts reduce ||r_{i+1}||^2 separately, overlapped with the next p_k(A) r:
-// k_cg_rrcheck.)
-__global__ void k_cg_scalars(CgDev *st, const double *sums) {
+// k_cg_rrcheck.)  multi == 2 is the north star's single fused allreduce:
+// sums[2] = ||r_i||^2 of the previous update rode in the same allreduce, and the exit check
+// happens here, one (k+1)-application block late.
+__global__ void k_cg_scalars(CgDev *st, const double *sums, double *history) {
     if (st->done) return;
+    if (st->multi == 2) {
+        const double t = sums[2];
+        st->rr = t;
+        if (history) history[st->iters] = sqrt(t / st->bnorm2);
+        if (t <= st->tol2) {
+            st->converged = 1;
+            st->done = 1;
+            return;
+        }
+        if (st->iters >= st->maxit) {
+            st->done = 1;
+            return;
+        }
+    }
     const double g = sums[0], dl = sums[1];
     if (!(g > 0.0)) {
         st->breakdown = 1;
@@ -496,7 +512,9 @@ __global__ void __launch_bounds__(1024) k_cg_rr(CgDev *st, const double *__restr
     t = block_sum<1024>(t, red);
     if (threadIdx.x == 0) {
         st->iters += 1;
-        sums[st->multi ? 4 : 2] = t;  // multi: the local partial, allreduced on the side stream
+        // multi 1: the local partial, allreduced on the side stream; multi 2: the local partial
+        // rides in the next iteration's fused allreduce
+        sums[st->multi == 1 ? 4 : 2] = t;
         if (!st->multi) {
             st->rr = t;
             if (history) history[st->iters] = sqrt(t / st->bnorm2);
@@ -830,7 +848,11 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     h.tol2 = tol * tol * bnorm2;
     h.maxit = maxit;
     h.first = 1;
-    h.multi = ctx->distributed();
+    // 1 = side-stream ||r||^2 check (default), 2 = one fused {gamma, delta, ||r||^2} allreduce
+    h.multi = ctx->distributed() ? (ctx->fused_allreduce ? 2 : 1) : 0;
+    const bool side_rr = h.multi == 1, fused_rr = h.multi == 2;
+    // the fused allreduce sums sums[2] over the ranks: a global value is seeded as its 1/P share
+    const double rr_share = fused_rr ? 1.0 / ctx->nranks : 1.0;
     bool done = rr0 <= h.tol2;
     st.relres_recursive = sqrt(rr0 / bnorm2);
     if (done) {
@@ -852,8 +874,9 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         NPC_CUDA_TRY(cudaMemcpyAsync(r, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
         h.rr = tr * tr * bnorm2;
     }
+    double rr_seed = h.rr * rr_share;
     NPC_CUDA_TRY(cudaMemcpyAsync(cg, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
-    NPC_CUDA_TRY(cudaMemcpyAsync(sums + 2, &h.rr, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    NPC_CUDA_TRY(cudaMemcpyAsync(sums + 2, &rr_seed, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     const int *dflag = &cg->done;
     int chunk = 4;
     // Iterations between host checks grow 4, 8, ..., 64 for short iterations; when one chunk of
@@ -872,7 +895,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         }
         return NPC_SUCCESS;
     };
-    if (h.multi && !ctx->ev_rr0) {
+    if (side_rr && !ctx->ev_rr0) {
         NPC_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_rr0, cudaEventDisableTiming));
         NPC_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_rr1, cudaEventDisableTiming));
     }
@@ -902,11 +925,11 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                 TimedScope ts(ctx, T_REDUCE);
                 NPC_TRY(launch_reduce_sum(ctx, P0, npg, sums + 0, 1, P1, np_op, sums + 1));
             }
-            NPC_TRY(ctx->allreduce_sum(sums, 2));  // the single global reduction
+            NPC_TRY(ctx->allreduce_sum(sums, fused_rr ? 3 : 2));  // the single global reduction
             NPC_TRY(join_rr());  // ||r_i||^2 of the previous update is known (and checked)
             {
                 TimedScope ts(ctx, T_REDUCE);
-                k_cg_scalars<<<1, 1, 0, ctx->stream>>>(cg, sums);
+                k_cg_scalars<<<1, 1, 0, ctx->stream>>>(cg, sums, dhist);
                 NPC_LAUNCH_CHECK();
             }
             {
@@ -919,7 +942,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                 k_cg_rr<<<1, 1024, 0, ctx->stream>>>(cg, P2, np_vec, sums, dhist);
                 NPC_LAUNCH_CHECK();
             }
-            if (h.multi) {  // ||r_{i+1}||^2: allreduce + check on the side stream
+            if (side_rr) {  // ||r_{i+1}||^2: allreduce + check on the side stream
                 NvtxRange nv("npc:allreduce_rr");
                 NPC_CUDA_TRY(cudaEventRecord(ctx->ev_rr0, ctx->stream));
                 NPC_CUDA_TRY(cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_rr0, 0));
@@ -939,7 +962,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     // launches; NCCL calls and the halo fork/join are captured too.  Off while timing.
     // With timing on, the captured graph carries event-record nodes around every launch and is
     // replayed one graph per host sync so that its events can be read after each replay.
-    if (cache.exec && cache.timed != ctx->timing) cache.invalidate();
+    if (cache.exec && (cache.timed != ctx->timing || cache.fused != fused_rr)) cache.invalidate();
     GraphRun gr(ctx, cache);
     const bool graph_ok = op->capture_safe() && (!ctx->tr || ctx->tr->capturable()) && !getenv("NPC_NO_GRAPH");
     // A new graph costs capture + instantiation: milliseconds with NCCL calls in it (16 ms for a
@@ -962,6 +985,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     if (graph_ok && !deferred) {
         iter_calls = 0;
         NPC_TRY(gr.capture(iteration, cond ? dflag : nullptr));
+        cache.fused = fused_rr;
     }
     t_chunk = now_s();  // the first chunk's clock starts after the capture
     for (;;) {
@@ -990,6 +1014,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
                 deferred = false;
                 iter_calls = 0;
                 NPC_TRY(gr.capture(iteration, cond ? dflag : nullptr));
+                cache.fused = fused_rr;
             }
             if (chunk_max == 64 && now_s() - t_chunk >= 2e-3) chunk_max = GraphRun::ITERS;
             chunk = std::min(chunk * 2, chunk_max);
@@ -998,6 +1023,8 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
         }
         st.iters = h.iters;
         st.relres_recursive = sqrt(h.rr / bnorm2);
+        // fused allreduce: the exit was seen after u = p_k(A) r and w = A u of the next iteration
+        if (fused_rr && !h.breakdown) st.op_applications += k + 1, st.reductions += 1;
         if (h.breakdown) {
             set_error("PCG breakdown (%s <= 0) at iteration %d", h.breakdown == 1 ? "<r,z>" : "<p,Ap>", h.iters);
             result = NPC_ERR_BREAKDOWN;
@@ -1022,8 +1049,9 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
             h.converged = 0;
             h.done = 0;
             h.first = 1;
+            rr_seed = h.rr * rr_share;
             NPC_CUDA_TRY(cudaMemcpyAsync(cg, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
-            NPC_CUDA_TRY(cudaMemcpyAsync(sums + 2, &h.rr, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            NPC_CUDA_TRY(cudaMemcpyAsync(sums + 2, &rr_seed, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
             if (h.iters >= maxit) {
                 result = NPC_ERR_NOT_CONVERGED;
                 break;
@@ -1043,7 +1071,7 @@ npc_status pcg(npc_poly P, npc_operator H, const double *b_ext, double *x_ext, d
     // ||r||^2 in a second (overlapped) allreduce per iteration.  Not counted: the application
     // in flight when the overlapped check raises the done flag (its remaining kernels no-op).
     st.op_applications += (long long)h.iters * (k + 1);
-    st.reductions += h.iters * (h.multi ? 2 : 1);
+    st.reductions += h.iters * (side_rr ? 2 : 1);
     if (P && P->lr_p > 0)  // V^T r inside every application of the preconditioner
         st.reductions += h.iters;
     if (host_hist && h.iters > 0)

@@ -221,3 +221,54 @@ def test_multirank_with_an_empty_rank(kind):
     assert len(its) == 1 and abs(its.pop() - st_o["iters"]) <= 2
     xs = np.concatenate([q["x"] for q in res])
     assert np.linalg.norm(w["b"] - orc.apply(xs)) / np.linalg.norm(w["b"]) <= w["tol"]
+
+
+# ---------------------------------------------------------------- single fused allreduce
+FUSED = [("c3", "csr", 2, "local"), ("c2", "stencil", 3, "local"), ("c5", "schur", 2, "local"),
+         ("c3", "csr", 1, "nccl"), ("c4", "sell", 1, "nccl"), ("c6", "dfn", 1, "nccl")]
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("name,kind,ws,transport", FUSED)
+def test_pcg_single_fused_allreduce(wl, name, kind, ws, transport):
+    """npc_context_set_fused_allreduce(1): ONE allreduce of {gamma, delta, ||r||^2} per PCG
+    iteration (north star).  Same iterates as the default side-stream check --
+    identical iteration count and solution -- but the exit is seen one (k+1)-application block
+    late: op_applications = (iters + 1)(k + 1) + 1 (SURVEY §8(b) "naive single-allreduce
+    exit"), reductions = iters + 1 (the block that sees the exit) + 3."""
+    w = wl(name)
+    orc = oracle.Operator(w)
+    n = w["n"]
+    lo_o, hi_o = oracle.estimate_spectrum(orc, 20, W.lanczos_start(n))
+    k = 12
+    _, st_o = oracle.pcg(orc, w["b"], k, lo_o, hi_o, 0.0, tol=w["tol"], maxit=5000)
+
+    def fn(rank, ctx, stream):
+        op, r0, r1 = bench.create_operator(npc, ctx, w, kind, ws, rank, CFG[name])
+        b = torch.tensor(np.ascontiguousarray(w["b"][r0:r1]), device="cuda")
+        poly = npc.npc_set_poly(op, k, lo_o, hi_o, 0.0)
+        out = {}
+        for fused in (False, True, True):  # the second fused solve replays the cached graph
+            npc.npc_context_set_fused_allreduce(ctx, fused)
+            xs = torch.zeros_like(b)
+            st = npc.npc_pcg_solve(poly, op, b, xs, w["tol"], 5000)
+            stream.synchronize()
+            out[fused] = (st, xs.cpu().numpy())
+        # maxit: the fused form stops after exactly maxit x-updates too
+        xs = torch.zeros_like(b)
+        stm = npc.npc_pcg_solve(poly, op, b, xs, 1e-14, 3, raise_on_error=False)
+        assert stm["status"] != "NPC_SUCCESS" and stm["iters"] == 3 and not stm["converged"], stm
+        return out
+
+    res = (run_ranks if transport == "local" else run_nccl_one_rank)(ws, fn)
+    st0, st1 = res[0][False][0], res[0][True][0]
+    assert st0["iters"] == st1["iters"] and abs(st1["iters"] - st_o["iters"]) <= 2
+    assert st1["converged"] and st1["relres_true"] <= w["tol"]
+    assert st1["op_applications"] == (st1["iters"] + 1) * (k + 1) + 1
+    assert st1["reductions"] == st1["iters"] + 1 + 3
+    assert st0["reductions"] == 2 * st0["iters"] + 3
+    x0 = np.concatenate([q[False][1] for q in res])
+    x1 = np.concatenate([q[True][1] for q in res])
+    # the two forms run the same arithmetic on the same data
+    assert np.array_equal(x0, x1)
+    assert np.linalg.norm(w["b"] - orc.apply(x1)) / np.linalg.norm(w["b"]) <= w["tol"]
