@@ -634,7 +634,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 3),
         "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded workloads/)",
         "config": config_dict(cfg, w, kind, k, args.xi, M, V),
         "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",

@@ -269,6 +269,10 @@ def test_pcg_single_fused_allreduce(wl, name, kind, ws, transport):
     assert st0["reductions"] == 2 * st0["iters"] + 3
     x0 = np.concatenate([q[False][1] for q in res])
     x1 = np.concatenate([q[True][1] for q in res])
-    # the two forms run the same arithmetic on the same data
-    assert np.array_equal(x0, x1)
+    # the two forms run the same arithmetic on the same data (the multi-rank Schur operator
+    # accumulates B^T t with fp64 atomics, so its bits vary from run to run)
+    if kind == "schur" and ws > 1:
+        assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x0)
+    else:
+        assert np.array_equal(x0, x1)
     assert np.linalg.norm(w["b"] - orc.apply(x1)) / np.linalg.norm(w["b"]) <= w["tol"]
