@@ -513,7 +513,11 @@ def run_ours(args):
                     "op_applications_per_s": round(stats[-1]["op_applications"] / (ms_step * 1e-3), 1)},
             "roofline": {"bound": "hbm", "kernel": f"fused degree step ({kind})", "achieved": round(ach, 1),
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / peak, 4),
-                         "frac_vs_8TBs_nominal": round(ach / 8000.0, 4), "traffic": traffic,
+                         "frac_vs_8TBs_nominal": round(ach / 8000.0, 4),
+                         # the same launches on SURVEY §8(d)'s format-independent bytes (CSR 12 B per
+                         # nonzero): > 1 when the stored format streams less than that floor assumes
+                         "frac_survey_8d_bytes": round(ach * poly_bytes(M / ws, Vf, k) / max(apply_bytes, 1) / peak, 4),
+                         "traffic": traffic,
                          "bytes_per_launch": apply_bytes / max(k, 1), "launch_ms": round(per_launch_ms, 5),
                          "bytes_basis": ("operator data in the stored format (npc_operator_matrix_bytes: "
                                          f"{Mf / 1e6:.1f} MB per application) + the recurrence's vector streams; "
