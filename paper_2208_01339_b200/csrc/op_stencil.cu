@@ -93,6 +93,92 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
     }
 }
 
+// ---------------------------------------------------------------- two x-points per thread
+// k_stencil_step with 128-bit accesses: a thread owns the points (x0, x0 + 1), x0 even, of its
+// row and marches z as above, so every stream (s_{j-1} planes, the y neighbours, s_{j-2}, r,
+// the store) moves as double2 and the kernel issues 7 loads + 1 store per TWO points instead of
+// per point (config 2 is latency / LSU-issue bound, not bandwidth bound: profiles/
+// r02_ncu_summary.md).  A CTA is 16 x 8 threads on the SAME 32 x 8 point tile and grid as
+// k_stencil_step (same partial slots).  The neighbour sum keeps k_stencil_step's order
+// (z-1, y-1, x-1, x+1, y+1, z+1) and explicit FMAs, so out is bitwise the same.  Needs an even
+// nx and 16-byte aligned vectors (checked at dispatch).
+static constexpr int SV_BX = ST_BX / 2;
+template <int DIM, bool HAS_S2, bool HAS_R, bool DOT>
+__global__ void __launch_bounds__(SV_BX *ST_BY) k_stencil_step_v2(StencilDev S, StepArgs s, int z_lo, int z_hi, int zc) {
+    if (s.done && *s.done) return;
+    __shared__ double red[SV_BX * ST_BY / 32];
+    const int x0 = blockIdx.x * ST_BX + 2 * threadIdx.x;
+    const int y = blockIdx.y * ST_BY + threadIdx.y;
+    const int z0 = z_lo + blockIdx.z * zc;
+    const int z1 = min(z0 + zc, z_hi);
+    const long long plane = (long long)S.nx * S.ny;
+    const double *__restrict__ X = s.x;
+    double acc = 0.0;
+    if (x0 < S.nx && y < S.ny && z0 < z1) {
+        const int pidx = x0 + S.nx * y;
+        long long i = pidx + plane * z0;
+        const bool has_l = x0 > 0, has_r = x0 + 2 < S.nx, has_d = y > 0, has_u = y < S.ny - 1;
+        double2 below = make_double2(0.0, 0.0), cur = *reinterpret_cast<const double2 *>(X + i);
+        if (DIM == 3) {
+            if (z0 > 0)
+                below = *reinterpret_cast<const double2 *>(X + i - plane);
+            else if (S.glo)
+                below = *reinterpret_cast<const double2 *>(S.glo + pidx);
+        }
+        for (int z = z0; z < z1; ++z, i += plane) {
+            double2 above = make_double2(0.0, 0.0);
+            if (DIM == 3) {
+                if (z + 1 < S.nzl)
+                    above = *reinterpret_cast<const double2 *>(X + i + plane);
+                else if (S.ghi)
+                    above = *reinterpret_cast<const double2 *>(S.ghi + pidx);
+            }
+            double na = below.x, nb = below.y;
+            if (has_d) {
+                const double2 t = *reinterpret_cast<const double2 *>(X + i - S.nx);
+                na += t.x;
+                nb += t.y;
+            }
+            if (has_l) na += X[i - 1];
+            nb += cur.x;
+            na += cur.y;
+            if (has_r) nb += X[i + 2];
+            if (has_u) {
+                const double2 t = *reinterpret_cast<const double2 *>(X + i + S.nx);
+                na += t.x;
+                nb += t.y;
+            }
+            na += above.x;
+            nb += above.y;
+            double2 o;
+            o.x = st_lin(s.a, st_ax(S.diag, cur.x, S.off, na), s.b, cur.x);
+            o.y = st_lin(s.a, st_ax(S.diag, cur.y, S.off, nb), s.b, cur.y);
+            if (HAS_S2) {
+                const double2 t = *reinterpret_cast<const double2 *>(s.s2 + i);
+                o.x = __fma_rn(s.c, t.x, o.x);
+                o.y = __fma_rn(s.c, t.y, o.y);
+            }
+            if (HAS_R) {
+                const double2 t = *reinterpret_cast<const double2 *>(s.r + i);
+                o.x = __fma_rn(s.d, t.x, o.x);
+                o.y = __fma_rn(s.d, t.y, o.y);
+            }
+            *reinterpret_cast<double2 *>(s.out + i) = o;
+            if (DOT) {
+                const double2 t = *reinterpret_cast<const double2 *>(s.dotv + i);
+                acc += o.x * t.x;
+                acc += o.y * t.y;
+            }
+            below = cur;
+            cur = above;
+        }
+    }
+    if (DOT) {
+        acc = block_sum<SV_BX * ST_BY>(acc, red);
+        if (threadIdx.x == 0 && threadIdx.y == 0) s.partials[linear_bid()] = acc;
+    }
+}
+
 // ---------------------------------------------------------------- all k degrees in one launch
 // For grids whose vectors sit in L2 (config 2: 4 x 16.8 MB), a degree takes ~10 us and kernel
 // boundaries (launch gap, ramp-up, tail) are a large part of it.  This cooperative kernel runs
@@ -107,12 +193,17 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
 #ifndef NPC_GRID_MINB
 #define NPC_GRID_MINB 4  // A/B (config 2): 4 CTAs per SM (62 registers, no spill); 6 or 8 spill and run 1.8x slower
 #endif
-template <int DIM>
-__global__ void __launch_bounds__(ST_BX *ST_BY, NPC_GRID_MINB) k_stencil_poly_grid(StencilDev S, const double *__restrict__ r,
-                                                                    double *z, double *tmp,
-                                                                    const double *__restrict__ coef, int k, double tb,
-                                                                    int zc, const double *__restrict__ dotv,
-                                                                    double *partials, const int *done) {
+// V2: two x-points per thread with 128-bit accesses, as k_stencil_step_v2 (a CTA is 16 x 8
+// threads on the same 32 x 8 tile, twice as many CTAs per SM at the same register cap); needs an
+// even nx and 16-byte aligned vectors.  Same element arithmetic, so s_k is bitwise the same.
+#ifndef NPC_GRID_MINB_V2
+#define NPC_GRID_MINB_V2 8  // CTAs of 128 threads per SM (64 registers)
+#endif
+template <int DIM, bool V2>
+__global__ void __launch_bounds__((V2 ? SV_BX : ST_BX) * ST_BY, V2 ? NPC_GRID_MINB_V2 : NPC_GRID_MINB)
+    k_stencil_poly_grid(StencilDev S, const double *__restrict__ r, double *z, double *tmp,
+                        const double *__restrict__ coef, int k, double tb, int zc, const double *__restrict__ dotv,
+                        double *partials, const int *done) {
     if (done && *done) return;  // uniform over the grid (no kernel writes the flag meanwhile)
     cg::grid_group grid = cg::this_grid();
     __shared__ double red[ST_BX * ST_BY / 32];
@@ -141,9 +232,59 @@ __global__ void __launch_bounds__(ST_BX *ST_BY, NPC_GRID_MINB) k_stencil_poly_gr
         }
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             const int bx = it % gx, by = (it / gx) % gy, bz = it / (gx * gy);
-            const int x = bx * ST_BX + threadIdx.x, y = by * ST_BY + threadIdx.y;
+            const int x = bx * ST_BX + (V2 ? 2 : 1) * threadIdx.x, y = by * ST_BY + threadIdx.y;
             const int z0 = DIM == 3 ? bz * zc : 0, z1 = DIM == 3 ? min(z0 + zc, S.nzl) : 1;
             if (x >= S.nx || y >= S.ny) continue;
+            if (V2) {
+                const int pidx = x + S.nx * y;
+                long long i = pidx + plane * z0;
+                const bool has_l = x > 0, has_r = x + 2 < S.nx, has_d = y > 0, has_u = y < S.ny - 1;
+                double2 below = make_double2(0.0, 0.0), cur = *reinterpret_cast<const double2 *>(X + i);
+                if (DIM == 3 && z0 > 0) below = *reinterpret_cast<const double2 *>(X + i - plane);
+                for (int zz = z0; zz < z1; ++zz, i += plane) {
+                    double2 above = make_double2(0.0, 0.0);
+                    if (DIM == 3 && zz + 1 < S.nzl) above = *reinterpret_cast<const double2 *>(X + i + plane);
+                    double na = below.x, nb = below.y;
+                    if (has_d) {
+                        const double2 t = *reinterpret_cast<const double2 *>(X + i - S.nx);
+                        na += t.x;
+                        nb += t.y;
+                    }
+                    if (has_l) na += X[i - 1];
+                    nb += cur.x;
+                    na += cur.y;
+                    if (has_r) nb += X[i + 2];
+                    if (has_u) {
+                        const double2 t = *reinterpret_cast<const double2 *>(X + i + S.nx);
+                        na += t.x;
+                        nb += t.y;
+                    }
+                    na += above.x;
+                    nb += above.y;
+                    double2 o;
+                    o.x = st_lin(a, st_ax(S.diag, cur.x, S.off, na), b, cur.x);
+                    o.y = st_lin(a, st_ax(S.diag, cur.y, S.off, nb), b, cur.y);
+                    if (j >= 3) {
+                        const double2 t = *reinterpret_cast<const double2 *>(out + i);
+                        o.x = __fma_rn(c, t.x, o.x);
+                        o.y = __fma_rn(c, t.y, o.y);
+                    }
+                    if (j >= 2) {
+                        const double2 t = *reinterpret_cast<const double2 *>(r + i);
+                        o.x = __fma_rn(d, t.x, o.x);
+                        o.y = __fma_rn(d, t.y, o.y);
+                    }
+                    *reinterpret_cast<double2 *>(out + i) = o;
+                    if (j == k && dotv) {
+                        const double2 t = *reinterpret_cast<const double2 *>(dotv + i);
+                        acc += o.x * t.x;
+                        acc += o.y * t.y;
+                    }
+                    below = cur;
+                    cur = above;
+                }
+                continue;
+            }
             const int pidx = x + S.nx * y;
             long long i = pidx + plane * z0;
             double below = 0.0, cur = X[i];
@@ -170,7 +311,7 @@ __global__ void __launch_bounds__(ST_BX *ST_BY, NPC_GRID_MINB) k_stencil_poly_gr
         if (j < k) grid.sync();
     }
     if (dotv) {
-        acc = block_sum<ST_BX * ST_BY>(acc, red);
+        acc = block_sum<(V2 ? SV_BX : ST_BX) * ST_BY>(acc, red);
         if (threadIdx.x == 0 && threadIdx.y == 0) partials[blockIdx.x] = acc;
     }
 }
@@ -642,10 +783,11 @@ class StencilOperator : public Operator {
     // TMA-staged kernel (k_stencil_tma): single rank, even nx (16-byte row strides), 16-byte
     // aligned vectors; tensor maps cached per (pointer, box kind)
     bool tma = false;
+    bool vec2 = false;  // k_stencil_step_v2 (two x-points per thread, 128-bit accesses)
     int tma_blocks = 0, tma_zc = 0, tma_items = 0;
     bool tma2 = false;  // k_stencil_tma2 for the paired degrees (step2)
     // k_stencil_poly_grid: single rank, vectors L2-resident; co-resident grid size (0 = off)
-    int grid_blocks = 0, grid_zc = 1;
+    int grid_blocks = 0, grid_zc = 1, grid_cap_scalar = 0;
     DevBuf poly_tmp;  // its scratch vector (s_{k-1}, s_{k-3}, ...), allocated at create
     int tma2_blocks = 0, tma2_zc = 0, tma2_items = 0;
     std::map<std::pair<const void *, int>, CUtensorMap> tmaps;
@@ -755,7 +897,10 @@ class StencilOperator : public Operator {
         }
         StepArgs a = s;
         a.partials = partials;
-        k_stencil_step<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(ST_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
+        if (vec2 && al16(s.x) && al16(s.s2) && al16(s.r) && al16(s.out) && al16(s.dotv) && al16(S.glo) && al16(S.ghi))
+            k_stencil_step_v2<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(SV_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
+        else
+            k_stencil_step<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(ST_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
     }
@@ -859,8 +1004,12 @@ class StencilOperator : public Operator {
         StencilDev S{nx, ny, nzl, diag, off, nullptr, nullptr};
         const int zc = grid_zc;
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(grid_blocks, 1, 1);
-        cfg.blockDim = dim3(ST_BX, ST_BY, 1);
+        // the 128-bit form needs aligned vectors; otherwise the scalar form on at most its own
+        // co-resident grid (items are strided over whatever grid is launched)
+        const bool v2 = vec2 && al16(r) && al16(z) && al16(dotv);
+        const int gb = v2 ? grid_blocks : std::min(grid_blocks, grid_cap_scalar);
+        cfg.gridDim = dim3(gb, 1, 1);
+        cfg.blockDim = dim3(v2 ? SV_BX : ST_BX, ST_BY, 1);
         cfg.dynamicSmemBytes = 0;
         cfg.stream = ctx->stream;
         cudaLaunchAttribute at[1];
@@ -868,14 +1017,20 @@ class StencilOperator : public Operator {
         at[0].val.cooperative = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        if (dim == 3)
-            NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_poly_grid<3>, S, r, z, tmp, coef_dev, k, tb, zc, dotv,
+        if (dim == 3 && v2)
+            NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_poly_grid<3, true>, S, r, z, tmp, coef_dev, k, tb, zc, dotv,
+                                            partials, done));
+        else if (dim == 3)
+            NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_poly_grid<3, false>, S, r, z, tmp, coef_dev, k, tb, zc,
+                                            dotv, partials, done));
+        else if (v2)
+            NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_poly_grid<2, true>, S, r, z, tmp, coef_dev, k, tb, zc, dotv,
                                             partials, done));
         else
-            NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_poly_grid<2>, S, r, z, tmp, coef_dev, k, tb, zc, dotv,
-                                            partials, done));
+            NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_poly_grid<2, false>, S, r, z, tmp, coef_dev, k, tb, zc,
+                                            dotv, partials, done));
         NPC_LAUNCH_CHECK();
-        if (dotv && nparts) *nparts = grid_blocks;
+        if (dotv && nparts) *nparts = gb;
         return NPC_SUCCESS;
     }
 
@@ -935,6 +1090,7 @@ npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::
     op->diag = d->diag;
     op->off = d->offdiag;
     if (const char *e = getenv("NPC_ST_ZC")) op->zc_main = std::max(1, atoi(e));
+    op->vec2 = op->nx % 2 == 0 && !getenv("NPC_ST_NOV2");  // A/B: NPC_ST_NOV2=1 keeps the scalar kernels
     const long long plane = (long long)op->nx * op->ny;
     if (plane * op->nzl >= (1LL << 31)) {
         set_error("stencil: more than 2^31 local rows");
@@ -983,12 +1139,19 @@ npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::
     // all degrees in one cooperative launch when the vectors are L2-resident (single rank):
     // grid = min(items, co-resident CTAs)
     if (!ctx->distributed() && !big && !op->tma && op->n_local > 0 && !getenv("NPC_NO_GRID_POLY")) {
-        int per_sm = 0, coop = 0;
+        int per_sm = 0, per_sm_s = 0, coop = 0;
+        auto occ = [&](bool v2, int *out) {
+            return v2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                            out, op->dim == 3 ? k_stencil_poly_grid<3, true> : k_stencil_poly_grid<2, true>,
+                            SV_BX * ST_BY, 0)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                            out, op->dim == 3 ? k_stencil_poly_grid<3, false> : k_stencil_poly_grid<2, false>,
+                            ST_BX * ST_BY, 0);
+        };
         if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device) == cudaSuccess && coop &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, op->dim == 3 ? k_stencil_poly_grid<3> : k_stencil_poly_grid<2>, ST_BX * ST_BY, 0) ==
-                cudaSuccess &&
-            per_sm > 0) {
+            occ(op->vec2, &per_sm) == cudaSuccess && occ(false, &per_sm_s) == cudaSuccess && per_sm > 0 &&
+            per_sm_s > 0) {
+            op->grid_cap_scalar = per_sm_s * ctx->num_sms;
             // z-chunks sized so that every (x, y, z-chunk) item has its own co-resident CTA (one
             // round per degree, no tail): chunks = co-resident CTAs / (x, y) tiles
             const long long tiles = (long long)ceil_div(op->nx, ST_BX) * ceil_div(op->ny, ST_BY);
