@@ -105,6 +105,11 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
 static constexpr int SV_BX = ST_BX / 2;
 template <int DIM, bool HAS_S2, bool HAS_R, bool DOT>
 __global__ void __launch_bounds__(SV_BX *ST_BY) k_stencil_step_v2(StencilDev S, StepArgs s, int z_lo, int z_hi, int zc) {
+    // Programmatic dependent launch (opt-in, NPC_ST_PDL=1): let the next launch's CTAs become
+    // resident now, and wait here for the previous grid to complete (and flush) before reading
+    // anything it wrote -- the done flag included.  Both are no-ops in an ordinary launch.
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (s.done && *s.done) return;
     __shared__ double red[SV_BX * ST_BY / 32];
     const int x0 = blockIdx.x * ST_BX + 2 * threadIdx.x;
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(SV_BX *ST_BY) k_stencil_step_v2(StencilDev S, 
 // threads on the same 32 x 8 tile, twice as many CTAs per SM at the same register cap); needs an
 // even nx and 16-byte aligned vectors.  Same element arithmetic, so s_k is bitwise the same.
 #ifndef NPC_GRID_MINB_V2
-#define NPC_GRID_MINB_V2 8  // CTAs of 128 threads per SM (64 registers)
+#define NPC_GRID_MINB_V2 4  // A/B (config 2 p_30): 4 CTAs of 128 threads per SM 0.257 ms, 6 0.265, 8 (64 registers) 0.294
 #endif
 template <int DIM, bool V2>
 __global__ void __launch_bounds__((V2 ? SV_BX : ST_BX) * ST_BY, V2 ? NPC_GRID_MINB_V2 : NPC_GRID_MINB)
@@ -783,6 +788,7 @@ class StencilOperator : public Operator {
     // TMA-staged kernel (k_stencil_tma): single rank, even nx (16-byte row strides), 16-byte
     // aligned vectors; tensor maps cached per (pointer, box kind)
     bool tma = false;
+    bool pdl = false;   // A/B: programmatic dependent launch of k_stencil_step_v2 (NPC_ST_PDL=1)
     bool vec2 = false;  // k_stencil_step_v2 (two x-points per thread, 128-bit accesses)
     int tma_blocks = 0, tma_zc = 0, tma_items = 0;
     bool tma2 = false;  // k_stencil_tma2 for the paired degrees (step2)
@@ -897,9 +903,22 @@ class StencilOperator : public Operator {
         }
         StepArgs a = s;
         a.partials = partials;
-        if (vec2 && al16(s.x) && al16(s.s2) && al16(s.r) && al16(s.out) && al16(s.dotv) && al16(S.glo) && al16(S.ghi))
-            k_stencil_step_v2<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(SV_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
-        else
+        if (vec2 && al16(s.x) && al16(s.s2) && al16(s.r) && al16(s.out) && al16(s.dotv) && al16(S.glo) && al16(S.ghi)) {
+            if (pdl) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = grid_for(z_hi - z_lo, zc);
+                cfg.blockDim = dim3(SV_BX, ST_BY, 1);
+                cfg.stream = ctx->stream;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_step_v2<D, H2, HR, DT>, S, a, z_lo, z_hi, zc));
+            } else {
+                k_stencil_step_v2<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(SV_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
+            }
+        } else
             k_stencil_step<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(ST_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
         NPC_LAUNCH_CHECK();
         return NPC_SUCCESS;
@@ -995,6 +1014,9 @@ class StencilOperator : public Operator {
     bool supports_fused_poly() const override {
         if (grid_blocks <= 0 || getenv("NPC_NO_GRID_POLY")) return false;
         if (getenv("NPC_GRID_IN_GRAPH")) return true;  // A/B
+        // with the 128-bit kernels k per-degree launches beat the cooperative launch even eagerly
+        // (config 2 p_30: 0.248 vs 0.257 ms, profiles/r02_stencil_vec2_ab.md); NPC_GRID_POLY=1 forces it
+        if (vec2 && !getenv("NPC_GRID_POLY")) return false;
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         return cudaStreamIsCapturing(ctx->stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
     }
@@ -1090,6 +1112,7 @@ npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::
     op->diag = d->diag;
     op->off = d->offdiag;
     if (const char *e = getenv("NPC_ST_ZC")) op->zc_main = std::max(1, atoi(e));
+    op->pdl = !ctx->distributed() && getenv("NPC_ST_PDL") != nullptr;
     op->vec2 = op->nx % 2 == 0 && !getenv("NPC_ST_NOV2");  // A/B: NPC_ST_NOV2=1 keeps the scalar kernels
     const long long plane = (long long)op->nx * op->ny;
     if (plane * op->nzl >= (1LL << 31)) {

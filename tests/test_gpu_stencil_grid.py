@@ -1,6 +1,6 @@
 """GPU: all k degrees of p_k(A) r in one cooperative launch for L2-resident stencils
-(op_stencil.cu k_stencil_poly_grid, the default for single-rank stencils whose four vectors fit
-L2, e.g. config 2) against k launches of the per-degree kernel (NPC_NO_GRID_POLY=1,
+(op_stencil.cu k_stencil_poly_grid: the default for single-rank odd-nx stencils whose four vectors
+fit L2, NPC_GRID_POLY=1 for even nx, where the 128-bit per-degree kernels are faster) against k launches of the per-degree kernel (NPC_NO_GRID_POLY=1,
 k_stencil_step) and the oracle (Alg. 2 verbatim), through the C ABI.
 
 Same decomposition and the same explicit FMAs per element, so s_k must be BITWISE equal to
@@ -80,7 +80,11 @@ def test_grid_poly_bitwise_equals_per_degree_and_oracle(ctx, name):
     ks = (1, 2, 3, 30) if n > 1_000_000 else (1, 2, 3, 8, 30, 200)
     for k in ks:
         for xi in (0.0, 1e-3):
-            npc.npc_apply_poly(npc.npc_set_poly(op, k, lo, hi, xi), dev(r), zg)
+            os.environ["NPC_GRID_POLY"] = "1"  # even nx: the per-degree 128-bit kernels are the default
+            try:
+                npc.npc_apply_poly(npc.npc_set_poly(op, k, lo, hi, xi), dev(r), zg)
+            finally:
+                os.environ.pop("NPC_GRID_POLY", None)
             with per_degree():
                 npc.npc_apply_poly(npc.npc_set_poly(op, k, lo, hi, xi), dev(r), zd)
             assert torch.equal(zg, zd), (k, xi)
