@@ -105,11 +105,10 @@ __global__ void __launch_bounds__(ST_BX *ST_BY) k_stencil_step(StencilDev S, Ste
 static constexpr int SV_BX = ST_BX / 2;
 template <int DIM, bool HAS_S2, bool HAS_R, bool DOT>
 __global__ void __launch_bounds__(SV_BX *ST_BY) k_stencil_step_v2(StencilDev S, StepArgs s, int z_lo, int z_hi, int zc) {
-    // Programmatic dependent launch (opt-in, NPC_ST_PDL=1): let the next launch's CTAs become
-    // resident now, and wait here for the previous grid to complete (and flush) before reading
-    // anything it wrote -- the done flag included.  Both are no-ops in an ordinary launch.
-    asm volatile("griddepcontrol.launch_dependents;");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (Programmatic dependent launch -- griddepcontrol.launch_dependents / .wait here and the
+    // stream-serialization launch attribute -- was measured and removed: config 2 p_30 0.278 vs
+    // 0.270 ms, PCG 9.3 vs 8.3 ms, and the two instructions alone cost an ordinary launch 9 %:
+    // profiles/r02_stencil_vec2_ab.md.)
     if (s.done && *s.done) return;
     __shared__ double red[SV_BX * ST_BY / 32];
     const int x0 = blockIdx.x * ST_BX + 2 * threadIdx.x;
@@ -788,7 +787,6 @@ class StencilOperator : public Operator {
     // TMA-staged kernel (k_stencil_tma): single rank, even nx (16-byte row strides), 16-byte
     // aligned vectors; tensor maps cached per (pointer, box kind)
     bool tma = false;
-    bool pdl = false;   // A/B: programmatic dependent launch of k_stencil_step_v2 (NPC_ST_PDL=1)
     bool vec2 = false;  // k_stencil_step_v2 (two x-points per thread, 128-bit accesses)
     int tma_blocks = 0, tma_zc = 0, tma_items = 0;
     bool tma2 = false;  // k_stencil_tma2 for the paired degrees (step2)
@@ -904,20 +902,7 @@ class StencilOperator : public Operator {
         StepArgs a = s;
         a.partials = partials;
         if (vec2 && al16(s.x) && al16(s.s2) && al16(s.r) && al16(s.out) && al16(s.dotv) && al16(S.glo) && al16(S.ghi)) {
-            if (pdl) {
-                cudaLaunchConfig_t cfg = {};
-                cfg.gridDim = grid_for(z_hi - z_lo, zc);
-                cfg.blockDim = dim3(SV_BX, ST_BY, 1);
-                cfg.stream = ctx->stream;
-                cudaLaunchAttribute at[1];
-                at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-                at[0].val.programmaticStreamSerializationAllowed = 1;
-                cfg.attrs = at;
-                cfg.numAttrs = 1;
-                NPC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stencil_step_v2<D, H2, HR, DT>, S, a, z_lo, z_hi, zc));
-            } else {
-                k_stencil_step_v2<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(SV_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
-            }
+            k_stencil_step_v2<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(SV_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
         } else
             k_stencil_step<D, H2, HR, DT><<<grid_for(z_hi - z_lo, zc), dim3(ST_BX, ST_BY), 0, ctx->stream>>>(S, a, z_lo, z_hi, zc);
         NPC_LAUNCH_CHECK();
@@ -1112,7 +1097,6 @@ npc_status make_stencil_operator(Context *ctx, const npc_operator_desc *d, std::
     op->diag = d->diag;
     op->off = d->offdiag;
     if (const char *e = getenv("NPC_ST_ZC")) op->zc_main = std::max(1, atoi(e));
-    op->pdl = !ctx->distributed() && getenv("NPC_ST_PDL") != nullptr;
     op->vec2 = op->nx % 2 == 0 && !getenv("NPC_ST_NOV2");  // A/B: NPC_ST_NOV2=1 keeps the scalar kernels
     const long long plane = (long long)op->nx * op->ny;
     if (plane * op->nzl >= (1LL << 31)) {
