@@ -5,6 +5,8 @@
 // regime)".  Kernel: 32x8 threads own an (x, y) tile and march along z,
 // keeping x[z-1], x[z], x[z+1] in registers (2.5D blocking) so each plane of the input is
 // read from L2/HBM once; the in-plane neighbours come from L1.  Epilogue as in op_csr.cu.
+// Default for even nx: the 128-bit form k_stencil_step_v2 (two x-points per thread, every
+// stream as double2); grids whose vectors exceed L2 take the TMA-staged kernel k_stencil_tma.
 // Multi-rank: z-slabs; ghost planes z_begin-1 and z_end arrive through the generic halo
 // (planes are contiguous row ranges), overlapped with the interior planes.
 #include <algorithm>
