@@ -489,12 +489,23 @@ __global__ void __launch_bounds__(256) k_cg_update(const CgDev *st, const double
     __shared__ double red[8];
     const double alpha = st->alpha, beta = st->beta;
     double acc = 0.0;
+    // p, s and x are touched only here, once per iteration: streaming (evict-first) accesses
+    // keep them from displacing r, u, w and the polynomial's ping-pong vector in L2, which
+    // matters when those fit and the whole PCG working set does not (config 2: 8 x 16.8 MB).
     for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+#ifndef NPC_CG_NOCS
+        const double pi = u[i] + beta * __ldcs(p + i);
+        const double si = w[i] + beta * __ldcs(s + i);
+        __stcs(p + i, pi);
+        __stcs(s + i, si);
+        __stcs(x + i, __ldcs(x + i) + alpha * pi);
+#else
         const double pi = u[i] + beta * p[i];
         const double si = w[i] + beta * s[i];
         p[i] = pi;
         s[i] = si;
         x[i] += alpha * pi;
+#endif
         const double ri = r[i] - alpha * si;
         r[i] = ri;
         acc += ri * ri;
